@@ -1,0 +1,126 @@
+"""Pins for the oracle's whole blend (§3.2, §3.3) against what the
+paper and the mathematics fix: r = 100 % is full prefill, r = 0 is the realigned cache, a single
+chunk is prefix reuse, sets nest, untouched entries are bitwise the realigned cache, and compute
+is proportional to the recompute ratio."""
+import numpy as np
+import pytest
+
+from oracle import cacheblend_oracle as O
+from synth import workload as W
+from tests.helpers import oracle_model, request_inputs, shape
+
+
+def _setup(name="tiny", seed=0, lens=(32, 32, 32), n_suf=0, dtype="f32", **over):
+    s = shape(name, **over)
+    m = oracle_model(s, seed, dtype)
+    req = W.Request(list(lens), n_suf, seed, 0.15)
+    tok, pos, cs, Kc, Vc = request_inputs(s, req, m, dtype)
+    return s, m, req, tok, pos, cs, Kc, Vc
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_full_ratio_equals_full_prefill(seed):
+    """S:290 / S:611: r = 1 -> KV^new = KV^full and h = full-prefill h (20 seeds, tiny config)."""
+    s, m, req, tok, pos, cs, Kc, Vc = _setup(seed=seed)
+    ks = O.schedule(1.0, req.n_ctx, s.n_layers)
+    # chunk caches in fp64 (no storage rounding) so the identity is exact up to fp64 rounding
+    Kc64, Vc64 = O.precompute_chunk_caches(m, tok, cs)
+    res = O.blend_forward(m, tok, pos, cs, 0, Kc64, Vc64, ks)
+    Kf, Vf, hf = O.full_prefill(m, tok, pos)
+    np.testing.assert_allclose(res.K, Kf, atol=1e-11)
+    np.testing.assert_allclose(res.V, Vf, atol=1e-11)
+    np.testing.assert_allclose(res.h_final, hf, atol=1e-10)
+
+
+def test_full_ratio_with_suffix_and_gqa():
+    s, m, req, tok, pos, cs, Kc, Vc = _setup(lens=(17, 40, 9), n_suf=5, n_kv_heads=2, n_layers=4)
+    Kc64, Vc64 = O.precompute_chunk_caches(m, tok[:req.n_ctx], cs)
+    res = O.blend_forward(m, tok, pos, cs, 5, Kc64, Vc64, O.schedule(1.0, req.n_ctx, 4))
+    Kf, Vf, hf = O.full_prefill(m, tok, pos)
+    np.testing.assert_allclose(res.K, Kf, atol=1e-11)
+    np.testing.assert_allclose(res.h_final, hf, atol=1e-10)
+
+
+def test_zero_ratio_is_realigned_cache():
+    """r = 0: KV^new = concatenated chunk caches after realignment; V bitwise (BASELINE north_star)."""
+    s, m, req, tok, pos, cs, Kc, Vc = _setup(seed=4)
+    res = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, O.schedule(0.0, req.n_ctx, s.n_layers))
+    loc = req.local_positions()
+    for i in range(s.n_layers):
+        np.testing.assert_array_equal(res.V[i], Vc[i])
+        np.testing.assert_allclose(res.K[i], O.realign(Kc[i], loc, pos, s.rope_theta), atol=0)
+        assert len(res.sel[i]) == (req.n_ctx if i == 0 else 0)
+
+
+@pytest.mark.parametrize("r", [0.0, 0.15, 0.5])
+def test_single_chunk_equals_prefix_reuse(r):
+    """S:291 / S:612: one chunk (+ suffix) -> blend equals full prefill for any r (prefix caching)."""
+    s, m, req, tok, pos, cs, _, _ = _setup(lens=(40,), n_suf=6, n_layers=3, seed=9)
+    Kc64, Vc64 = O.precompute_chunk_caches(m, tok[:req.n_ctx], cs)
+    res = O.blend_forward(m, tok, pos, cs, 6, Kc64, Vc64, O.schedule(r, req.n_ctx, 3))
+    Kf, Vf, hf = O.full_prefill(m, tok, pos)
+    np.testing.assert_allclose(res.K, Kf, atol=1e-11)
+    np.testing.assert_allclose(res.V, Vf, atol=1e-11)
+    np.testing.assert_allclose(res.h_final, hf[np.concatenate([res.sel[-1], 40 + np.arange(6)])], atol=1e-10)
+
+
+def test_structural_invariants():
+    """S_{i+1} subset of S_i, |S_i| = k_i; entries outside S_i are bitwise the realigned
+    cache; first-chunk deviation is 0 (prefix stability, R7); layer-0 K/V equal the cache."""
+    s, m, req, tok, pos, cs, Kc, Vc = _setup(seed=5, n_layers=5, lens=(24, 30, 18))
+    ks = O.schedule(0.3, req.n_ctx, 5)
+    res = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks)
+    loc = req.local_positions()
+    for i in range(1, 5):
+        assert len(res.sel[i]) == ks[i]
+        assert set(res.sel[i]) <= set(res.cand[i])
+        np.testing.assert_array_equal(res.cand[i], res.sel[i - 1] if i > 1 else np.arange(req.n_ctx))
+        untouched = np.setdiff1d(np.arange(req.n_ctx), res.sel[i])
+        np.testing.assert_array_equal(res.V[i][untouched], Vc[i][untouched])
+        np.testing.assert_array_equal(res.K[i][untouched],
+                                      O.realign(Kc[i], loc, pos, s.rope_theta)[untouched])
+    Kc64, Vc64 = O.precompute_chunk_caches(m, tok, cs)
+    r64 = O.blend_forward(m, tok, pos, cs, 0, Kc64, Vc64, ks)
+    first = r64.cand[1] < cs[1]
+    assert np.abs(r64.dev[1][first]).max() < 1e-20
+    assert r64.dev[1][~first].max() > 1e-6
+    # layer 0 fresh K/V of context rows equal the realigned cache (deviation identically 0)
+    _, k0, v0 = O.qkv(m, 0, m.embed[tok], pos)
+    np.testing.assert_allclose(O.kv_deviation(k0, v0, r64.K[0], r64.V[0]), 0, atol=1e-20)
+
+
+def test_hkvd_are_top_deviation_tokens():
+    """S_i is exactly the top-k_i of Delta_kv over C_i (brute-force re-rank) at every layer."""
+    s, m, req, tok, pos, cs, Kc, Vc = _setup(seed=6, n_layers=4)
+    ks = O.schedule(0.25, req.n_ctx, 4)
+    res = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks)
+    for i in range(1, 4):
+        order = sorted(range(len(res.cand[i])), key=lambda j: (-res.dev[i][j], res.cand[i][j]))
+        assert sorted(res.cand[i][order[:ks[i]]].tolist()) == res.sel[i].tolist()
+
+
+def test_replay_mode_uses_forced_selection():
+    s, m, req, tok, pos, cs, Kc, Vc = _setup(seed=7, n_layers=3)
+    ks = O.schedule(0.2, req.n_ctx, 3)
+    free = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks)
+    forced = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks, force_sel=free.sel)
+    np.testing.assert_array_equal(forced.K, free.K)
+    np.testing.assert_array_equal(forced.h_final, free.h_final)
+    other = [None, np.arange(ks[1]), np.arange(ks[2])]
+    alt = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks, force_sel=other)
+    assert alt.sel[1].tolist() == list(range(ks[1]))
+    with pytest.raises(ValueError):
+        O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks, force_sel=[None, np.arange(ks[1]), np.array([90, 95])])
+
+
+@pytest.mark.parametrize("r", [0.10, 0.15, 0.20])
+def test_mac_proportionality(r):
+    """S:316 / P:159-161: blend MACs / full-prefill MACs in [r - 0.05, r + 0.10] (32-layer model)."""
+    s = shape("tiny", n_layers=32, d_model=32, n_q_heads=4, n_kv_heads=2, head_dim=8, d_ff=64)
+    m = oracle_model(s, 1)
+    req = W.Request([40, 40, 40], 0, 1, r)
+    tok, pos, cs = req.tokens(s.vocab), req.global_positions(), req.chunk_starts()
+    Kc = np.zeros((32, 120, 2, 8))
+    res = O.blend_forward(m, tok, pos, cs, 0, Kc, Kc, O.schedule(r, 120, 32), count_macs=True)
+    ratio = res.macs / O.full_prefill_macs(m, tok, pos)
+    assert r - 0.05 <= ratio <= r + 0.10, ratio
