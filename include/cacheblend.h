@@ -1,0 +1,168 @@
+/* cacheblend.h — C-ABI boundary of the B200-native CacheBlend blend path (libcacheblend.so).
+ *
+ * CacheBlend (arXiv 2405.16444) fuses per-chunk precomputed KV caches of retrieved text that is
+ * not a prefix of the input, recomputing only the high-KV-deviation (HKVD) tokens per layer.
+ * Citations: P:<line> = PAPER.md line, S:<line> = SPEC.md line, R<n> = reading in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Tensor pointers are DEVICE pointers owned by the caller unless marked "host". The library
+ *    never frees caller memory. Rows are token-major and contiguous.
+ *  - Storage dtype is cb_model.dtype: CB_BF16 (hot path; fp32 accumulation, fp32 residual
+ *    stream h) or CB_FP32 (parity mode: fp32 everywhere). Norm gains are always fp32 [d_model].
+ *  - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream). Argument/shape errors are detected on the host BEFORE any launch and
+ *    return a negative cb_status; kernel faults surface as CB_E_CUDA at a later call or sync.
+ *  - cb_last_error() returns a thread-local message for the last non-OK status.
+ *  - A cb_ctx may be used by one host thread at a time; distinct contexts are independent.
+ *  - There is no CPU fallback: every step runs in the library's sm_100a kernels.
+ */
+#ifndef CACHEBLEND_H
+#define CACHEBLEND_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CB_API __attribute__((visibility("default")))
+#else
+#define CB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CB_OK = 0,
+  CB_E_INVALID_ARG = -1, /* bad configuration / value (odd head_dim, k_keep > n_cand, NULL ...) */
+  CB_E_SHAPE = -2,       /* size / length mismatch or exceeds the context's max_tokens          */
+  CB_E_UNSUPPORTED = -3, /* valid but not built (e.g. world > 1 without NCCL)                   */
+  CB_E_CUDA = -4,        /* CUDA runtime / launch error                                         */
+  CB_E_NCCL = -5,
+  CB_E_WORKSPACE = -6,   /* caller workspace too small                                          */
+  CB_E_DEVICE = -7       /* device-side precondition violated (see cb_check_device_errors)      */
+} cb_status;
+
+typedef enum { CB_BF16 = 0, CB_FP32 = 1 } cb_dtype;
+
+/* Delta_kv variant (R1): squared L2 over K and V of all kv heads (default), K only, V only
+ * (the paper notes either suffices). */
+typedef enum { CB_DEV_KV = 0, CB_DEV_K = 1, CB_DEV_V = 2 } cb_dev_mode;
+
+/* Llama/Mistral-style decoder (the paper names the models, not the block; R-model in
+ * DESIGN.md): RMSNorm pre-norm, GQA attention with RoPE (interleaved pairs (2i,2i+1), P:2531-2538,
+ * theta_i = rope_theta^(-2i/head_dim), R8), SwiGLU MLP, residual connections. */
+typedef struct {
+  int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, d_ff, vocab;
+  double rope_theta;
+  float rms_eps;
+  int32_t dtype;   /* cb_dtype */
+  int32_t max_pos; /* exclusive upper bound of |positions| and |g - l| used with this model */
+} cb_model;
+
+/* One layer's weights (device). Layouts are [out_features][in_features] (K-contiguous):
+ *   attn_norm, mlp_norm : fp32 [d_model]
+ *   w_qkv     : [(n_q + 2 n_kv) * head_dim][d_model]  rows = q heads, then k heads, then v heads
+ *   w_o       : [d_model][n_q * head_dim]
+ *   w_gate_up : [2 d_ff][d_model]  rows [0, d_ff) = gate, [d_ff, 2 d_ff) = up
+ *   w_down    : [d_model][d_ff]                                                              */
+typedef struct {
+  const void *attn_norm, *w_qkv, *w_o, *mlp_norm, *w_gate_up, *w_down;
+} cb_layer_w;
+
+typedef struct cb_ctx cb_ctx; /* opaque: RoPE tables, tensor-map cache, workspace, scratch */
+
+/* ---- context ------------------------------------------------------------------------------ */
+/* Bytes of device workspace a context needs for max_tokens = N + n_suffix rows. */
+CB_API cb_status cb_workspace_size(const cb_model* model, int32_t max_tokens, size_t* bytes);
+
+/* Create a context on the current CUDA device. workspace: device buffer of at least
+ * cb_workspace_size() bytes, owned by the caller, or NULL to let the library cudaMalloc (and
+ * free in cb_destroy). Errors: odd head_dim, n_q % n_kv != 0, non-positive sizes -> INVALID_ARG. */
+CB_API cb_status cb_create(const cb_model* model, int32_t max_tokens, void* workspace, size_t workspace_bytes,
+                    cb_ctx** out);
+CB_API cb_status cb_destroy(cb_ctx* ctx);
+CB_API const char* cb_last_error(void);
+
+/* Synchronises the context's device-side error word (e.g. a force_sel token that is not a
+ * candidate) and clears it: CB_OK or CB_E_DEVICE. Blocking. */
+CB_API cb_status cb_check_device_errors(cb_ctx* ctx);
+
+/* Gradual-filtering schedule (R4/R5), host only: k_sched_out[0] = n_ctx (layer 0 is
+ * the full layer, R2); for i >= 1, k_i = min(N, ceil(r_i N - 1e-9)) non-increasing, with
+ * r_i = r + d (1 - 2(i-1)/(L-2)), d = 0.2 min(r, 1-r) (L = 2: r_1 = r).
+ * k_sched_out: host int32[n_layers]. ratio outside [0,1] -> INVALID_ARG. */
+CB_API cb_status cb_schedule(double ratio, int32_t n_ctx, int32_t n_layers, int32_t* k_sched_out);
+
+/* ---- (a) positional recovery --------------------------------------------------------------- */
+/* Footnote P:208-211, Appendix: K_out[s][t] = R(dst_pos[t] - src_pos[t]) K_src[s][t]
+ * for every slice s (a layer) and token t, per kv head; V is untouched. src_pos = chunk-local
+ * position l (all zeros = position-free storage, R11), dst_pos = global position g.
+ * k_src/k_out: [n_slices][n_tok][n_kv][head_dim], slices slice_stride elements apart
+ * (>= n_tok * n_kv * head_dim); in place (k_out == k_src) allowed. Positions: device int32[n_tok],
+ * |dst - src| < max_pos (violations are clamped and flagged in the device error word). */
+CB_API cb_status cb_rope_realign(cb_ctx* ctx, void* k_out, const void* k_src, const int32_t* src_pos,
+                          const int32_t* dst_pos, int32_t n_slices, int32_t n_tok, int64_t slice_stride,
+                          void* stream);
+
+/* ---- (b) KV deviation + HKVD top-k ----------------------------------------------------------- */
+/* Delta_kv (R1) of each candidate j against the loaded entry of its token, and
+ * the k_keep largest (Insight 1), ties -> lower token index (R6):
+ *   dev[j] = sum_heads ||k_new[j] - k_ref[cand_tok[j]]||^2 + ||v_new[j] - v_ref[cand_tok[j]]||^2
+ * k_new, v_new : [n_cand][n_kv][head_dim]   fresh rows in candidate order (K RoPE'd at g)
+ * k_ref, v_ref : [>= max cand_tok + 1][n_kv][head_dim]   the layer's blended cache
+ * cand_tok     : int32[n_cand], strictly ascending token indices
+ * sel_tok      : out int32[k_keep], ascending;  sel_slot: out int32[k_keep] (index into cand_tok)
+ * dev_out      : out fp32[n_cand] or NULL.   0 <= k_keep <= n_cand <= max_tokens.
+ * The sum runs per kv head in a fixed order, so results are bitwise reproducible. */
+CB_API cb_status cb_kv_deviation_topk(cb_ctx* ctx, const void* k_new, const void* v_new, const void* k_ref,
+                               const void* v_ref, const int32_t* cand_tok, int32_t n_cand, int32_t k_keep,
+                               int32_t dev_mode, int32_t* sel_tok, int32_t* sel_slot, float* dev_out,
+                               void* stream);
+
+/* ---- (c) one layer of selective recompute ------------------------------------------------------ */
+/* prefill_layer on layer `layer` (§3.2 workflow P:150-161):
+ *  layer >= 1 (check_flag <=> k_keep < n_cand): x = RMSNorm(h); q,k,v = RoPE(x Wq), RoPE(x Wk), x Wv
+ *    for the n_cand candidate rows and the n_suffix suffix rows; Delta_kv over the candidates;
+ *    S = top-k_keep (or force_sel, replay mode R14); write fresh K,V of S and of the suffix into
+ *    k_blend/v_blend (untouched rows keep their bytes, R3); attention of the S + suffix queries over
+ *    all N + n_suffix keys masked by original position; h += attn W_o; h += MLP(RMSNorm(h)).
+ *  layer == 0 (the full layer, R2): n_cand must equal N, cand_tok = 0..N-1, k_keep = N.
+ *    Context rows keep the cached K,V (layer-0 KV depend only on the token); suffix rows
+ *    write theirs; every row is a query.
+ * h        : fp32 [n_cand + n_suffix][d_model] in (rows of cand_tok, then suffix) and out (rows
+ *            [0, k_keep + n_suffix) = S ascending, then suffix).
+ * k_blend, v_blend : this layer's [N + n_suffix][n_kv][head_dim], updated in place.
+ * pos      : int32[N + n_suffix] strictly increasing global positions (context, then suffix).
+ * force_sel: int32[k_keep] ascending subset of cand_tok, or NULL.
+ * sel_tok  : out int32[k_keep];  dev_out: out fp32[n_cand] or NULL.                               */
+CB_API cb_status cb_blend_layer(cb_ctx* ctx, int32_t layer, const cb_layer_w* w, float* h, const int32_t* cand_tok,
+                         int32_t n_cand, int32_t k_keep, int32_t n_suffix, void* k_blend, void* v_blend,
+                         const int32_t* pos, int32_t N, const int32_t* force_sel, int32_t* sel_tok,
+                         float* dev_out, void* stream);
+
+/* ---- the whole blend ------------------------------------------------------------------------- */
+/* SURVEY §8(c) steps 1-5 / P:2742-2748. Chunk c occupies context rows chunk_start[c]..chunk_start[c+1].
+ * w        : host array [n_layers] of device weight pointers;  embed: [vocab][d_model]
+ * tok, pos : device int32[N + n_suffix]
+ * chunk_start : HOST int32[n_chunks + 1], chunk_start[0] = 0, chunk_start[n_chunks] = N
+ * k_in, v_in  : chunk caches [n_layers][N][n_kv][head_dim], K RoPE'd at chunk-local positions
+ * k_blend, v_blend : out KV^new [n_layers][N + n_suffix][n_kv][head_dim]; may alias k_in/v_in
+ *                    (in place) when n_suffix == 0
+ * k_sched  : HOST int32[n_layers] (k_sched[0] ignored; k_sched[i] <= k_sched[i-1] <= N)
+ * force_sel: device int32[n_layers][N] (row i: S_i ascending in its first k_sched[i] entries) or NULL
+ * sel_out  : device int32[n_layers][N] or NULL: row i = S_i ascending, padded with -1 (row 0 = 0..N-1)
+ * dev_out  : device fp32[n_layers][N] or NULL: row i, entry j < |C_i| = Delta_kv of the j-th
+ *            candidate (C_1 = 0..N-1, C_i = S_{i-1}); other entries untouched
+ * h_out    : device fp32[k_sched[L-1] + n_suffix][d_model]: final hidden rows of S_{L-1} then suffix
+ *            (for n_layers == 1: all N + n_suffix rows).                                             */
+CB_API cb_status cb_blend_forward(cb_ctx* ctx, const cb_layer_w* w, const void* embed, const int32_t* tok,
+                           const int32_t* pos, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                           int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend, void* v_blend,
+                           const int32_t* k_sched, const int32_t* force_sel, int32_t* sel_out, float* dev_out,
+                           float* h_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CACHEBLEND_H */

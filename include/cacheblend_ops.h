@@ -1,0 +1,52 @@
+/* cacheblend_ops.h — building-block entry points of libcacheblend.so, exported for per-kernel
+ * parity tests and tooling. Same conventions as cacheblend.h (device pointers, caller-owned,
+ * stream-ordered, host-side argument checks, negative cb_status on error).
+ * These are the kernels cb_blend_layer / cb_blend_forward launch; the product path calls them
+ * through the blend entry points. */
+#ifndef CACHEBLEND_OPS_H
+#define CACHEBLEND_OPS_H
+
+#include "cacheblend.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- synthetic input generation (NOT method arithmetic) -----------------------------------
+ * Device implementation of the counter-RNG spec in synth/counter_rng.py (the spec, not the code,
+ * is shared with the oracle; tests/test_gen_parity.py pins the two bit-for-bit):
+ *   raw(i) = mix64(mix64(mix64(seed) ^ stream_id) + i), u = fp32(raw >> 40) * 2^-23 - 1,
+ *   out[i - start] = fp32(offset + fp32(u * scale)) [-> bf16 RNE when dtype == CB_BF16]
+ * for i in [start, start + count).  cb_gen_ints: out[i - start] = raw(i) % modulus. */
+CB_API cb_status cb_gen_fill(void* out, int32_t dtype, int64_t count, uint64_t seed, uint64_t stream_id,
+                      int64_t start, float scale, float offset, void* stream);
+CB_API cb_status cb_gen_ints(int32_t* out, int64_t count, uint64_t seed, uint64_t stream_id, int64_t start,
+                      int64_t modulus, void* stream);
+
+/* h[t] = embed[tok[t]] widened to fp32.  h: fp32 [n][d_model]. */
+CB_API cb_status cb_op_embed(cb_ctx* ctx, const void* embed, const int32_t* tok, int32_t n, float* h, void* stream);
+
+/* x[r] = h[r] / sqrt(mean(h[r]^2) + eps) * gain   (x in the model dtype). */
+CB_API cb_status cb_op_rmsnorm(cb_ctx* ctx, const float* h, const float* gain, int32_t n_rows, void* x, void* stream);
+
+/* C[M][N] = A[M][K] . B[N][K]^T with fp32 accumulation; C is fp32 when out_f32 != 0, else the model
+ * dtype. impl: 0 = auto (tcgen05 for bf16), 1 = SIMT, 2 = tcgen05 (bf16 only; K % 8 == 0). */
+CB_API cb_status cb_op_gemm(cb_ctx* ctx, const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                     int32_t out_f32, int32_t impl, void* stream);
+
+/* Sparse-query causal attention: for query row r (q row q_row[r] of q [*][n_q][hd], token
+ * index q_tok[r]) and q head h: out[r][h] = softmax_j(q.k_j / sqrt(hd)) v_j over keys j <= q_tok[r]
+ * of k, v [n_keys][n_kv][hd], kv head h / (n_q / n_kv).  Token positions are strictly increasing, so
+ * "key position <= query position" is "j <= q_tok[r]".  out: [n_rows][n_q * hd] (model dtype).
+ * impl: 0 = auto, 1 = SIMT, 2 = tensor-core (bf16, head_dim 128). */
+CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_row, const int32_t* q_tok,
+                          int32_t n_rows, const void* k, const void* v, int32_t n_keys, void* out, int32_t impl,
+                          void* stream);
+
+/* Number of kernel launches the context issued since creation (for bench's gpu_launches). */
+CB_API int64_t cb_launch_count(cb_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

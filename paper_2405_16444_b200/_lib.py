@@ -1,0 +1,81 @@
+"""ctypes declarations for libcacheblend.so (include/cacheblend.h, include/cacheblend_ops.h).
+
+Argument marshalling only. There is no fallback: if the shared library is missing or fails to
+load, every call raises."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcacheblend.so")
+
+c_i32, c_i64, c_u64, c_f32, c_f64, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
+                                           ctypes.c_double, ctypes.c_void_p)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+
+
+class CbModel(ctypes.Structure):
+    _fields_ = [("n_layers", c_i32), ("d_model", c_i32), ("n_q_heads", c_i32), ("n_kv_heads", c_i32),
+                ("head_dim", c_i32), ("d_ff", c_i32), ("vocab", c_i32), ("rope_theta", c_f64),
+                ("rms_eps", c_f32), ("dtype", c_i32), ("max_pos", c_i32)]
+
+
+class CbLayerW(ctypes.Structure):
+    _fields_ = [("attn_norm", c_vp), ("w_qkv", c_vp), ("w_o", c_vp), ("mlp_norm", c_vp),
+                ("w_gate_up", c_vp), ("w_down", c_vp)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "cb_workspace_size": (c_i32, [ctypes.POINTER(CbModel), c_i32, ctypes.POINTER(ctypes.c_size_t)]),
+    "cb_create": (c_i32, [ctypes.POINTER(CbModel), c_i32, c_vp, ctypes.c_size_t, ctypes.POINTER(c_vp)]),
+    "cb_destroy": (c_i32, [c_vp]),
+    "cb_last_error": (ctypes.c_char_p, []),
+    "cb_check_device_errors": (c_i32, [c_vp]),
+    "cb_schedule": (c_i32, [c_f64, c_i32, c_i32, c_i32p]),
+    "cb_rope_realign": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp]),
+    "cb_kv_deviation_topk": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                     c_vp]),
+    "cb_blend_layer": (c_i32, [c_vp, c_i32, ctypes.POINTER(CbLayerW), c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp,
+                               c_vp, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "cb_blend_forward": (c_i32, [c_vp, ctypes.POINTER(CbLayerW), c_vp, c_vp, c_vp, c_i32, c_i32, c_i32p, c_i32,
+                                 c_vp, c_vp, c_vp, c_vp, c_i32p, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "cb_gen_fill": (c_i32, [c_vp, c_i32, c_i64, c_u64, c_u64, c_i64, c_f32, c_f32, c_vp]),
+    "cb_gen_ints": (c_i32, [c_vp, c_i64, c_u64, c_u64, c_i64, c_i64, c_vp]),
+    "cb_op_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "cb_op_rmsnorm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_vp, c_vp]),
+    "cb_op_gemm": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
+    "cb_op_attention": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
+    "cb_launch_count": (c_i64, [c_vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcacheblend.so (once). Raises if it was not built -- there is no CPU path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2405_16444_b200.build` "
+                               "(the CacheBlend path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_LOCAL)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+class CacheBlendError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cacheblend status {status}: {msg}")
+        self.status = status
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise CacheBlendError(status, (lib().cb_last_error() or b"").decode(errors="replace"))

@@ -1,0 +1,519 @@
+// cacheblend.cu — C-ABI of libcacheblend: context, argument checks, and the layer orchestration
+// of the blend. Every step is a device kernel on the caller's stream;
+// there is no host synchronisation inside cb_blend_layer / cb_blend_forward (all k_i are host
+// integers, so every shape is static and the whole forward is CUDA-graph capturable).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ctx.h"
+
+// ---- launchers implemented in the other translation units ----------------------------------------
+cb_status launch_gemm_simt(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
+                           const EpiParams& e, cudaStream_t s);
+cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
+                         const EpiParams& e, cudaStream_t s);
+bool gemm_tc_ok(const cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e);
+cb_status launch_attention_simt(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
+                                const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
+cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
+                              const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
+bool attention_tc_ok(const cb_ctx* c);
+cb_status topk_init_attrs();
+cb_status gemm_tc_init(cb_ctx* c);
+void gemm_tc_destroy(cb_ctx* c);
+cb_status attention_tc_init();
+
+// ---- error reporting ------------------------------------------------------------------------------
+static thread_local char g_err[1024] = "";
+
+void cb_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char* cb_last_error(void) { return g_err; }
+
+// ---- dispatch -------------------------------------------------------------------------------------
+cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
+                      int impl, cudaStream_t s) {
+  if (M == 0 || e.N == 0) return CB_OK;
+  if (impl == 2 || (impl == 0 && c->m.dtype == CB_BF16)) {
+    if (gemm_tc_ok(c, A, lda, B, ldb, M, K, e)) return launch_gemm_tc(c, A, lda, B, ldb, M, K, e, s);
+    CB_REQUIRE(impl != 2, CB_E_UNSUPPORTED, "tcgen05 GEMM does not take this shape (M=%d N=%d K=%d)", M, e.N, K);
+  }
+  return launch_gemm_simt(c, A, lda, B, ldb, M, K, e, s);
+}
+
+cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
+                           const void* v, int n_keys, void* out, int impl, cudaStream_t s) {
+  if (n_rows == 0) return CB_OK;
+  if (impl == 2 || (impl == 0 && attention_tc_ok(c))) {
+    CB_REQUIRE(attention_tc_ok(c), CB_E_UNSUPPORTED, "tensor-core attention needs bf16 and head_dim 128");
+    return launch_attention_tc(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
+  }
+  return launch_attention_simt(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
+}
+
+// ---- context --------------------------------------------------------------------------------------
+namespace {
+constexpr size_t kAlign = 256;
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <typename P> P* take(size_t bytes) {
+    off = (off + kAlign - 1) / kAlign * kAlign;
+    P* p = base ? reinterpret_cast<P*>(base + off) : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+cb_status check_model(const cb_model* m) {
+  CB_REQUIRE(m != nullptr, CB_E_INVALID_ARG, "model is NULL");
+  CB_REQUIRE(m->n_layers >= 1 && m->d_model >= 1 && m->n_q_heads >= 1 && m->n_kv_heads >= 1 && m->head_dim >= 2 &&
+                 m->d_ff >= 1 && m->vocab >= 1,
+             CB_E_INVALID_ARG, "model sizes must be positive");
+  CB_REQUIRE(m->head_dim % 2 == 0, CB_E_INVALID_ARG, "head_dim must be even (paired RoPE rotation), got %d",
+             m->head_dim);
+  CB_REQUIRE(m->n_q_heads % m->n_kv_heads == 0, CB_E_INVALID_ARG, "n_q_heads %% n_kv_heads != 0");
+  CB_REQUIRE(m->dtype == CB_BF16 || m->dtype == CB_FP32, CB_E_INVALID_ARG, "bad dtype %d", m->dtype);
+  const int V = 16 / (int)dtype_bytes(m->dtype);
+  CB_REQUIRE(m->head_dim % V == 0 && m->d_model % 8 == 0 && m->d_ff % 8 == 0, CB_E_UNSUPPORTED,
+             "head_dim must be a multiple of %d and d_model, d_ff multiples of 8", V);
+  CB_REQUIRE(m->head_dim <= 256, CB_E_UNSUPPORTED, "head_dim > 256");
+  CB_REQUIRE(m->max_pos >= 1, CB_E_INVALID_ARG, "max_pos must be >= 1");
+  CB_REQUIRE(m->rope_theta > 0.0 && m->rms_eps >= 0.f, CB_E_INVALID_ARG, "rope_theta/rms_eps out of range");
+  return CB_OK;
+}
+
+size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
+  Carve cv{base};
+  const size_t B = dtype_bytes(m->dtype);
+  const size_t d = m->d_model, qd = (size_t)m->n_q_heads * m->head_dim, kvd = (size_t)m->n_kv_heads * m->head_dim;
+  cb_ctx tmp;
+  cb_ctx* o = c ? c : &tmp;
+  o->h[0] = cv.take<float>((size_t)T * d * 4);
+  o->h[1] = cv.take<float>((size_t)T * d * 4);
+  o->x = cv.take<void>((size_t)T * d * B);
+  o->q = cv.take<void>((size_t)T * qd * B);
+  o->kf = cv.take<void>((size_t)T * kvd * B);
+  o->vf = cv.take<void>((size_t)T * kvd * B);
+  o->attn = cv.take<void>((size_t)T * qd * B);
+  o->act = cv.take<void>((size_t)T * m->d_ff * B);
+  o->dev = cv.take<float>((size_t)T * 4);
+  o->row_tok[0] = cv.take<int>((size_t)T * 4);
+  o->row_tok[1] = cv.take<int>((size_t)T * 4);
+  o->qrow = cv.take<int>((size_t)T * 4);
+  o->iota = cv.take<int>((size_t)T * 4);
+  o->src_pos = cv.take<int>((size_t)T * 4);
+  return cv.off + kAlign;
+}
+
+__global__ void iota_kernel(int* p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+// row_tok = [cand_tok..., N, N+1, ..., N+n_suf-1]
+__global__ void make_rows_kernel(const int* __restrict__ cand, int n_cand, int n_suf, int N, int* __restrict__ rows) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cand + n_suf; i += gridDim.x * blockDim.x)
+    rows[i] = i < n_cand ? cand[i] : N + (i - n_cand);
+}
+}  // namespace
+
+extern "C" cb_status cb_workspace_size(const cb_model* model, int32_t max_tokens, size_t* bytes) {
+  CB_TRY(check_model(model));
+  CB_REQUIRE(bytes != nullptr && max_tokens >= 1, CB_E_INVALID_ARG, "bad arguments");
+  *bytes = carve(nullptr, model, max_tokens, nullptr);
+  return CB_OK;
+}
+
+extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* workspace, size_t workspace_bytes,
+                               cb_ctx** out) {
+  CB_TRY(check_model(model));
+  CB_REQUIRE(out != nullptr && max_tokens >= 1, CB_E_INVALID_ARG, "bad arguments to cb_create");
+  *out = nullptr;
+  const size_t need = carve(nullptr, model, max_tokens, nullptr);
+  CB_REQUIRE(workspace == nullptr || workspace_bytes >= need, CB_E_WORKSPACE,
+             "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  cb_ctx* c = new cb_ctx();
+  std::memset(c, 0, sizeof(*c));
+  c->m = *model;
+  c->max_tokens = max_tokens;
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  int cc_major = 0, cc_minor = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, c->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    CB_CUDA(e);
+  }
+  if (cc_major != 10 || cc_minor != 0) {
+    delete c;
+    cb_set_error("libcacheblend is built for sm_100a (B200); device is sm_%d%d", cc_major, cc_minor);
+    return CB_E_UNSUPPORTED;
+  }
+  c->ws_bytes = need;
+  if (workspace) {
+    c->ws = workspace;
+  } else {
+    e = cudaMalloc(&c->ws, need);
+    if (e != cudaSuccess) { delete c; CB_CUDA(e); }
+    c->ws_owned = true;
+  }
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(c->ws) + kAlign - 1) / kAlign * kAlign);
+  carve(c, model, max_tokens, base);
+
+  // RoPE table in fp64 -> fp32: (cos, sin)(p theta_i), theta_i = base^(-2i/hd) (R8)
+  const int half = model->head_dim / 2;
+  std::vector<float2> tab((size_t)model->max_pos * half);
+  for (int p = 0; p < model->max_pos; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double th = std::pow(model->rope_theta, -2.0 * i / model->head_dim);
+      const double a = (double)p * th;
+      tab[(size_t)p * half + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  auto fail = [&](cudaError_t err) {
+    cb_set_error("cb_create: %s", cudaGetErrorString(err));
+    if (c->rope_tab) cudaFree(c->rope_tab);
+    if (c->err_word) cudaFree(c->err_word);
+    if (c->ws_owned) cudaFree(c->ws);
+    delete c;
+    return CB_E_CUDA;
+  };
+  if ((e = cudaMalloc(&c->rope_tab, tab.size() * sizeof(float2))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpy(c->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return fail(e);
+  if ((e = cudaMalloc(&c->err_word, sizeof(int))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(c->err_word, 0, sizeof(int))) != cudaSuccess) return fail(e);
+  iota_kernel<<<std::min(1024, (max_tokens + 255) / 256), 256>>>(c->iota, max_tokens);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
+  if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
+  cb_status st = topk_init_attrs();
+  if (st == CB_OK) st = gemm_tc_init(c);
+  if (st == CB_OK) st = attention_tc_init();
+  if (st != CB_OK) {
+    cudaFree(c->rope_tab);
+    cudaFree(c->err_word);
+    if (c->ws_owned) cudaFree(c->ws);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_destroy(cb_ctx* c) {
+  if (!c) return CB_OK;
+  gemm_tc_destroy(c);
+  cudaFree(c->rope_tab);
+  cudaFree(c->err_word);
+  if (c->ws_owned) cudaFree(c->ws);
+  delete c;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_check_device_errors(cb_ctx* c) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  int h = 0;
+  CB_CUDA(cudaMemcpy(&h, c->err_word, sizeof(int), cudaMemcpyDeviceToHost));
+  CB_CUDA(cudaMemset(c->err_word, 0, sizeof(int)));
+  if (h & CB_DEVERR_FORCE_SEL) { cb_set_error("device: a force_sel token is not a candidate of its layer"); return CB_E_DEVICE; }
+  if (h & CB_DEVERR_POS_RANGE) { cb_set_error("device: |dst_pos - src_pos| >= max_pos in realign"); return CB_E_DEVICE; }
+  return CB_OK;
+}
+
+extern "C" int64_t cb_launch_count(cb_ctx* c) { return c ? c->launches : 0; }
+
+// ---- schedule (host) ----------------------------------------------------------------------------
+extern "C" cb_status cb_schedule(double ratio, int32_t n_ctx, int32_t n_layers, int32_t* k) {
+  CB_REQUIRE(k != nullptr && n_layers >= 1 && n_ctx >= 0, CB_E_INVALID_ARG, "bad arguments to cb_schedule");
+  CB_REQUIRE(ratio >= 0.0 && ratio <= 1.0, CB_E_INVALID_ARG, "ratio %g outside [0, 1]", ratio);
+  k[0] = n_ctx;
+  const double delta = 0.2 * std::min(ratio, 1.0 - ratio);
+  for (int i = 1; i < n_layers; ++i) {
+    double ri = ratio;
+    if (n_layers != 2) {
+      volatile double t = 2.0 * (double)(i - 1) / (double)(n_layers - 2);  // keep the oracle's op order
+      volatile double u = delta * (1.0 - t);
+      ri = ratio + u;
+    }
+    volatile double x = ri * (double)n_ctx;
+    long long ki = (long long)std::ceil(x - 1e-9);
+    ki = std::min<long long>(ki, n_ctx);
+    ki = std::min<long long>(ki, k[i - 1]);
+    k[i] = (int32_t)std::max<long long>(0, ki);
+  }
+  return CB_OK;
+}
+
+// ---- building-block entry points (cacheblend_ops.h) ---------------------------------------------
+extern "C" cb_status cb_op_embed(cb_ctx* c, const void* embed, const int32_t* tok, int32_t n, float* h, void* st) {
+  CB_REQUIRE(c && embed && tok && h && n >= 0, CB_E_INVALID_ARG, "cb_op_embed: bad arguments");
+  return launch_embed(c, embed, tok, n, h, (cudaStream_t)st);
+}
+
+extern "C" cb_status cb_op_rmsnorm(cb_ctx* c, const float* h, const float* gain, int32_t n_rows, void* x, void* st) {
+  CB_REQUIRE(c && h && gain && x && n_rows >= 0, CB_E_INVALID_ARG, "cb_op_rmsnorm: bad arguments");
+  return launch_rmsnorm(c, h, gain, n_rows, x, (cudaStream_t)st);
+}
+
+extern "C" cb_status cb_op_gemm(cb_ctx* c, const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                                int32_t out_f32, int32_t impl, void* st) {
+  CB_REQUIRE(c && A && B && C && M >= 0 && N >= 0 && K >= 1, CB_E_INVALID_ARG, "cb_op_gemm: bad arguments");
+  CB_REQUIRE(impl >= 0 && impl <= 2, CB_E_INVALID_ARG, "cb_op_gemm: impl must be 0, 1 or 2");
+  CB_REQUIRE(N % 2 == 0 && K % 8 == 0, CB_E_SHAPE, "cb_op_gemm: N must be even and K a multiple of 8");
+  EpiParams e{};
+  e.kind = out_f32 ? EPI_STORE_F32 : EPI_STORE;
+  e.M = M; e.N = N; e.ldo = N;
+  e.out = C; e.outf = (float*)C;
+  return launch_gemm(c, A, K, B, K, M, K, e, impl, (cudaStream_t)st);
+}
+
+extern "C" cb_status cb_op_attention(cb_ctx* c, const void* q, const int32_t* q_row, const int32_t* q_tok,
+                                     int32_t n_rows, const void* k, const void* v, int32_t n_keys, void* out,
+                                     int32_t impl, void* st) {
+  CB_REQUIRE(c && q && q_row && q_tok && k && v && out && n_rows >= 0 && n_keys >= 1, CB_E_INVALID_ARG,
+             "cb_op_attention: bad arguments");
+  CB_REQUIRE(impl >= 0 && impl <= 2, CB_E_INVALID_ARG, "cb_op_attention: impl must be 0, 1 or 2");
+  return launch_attention(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, impl, (cudaStream_t)st);
+}
+
+// ---- (a) realign ----------------------------------------------------------------------------------
+extern "C" cb_status cb_rope_realign(cb_ctx* c, void* k_out, const void* k_src, const int32_t* src_pos,
+                                     const int32_t* dst_pos, int32_t n_slices, int32_t n_tok, int64_t slice_stride,
+                                     void* st) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  CB_REQUIRE(n_slices >= 0 && n_tok >= 0, CB_E_INVALID_ARG, "negative sizes");
+  if (n_slices == 0 || n_tok == 0) return CB_OK;
+  CB_REQUIRE(k_out && k_src && src_pos && dst_pos, CB_E_INVALID_ARG, "cb_rope_realign: NULL pointer");
+  const long long kvd = (long long)c->m.n_kv_heads * c->m.head_dim;
+  CB_REQUIRE(slice_stride >= (long long)n_tok * kvd || n_slices == 1, CB_E_SHAPE,
+             "slice_stride %lld < n_tok * n_kv * head_dim", (long long)slice_stride);
+  return launch_realign(c, k_out, k_src, nullptr, nullptr, src_pos, dst_pos, n_slices, n_tok, slice_stride,
+                        slice_stride, (cudaStream_t)st);
+}
+
+// ---- (b) deviation + top-k -----------------------------------------------------------------------
+extern "C" cb_status cb_kv_deviation_topk(cb_ctx* c, const void* k_new, const void* v_new, const void* k_ref,
+                                          const void* v_ref, const int32_t* cand_tok, int32_t n_cand, int32_t k_keep,
+                                          int32_t dev_mode, int32_t* sel_tok, int32_t* sel_slot, float* dev_out,
+                                          void* st) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  CB_REQUIRE(n_cand >= 0 && k_keep >= 0 && k_keep <= n_cand, CB_E_INVALID_ARG,
+             "need 0 <= k_keep <= n_cand (k_keep=%d n_cand=%d)", k_keep, n_cand);
+  CB_REQUIRE(n_cand <= c->max_tokens, CB_E_SHAPE, "n_cand %d > max_tokens %d", n_cand, c->max_tokens);
+  CB_REQUIRE(dev_mode >= CB_DEV_KV && dev_mode <= CB_DEV_V, CB_E_INVALID_ARG, "bad dev_mode %d", dev_mode);
+  if (n_cand == 0) return CB_OK;
+  CB_REQUIRE(k_new && v_new && k_ref && v_ref && cand_tok, CB_E_INVALID_ARG, "NULL input pointer");
+  CB_REQUIRE(k_keep == 0 || (sel_tok && sel_slot), CB_E_INVALID_ARG, "sel_tok / sel_slot are NULL");
+  cudaStream_t s = (cudaStream_t)st;
+  float* dev = dev_out ? dev_out : c->dev;
+  CB_TRY(launch_deviation(c, k_new, v_new, k_ref, v_ref, cand_tok, n_cand, dev_mode, dev, s));
+  CB_TRY(launch_topk(c, dev, cand_tok, n_cand, k_keep, 0, 0, nullptr, sel_slot ? sel_slot : c->qrow,
+                     sel_tok ? sel_tok : c->row_tok[1], nullptr, s));
+  return CB_OK;
+}
+
+// ---- (c) one layer ---------------------------------------------------------------------------------
+namespace {
+struct LayerBufs {
+  const float* h_in;   // [rows][d]
+  float* h_out;        // [k + n_suf][d]
+  const int* row_tok;  // [n_cand + n_suf]
+  int* qtok;           // [k + n_suf] out
+};
+
+// Layer 0, the full layer (R2): every row is a query; context rows keep the realigned cache
+// (P:1750), suffix rows write fresh K,V.
+cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, int n_suf, void* kb, void* vb,
+                     const int* pos, cudaStream_t s) {
+  const cb_model& m = c->m;
+  const int T = N + n_suf, d = m.d_model, qd = m.n_q_heads * m.head_dim, kvd = m.n_kv_heads * m.head_dim;
+  const size_t B = dtype_bytes(m.dtype);
+  CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, T, c->x, s));
+  EpiParams e{};
+  e.kind = EPI_QKV; e.M = T; e.N = qd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
+  e.q_out = c->q; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, T, d, e, 0, s));
+  if (n_suf > 0) {
+    EpiParams ek = e;
+    ek.M = n_suf; ek.N = 2 * kvd; ek.col0 = qd;
+    ek.k_out = (char*)kb + (size_t)N * kvd * B;
+    ek.v_out = (char*)vb + (size_t)N * kvd * B;
+    ek.row_tok = b.row_tok + N;
+    CB_TRY(launch_gemm(c, (const char*)c->x + (size_t)N * d * B, d, (const char*)w.w_qkv + (size_t)qd * d * B, d,
+                       n_suf, d, ek, 0, s));
+  }
+  CB_TRY(launch_attention(c, c->q, c->iota, b.row_tok, T, kb, vb, T, c->attn, 0, s));
+  EpiParams eo{};
+  eo.kind = EPI_RESID; eo.M = T; eo.N = d; eo.ldo = d; eo.h_in = b.h_in; eo.h_out = b.h_out; eo.res_row = nullptr;
+  CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, T, qd, eo, 0, s));
+  CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, T, c->x, s));
+  EpiParams eg{};
+  eg.kind = EPI_SWIGLU; eg.M = T; eg.N = m.d_ff; eg.ff = m.d_ff; eg.act = c->act;
+  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, T, d, eg, 0, s));
+  EpiParams ed{};
+  ed.kind = EPI_RESID; ed.M = T; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
+  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, T, m.d_ff, ed, 0, s));
+  return CB_OK;
+}
+
+// Layers i >= 1: selective recompute with HKVD selection.
+cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_cand, int k, int n_suf, int N,
+                      void* kb, void* vb, const int* pos, const int* force_sel, int* sel_tok, float* dev_out,
+                      int dev_mode, cudaStream_t s) {
+  const cb_model& m = c->m;
+  const int R = n_cand + n_suf, Q = k + n_suf;
+  const int d = m.d_model, qd = m.n_q_heads * m.head_dim, kvd = m.n_kv_heads * m.head_dim;
+  if (R == 0) return CB_OK;
+  // 1. mask the input to the candidate rows and transform them into Q, K, V
+  CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, R, c->x, s));
+  EpiParams e{};
+  e.kind = EPI_QKV; e.M = R; e.N = qd + 2 * kvd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
+  e.q_out = c->q; e.k_out = c->kf; e.v_out = c->vf; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, R, d, e, 0, s));
+  // 2-3. Delta_kv against the loaded entries, HKVD = top-k
+  float* dev = dev_out ? dev_out : c->dev;
+  CB_TRY(launch_deviation(c, c->kf, c->vf, kb, vb, b.row_tok, n_cand, dev_mode, dev, s));
+  CB_TRY(launch_topk(c, dev, b.row_tok, n_cand, k, n_suf, N, force_sel, c->qrow, b.qtok, sel_tok, s));
+  if (Q == 0) return CB_OK;
+  // 4. only the KV of the HKVD tokens (and the suffix) is updated (R3)
+  CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));
+  // 5. attention of the selected queries over all tokens, then W_o + residual, MLP + residual
+  CB_TRY(launch_attention(c, c->q, c->qrow, b.qtok, Q, kb, vb, N + n_suf, c->attn, 0, s));
+  EpiParams eo{};
+  eo.kind = EPI_RESID; eo.M = Q; eo.N = d; eo.ldo = d; eo.h_in = b.h_in; eo.h_out = b.h_out; eo.res_row = c->qrow;
+  CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, Q, qd, eo, 0, s));
+  CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, Q, c->x, s));
+  EpiParams eg{};
+  eg.kind = EPI_SWIGLU; eg.M = Q; eg.N = m.d_ff; eg.ff = m.d_ff; eg.act = c->act;
+  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
+  EpiParams ed{};
+  ed.kind = EPI_RESID; ed.M = Q; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
+  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
+  return CB_OK;
+}
+
+cb_status check_weights(const cb_layer_w* w) {
+  CB_REQUIRE(w && w->attn_norm && w->w_qkv && w->w_o && w->mlp_norm && w->w_gate_up && w->w_down, CB_E_INVALID_ARG,
+             "NULL weight pointer");
+  return CB_OK;
+}
+}  // namespace
+
+extern "C" cb_status cb_blend_layer(cb_ctx* c, int32_t layer, const cb_layer_w* w, float* h, const int32_t* cand_tok,
+                                    int32_t n_cand, int32_t k_keep, int32_t n_suffix, void* k_blend, void* v_blend,
+                                    const int32_t* pos, int32_t N, const int32_t* force_sel, int32_t* sel_tok,
+                                    float* dev_out, void* st) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  CB_TRY(check_weights(w));
+  CB_REQUIRE(layer >= 0 && layer < c->m.n_layers, CB_E_INVALID_ARG, "layer %d out of range", layer);
+  CB_REQUIRE(n_cand >= 0 && n_suffix >= 0 && N >= 0 && k_keep >= 0 && k_keep <= n_cand && n_cand <= N,
+             CB_E_INVALID_ARG, "need 0 <= k_keep <= n_cand <= N, n_suffix >= 0");
+  CB_REQUIRE(N + n_suffix <= c->max_tokens, CB_E_SHAPE, "N + n_suffix = %d > max_tokens %d", N + n_suffix,
+             c->max_tokens);
+  CB_REQUIRE(N + n_suffix >= 1, CB_E_INVALID_ARG, "empty input");
+  CB_REQUIRE(h && k_blend && v_blend && pos, CB_E_INVALID_ARG, "NULL pointer");
+  CB_REQUIRE(n_cand == 0 || cand_tok, CB_E_INVALID_ARG, "cand_tok is NULL");
+  CB_REQUIRE(k_keep == 0 || sel_tok, CB_E_INVALID_ARG, "sel_tok is NULL");
+  cudaStream_t s = (cudaStream_t)st;
+  const int rows = n_cand + n_suffix;
+  if (rows > 0) {
+    make_rows_kernel<<<std::min(256, (rows + 255) / 256), 256, 0, s>>>(cand_tok, n_cand, n_suffix, N, c->row_tok[0]);
+    CB_LAUNCHED(c);
+  }
+  const size_t d = c->m.d_model;
+  LayerBufs b{h, c->h[0], c->row_tok[0], c->row_tok[1]};
+  int out_rows;
+  if (layer == 0) {
+    CB_REQUIRE(n_cand == N && k_keep == N, CB_E_INVALID_ARG, "layer 0 is the full layer: n_cand = k_keep = N");
+    CB_TRY(layer_full(c, *w, b, N, n_suffix, k_blend, v_blend, pos, s));
+    if (k_keep > 0) CB_CUDA(cudaMemcpyAsync(sel_tok, cand_tok, k_keep * 4, cudaMemcpyDeviceToDevice, s));
+    out_rows = rows;
+  } else {
+    CB_TRY(layer_blend(c, *w, b, n_cand, k_keep, n_suffix, N, k_blend, v_blend, pos, force_sel, sel_tok, dev_out,
+                       CB_DEV_KV, s));
+    out_rows = k_keep + n_suffix;
+  }
+  if (out_rows > 0)
+    CB_CUDA(cudaMemcpyAsync(h, c->h[0], (size_t)out_rows * d * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  return CB_OK;
+}
+
+// ---- the whole blend -------------------------------------------------------------------------------
+extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok,
+                                      const int32_t* pos, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                                      int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend,
+                                      void* v_blend, const int32_t* k_sched, const int32_t* force_sel,
+                                      int32_t* sel_out, float* dev_out, float* h_out, void* st) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  const cb_model& m = c->m;
+  const int L = m.n_layers;
+  CB_REQUIRE(w != nullptr && k_sched != nullptr, CB_E_INVALID_ARG, "w / k_sched is NULL");
+  for (int i = 0; i < L; ++i) CB_TRY(check_weights(&w[i]));
+  CB_REQUIRE(N >= 0 && n_suffix >= 0 && N + n_suffix >= 1, CB_E_INVALID_ARG, "empty input (N=%d, n_suffix=%d)", N,
+             n_suffix);
+  const int T = N + n_suffix;
+  CB_REQUIRE(T <= c->max_tokens, CB_E_SHAPE, "N + n_suffix = %d > max_tokens %d", T, c->max_tokens);
+  CB_REQUIRE(embed && tok && pos && k_blend && v_blend && h_out, CB_E_INVALID_ARG, "NULL pointer");
+  CB_REQUIRE(N == 0 || (k_in && v_in && chunk_start && n_chunks >= 1), CB_E_INVALID_ARG,
+             "chunk caches / chunk_start missing");
+  if (N > 0) {
+    CB_REQUIRE(chunk_start[0] == 0 && chunk_start[n_chunks] == N, CB_E_SHAPE,
+               "chunk_start must run from 0 to N=%d", N);
+    for (int ci = 0; ci < n_chunks; ++ci)
+      CB_REQUIRE(chunk_start[ci + 1] >= chunk_start[ci], CB_E_SHAPE, "chunk_start not non-decreasing");
+  }
+  for (int i = 1; i < L; ++i)
+    CB_REQUIRE(k_sched[i] >= 0 && k_sched[i] <= (i == 1 ? N : k_sched[i - 1]), CB_E_INVALID_ARG,
+               "k_sched must satisfy 0 <= k_i <= k_{i-1} <= N (layer %d: %d)", i, k_sched[i]);
+  const bool k_inplace = (k_blend == k_in), v_inplace = (v_blend == v_in);
+  CB_REQUIRE((!k_inplace && !v_inplace) || n_suffix == 0, CB_E_INVALID_ARG,
+             "in-place blend (k_blend == k_in) requires n_suffix == 0");
+  CB_REQUIRE(k_inplace == v_inplace, CB_E_INVALID_ARG, "k and v must both be in place or both out of place");
+
+  cudaStream_t s = (cudaStream_t)st;
+  const int kvd = m.n_kv_heads * m.head_dim;
+  const size_t B = dtype_bytes(m.dtype);
+  const size_t layer_stride = (size_t)T * kvd;  // elements per layer of the blended cache
+
+  // (a1) positional recovery of every layer's cached K (+ carry V over when out of place)
+  if (N > 0) {
+    CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, s));
+    CB_TRY(launch_realign(c, k_blend, k_in, v_inplace ? nullptr : v_blend, v_in, c->src_pos, pos, L, N,
+                          (long long)layer_stride, (long long)N * kvd, s));
+  }
+  // (a2) layer 0 in full
+  CB_TRY(launch_embed(c, embed, tok, T, c->h[0], s));
+  LayerBufs b0{c->h[0], c->h[1], c->iota, nullptr};
+  CB_TRY(layer_full(c, w[0], b0, N, n_suffix, k_blend, v_blend, pos, s));
+  if (sel_out) CB_TRY(launch_sel_out(c, c->iota, N, N, sel_out, s));
+  // (a3-a8) layers 1..L-1 with gradual filtering: C_1 = all context tokens, C_{i+1} = S_i
+  int cur = 1, n_cand = N;
+  const int* rows = c->iota;
+  int rt = 0;
+  for (int i = 1; i < L; ++i) {
+    const int k = k_sched[i];
+    LayerBufs b{c->h[cur], c->h[cur ^ 1], rows, c->row_tok[rt]};
+    char* kb = (char*)k_blend + (size_t)i * layer_stride * B;
+    char* vb = (char*)v_blend + (size_t)i * layer_stride * B;
+    CB_TRY(layer_blend(c, w[i], b, n_cand, k, n_suffix, N, kb, vb, pos, force_sel ? force_sel + (size_t)i * N : nullptr,
+                       nullptr, dev_out ? dev_out + (size_t)i * N : nullptr, CB_DEV_KV, s));
+    if (sel_out) CB_TRY(launch_sel_out(c, c->row_tok[rt], k, N, sel_out + (size_t)i * N, s));
+    rows = c->row_tok[rt];
+    rt ^= 1;
+    cur ^= 1;
+    n_cand = k;
+  }
+  const int final_rows = (L == 1 ? N : n_cand) + n_suffix;
+  if (final_rows > 0)
+    CB_CUDA(cudaMemcpyAsync(h_out, c->h[cur], (size_t)final_rows * m.d_model * sizeof(float),
+                            cudaMemcpyDeviceToDevice, s));
+  return CB_OK;
+}

@@ -1,0 +1,140 @@
+// common.cuh — shared device/host definitions for libcacheblend (sm_100a only).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/cacheblend.h"
+#include "../../include/cacheblend_ops.h"
+
+typedef __nv_bfloat16 bf16;
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libcacheblend is built for sm_100a only (-gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+// ---- scalar conversions ------------------------------------------------------------------------
+template <typename T> __device__ __forceinline__ float to_f(T x);
+template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ float to_f<bf16>(bf16 x) { return __bfloat162float(x); }
+
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// 16-byte vector of T: 8 bf16 or 4 fp32.
+template <typename T> struct Vec16 {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+
+template <typename T> __device__ __forceinline__ Vec16<T> ld16(const T* p) {
+  Vec16<T> r;
+  *reinterpret_cast<uint4*>(&r) = __ldg(reinterpret_cast<const uint4*>(p));
+  return r;
+}
+template <typename T> __device__ __forceinline__ Vec16<T> ld16_cg(const T* p) {
+  Vec16<T> r;
+  *reinterpret_cast<uint4*>(&r) = __ldcg(reinterpret_cast<const uint4*>(p));
+  return r;
+}
+template <typename T> __device__ __forceinline__ void st16(T* p, const Vec16<T>& v) {
+  *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(&v);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Device-side error word bits (cb_check_device_errors).
+enum : int { CB_DEVERR_FORCE_SEL = 1, CB_DEVERR_POS_RANGE = 2 };
+
+// ---- epilogues shared by the SIMT and tcgen05 GEMMs -----------------------------------------
+// acc[m][n] = sum_k A[m][k] B[n][k];   kinds:
+enum EpiKind : int {
+  EPI_STORE = 0,     // out[m*ldo + n] = T(acc)
+  EPI_STORE_F32 = 1, // outf[m*ldo + n] = acc
+  EPI_QKV = 2,       // logical column c = col0 + n of [q | k | v]; RoPE on q,k at pos[row_tok[m]]
+  EPI_RESID = 3,     // h_out[m][n] = h_in[res_row ? res_row[m] : m][n] + acc   (fp32)
+  EPI_SWIGLU = 4     // GEMM over 2*ff "virtual" columns; act[m][f] = T(silu(gate) * up)
+};
+
+struct EpiParams {
+  int kind;
+  int M, N;                    // GEMM output extent (N = ff for SWIGLU)
+  void* out; float* outf; int ldo;
+  // EPI_QKV
+  void* q_out; void* k_out; void* v_out;
+  int col0, qd, kvd, hd;
+  const int* row_tok; const int* pos; const float2* rope_tab;
+  // EPI_RESID
+  float* h_out; const float* h_in; const int* res_row;
+  // EPI_SWIGLU
+  int ff; void* act;
+};
+
+// Apply the epilogue to the adjacent column pair (n, n+1), n even. For SWIGLU a0/a1 are the gate
+// accumulators and u0/u1 the up accumulators of output columns n, n+1.
+template <typename T>
+__device__ __forceinline__ void epi_pair(const EpiParams& e, int m, int n, float a0, float a1,
+                                         float u0 = 0.f, float u1 = 0.f) {
+  const bool has1 = (n + 1) < e.N;
+  switch (e.kind) {
+    case EPI_STORE: {
+      T* o = reinterpret_cast<T*>(e.out) + (size_t)m * e.ldo + n;
+      o[0] = from_f<T>(a0);
+      if (has1) o[1] = from_f<T>(a1);
+    } break;
+    case EPI_STORE_F32: {
+      float* o = e.outf + (size_t)m * e.ldo + n;
+      o[0] = a0;
+      if (has1) o[1] = a1;
+    } break;
+    case EPI_QKV: {
+      const int c = e.col0 + n;  // logical column in [q | k | v]
+      if (c < e.qd + e.kvd) {    // q or k: rotate the pair (2i, 2i+1) of the head
+        const int dim = (c < e.qd ? c : c - e.qd) % e.hd;
+        const int p = e.pos[e.row_tok[m]];
+        const float2 cs = e.rope_tab[(size_t)p * (e.hd >> 1) + (dim >> 1)];
+        const float r0 = cs.x * a0 - cs.y * a1;
+        const float r1 = cs.y * a0 + cs.x * a1;
+        T* o = (c < e.qd) ? reinterpret_cast<T*>(e.q_out) + (size_t)m * e.qd + c
+                          : reinterpret_cast<T*>(e.k_out) + (size_t)m * e.kvd + (c - e.qd);
+        o[0] = from_f<T>(r0);
+        o[1] = from_f<T>(r1);
+      } else {
+        T* o = reinterpret_cast<T*>(e.v_out) + (size_t)m * e.kvd + (c - e.qd - e.kvd);
+        o[0] = from_f<T>(a0);
+        if (has1) o[1] = from_f<T>(a1);
+      }
+    } break;
+    case EPI_RESID: {
+      const int src = e.res_row ? e.res_row[m] : m;
+      const float* hi = e.h_in + (size_t)src * e.ldo + n;
+      float* ho = e.h_out + (size_t)m * e.ldo + n;
+      const float h0 = hi[0];
+      const float h1 = has1 ? hi[1] : 0.f;
+      ho[0] = h0 + a0;
+      if (has1) ho[1] = h1 + a1;
+    } break;
+    case EPI_SWIGLU: {
+      T* o = reinterpret_cast<T*>(e.act) + (size_t)m * e.ff + n;
+      const float s0 = a0 / (1.f + expf(-a0));
+      o[0] = from_f<T>(s0 * u0);
+      if (has1) {
+        const float s1 = a1 / (1.f + expf(-a1));
+        o[1] = from_f<T>(s1 * u1);
+      }
+    } break;
+  }
+}

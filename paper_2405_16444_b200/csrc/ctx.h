@@ -1,0 +1,95 @@
+// ctx.h — host-side context of libcacheblend (internal).
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+struct TmapCache;  // tcgen05 GEMM tensor-map cache (gemm_tc.cu)
+
+struct cb_ctx {
+  cb_model m;
+  int max_tokens;
+  int device;
+  int num_sms;
+  // RoPE table: (cos, sin)(p * theta_i) for p in [0, max_pos), i in [0, hd/2); built in fp64.
+  float2* rope_tab;
+  int* err_word;  // device error bits
+  // workspace
+  void* ws;
+  size_t ws_bytes;
+  bool ws_owned;
+  float* h[2];      // fp32 [T][d] residual stream ping-pong
+  void* x;          // [T][d]      normed rows (model dtype)
+  void* q;          // [T][qd]
+  void* kf;         // [T][kvd]    fresh k (RoPE'd) of the current rows
+  void* vf;         // [T][kvd]
+  void* attn;       // [T][qd]
+  void* act;        // [T][ff]
+  float* dev;       // [T]
+  int* row_tok[2];  // [T] token index of each current row (candidates, then suffix)
+  int* qrow;        // [T] row (in the current compact buffers) of each kept query
+  int* iota;        // [T] 0..T-1
+  int* src_pos;     // [T] chunk-local positions (blend_forward)
+  long long launches;
+  TmapCache* tmaps;
+};
+
+void cb_set_error(const char* fmt, ...);
+
+#define CB_REQUIRE(cond, code, ...)        \
+  do {                                     \
+    if (!(cond)) {                         \
+      cb_set_error(__VA_ARGS__);           \
+      return (code);                       \
+    }                                      \
+  } while (0)
+
+#define CB_CUDA(call)                                                               \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      cb_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__,    \
+                   __LINE__, cudaGetErrorString(e_));                               \
+      return CB_E_CUDA;                                                             \
+    }                                                                               \
+  } while (0)
+
+#define CB_LAUNCHED(ctx)                  \
+  do {                                    \
+    (ctx)->launches++;                    \
+    CB_CUDA(cudaGetLastError());          \
+  } while (0)
+
+#define CB_TRY(expr)                  \
+  do {                                \
+    cb_status s_ = (expr);            \
+    if (s_ != CB_OK) return s_;       \
+  } while (0)
+
+static inline size_t dtype_bytes(int dt) { return dt == CB_BF16 ? 2 : 4; }
+
+// ---- internal launchers (implemented per .cu file) ------------------------------------------
+cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out, const void* v_src,
+                         const int* src_pos, const int* dst_pos, int n_slices, int n_tok, long long out_stride,
+                         long long src_stride, cudaStream_t s);
+cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, float* h, cudaStream_t s);
+cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s);
+cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int* qrow, const int* qtok, int n,
+                            void* kb, void* vb, cudaStream_t s);
+cb_status launch_local_pos(cb_ctx* c, const int* chunk_start_host, int n_chunks, int* src_pos, cudaStream_t s);
+cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* sel_row, cudaStream_t s);
+cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, const void* k_ref, const void* v_ref,
+                           const int* cand_tok, int n_cand, int dev_mode, float* dev, cudaStream_t s);
+cb_status launch_topk(cb_ctx* c, const float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix,
+                      int N, const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s);
+// GEMM: acc = A[M][K] . B[N_b][K]^T; for SWIGLU B holds 2*ff rows and e.N = ff.
+// impl: 0 auto, 1 simt, 2 tcgen05.
+cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
+                      int impl, cudaStream_t s);
+cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
+                           const void* v, int n_keys, void* out, int impl, cudaStream_t s);
+cb_status launch_gen_fill(void* out, int dtype, long long count, unsigned long long seed, unsigned long long stream_id,
+                          long long start, float scale, float offset, cudaStream_t s);

@@ -1,0 +1,230 @@
+// elementwise.cu — HBM-bound kernels of the blend path: RoPE realign (step a1), embedding gather,
+// RMSNorm, KV scatter (step a5) and small index utilities.
+#include <algorithm>
+
+#include "ctx.h"
+
+// ---------------------------------------------------------------------------------------------
+// (a1) positional recovery: K_out[s][t] = R(dst[t] - src[t]) K_src[s][t]   (footnote P:208-211,
+// Appendix). One thread owns one 16-byte vector (4 or 2 RoPE pairs) of one token and
+// loops over all slices (layers), so the (cos, sin) pairs are read once per token and reused
+// n_slices times; K moves through 128-bit coalesced loads/stores exactly once (read + write).
+// ---------------------------------------------------------------------------------------------
+template <typename T, int UNROLL>
+__global__ void __launch_bounds__(256) realign_kernel(T* __restrict__ k_out, const T* __restrict__ k_src,
+                                                      T* __restrict__ v_out, const T* __restrict__ v_src,
+                                                      const int* __restrict__ src_pos, const int* __restrict__ dst_pos,
+                                                      int n_slices, int n_tok, long long out_stride,
+                                                      long long src_stride, int kvd, int hd,
+                                                      const float2* __restrict__ tab, int max_pos, int* err) {
+  constexpr int V = Vec16<T>::N;  // elements per vector
+  const int nvec = kvd / V;
+  const long long total = (long long)n_tok * nvec;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / nvec);
+    const int j = (int)(idx - (long long)t * nvec);
+    const int e0 = j * V;
+    int delta = __ldg(dst_pos + t) - __ldg(src_pos + t);
+    float sgn = 1.f;
+    if (delta < 0) { delta = -delta; sgn = -1.f; }
+    if (delta >= max_pos) { atomicOr(err, CB_DEVERR_POS_RANGE); delta = max_pos - 1; }
+    const float2* cs_row = tab + (size_t)delta * (hd >> 1) + ((e0 % hd) >> 1);
+    float c[V / 2], s[V / 2];
+#pragma unroll
+    for (int p = 0; p < V / 2; ++p) {
+      const float2 cs = __ldg(cs_row + p);
+      c[p] = cs.x;
+      s[p] = sgn * cs.y;
+    }
+    const size_t off = (size_t)t * kvd + e0;
+    for (int s0 = 0; s0 < n_slices; s0 += UNROLL) {
+      Vec16<T> v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (s0 + u < n_slices) v[u] = ld16_cg(k_src + (size_t)(s0 + u) * src_stride + off);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        if (s0 + u < n_slices) {
+          Vec16<T> o;
+#pragma unroll
+          for (int p = 0; p < V / 2; ++p) {
+            const float x0 = to_f(v[u].v[2 * p]), x1 = to_f(v[u].v[2 * p + 1]);
+            o.v[2 * p] = from_f<T>(c[p] * x0 - s[p] * x1);
+            o.v[2 * p + 1] = from_f<T>(s[p] * x0 + c[p] * x1);
+          }
+          st16(k_out + (size_t)(s0 + u) * out_stride + off, o);
+        }
+      }
+      if (v_out != nullptr) {  // out-of-place blend: V is carried over unchanged in the same pass
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (s0 + u < n_slices) v[u] = ld16_cg(v_src + (size_t)(s0 + u) * src_stride + off);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (s0 + u < n_slices) st16(v_out + (size_t)(s0 + u) * out_stride + off, v[u]);
+      }
+    }
+  }
+}
+
+cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out, const void* v_src,
+                         const int* src_pos, const int* dst_pos, int n_slices, int n_tok, long long out_stride,
+                         long long src_stride, cudaStream_t s) {
+  if (n_tok == 0 || n_slices == 0) return CB_OK;
+  const int kvd = c->m.n_kv_heads * c->m.head_dim;
+  const int V = 16 / (int)dtype_bytes(c->m.dtype);
+  const long long total = (long long)n_tok * (kvd / V);
+  const int grid = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c->num_sms * 8));
+  if (c->m.dtype == CB_BF16)
+    realign_kernel<bf16, 4><<<grid, 256, 0, s>>>((bf16*)k_out, (const bf16*)k_src, (bf16*)v_out, (const bf16*)v_src,
+                                                 src_pos, dst_pos, n_slices, n_tok, out_stride, src_stride, kvd,
+                                                 c->m.head_dim, c->rope_tab, c->m.max_pos, c->err_word);
+  else
+    realign_kernel<float, 4><<<grid, 256, 0, s>>>((float*)k_out, (const float*)k_src, (float*)v_out,
+                                                  (const float*)v_src, src_pos, dst_pos, n_slices, n_tok, out_stride,
+                                                  src_stride, kvd, c->m.head_dim, c->rope_tab, c->m.max_pos,
+                                                  c->err_word);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// embedding gather: h[t] = fp32(embed[tok[t]])
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ tok, float* __restrict__ h, int d) {
+  const int t = blockIdx.x;
+  const T* src = emb + (size_t)__ldg(tok + t) * d;
+  float* dst = h + (size_t)t * d;
+  for (int e = threadIdx.x * Vec16<T>::N; e < d; e += blockDim.x * Vec16<T>::N) {
+    Vec16<T> v = ld16(src + e);
+#pragma unroll
+    for (int q = 0; q < Vec16<T>::N; ++q) dst[e + q] = to_f(v.v[q]);
+  }
+}
+
+cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, float* h, cudaStream_t s) {
+  if (n == 0) return CB_OK;
+  if (c->m.dtype == CB_BF16)
+    embed_kernel<bf16><<<n, 128, 0, s>>>((const bf16*)embed, tok, h, c->m.d_model);
+  else
+    embed_kernel<float><<<n, 128, 0, s>>>((const float*)embed, tok, h, c->m.d_model);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// RMSNorm: x = h / sqrt(mean(h^2) + eps) * gain  (fixed-order block reduction: deterministic)
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
+                                                      T* __restrict__ x, int d, float eps) {
+  const int r = blockIdx.x;
+  const float* hr = h + (size_t)r * d;
+  __shared__ float red[8];
+  float ss = 0.f;
+  for (int e = threadIdx.x * 4; e < d; e += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(hr + e);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+  T* xr = x + (size_t)r * d;
+  for (int e = threadIdx.x * 4; e < d; e += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(hr + e);
+    const float4 gg = __ldg(reinterpret_cast<const float4*>(g + e));
+    xr[e + 0] = from_f<T>(v.x * inv * gg.x);
+    xr[e + 1] = from_f<T>(v.y * inv * gg.y);
+    xr[e + 2] = from_f<T>(v.z * inv * gg.z);
+    xr[e + 3] = from_f<T>(v.w * inv * gg.w);
+  }
+}
+
+cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s) {
+  if (n_rows == 0) return CB_OK;
+  if (c->m.dtype == CB_BF16)
+    rmsnorm_kernel<bf16><<<n_rows, 256, 0, s>>>(h, gain, (bf16*)x, c->m.d_model, c->m.rms_eps);
+  else
+    rmsnorm_kernel<float><<<n_rows, 256, 0, s>>>(h, gain, (float*)x, c->m.d_model, c->m.rms_eps);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// (a5) KV scatter: blended[qtok[r]] <- fresh[qrow[r]] for the kept rows (R3)
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void scatter_kv_kernel(const T* __restrict__ kf, const T* __restrict__ vf, const int* __restrict__ qrow,
+                                  const int* __restrict__ qtok, T* __restrict__ kb, T* __restrict__ vb, int kvd) {
+  const int r = blockIdx.x;
+  const size_t src = (size_t)__ldg(qrow + r) * kvd, dst = (size_t)__ldg(qtok + r) * kvd;
+  for (int e = threadIdx.x * Vec16<T>::N; e < kvd; e += blockDim.x * Vec16<T>::N) {
+    st16(kb + dst + e, ld16(kf + src + e));
+    st16(vb + dst + e, ld16(vf + src + e));
+  }
+}
+
+cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int* qrow, const int* qtok, int n,
+                            void* kb, void* vb, cudaStream_t s) {
+  if (n == 0) return CB_OK;
+  const int kvd = c->m.n_kv_heads * c->m.head_dim;
+  if (c->m.dtype == CB_BF16)
+    scatter_kv_kernel<bf16><<<n, 128, 0, s>>>((const bf16*)kf, (const bf16*)vf, qrow, qtok, (bf16*)kb, (bf16*)vb, kvd);
+  else
+    scatter_kv_kernel<float><<<n, 128, 0, s>>>((const float*)kf, (const float*)vf, qrow, qtok, (float*)kb, (float*)vb,
+                                               kvd);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// chunk-local positions from chunk starts passed by value (no host->device copy, graph-safe)
+// ---------------------------------------------------------------------------------------------
+struct ChunkTable {
+  int n;
+  int start[129];
+};
+
+__global__ void local_pos_kernel(ChunkTable ct, int base_chunk, int* __restrict__ src_pos) {
+  const int t0 = ct.start[0], t1 = ct.start[ct.n];
+  for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
+    int lo = 0, hi = ct.n - 1;  // largest c with start[c] <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ct.start[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    src_pos[t] = t - ct.start[lo];
+  }
+  (void)base_chunk;
+}
+
+cb_status launch_local_pos(cb_ctx* c, const int* cs, int n_chunks, int* src_pos, cudaStream_t s) {
+  for (int b = 0; b < n_chunks; b += 128) {
+    ChunkTable ct;
+    ct.n = std::min(128, n_chunks - b);
+    for (int i = 0; i <= ct.n; ++i) ct.start[i] = cs[b + i];
+    const int len = ct.start[ct.n] - ct.start[0];
+    if (len <= 0) continue;
+    local_pos_kernel<<<std::min(1024, (len + 255) / 256), 256, 0, s>>>(ct, b, src_pos);
+    CB_LAUNCHED(c);
+  }
+  return CB_OK;
+}
+
+__global__ void sel_out_kernel(const int* __restrict__ qtok, int k, int N, int* __restrict__ row) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x)
+    row[j] = j < k ? qtok[j] : -1;
+}
+
+cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* row, cudaStream_t s) {
+  if (N == 0) return CB_OK;
+  sel_out_kernel<<<std::min(256, (N + 255) / 256), 256, 0, s>>>(qtok, k, N, row);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}

@@ -1,0 +1,224 @@
+// select.cu — HKVD selection (step a4): KV deviation (R1) and the top-k_i
+// select over the candidates (Insight 1; ties -> lower token index, R6).
+#include <algorithm>
+
+#include "ctx.h"
+
+// ---------------------------------------------------------------------------------------------
+// Delta_kv[j] = sum_h ( ||k_new[j,h] - k_ref[tok_j,h]||^2 + ||v_new[j,h] - v_ref[tok_j,h]||^2 ).
+// One warp per candidate; per-head partials are warp-reduced in a fixed tree and summed over heads
+// in index order, so the value is bitwise reproducible (and decomposes per kv head for TP).
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) deviation_kernel(const T* __restrict__ kn, const T* __restrict__ vn,
+                                                        const T* __restrict__ kr, const T* __restrict__ vr,
+                                                        const int* __restrict__ cand_tok, int n_cand, int n_kv,
+                                                        int hd, int mode, float* __restrict__ dev) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_cand) return;
+  const int kvd = n_kv * hd;
+  const size_t a = (size_t)warp * kvd, b = (size_t)__ldg(cand_tok + warp) * kvd;
+  float tot = 0.f;
+  for (int h = 0; h < n_kv; ++h) {
+    float p = 0.f;
+    for (int e = h * hd + lane; e < (h + 1) * hd; e += 32) {
+      if (mode != CB_DEV_V) {
+        const float d = to_f(kn[a + e]) - to_f(kr[b + e]);
+        p += d * d;
+      }
+      if (mode != CB_DEV_K) {
+        const float d = to_f(vn[a + e]) - to_f(vr[b + e]);
+        p += d * d;
+      }
+    }
+    tot += warp_sum(p);
+  }
+  if (lane == 0) dev[warp] = tot;
+}
+
+cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, const void* k_ref, const void* v_ref,
+                           const int* cand_tok, int n_cand, int dev_mode, float* dev, cudaStream_t s) {
+  if (n_cand == 0) return CB_OK;
+  const int grid = (n_cand + 7) / 8;
+  if (c->m.dtype == CB_BF16)
+    deviation_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)k_new, (const bf16*)v_new, (const bf16*)k_ref,
+                                                (const bf16*)v_ref, cand_tok, n_cand, c->m.n_kv_heads,
+                                                c->m.head_dim, dev_mode, dev);
+  else
+    deviation_kernel<float><<<grid, 256, 0, s>>>((const float*)k_new, (const float*)v_new, (const float*)k_ref,
+                                                 (const float*)v_ref, cand_tok, n_cand, c->m.n_kv_heads,
+                                                 c->m.head_dim, dev_mode, dev);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Top-k select, one CTA of 1024 threads. Deviations are non-negative, so their fp32 bit patterns
+// order like the values: an MSB-first 4 x 8-bit radix select finds the k-th largest value v*;
+// every candidate above v* is kept, and of those equal to v* the lowest slots (= lowest token
+// indices, candidates are ascending) fill the remainder. Output is compacted in slot order, i.e.
+// ascending token index. Replay mode (force_sel) maps forced tokens to their candidate slots.
+// Outputs cover the kept rows then the suffix rows:
+//   qrow[r] = row in the current compact buffers,  qtok[r] = token index.
+// ---------------------------------------------------------------------------------------------
+constexpr int TOPK_THREADS = 1024;
+constexpr int TOPK_MAX_CAND = 49152;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* sm_warp, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = sm_warp[lane];
+    int u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += y;
+    }
+    sm_warp[lane] = u - t;  // exclusive prefix of warp totals
+    if (lane == 31) *total = u;
+  }
+  __syncthreads();
+  const int r = sm_warp[w] + x - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float* __restrict__ dev,
+                                                            const int* __restrict__ cand_tok, int n_cand, int k,
+                                                            int n_suf, int N, const int* __restrict__ force_sel,
+                                                            int* __restrict__ qrow, int* __restrict__ qtok,
+                                                            int* __restrict__ sel_tok, int* err) {
+  extern __shared__ unsigned keys[];
+  __shared__ int hist[256];
+  __shared__ int sm_warp[32];
+  __shared__ int sm_total;
+  __shared__ int sm_digit, sm_rem;
+  const int tid = threadIdx.x;
+
+  // suffix rows are always kept
+  for (int s = tid; s < n_suf; s += blockDim.x) {
+    qrow[k + s] = n_cand + s;
+    qtok[k + s] = N + s;
+  }
+  if (force_sel != nullptr) {  // replay mode (R14)
+    for (int r = tid; r < k; r += blockDim.x) {
+      const int t = force_sel[r];
+      int lo = 0, hi = n_cand;  // lower_bound
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cand_tok[mid] < t) lo = mid + 1; else hi = mid;
+      }
+      if (lo >= n_cand || cand_tok[lo] != t) {
+        atomicOr(err, CB_DEVERR_FORCE_SEL);
+        lo = min(lo, n_cand - 1);
+      }
+      qrow[r] = lo;
+      qtok[r] = t;
+      if (sel_tok) sel_tok[r] = t;
+    }
+    return;
+  }
+  if (k == 0) return;
+
+  for (int j = tid; j < n_cand; j += blockDim.x) {
+    unsigned u = __float_as_uint(dev[j]);
+    keys[j] = (u & 0x80000000u) ? 0u : u;  // -0.0 -> 0
+  }
+  unsigned prefix = 0, mask = 0;
+  int rem = k;
+  if (k < n_cand) {
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      if (tid < 256) hist[tid] = 0;
+      __syncthreads();
+      for (int j = tid; j < n_cand; j += blockDim.x) {
+        const unsigned key = keys[j];
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (tid < 32) {  // warp 0: lane l owns bins [8l, 8l+8); find the digit holding the rem-th largest
+        int cnt[8], lane_tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { cnt[q] = hist[tid * 8 + q]; lane_tot += cnt[q]; }
+        int above = lane_tot;  // inclusive suffix sum over lanes >= tid
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_down_sync(0xffffffffu, above, o);
+          if (tid + o < 32) above += y;
+        }
+        const int strictly_above = above - lane_tot;  // keys in bins of higher lanes
+        if (strictly_above < rem && rem <= above) {
+          int cum = strictly_above;
+          for (int q = 7; q >= 0; --q) {
+            if (cum + cnt[q] >= rem) { sm_digit = tid * 8 + q; sm_rem = rem - cum; break; }
+            cum += cnt[q];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= (unsigned)sm_digit << shift;
+      mask |= 255u << shift;
+      rem = sm_rem;
+      __syncthreads();
+    }
+  } else {
+    prefix = 0; rem = n_cand;  // take everything: every key >= 0 qualifies via the eq path below
+  }
+  const unsigned vstar = prefix;
+  const bool all = (k >= n_cand);
+
+  // contiguous segment per thread so that slot order is preserved by the scans
+  const int seg = (n_cand + blockDim.x - 1) / blockDim.x;
+  const int j0 = min(n_cand, tid * seg), j1 = min(n_cand, j0 + seg);
+  int n_eq = 0;
+  if (!all)
+    for (int j = j0; j < j1; ++j) n_eq += (keys[j] == vstar);
+  const int eq_before = block_excl_scan(n_eq, sm_warp, &sm_total);
+  int n_sel = 0, eq = eq_before;
+  for (int j = j0; j < j1; ++j) {
+    const unsigned key = keys[j];
+    bool sel = all || key > vstar;
+    if (!all && key == vstar) { sel = eq < rem; ++eq; }
+    n_sel += sel;
+  }
+  int out = block_excl_scan(n_sel, sm_warp, &sm_total);
+  eq = eq_before;
+  for (int j = j0; j < j1; ++j) {
+    const unsigned key = keys[j];
+    bool sel = all || key > vstar;
+    if (!all && key == vstar) { sel = eq < rem; ++eq; }
+    if (sel) {
+      const int t = cand_tok[j];
+      qrow[out] = j;
+      qtok[out] = t;
+      if (sel_tok) sel_tok[out] = t;
+      ++out;
+    }
+  }
+}
+
+cb_status launch_topk(cb_ctx* c, const float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix, int N,
+                      const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s) {
+  CB_REQUIRE(n_cand <= TOPK_MAX_CAND, CB_E_SHAPE, "top-k: n_cand %d exceeds %d", n_cand, TOPK_MAX_CAND);
+  if (k_keep + n_suffix == 0) return CB_OK;
+  const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
+  topk_kernel<<<1, TOPK_THREADS, smem, s>>>(dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
+                                            c->err_word);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+cb_status topk_init_attrs() {
+  CB_CUDA(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               TOPK_MAX_CAND * (int)sizeof(unsigned)));
+  return CB_OK;
+}
