@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark: CacheBlend blend_forward at 15 % recompute, Mistral-7B shape, 6 x 512-token chunks
+(BASELINE.json metric / configs[1]) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config mistral]
+
+One step = one cb_blend_forward over one request (realign + layer 0 + 31 selective layers), inputs
+resident in HBM. Multi-GPU (torchrun, N>1): request-parallel, each rank blends its own request
+(weak scaling, no collective on the data path; SURVEY §8(e) partitioning 2). Prints ONE JSON line
+on rank 0. --impl reference times the fp64 CPU oracle (bounded sample) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import workload as W  # noqa: E402
+
+CONFIGS = {  # name -> (model shape, chunk lens, ratio)
+    "mistral": ("mistral-7b", [512] * 6, 0.15),
+    "yi": ("yi-34b", [1024] * 8, 0.15),
+    "small": ("small", [200, 317, 150], 0.15),
+}
+METRIC = "blend latency ms & context tok/s at 15% recompute (Mistral-7B shape)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mistral", choices=sorted(CONFIGS))
+    ap.add_argument("--ratio", type=float, default=None)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------------
+# algorithmic work; the avoided dense work is not counted
+# ---------------------------------------------------------------------------------------------------
+def algorithmic_work(s, N, n_suf, ks):
+    d, qd, kvd, ff, L = s.d_model, s.qd, s.kvd, s.d_ff, s.n_layers
+    T = N + n_suf
+    g = np.arange(T, dtype=np.float64)  # positions 0..T-1: causal span of token t is t + 1
+    gemm = {}
+    gemm["l0"] = 2.0 * T * (d * qd + qd * d + 3 * d * ff) + 2.0 * n_suf * d * 2 * kvd
+    attn = 4.0 * qd * float(np.sum(g + 1))
+    cand, sel_rows = N, None
+    tot_gemm = gemm["l0"]
+    for i in range(1, L):
+        k = ks[i]
+        tot_gemm += 2.0 * (cand + n_suf) * d * (qd + 2 * kvd) + 2.0 * (k + n_suf) * (qd * d + 3 * d * ff)
+        # attention over each kept query's causal span: the bench's later-layer rows are the top-k of
+        # the candidates; counted with the mean span (N+1)/2 per query (exact spans are data dependent)
+        attn += 4.0 * qd * (k + n_suf) * (T + 1) / 2.0
+        cand = k
+    B = 2
+    wbytes = L * B * (d * qd + 2 * d * kvd + qd * d + 3 * d * ff)
+    realign_bytes = 2.0 * L * N * kvd * B * 2  # K read+write, V carried over (read+write)
+    return dict(gemm_flops=tot_gemm, attn_flops=attn, weight_bytes=wbytes, realign_bytes=realign_bytes)
+
+
+# ---------------------------------------------------------------------------------------------------
+# clocks sampled DURING the timed region
+# ---------------------------------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j["hbm_gbs"], j["bf16_tflops"], j.get("bf16_tflops_sustained", j["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ---------------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference): bounded sample of the same workload
+# ---------------------------------------------------------------------------------------------------
+class OracleSample:
+    """Realign of every layer + layers 0, 1, 2 of the blend, run by the fp64 oracle as it stands, on the
+    same shapes (random-cache mode inputs: values do not change the oracle's cost). Later layers are
+    extrapolated from layer 2 in proportion to their candidate/kept row counts."""
+
+    def __init__(self, s, lens, ratio, seed):
+        from oracle import cacheblend_oracle as O
+        self.O, self.s = O, s
+        self.req = W.Request(list(lens), 0, seed, ratio)
+        N = self.req.n_ctx
+        self.ks = O.schedule(ratio, N, s.n_layers)
+        n_layers = min(3, s.n_layers)
+        self.model = O.Model.build(s, W.embed_weights(s, seed, "bf16"),
+                                   [W.layer_weights(s, i, seed, "bf16") for i in range(n_layers)])
+        self.tok, self.pos = self.req.tokens(s.vocab), self.req.global_positions()
+        self.loc = self.req.local_positions()
+        self.Kc = W.random_cache(s, 0, N, seed, "bf16", "k").astype(np.float64)
+        self.Vc = W.random_cache(s, 0, N, seed, "bf16", "v").astype(np.float64)
+
+    def run(self):
+        O, s, m = self.O, self.s, self.model
+        N, L = self.req.n_ctx, s.n_layers
+        t0 = time.perf_counter()
+        K = np.zeros((3, N, s.n_kv_heads, s.head_dim))
+        V = np.zeros_like(K)
+        for i in range(L):  # realign every layer (the oracle's step 1)
+            Ki = O.realign(self.Kc, self.loc, self.pos, s.rope_theta)
+            if i < 3:
+                K[i], V[i] = Ki, self.Vc
+        t_realign = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        h = m.embed[self.tok]
+        q, _, _ = O.qkv(m, 0, h, self.pos)
+        a = O.causal_attention(q, self.pos, K[0], V[0], self.pos)
+        h = O.attn_out_mlp(m, 0, h, a)
+        t_l0 = time.perf_counter() - t1
+        cand = np.arange(N)
+        t_layers = []
+        for i in (1, 2):
+            t2 = time.perf_counter()
+            h, sel, _ = O.blend_layer(m, i, h, cand, N, 0, self.ks[i], K, V, self.pos)
+            t_layers.append(time.perf_counter() - t2)
+            cand = sel
+        # layers 3..L-1 ~ layer 2 scaled by rows (candidates for QKV, kept rows for the rest)
+        w2 = self.ks[1] + self.ks[2]
+        rest = sum(self.ks[i - 1] + self.ks[i] for i in range(3, L)) / w2 * t_layers[1]
+        total = t_realign + t_l0 + sum(t_layers) + rest
+        sample = time.perf_counter() - t0
+        return total, sample
+
+    @staticmethod
+    def cores():
+        try:
+            from threadpoolctl import threadpool_info
+            return max(int(x.get("num_threads", 1)) for x in threadpool_info()) or os.cpu_count()
+        except Exception:
+            return os.cpu_count()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    shape_name, lens, ratio = CONFIGS[args.config]
+    ratio = args.ratio if args.ratio is not None else ratio
+    s = W.MODELS[shape_name]
+    smp = OracleSample(s, lens, ratio, args.seed)
+    for _ in range(args.warmup):
+        smp.run()
+    est, samples = [], []
+    for _ in range(args.steps):
+        e, t = smp.run()
+        est.append(e)
+        samples.append(t)
+    ms = float(np.mean(est)) * 1e3
+    N = sum(lens)
+    v = N / (ms / 1e3)
+    cores = OracleSample.cores()
+    line = {"metric": METRIC, "value": v, "unit": "ctx_tok/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter RNG)", "impl": "reference",
+            "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} r={ratio}", "recompute_ratio": ratio,
+                       "n_ctx": N},
+            "cpu_baseline": {"value": v, "unit": "ctx_tok/s", "cores": cores, "kind": "oracle",
+                             "sample": "per step: realign all layers + layers 0-2 in full (fp64 numpy); layers 3.."
+                                       f"{s.n_layers - 1} extrapolated from layer 2 by row counts; "
+                                       f"{float(np.mean(samples)):.1f} s of CPU work per step"},
+            "e2e": {"value": v, "unit": "ctx_tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2405_16444_b200.build import build
+    if rank == 0 or world == 1:
+        build()
+    if world > 1:
+        dist.barrier()
+    import paper_2405_16444_b200 as P
+
+    shape_name, lens, ratio = CONFIGS[args.config]
+    ratio = args.ratio if args.ratio is not None else ratio
+    s = W.MODELS[shape_name]
+    seed = args.seed + rank  # weak scaling: every rank blends its own request
+    req = W.Request(list(lens), 0, seed, ratio)
+    N, L, kvd = req.n_ctx, s.n_layers, s.kvd
+    dev = torch.device("cuda", local)
+    ctx = P.Context(s, "bf16", max_tokens=max(N, max(lens)), max_pos=max(2 * N, 4096))
+    mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
+    tok_h = req.tokens(s.vocab)
+    tok = torch.from_numpy(tok_h).to(dev)
+    pos = torch.from_numpy(req.global_positions()).to(dev)
+    # chunk caches: standalone prefill of each chunk at local positions 0..L_c-1, produced by
+    # this library (cb_blend_forward with the whole chunk as uncached suffix = full prefill)
+    k_in = torch.empty(L, N, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+    v_in = torch.empty_like(k_in)
+    cs = req.chunk_starts()
+    for c in range(len(lens)):
+        a, b = int(cs[c]), int(cs[c + 1])
+        n = b - a
+        kc = torch.empty(L, n, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+        vc = torch.empty_like(kc)
+        P.blend_forward(ctx, mw, tok[a:b].contiguous(), torch.arange(n, dtype=torch.int32, device=dev), [0], n,
+                        None, None, kc, vc, [0] * L)
+        k_in[:, a:b] = kc
+        v_in[:, a:b] = vc
+    del kc, vc
+    ks = P.schedule(ratio, N, L)
+    k_out, v_out = torch.empty_like(k_in), torch.empty_like(v_in)
+    h_out = torch.empty(ks[-1], s.d_model, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, k_out, v_out, ks, h_out=h_out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = (ctx.launch_count() - l0) // args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * N / (ms_max / 1e3)
+
+    # per-kernel profile pass (same steps, per-launch CUDA events on the launching stream)
+    prof = P.api.profile_steps(ctx, step, max(3, min(args.steps, 10)))
+    work = algorithmic_work(s, N, 0, ks)
+    hbm, tf_burst, tf_sus, peak_src = measured_peaks()
+    gemm_ms = prof.get("gemm", 0.0)
+    roof = None
+    if gemm_ms > 0:
+        achieved = work["gemm_flops"] / (gemm_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": "gemm (all projections)", "achieved": achieved, "peak": tf_sus,
+                "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": None,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                "share_of_step": gemm_ms / ms}
+    # end to end through the public API: chunk caches + tokens from pinned host memory, h_out back
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args)
+        if world > 1:
+            tt = torch.tensor([e2e["ms"]], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e["value"] = world * N / (float(tt.item()) / 1e3)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        smp = OracleSample(s, lens, ratio, args.seed)
+        est, sample_s = smp.run()
+        cpu = {"value": N / est, "unit": "ctx_tok/s", "cores": OracleSample.cores(), "kind": "oracle",
+               "ms_per_blend": est * 1e3,
+               "sample": f"realign all {L} layers + layers 0-2 in full (fp64 numpy, {sample_s:.1f} s); "
+                         f"layers 3..{L - 1} extrapolated from layer 2 by row counts"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "ctx_tok/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter RNG weights/tokens; "
+                "chunk caches from standalone prefill of each chunk)",
+                "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} tokens, r={ratio}, 1 request per GPU",
+                           "recompute_ratio": ratio, "n_ctx": N, "k_sched_first_last": [ks[1], ks[-1]],
+                           "parallelism": f"request-parallel x{world}",
+                           "l2": "inputs larger than L2 (14.5 GB of weights streamed per step)"},
+                "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
+                "cpu_baseline": cpu, "e2e": e2e,
+                "kernel_ms": {k: round(v, 4) for k, v in prof.items()},
+                "work": {k: float(v) for k, v in work.items()}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args):
+    import torch
+    N, L = req.n_ctx, s.n_layers
+    kh = k_in.cpu().pin_memory()
+    vh = v_in.cpu().pin_memory()
+    toks = torch.from_numpy(tok_h).pin_memory()
+    poss = torch.from_numpy(req.global_positions()).pin_memory()
+    hh = torch.empty(ks[-1], s.d_model, dtype=torch.float32).pin_memory()
+    kb, vb = torch.empty_like(k_in), torch.empty_like(v_in)
+    cs = list(req.chunk_starts())
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.api.blend_request(ctx, mw, toks, poss, cs, 0, kh, vh, kb, vb, ks, hh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    h2d = kh.numel() * 2 + vh.numel() * 2 + toks.numel() * 4 + poss.numel() * 4
+    d2h = hh.numel() * 4
+    return {"value": N / (ms / 1e3), "unit": "ctx_tok/s", "ms": ms, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h),
+            "path": "cb_blend_request: pinned host chunk KV + tokens, layer-pipelined H2D on a copy stream, "
+                    "h_out D2H; KV^new stays on the GPU"}
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -162,6 +162,22 @@ CB_API cb_status cb_blend_forward(cb_ctx* ctx, const cb_layer_w* w, const void* 
                            const int32_t* k_sched, const int32_t* force_sel, int32_t* sel_out, float* dev_out,
                            float* h_out, void* stream);
 
+/* ---- end to end from host memory ----------------------------------------------------------------- */
+/* The same blend with the request's inputs in HOST memory (pinned for asynchronous copies), as the
+ * paper's loading path does (fetch_kv -> synchronize -> prefill_layer): layer i's chunk
+ * KV is copied into k_blend/v_blend layer i on the context's copy stream while layer i-1 computes,
+ * and layer i waits only for its own copy (two-stream layer pipelining).
+ * tok_host, pos_host : host int32[N + n_suffix];  k_in_host, v_in_host: host [n_layers][N][n_kv][hd]
+ * k_blend, v_blend   : DEVICE out KV^new [n_layers][N + n_suffix][n_kv][hd] (stays on the GPU for decode)
+ * sel_out_host       : host int32[k_sched[L-1]] (S_{L-1}) or NULL;  h_out_host: host fp32 rows as in
+ *                      cb_blend_forward. Other arguments as cb_blend_forward. Returns after enqueueing;
+ *                      host outputs are valid once `stream` is synchronised. */
+CB_API cb_status cb_blend_request(cb_ctx* ctx, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                                  const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                                  int32_t n_chunks, const void* k_in_host, const void* v_in_host, void* k_blend,
+                                  void* v_blend, const int32_t* k_sched, int32_t* sel_out_host, float* h_out_host,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

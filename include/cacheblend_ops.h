@@ -46,6 +46,13 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */
 CB_API int64_t cb_launch_count(cb_ctx* ctx);
 
+/* Per-launch profile: between begin and end every library launch is bracketed by a CUDA event pair
+ * on its stream. cb_profile_end synchronises the device and writes, per kernel class
+ * (cb_profile_class_name), the summed device milliseconds and the launch count (n_classes entries). */
+CB_API cb_status cb_profile_begin(cb_ctx* ctx);
+CB_API cb_status cb_profile_end(cb_ctx* ctx, double* ms_out, int64_t* counts_out, int32_t n_classes);
+CB_API const char* cb_profile_class_name(int32_t cls);
+
 #ifdef __cplusplus
 }
 #endif

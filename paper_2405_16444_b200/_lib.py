@@ -48,6 +48,11 @@ _SIGS = {
     "cb_op_gemm": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "cb_op_attention": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_vp, c_i32, c_vp]),
     "cb_launch_count": (c_i64, [c_vp]),
+    "cb_blend_request": (c_i32, [c_vp, ctypes.POINTER(CbLayerW), c_vp, c_vp, c_vp, c_i32, c_i32, c_i32p, c_i32,
+                                 c_vp, c_vp, c_vp, c_vp, c_i32p, c_vp, c_vp, c_vp]),
+    "cb_profile_begin": (c_i32, [c_vp]),
+    "cb_profile_end": (c_i32, [c_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
+    "cb_profile_class_name": (ctypes.c_char_p, [c_i32]),
 }
 
 EXPORTED = tuple(_SIGS)

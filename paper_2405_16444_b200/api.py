@@ -199,6 +199,29 @@ def blend_forward(ctx: Context, weights: ModelWeights, tok: torch.Tensor, pos: t
     return h_out[:rows]
 
 
+def blend_request(ctx: Context, weights: ModelWeights, tok_host: torch.Tensor, pos_host: torch.Tensor,
+                  chunk_start: Sequence[int], n_suffix: int, k_in_host: torch.Tensor, v_in_host: torch.Tensor,
+                  k_blend: torch.Tensor, v_blend: torch.Tensor, k_sched: Sequence[int], h_out_host: torch.Tensor,
+                  sel_out_host: Optional[torch.Tensor] = None, stream=None):
+    """cb_blend_request: inputs in (pinned) host memory, KV^new on the device, h_out back in host memory."""
+    N = int(chunk_start[-1])
+    check(lib().cb_blend_request(ctx.handle, weights.cw, _p(weights.embed), _p(tok_host), _p(pos_host), N, n_suffix,
+                                 _i32(chunk_start), len(chunk_start) - 1, _p(k_in_host), _p(v_in_host), _p(k_blend),
+                                 _p(v_blend), _i32(k_sched), _p(sel_out_host), _p(h_out_host), _stream(stream)))
+
+
+def profile_steps(ctx: Context, step, n: int) -> Dict[str, float]:
+    """Runs `step` n times with per-launch CUDA events; returns device ms per step for each kernel class."""
+    N_CLS = 9
+    check(lib().cb_profile_begin(ctx.handle))
+    for _ in range(n):
+        step()
+    ms = (ctypes.c_double * N_CLS)()
+    cnt = (ctypes.c_int64 * N_CLS)()
+    check(lib().cb_profile_end(ctx.handle, ms, cnt, N_CLS))
+    return {lib().cb_profile_class_name(i).decode(): ms[i] / n for i in range(N_CLS) if cnt[i]}
+
+
 def op_gemm(ctx: Context, A: torch.Tensor, B: torch.Tensor, out_f32: bool = False, impl: int = 0, stream=None):
     M, K = A.shape
     N = B.shape[0]

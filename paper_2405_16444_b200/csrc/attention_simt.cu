@@ -82,6 +82,7 @@ cb_status launch_attention_simt(cb_ctx* c, const void* q, const int* q_row, cons
                                 const void* k, const void* v, int n_keys, void* out, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
   CB_REQUIRE(c->m.head_dim <= 256, CB_E_UNSUPPORTED, "attention: head_dim > 256");
+  ProfScope ps_(c, PROF_ATTN, s);
   if (c->m.dtype == CB_BF16)
     launch_t<bf16>(c->m, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
   else

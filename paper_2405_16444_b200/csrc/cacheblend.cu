@@ -37,6 +37,61 @@ void cb_set_error(const char* fmt, ...) {
 
 extern "C" const char* cb_last_error(void) { return g_err; }
 
+// ---- per-launch profile ---------------------------------------------------------------------------
+static cudaEvent_t pool_event(cb_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+ProfScope::ProfScope(cb_ctx* c_, int cls, cudaStream_t s_) : c(c_), s(s_), idx(-1) {
+  if (!c || !c->prof_on) return;
+  ProfRec r{cls, pool_event(c), pool_event(c)};
+  cudaEventRecord(r.a, s);
+  c->prof.push_back(r);
+  idx = (int)c->prof.size() - 1;
+}
+
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(c->prof[idx].b, s);
+}
+
+static const char* kProfNames[PROF_N] = {"realign", "embed", "rmsnorm", "gemm", "deviation", "topk", "scatter",
+                                         "attention", "misc"};
+
+extern "C" const char* cb_profile_class_name(int32_t cls) {
+  return (cls >= 0 && cls < PROF_N) ? kProfNames[cls] : "";
+}
+
+extern "C" cb_status cb_profile_begin(cb_ctx* c) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  for (auto& r : c->prof) { c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b); }
+  c->prof.clear();
+  c->prof_on = true;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_profile_end(cb_ctx* c, double* ms, int64_t* counts, int32_t n) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  c->prof_on = false;
+  CB_CUDA(cudaDeviceSynchronize());
+  for (int i = 0; i < n; ++i) { if (ms) ms[i] = 0.0; if (counts) counts[i] = 0; }
+  for (auto& r : c->prof) {
+    float t = 0.f;
+    CB_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.cls < n) {
+      if (ms) ms[r.cls] += t;
+      if (counts) counts[r.cls] += 1;
+    }
+  }
+  return CB_OK;
+}
+
 // ---- dispatch -------------------------------------------------------------------------------------
 cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
                       int impl, cudaStream_t s) {
@@ -111,6 +166,8 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->qrow = cv.take<int>((size_t)T * 4);
   o->iota = cv.take<int>((size_t)T * 4);
   o->src_pos = cv.take<int>((size_t)T * 4);
+  o->tok_d = cv.take<int>((size_t)T * 4);
+  o->pos_d = cv.take<int>((size_t)T * 4);
   return cv.off + kAlign;
 }
 
@@ -140,8 +197,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   const size_t need = carve(nullptr, model, max_tokens, nullptr);
   CB_REQUIRE(workspace == nullptr || workspace_bytes >= need, CB_E_WORKSPACE,
              "workspace too small: %zu < %zu bytes", workspace_bytes, need);
-  cb_ctx* c = new cb_ctx();
-  std::memset(c, 0, sizeof(*c));
+  cb_ctx* c = new cb_ctx();  // value-initialised: pointers null, counters zero
   c->m = *model;
   c->max_tokens = max_tokens;
   cudaError_t e = cudaGetDevice(&c->device);
@@ -194,6 +250,11 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   iota_kernel<<<std::min(1024, (max_tokens + 255) / 256), 256>>>(c->iota, max_tokens);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+  if ((e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+  c->layer_ev.resize(model->n_layers + 1);
+  for (auto& ev : c->layer_ev)
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   cb_status st = topk_init_attrs();
   if (st == CB_OK) st = gemm_tc_init(c);
   if (st == CB_OK) st = attention_tc_init();
@@ -210,6 +271,12 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
 
 extern "C" cb_status cb_destroy(cb_ctx* c) {
   if (!c) return CB_OK;
+  cudaDeviceSynchronize();
+  for (auto& r : c->prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto ev : c->ev_pool) cudaEventDestroy(ev);
+  for (auto ev : c->layer_ev) if (ev) cudaEventDestroy(ev);
+  if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   gemm_tc_destroy(c);
   cudaFree(c->rope_tab);
   cudaFree(c->err_word);
@@ -425,6 +492,7 @@ extern "C" cb_status cb_blend_layer(cb_ctx* c, int32_t layer, const cb_layer_w* 
   cudaStream_t s = (cudaStream_t)st;
   const int rows = n_cand + n_suffix;
   if (rows > 0) {
+    ProfScope ps_(c, PROF_MISC, s);
     make_rows_kernel<<<std::min(256, (rows + 255) / 256), 256, 0, s>>>(cand_tok, n_cand, n_suffix, N, c->row_tok[0]);
     CB_LAUNCHED(c);
   }
@@ -447,14 +515,12 @@ extern "C" cb_status cb_blend_layer(cb_ctx* c, int32_t layer, const cb_layer_w* 
 }
 
 // ---- the whole blend -------------------------------------------------------------------------------
-extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok,
-                                      const int32_t* pos, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
-                                      int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend,
-                                      void* v_blend, const int32_t* k_sched, const int32_t* force_sel,
-                                      int32_t* sel_out, float* dev_out, float* h_out, void* st) {
+namespace {
+cb_status check_forward(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok, const int32_t* pos,
+                        int32_t N, int32_t n_suffix, const int32_t* chunk_start, int32_t n_chunks, const void* k_in,
+                        const void* v_in, void* k_blend, void* v_blend, const int32_t* k_sched, const void* h_out) {
   CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
-  const cb_model& m = c->m;
-  const int L = m.n_layers;
+  const int L = c->m.n_layers;
   CB_REQUIRE(w != nullptr && k_sched != nullptr, CB_E_INVALID_ARG, "w / k_sched is NULL");
   for (int i = 0; i < L; ++i) CB_TRY(check_weights(&w[i]));
   CB_REQUIRE(N >= 0 && n_suffix >= 0 && N + n_suffix >= 1, CB_E_INVALID_ARG, "empty input (N=%d, n_suffix=%d)", N,
@@ -465,41 +531,46 @@ extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void
   CB_REQUIRE(N == 0 || (k_in && v_in && chunk_start && n_chunks >= 1), CB_E_INVALID_ARG,
              "chunk caches / chunk_start missing");
   if (N > 0) {
-    CB_REQUIRE(chunk_start[0] == 0 && chunk_start[n_chunks] == N, CB_E_SHAPE,
-               "chunk_start must run from 0 to N=%d", N);
+    CB_REQUIRE(chunk_start[0] == 0 && chunk_start[n_chunks] == N, CB_E_SHAPE, "chunk_start must run from 0 to N=%d",
+               N);
     for (int ci = 0; ci < n_chunks; ++ci)
       CB_REQUIRE(chunk_start[ci + 1] >= chunk_start[ci], CB_E_SHAPE, "chunk_start not non-decreasing");
   }
   for (int i = 1; i < L; ++i)
     CB_REQUIRE(k_sched[i] >= 0 && k_sched[i] <= (i == 1 ? N : k_sched[i - 1]), CB_E_INVALID_ARG,
                "k_sched must satisfy 0 <= k_i <= k_{i-1} <= N (layer %d: %d)", i, k_sched[i]);
-  const bool k_inplace = (k_blend == k_in), v_inplace = (v_blend == v_in);
-  CB_REQUIRE((!k_inplace && !v_inplace) || n_suffix == 0, CB_E_INVALID_ARG,
-             "in-place blend (k_blend == k_in) requires n_suffix == 0");
-  CB_REQUIRE(k_inplace == v_inplace, CB_E_INVALID_ARG, "k and v must both be in place or both out of place");
+  return CB_OK;
+}
 
-  cudaStream_t s = (cudaStream_t)st;
-  const int kvd = m.n_kv_heads * m.head_dim;
+// Layers 0..L-1 of the blend. realign_per_layer: request mode, where layer i's chunk KV lands in
+// k_blend/v_blend on the copy stream (event layer_ev[i]) and is realigned in place right before
+// layer i (fetch_kv / synchronize / prefill_layer); otherwise the realign already ran.
+cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const int* tok, const int* pos, int N,
+                       int n_suffix, void* k_blend, void* v_blend, const int* k_sched, const int* force_sel,
+                       int* sel_out, float* dev_out, float* h_out, cudaStream_t s, bool realign_per_layer) {
+  const cb_model& m = c->m;
+  const int L = m.n_layers, T = N + n_suffix, kvd = m.n_kv_heads * m.head_dim;
   const size_t B = dtype_bytes(m.dtype);
-  const size_t layer_stride = (size_t)T * kvd;  // elements per layer of the blended cache
-
-  // (a1) positional recovery of every layer's cached K (+ carry V over when out of place)
-  if (N > 0) {
-    CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, s));
-    CB_TRY(launch_realign(c, k_blend, k_in, v_inplace ? nullptr : v_blend, v_in, c->src_pos, pos, L, N,
-                          (long long)layer_stride, (long long)N * kvd, s));
-  }
+  const size_t layer_stride = (size_t)T * kvd;
+  auto realign_layer = [&](int i) -> cb_status {
+    if (!realign_per_layer || N == 0) return CB_OK;
+    CB_CUDA(cudaStreamWaitEvent(s, c->layer_ev[i], 0));  // synchronize(): layer i's KV is on the GPU
+    char* kb = (char*)k_blend + (size_t)i * layer_stride * B;
+    return launch_realign(c, kb, kb, nullptr, nullptr, c->src_pos, pos, 1, N, (long long)layer_stride,
+                          (long long)layer_stride, s);
+  };
   // (a2) layer 0 in full
   CB_TRY(launch_embed(c, embed, tok, T, c->h[0], s));
+  CB_TRY(realign_layer(0));
   LayerBufs b0{c->h[0], c->h[1], c->iota, nullptr};
   CB_TRY(layer_full(c, w[0], b0, N, n_suffix, k_blend, v_blend, pos, s));
   if (sel_out) CB_TRY(launch_sel_out(c, c->iota, N, N, sel_out, s));
   // (a3-a8) layers 1..L-1 with gradual filtering: C_1 = all context tokens, C_{i+1} = S_i
-  int cur = 1, n_cand = N;
+  int cur = 1, n_cand = N, rt = 0;
   const int* rows = c->iota;
-  int rt = 0;
   for (int i = 1; i < L; ++i) {
     const int k = k_sched[i];
+    CB_TRY(realign_layer(i));
     LayerBufs b{c->h[cur], c->h[cur ^ 1], rows, c->row_tok[rt]};
     char* kb = (char*)k_blend + (size_t)i * layer_stride * B;
     char* vb = (char*)v_blend + (size_t)i * layer_stride * B;
@@ -513,7 +584,68 @@ extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void
   }
   const int final_rows = (L == 1 ? N : n_cand) + n_suffix;
   if (final_rows > 0)
-    CB_CUDA(cudaMemcpyAsync(h_out, c->h[cur], (size_t)final_rows * m.d_model * sizeof(float),
-                            cudaMemcpyDeviceToDevice, s));
+    CB_CUDA(cudaMemcpyAsync(h_out, c->h[cur], (size_t)final_rows * m.d_model * sizeof(float), cudaMemcpyDefault, s));
+  return CB_OK;
+}
+}  // namespace
+
+extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok,
+                                      const int32_t* pos, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                                      int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend,
+                                      void* v_blend, const int32_t* k_sched, const int32_t* force_sel,
+                                      int32_t* sel_out, float* dev_out, float* h_out, void* st) {
+  CB_TRY(check_forward(c, w, embed, tok, pos, N, n_suffix, chunk_start, n_chunks, k_in, v_in, k_blend, v_blend,
+                       k_sched, h_out));
+  const bool k_inplace = (k_blend == k_in), v_inplace = (v_blend == v_in);
+  CB_REQUIRE((!k_inplace && !v_inplace) || n_suffix == 0, CB_E_INVALID_ARG,
+             "in-place blend (k_blend == k_in) requires n_suffix == 0");
+  CB_REQUIRE(k_inplace == v_inplace, CB_E_INVALID_ARG, "k and v must both be in place or both out of place");
+  cudaStream_t s = (cudaStream_t)st;
+  const cb_model& m = c->m;
+  const int T = N + n_suffix, kvd = m.n_kv_heads * m.head_dim;
+  // (a1) positional recovery of every layer's cached K in one launch (+ carry V over when out of place)
+  if (N > 0) {
+    CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, s));
+    CB_TRY(launch_realign(c, k_blend, k_in, v_inplace ? nullptr : v_blend, v_in, c->src_pos, pos, m.n_layers, N,
+                          (long long)T * kvd, (long long)N * kvd, s));
+  }
+  return blend_layers(c, w, embed, tok, pos, N, n_suffix, k_blend, v_blend, k_sched, force_sel, sel_out, dev_out,
+                      h_out, s, false);
+}
+
+extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                                      const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                                      int32_t n_chunks, const void* k_in_host, const void* v_in_host, void* k_blend,
+                                      void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,
+                                      float* h_out_host, void* st) {
+  CB_TRY(check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in_host, v_in_host,
+                       k_blend, v_blend, k_sched, h_out_host));
+  cudaStream_t s = (cudaStream_t)st, cs = c->copy_stream;
+  const cb_model& m = c->m;
+  const int L = m.n_layers, T = N + n_suffix, kvd = m.n_kv_heads * m.head_dim;
+  const size_t B = dtype_bytes(m.dtype);
+  // the copy stream may only overwrite k_blend / tok / pos once the compute stream is done with them
+  CB_CUDA(cudaEventRecord(c->ev_ready, s));
+  CB_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
+  CB_CUDA(cudaMemcpyAsync(c->tok_d, tok_host, (size_t)T * 4, cudaMemcpyHostToDevice, cs));
+  CB_CUDA(cudaMemcpyAsync(c->pos_d, pos_host, (size_t)T * 4, cudaMemcpyHostToDevice, cs));
+  CB_CUDA(cudaEventRecord(c->layer_ev[L], cs));
+  // fetch_kv(layer i) for every layer, in layer order on the copy stream
+  for (int i = 0; i < L && N > 0; ++i) {
+    const size_t row = (size_t)kvd * B;
+    CB_CUDA(cudaMemcpy2DAsync((char*)k_blend + (size_t)i * T * row, row * T, (const char*)k_in_host + (size_t)i * N * row,
+                              row * N, row * N, 1, cudaMemcpyHostToDevice, cs));
+    CB_CUDA(cudaMemcpy2DAsync((char*)v_blend + (size_t)i * T * row, row * T, (const char*)v_in_host + (size_t)i * N * row,
+                              row * N, row * N, 1, cudaMemcpyHostToDevice, cs));
+    CB_CUDA(cudaEventRecord(c->layer_ev[i], cs));
+  }
+  CB_CUDA(cudaStreamWaitEvent(s, c->layer_ev[L], 0));
+  if (N > 0) CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, s));
+  const int final_rows = (L == 1 ? N : k_sched[L - 1]) + n_suffix;
+  CB_TRY(blend_layers(c, w, embed, c->tok_d, c->pos_d, N, n_suffix, k_blend, v_blend, k_sched, nullptr, nullptr,
+                      nullptr, h_out_host, s, true));
+  if (sel_out_host && L > 1 && final_rows - n_suffix > 0)
+    CB_CUDA(cudaMemcpyAsync(sel_out_host, c->row_tok[(L - 2) & 1], (size_t)(final_rows - n_suffix) * 4,
+                            cudaMemcpyDeviceToHost, s));
   return CB_OK;
 }

@@ -7,7 +7,20 @@
 
 #include "common.cuh"
 
+#include <vector>
+
 struct TmapCache;  // tcgen05 GEMM tensor-map cache (gemm_tc.cu)
+
+// Kernel classes for the per-launch profile (bench roofline: CUDA events on the launching stream).
+enum ProfClass : int {
+  PROF_REALIGN = 0, PROF_EMBED, PROF_RMSNORM, PROF_GEMM, PROF_DEVIATION, PROF_TOPK, PROF_SCATTER, PROF_ATTN,
+  PROF_MISC, PROF_N
+};
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
 
 struct cb_ctx {
   cb_model m;
@@ -33,8 +46,27 @@ struct cb_ctx {
   int* qrow;        // [T] row (in the current compact buffers) of each kept query
   int* iota;        // [T] 0..T-1
   int* src_pos;     // [T] chunk-local positions (blend_forward)
+  int* tok_d;       // [T] request-mode device copies of tokens / positions
+  int* pos_d;       // [T]
   long long launches;
   TmapCache* tmaps;
+  // request mode: copy stream + per-layer "layer KV landed" events (P:2509 fetch/synchronize)
+  cudaStream_t copy_stream;
+  cudaEvent_t ev_ready;
+  std::vector<cudaEvent_t> layer_ev;
+  // profiling
+  bool prof_on;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+};
+
+// Records an event pair around the launches in its scope when the context is profiling.
+struct ProfScope {
+  cb_ctx* c;
+  cudaStream_t s;
+  int idx;
+  ProfScope(cb_ctx* c_, int cls, cudaStream_t s_);
+  ~ProfScope();
 };
 
 void cb_set_error(const char* fmt, ...);

@@ -76,6 +76,7 @@ cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out,
   const int V = 16 / (int)dtype_bytes(c->m.dtype);
   const long long total = (long long)n_tok * (kvd / V);
   const int grid = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c->num_sms * 8));
+  ProfScope ps_(c, PROF_REALIGN, s);
   if (c->m.dtype == CB_BF16)
     realign_kernel<bf16, 4><<<grid, 256, 0, s>>>((bf16*)k_out, (const bf16*)k_src, (bf16*)v_out, (const bf16*)v_src,
                                                  src_pos, dst_pos, n_slices, n_tok, out_stride, src_stride, kvd,
@@ -106,6 +107,7 @@ __global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ 
 
 cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, float* h, cudaStream_t s) {
   if (n == 0) return CB_OK;
+  ProfScope ps_(c, PROF_EMBED, s);
   if (c->m.dtype == CB_BF16)
     embed_kernel<bf16><<<n, 128, 0, s>>>((const bf16*)embed, tok, h, c->m.d_model);
   else
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ 
 
 cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
+  ProfScope ps_(c, PROF_RMSNORM, s);
   if (c->m.dtype == CB_BF16)
     rmsnorm_kernel<bf16><<<n_rows, 256, 0, s>>>(h, gain, (bf16*)x, c->m.d_model, c->m.rms_eps);
   else
@@ -174,6 +177,7 @@ cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int
                             void* kb, void* vb, cudaStream_t s) {
   if (n == 0) return CB_OK;
   const int kvd = c->m.n_kv_heads * c->m.head_dim;
+  ProfScope ps_(c, PROF_SCATTER, s);
   if (c->m.dtype == CB_BF16)
     scatter_kv_kernel<bf16><<<n, 128, 0, s>>>((const bf16*)kf, (const bf16*)vf, qrow, qtok, (bf16*)kb, (bf16*)vb, kvd);
   else
@@ -211,6 +215,7 @@ cb_status launch_local_pos(cb_ctx* c, const int* cs, int n_chunks, int* src_pos,
     for (int i = 0; i <= ct.n; ++i) ct.start[i] = cs[b + i];
     const int len = ct.start[ct.n] - ct.start[0];
     if (len <= 0) continue;
+    ProfScope ps_(c, PROF_MISC, s);
     local_pos_kernel<<<std::min(1024, (len + 255) / 256), 256, 0, s>>>(ct, b, src_pos);
     CB_LAUNCHED(c);
   }
@@ -224,6 +229,7 @@ __global__ void sel_out_kernel(const int* __restrict__ qtok, int k, int N, int* 
 
 cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* row, cudaStream_t s) {
   if (N == 0) return CB_OK;
+  ProfScope ps_(c, PROF_MISC, s);
   sel_out_kernel<<<std::min(256, (N + 255) / 256), 256, 0, s>>>(qtok, k, N, row);
   CB_LAUNCHED(c);
   return CB_OK;

@@ -65,6 +65,7 @@ cb_status launch_gemm_simt(cb_ctx* c, const void* A, int lda, const void* B, int
   if (M == 0 || e.N == 0) return CB_OK;
   dim3 grid((e.N + BN - 1) / BN, (M + BM - 1) / BM);
   const bool sw = e.kind == EPI_SWIGLU;
+  ProfScope ps_(c, PROF_GEMM, s);
   if (c->m.dtype == CB_BF16) {
     if (sw) gemm_simt_kernel<bf16, true><<<grid, 256, 0, s>>>((const bf16*)A, lda, (const bf16*)B, ldb, M, K, e);
     else gemm_simt_kernel<bf16, false><<<grid, 256, 0, s>>>((const bf16*)A, lda, (const bf16*)B, ldb, M, K, e);

@@ -41,6 +41,7 @@ cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, cons
                            const int* cand_tok, int n_cand, int dev_mode, float* dev, cudaStream_t s) {
   if (n_cand == 0) return CB_OK;
   const int grid = (n_cand + 7) / 8;
+  ProfScope ps_(c, PROF_DEVIATION, s);
   if (c->m.dtype == CB_BF16)
     deviation_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)k_new, (const bf16*)v_new, (const bf16*)k_ref,
                                                 (const bf16*)v_ref, cand_tok, n_cand, c->m.n_kv_heads,
@@ -211,6 +212,7 @@ cb_status launch_topk(cb_ctx* c, const float* dev, const int* cand_tok, int n_ca
   CB_REQUIRE(n_cand <= TOPK_MAX_CAND, CB_E_SHAPE, "top-k: n_cand %d exceeds %d", n_cand, TOPK_MAX_CAND);
   if (k_keep + n_suffix == 0) return CB_OK;
   const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
+  ProfScope ps_(c, PROF_TOPK, s);
   topk_kernel<<<1, TOPK_THREADS, smem, s>>>(dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
                                             c->err_word);
   CB_LAUNCHED(c);

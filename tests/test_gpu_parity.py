@@ -262,3 +262,26 @@ def test_force_sel_not_candidate_is_reported(P):
     bad = [None, np.arange(ks[1]), np.arange(ks[2]) + 40]     # layer-2 set not inside S_1
     with pytest.raises(P.CacheBlendError):
         run_blend(P, s, "f32", 1, req, tok, pos, cs, Kc, Vc, ks, force_sel=bad)
+
+
+@pytest.mark.parametrize("name,dtype,n_suf", [("tiny", "f32", 0), ("tiny", "f32", 6), ("small", "bf16", 9)])
+def test_blend_request_equals_forward(P, name, dtype, n_suf):
+    """cb_blend_request (host inputs, layer-pipelined copies) produces exactly cb_blend_forward's result."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case(name, 4, [40, 57, 31], n_suf, dtype, 0.2)
+    a = run_blend(P, s, dtype, 4, req, tok, pos, cs, Kc, Vc, ks)
+    td = P.api.TORCH_DTYPES[dtype]
+    kh = torch.from_numpy(np.ascontiguousarray(Kc)).to(td).pin_memory()
+    vh = torch.from_numpy(np.ascontiguousarray(Vc)).to(td).pin_memory()
+    T = req.n_total
+    kb = torch.empty(s.n_layers, T, s.n_kv_heads, s.head_dim, dtype=td, device=DEV)
+    vb = torch.empty_like(kb)
+    hh = torch.empty(ks[-1] + n_suf, s.d_model, dtype=torch.float32).pin_memory()
+    sel = torch.empty(max(ks[-1], 1), dtype=torch.int32).pin_memory()
+    P.api.blend_request(a["ctx"], a["mw"], torch.from_numpy(tok.astype(np.int32)).pin_memory(),
+                        torch.from_numpy(pos.astype(np.int32)).pin_memory(), list(cs), n_suf, kh, vh, kb, vb, ks, hh,
+                        sel_out_host=sel)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(np32(kb), a["K"])
+    np.testing.assert_array_equal(np32(vb), a["V"])
+    np.testing.assert_array_equal(hh.numpy(), a["h"])
+    np.testing.assert_array_equal(sel.numpy()[:ks[-1]], a["sel"][-1])
