@@ -114,6 +114,21 @@ def test_gemm_simt(P, dtype, M, N, K):
     assert rel_err(np32(C), ref.cpu().numpy()) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 256, 64), (100, 512, 200), (128, 256, 4096), (553, 6144, 4096),
+                                   (300, 48, 1024), (3072, 4096, 4096), (369, 4096, 14336), (129, 1040, 136)])
+def test_gemm_tcgen05(P, M, N, K):
+    """tcgen05/TMEM/TMA GEMM against an fp64 torch matmul of the same bf16 operands (ragged M, N, K tails)."""
+    ctx = P.Context(shape("small"), "bf16", max_tokens=8)
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)
+    C = P.api.op_gemm(ctx, A, B, out_f32=True, impl=2)
+    ref = (A.double() @ B.double().T).cpu().numpy()
+    assert rel_err(np32(C), ref) < 5e-5   # tensor-core fp32 accumulation over K up to 14336
+    Cb = P.api.op_gemm(ctx, A, B, out_f32=False, impl=2)
+    assert rel_err(np32(Cb), ref) < 5e-3
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("name", ["tiny", "small"])
 def test_attention_parity(P, dtype, name):
