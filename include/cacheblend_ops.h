@@ -43,6 +43,12 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
                           int32_t n_rows, const void* k, const void* v, int32_t n_keys, void* out, int32_t impl,
                           void* stream);
 
+/* Tuning knobs (for experiments; defaults are the tuned choices). Unknown names -> INVALID_ARG.
+ *   "gemm_sched"  0 = auto (cost model picks data-parallel or data-parallel + stream-K tail),
+ *                 1 = data-parallel only, 2 = data-parallel rounds + stream-K tail
+ *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width */
+CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
+
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */
 CB_API int64_t cb_launch_count(cb_ctx* ctx);
 

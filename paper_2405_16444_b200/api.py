@@ -67,6 +67,9 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().cb_launch_count(self.handle))
 
+    def set_option(self, name: str, value: int):
+        check(lib().cb_set_option(self.handle, name.encode(), int(value)))
+
 
 class ModelWeights:
     """Device weights in the C-ABI layouts (cacheblend.h cb_layer_w)."""

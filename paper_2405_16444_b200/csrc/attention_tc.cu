@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
                                                       const int* __restrict__ q_tok, int n_rows,
                                                       const bf16* __restrict__ k, const bf16* __restrict__ v,
                                                       int n_keys, bf16* __restrict__ out, int n_q, int n_kv,
-                                                      float scale_log2) {
+                                                      float scale_log2, int kt_per_split, float* __restrict__ opart,
+                                                      float2* __restrict__ ml) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(sm);
   const uint32_t sK0 = sQ + BR * HD * 2;  // K[2], then V[2]
@@ -67,6 +68,16 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
     kmin = min(kmin, t);
   }
   const int n_kt = (kmax + BC) / BC;
+  // split-KV: this CTA covers key tiles [j_begin, j_end) (split = blockIdx.z)
+  const int split = blockIdx.z;
+  const int j_begin = split * kt_per_split, j_end = min(n_kt, j_begin + kt_per_split);
+  const size_t part_row0 = ((size_t)split * n_kv + g) * R;  // partial rows of (split, g)
+  if (j_begin >= j_end) {  // no keys for this split: neutral partial (m = -inf, l = 0)
+    if (opart != nullptr)
+      for (int i = tid; i < BR; i += NT)
+        if (rho0 + i < R) ml[part_row0 + rho0 + i] = make_float2(-INFINITY, 0.f);
+    return;
+  }
 
   // ---- stage Q (64 rows x 128) ----
   for (int i = tid; i < BR * 16; i += NT) {
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
       cp_async16(dv + swz(row, ch), v + off, ok);
     }
   };
-  load_kv(0, 0);
+  load_kv(j_begin, 0);
   cp_commit();
 
   // per-thread rows (within the warp's 16): lane/4 and lane/4 + 8
@@ -102,13 +113,13 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   uint32_t qa[8][4];
 
-  for (int j = 0; j < n_kt; ++j) {
-    const int buf = j & 1;
-    if (j + 1 < n_kt) load_kv(j + 1, buf ^ 1);
+  for (int j = j_begin; j < j_end; ++j) {
+    const int buf = (j - j_begin) & 1;
+    if (j + 1 < j_end) load_kv(j + 1, buf ^ 1);
     cp_commit();
     cp_wait<1>();
     __syncthreads();
-    if (j == 0) {  // Q fragments once
+    if (j == j_begin) {  // Q fragments once
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const int row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8, ch = kk * 2 + (lane >> 4);
@@ -152,8 +163,12 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
     for (int hr = 0; hr < 2; ++hr) {
       mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 1));
       mx[hr] = fmaxf(mx[hr], __shfl_xor_sync(0xffffffffu, mx[hr], 2));
-      corr[hr] = exp2f(m_i[hr] - mx[hr]);  // m_i = -inf on the first tile -> 0
+      const float m_old = m_i[hr];
       m_i[hr] = mx[hr];
+      // a row with no visible key yet (split-KV) keeps m = -inf: use 0 as the exponent reference
+      const float mref = (mx[hr] == -INFINITY) ? 0.f : mx[hr];
+      corr[hr] = exp2f(m_old - mref);  // m_old = -inf -> 0
+      mx[hr] = mref;
     }
     uint32_t pa[4][4];
 #pragma unroll
@@ -192,6 +207,19 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
   }
   cp_wait<0>();
 
+  if (opart != nullptr) {  // split-KV: unnormalised fp32 partial + (m, l) per row
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      const int rho = rho0 + warp * 16 + (lane >> 2) + hr * 8;
+      if (rho >= R) continue;
+      float* dst = opart + (part_row0 + rho) * HD + (lane & 3) * 2;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt)
+        *reinterpret_cast<float2*>(dst + nt * 8) = make_float2(o[nt][2 * hr], o[nt][2 * hr + 1]);
+      if ((lane & 3) == 0) ml[part_row0 + rho] = make_float2(m_i[hr], l_i[hr]);
+    }
+    return;
+  }
   // ---- normalise and store ----
 #pragma unroll
   for (int hr = 0; hr < 2; ++hr) {
@@ -205,6 +233,33 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
       *reinterpret_cast<uint32_t*>(dst + nt * 8) = pack2(o[nt][2 * hr] * inv, o[nt][2 * hr + 1] * inv);
   }
 }
+
+// Combine split-KV partials of one (query row, q head) per warp, splits in fixed order:
+// m* = max m_s, l* = sum l_s 2^(m_s - m*), O = sum O_s 2^(m_s - m*) / l*.
+__global__ void attn_merge_kernel(const float* __restrict__ opart, const float2* __restrict__ ml, int R, int n_kv,
+                                  int G, int n_splits, bf16* __restrict__ out, int qd) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= R * n_kv) return;
+  const int g = w / R, rho = w - g * R;
+  float mstar = -INFINITY;
+  for (int s = 0; s < n_splits; ++s) mstar = fmaxf(mstar, ml[((size_t)s * n_kv + g) * R + rho].x);
+  float l = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < n_splits; ++s) {
+    const size_t pr = ((size_t)s * n_kv + g) * R + rho;
+    const float2 m_l = ml[pr];
+    if (m_l.x == -INFINITY) continue;
+    const float f = exp2f(m_l.x - mstar);
+    l += m_l.y * f;
+    const float4 o = reinterpret_cast<const float4*>(opart + pr * HD)[lane];
+    acc.x += o.x * f; acc.y += o.y * f; acc.z += o.z * f; acc.w += o.w * f;
+  }
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  const int r = rho / G, h = g * G + rho % G;
+  bf16* dst = out + (size_t)r * qd + h * HD + lane * 4;
+  reinterpret_cast<uint32_t*>(dst)[0] = pack2(acc.x * inv, acc.y * inv);
+  reinterpret_cast<uint32_t*>(dst)[1] = pack2(acc.z * inv, acc.w * inv);
+}
 }  // namespace
 
 bool attention_tc_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.head_dim == HD; }
@@ -212,14 +267,34 @@ bool attention_tc_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.hea
 cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                               const void* v, int n_keys, void* out, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
-  const int G = c->m.n_q_heads / c->m.n_kv_heads;
-  const int tiles = (n_rows * G + BR - 1) / BR;
+  const int n_kv = c->m.n_kv_heads, G = c->m.n_q_heads / n_kv;
+  const int R = n_rows * G;
+  const int tiles = (R + BR - 1) / BR;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
-  dim3 grid(tiles, c->m.n_kv_heads);
+  // split-KV when the (tile, kv head) grid is too small or too unbalanced to fill the SMs (later layers:
+  // a few hundred selected queries, some of them at the end of a long context)
+  const int max_kt = (n_keys + BC - 1) / BC;
+  const long long base = (long long)tiles * n_kv;
+  int n_splits = 1;
+  if (base < 4LL * c->num_sms && c->attn_part != nullptr) {
+    n_splits = (int)std::min<long long>((6LL * c->num_sms + base - 1) / base, (max_kt + 3) / 4);
+    n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
+    n_splits = std::max(1, n_splits);
+  }
+  const int kt_per_split = (max_kt + n_splits - 1) / n_splits;
+  dim3 grid(tiles, n_kv, n_splits);
   ProfScope ps_(c, PROF_ATTN, s);
+  float* opart = n_splits > 1 ? c->attn_part : nullptr;
   attn_mma_kernel<<<grid, NT, SMEM, s>>>((const bf16*)q, q_row, q_tok, n_rows, (const bf16*)k, (const bf16*)v, n_keys,
-                                         (bf16*)out, c->m.n_q_heads, c->m.n_kv_heads, scale_log2);
+                                         (bf16*)out, c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart,
+                                         c->attn_ml);
   CB_LAUNCHED(c);
+  if (n_splits > 1) {
+    const int warps = R * n_kv;
+    attn_merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(c->attn_part, c->attn_ml, R, n_kv, G, n_splits, (bf16*)out,
+                                                      c->m.n_q_heads * HD);
+    CB_LAUNCHED(c);
+  }
   return CB_OK;
 }
 

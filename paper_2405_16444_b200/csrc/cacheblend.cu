@@ -23,6 +23,7 @@ bool attention_tc_ok(const cb_ctx* c);
 cb_status topk_init_attrs();
 cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
+void gemm_tc_force_bn(cb_ctx* c, int bn);
 cb_status attention_tc_init();
 
 // ---- error reporting ------------------------------------------------------------------------------
@@ -168,6 +169,10 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->src_pos = cv.take<int>((size_t)T * 4);
   o->tok_d = cv.take<int>((size_t)T * 4);
   o->pos_d = cv.take<int>((size_t)T * 4);
+  // split-KV attention partials: room for every (row, q head) twice
+  o->attn_part_rows = 2LL * T * m->n_q_heads;
+  o->attn_part = cv.take<float>((size_t)o->attn_part_rows * m->head_dim * 4);
+  o->attn_ml = cv.take<float2>((size_t)o->attn_part_rows * 8);
   return cv.off + kAlign;
 }
 
@@ -296,6 +301,22 @@ extern "C" cb_status cb_check_device_errors(cb_ctx* c) {
 }
 
 extern "C" int64_t cb_launch_count(cb_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
+  CB_REQUIRE(c != nullptr && name != nullptr, CB_E_INVALID_ARG, "ctx / name is NULL");
+  if (std::strcmp(name, "gemm_sched") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_sched must be 0, 1 or 2");
+    c->gemm_sched = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_bn") == 0) {
+    CB_REQUIRE(value == 0 || value == 128 || value == 256, CB_E_INVALID_ARG, "gemm_bn must be 0, 128 or 256");
+    gemm_tc_force_bn(c, (int)value);
+    return CB_OK;
+  }
+  cb_set_error("unknown option '%s'", name);
+  return CB_E_INVALID_ARG;
+}
 
 // ---- schedule (host) ----------------------------------------------------------------------------
 extern "C" cb_status cb_schedule(double ratio, int32_t n_ctx, int32_t n_layers, int32_t* k) {

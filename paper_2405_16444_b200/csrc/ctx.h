@@ -46,6 +46,10 @@ struct cb_ctx {
   int* qrow;        // [T] row (in the current compact buffers) of each kept query
   int* iota;        // [T] 0..T-1
   int* src_pos;     // [T] chunk-local positions (blend_forward)
+  float* attn_part;     // split-KV attention partials [attn_part_rows][head_dim] fp32
+  float2* attn_ml;      // [attn_part_rows] (m, l)
+  long long attn_part_rows;
+  int gemm_sched;   // cb_set_option("gemm_sched")
   int* tok_d;       // [T] request-mode device copies of tokens / positions
   int* pos_d;       // [T]
   long long launches;

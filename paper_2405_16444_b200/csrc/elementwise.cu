@@ -119,42 +119,47 @@ cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, floa
 // ---------------------------------------------------------------------------------------------
 // RMSNorm: x = h / sqrt(mean(h^2) + eps) * gain  (fixed-order block reduction: deterministic)
 // ---------------------------------------------------------------------------------------------
+// One warp per row: 16-byte loads, a fixed-order warp reduction (deterministic), second pass from L1.
+__device__ __forceinline__ void store4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void store4(bf16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 w;
+  w.x = *reinterpret_cast<uint32_t*>(&lo);
+  w.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = w;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
-                                                      T* __restrict__ x, int d, float eps) {
-  const int r = blockIdx.x;
+                                                      T* __restrict__ x, int n_rows, int d, float eps) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= n_rows) return;
   const float* hr = h + (size_t)r * d;
-  __shared__ float red[8];
   float ss = 0.f;
-  for (int e = threadIdx.x * 4; e < d; e += blockDim.x * 4) {
+  for (int e = lane * 4; e < d; e += 128) {
     const float4 v = *reinterpret_cast<const float4*>(hr + e);
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  float tot = 0.f;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) tot += red[w];
-  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+  const float inv = 1.0f / sqrtf(ss / (float)d + eps);
   T* xr = x + (size_t)r * d;
-  for (int e = threadIdx.x * 4; e < d; e += blockDim.x * 4) {
+  for (int e = lane * 4; e < d; e += 128) {
     const float4 v = *reinterpret_cast<const float4*>(hr + e);
     const float4 gg = __ldg(reinterpret_cast<const float4*>(g + e));
-    xr[e + 0] = from_f<T>(v.x * inv * gg.x);
-    xr[e + 1] = from_f<T>(v.y * inv * gg.y);
-    xr[e + 2] = from_f<T>(v.z * inv * gg.z);
-    xr[e + 3] = from_f<T>(v.w * inv * gg.w);
+    store4(xr + e, v.x * inv * gg.x, v.y * inv * gg.y, v.z * inv * gg.z, v.w * inv * gg.w);
   }
 }
 
 cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
   ProfScope ps_(c, PROF_RMSNORM, s);
+  const int blocks = (n_rows + 7) / 8;
   if (c->m.dtype == CB_BF16)
-    rmsnorm_kernel<bf16><<<n_rows, 256, 0, s>>>(h, gain, (bf16*)x, c->m.d_model, c->m.rms_eps);
+    rmsnorm_kernel<bf16><<<blocks, 256, 0, s>>>(h, gain, (bf16*)x, n_rows, c->m.d_model, c->m.rms_eps);
   else
-    rmsnorm_kernel<float><<<n_rows, 256, 0, s>>>(h, gain, (float*)x, c->m.d_model, c->m.rms_eps);
+    rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(h, gain, (float*)x, n_rows, c->m.d_model, c->m.rms_eps);
   CB_LAUNCHED(c);
   return CB_OK;
 }

@@ -3,13 +3,20 @@
 //   acc[M][N] = A[M][K] . B[N][K]^T     A = activation rows (K-major), B = weight rows (K-major)
 //
 // Persistent warp-specialised kernel, one CTA per SM:
-//   warp 0      TMA producer: 128x64 A box + 256x64 B box (two 128-row boxes for SwiGLU: gate rows
-//               and the matching up rows) per stage into a 4-stage SWIZZLE_128B ring
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=256, K=16) x 4 per stage,
-//               fp32 accumulator in TMEM, double-buffered (2 x 256 columns)
+//   warp 0      TMA producer: 128x64 A box + BNx64 B box (SwiGLU: two BN/2-row boxes, the gate rows and
+//               the matching up rows) per stage into a SWIZZLE_128B ring (4 stages at BN=256, 6 at 128)
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=BN, K=16) x 4 per stage,
+//               fp32 accumulator in TMEM, double-buffered (2 x BN columns)
 //   warps 2-5   epilogue: tcgen05.ld 32x32b -> registers -> fused epilogue (RoPE / residual gather /
 //               SwiGLU / store) -> global, overlapping the next tile's MMAs
-// Tiles are walked m-fastest so the CTAs working on one weight tile run together (L2 reuse).
+//
+// The blend's GEMMs have M = 370..3072 rows, so the schedule is chosen per launch by a small cost
+// model (host): whole-tile data-parallel rounds at BN = 256 or 128 (the narrower tile doubles the
+// tile count of the N = 4096 projections, which otherwise fill only 48-80 of 148 SMs), or a
+// data-parallel + stream-K hybrid where the tail's (tile, k-block) iterations are split evenly over
+// the CTAs: a CTA ending mid-tile stores its fp32 partial in its own slot and raises a flag; the CTA
+// owning the tile's last k-block adds the partials in fixed CTA order, so results are deterministic.
+// Tiles are walked m-fastest, so CTAs running concurrently share weight tiles in L2.
 #include <cudaTypedefs.h>
 
 #include <unordered_map>
@@ -18,16 +25,26 @@
 #include "tc_common.cuh"
 
 namespace {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NUM_THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BM = 128, BK = 64, NUM_THREADS = 192;
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int MAX_CONTRIB = 16;
+constexpr int MAX_SPLIT = 4;   // stream-K pieces per tile (bounds the fixup fan-in)
+constexpr int MIN_KB = 8;      // minimum k-blocks per stream-K CTA
+constexpr int SLOT_COLS = 256; // partial slot row pitch (floats)
+
+template <int BN> struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __forceinline__ void st_bf16x16(bf16* p, const float (&o)[16]) {
+__device__ __forceinline__ void st_bf16x16(bf16* p, const float* o) {
   uint4 w0, w1;
   w0.x = pack_bf16(o[0], o[1]); w0.y = pack_bf16(o[2], o[3]); w0.z = pack_bf16(o[4], o[5]); w0.w = pack_bf16(o[6], o[7]);
   w1.x = pack_bf16(o[8], o[9]); w1.y = pack_bf16(o[10], o[11]); w1.z = pack_bf16(o[12], o[13]);
@@ -38,7 +55,7 @@ __device__ __forceinline__ void st_bf16x16(bf16* p, const float (&o)[16]) {
 
 // Epilogue for 16 consecutive output columns n..n+15 of row m (all < N; N % 16 == 0).
 template <int KIND>
-__device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const float (&v)[16], const float (&u)[16]) {
+__device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const float* v, const float* u) {
   float o[16];
   if constexpr (KIND == EPI_STORE) {
     st_bf16x16(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + n, v);
@@ -84,57 +101,116 @@ __device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const fl
   }
 }
 
-template <int KIND>
+// Data-parallel rounds followed by an optional stream-K tail; every role walks the identical sequence.
+struct Sched {
+  int tiles, num_kb, G, b, dp_rounds, r;
+  long long sk_base, sk_iters, it, it_end;
+  __device__ void init(int tiles_, int num_kb_, int stream_k) {
+    tiles = tiles_; num_kb = num_kb_; G = gridDim.x; b = blockIdx.x; r = 0;
+    if (!stream_k) {
+      dp_rounds = (tiles + G - 1) / G;
+      sk_base = sk_iters = it = it_end = 0;
+      return;
+    }
+    dp_rounds = (tiles % G == 0) ? tiles / G : max(0, tiles / G - 1);
+    sk_base = (long long)dp_rounds * G * num_kb;
+    sk_iters = (long long)tiles * num_kb - sk_base;
+    it = sk_base + sk_start(b);
+    it_end = sk_base + sk_start(b + 1);
+  }
+  __device__ long long sk_start(int cta) const { return (long long)cta * sk_iters / G; }
+  // Next segment: tile and k-block range [kb0, kb1). The stream-K range is walked backwards, so a
+  // CTA's only non-final piece (the head of its last tile) is computed and published first; its
+  // final pieces then wait only on partials that other CTAs also publish first (no chains).
+  __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (it < it_end) {
+      const long long last = it_end - 1;
+      tile = (int)(last / num_kb);
+      const long long tstart = (long long)tile * num_kb;
+      const long long s = it > tstart ? it : tstart;
+      kb0 = (int)(s - tstart);
+      kb1 = (int)(last - tstart) + 1;
+      it_end = s;
+      return true;
+    }
+    if (r < dp_rounds) {
+      tile = r * G + b;
+      if (tile >= tiles) return false;
+      kb0 = 0; kb1 = num_kb; ++r;
+      return true;
+    }
+    return false;
+  }
+  // CTAs holding the earlier (non-final) pieces of `tile`, ascending; returns the count.
+  __device__ int contributors(int tile, int* out) const {
+    const long long t0 = (long long)tile * num_kb;
+    int n = 0;
+    for (int cb = b - 1; cb >= 0 && n < MAX_CONTRIB; --cb) {
+      out[n++] = cb;
+      if (sk_base + sk_start(cb) <= t0) break;
+    }
+    for (int i = 0; i < n / 2; ++i) { const int t = out[i]; out[i] = out[n - 1 - i]; out[n - 1 - i] = t; }
+    return n;
+  }
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int KIND, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
-                   int m_tiles, int n_tiles, EpiParams e) {
+                   int m_tiles, int n_tiles, EpiParams e, float* __restrict__ part, int* __restrict__ flags,
+                   int stream_k) {
+  using C = Cfg<BN>;
   constexpr bool SW = (KIND == EPI_SWIGLU);
   constexpr int OUT_N = SW ? BN / 2 : BN;  // output columns per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles_total = m_tiles * n_tiles;
   const int num_kb = (K + BK - 1) / BK;
+  Sched sch;
+  sch.init(m_tiles * n_tiles, num_kb, stream_k);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < C::STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 4); }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  int tile, kb0, kb1;
 
   if (warp == 0) {
     // ===== TMA producer =====
     if (tc::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-        const int m0 = (t % m_tiles) * BM, nb = t / m_tiles;
-        for (int kb = 0; kb < num_kb; ++kb) {
+      while (sch.next(tile, kb0, kb1)) {
+        const int m0 = (tile % m_tiles) * BM, nb = tile / m_tiles;
+        for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          tc::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           tc::tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
           if constexpr (SW) {
             tc::tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * OUT_N);
-            tc::tma_load_2d(sb + B_BYTES / 2, &tmB, &full[stage], kb * BK, e.ff + nb * OUT_N);
+            tc::tma_load_2d(sb + C::B_BYTES / 2, &tmB, &full[stage], kb * BK, e.ff + nb * OUT_N);
           } else {
             tc::tma_load_2d(sb, &tmB, &full[stage], kb * BK, nb * BN);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -143,48 +219,118 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr uint32_t IDESC = tc::idesc_bf16(BM, BN);
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+    for (int it = 0; sch.next(tile, kb0, kb1); ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc::fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::fence_after();
         if (tc::elect_one()) {
-          const uint8_t* sa = smem + stage * STAGE_BYTES;
+          const uint8_t* sa = smem + stage * C::STAGE_BYTES;
           const uint64_t adesc = tc::sdesc_sw128(sa), bdesc = tc::sdesc_sw128(sa + A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // advance 16 bf16 = 32 B (>> 4 = 2) inside the swizzle atom
-            tc::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb | k) != 0);
+            tc::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
           tc::mma_commit(&empty[stage]);
-          if (kb == num_kb - 1) tc::mma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
         }
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else {
     // ===== epilogue (warps 2..5; warp w reads TMEM lanes 32*(w%4) .. +31) =====
     const int q = warp & 3;
-    int it = 0;
-    for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x, ++it) {
+    const int row = q * 32 + lane;    // row within the tile
+    const int et = threadIdx.x - 64;  // 0..127 among epilogue threads
+    int contrib[MAX_CONTRIB];
+    for (int it = 0; sch.next(tile, kb0, kb1); ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (t % m_tiles) * BM, nb = t / m_tiles;
+      const int m0 = (tile % m_tiles) * BM, nb = tile / m_tiles;
+      const bool final_piece = (kb1 == num_kb);
+      const int n_con = (final_piece && kb0 > 0) ? sch.contributors(tile, contrib) : 0;
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
-      const int m = m0 + q * 32 + lane;
+      const int m = m0 + row;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if (!final_piece) {
+        // non-final stream-K piece: fp32 partial -> this CTA's slot, then raise its flag
+        float* slot = part + ((size_t)blockIdx.x * BM + row) * SLOT_COLS;
 #pragma unroll 1
-      for (int c = 0; c < OUT_N; c += 16) {
-        float v[16], u[16];
-        tc::tmem_ld16(trow + c, v);
-        if constexpr (SW) tc::tmem_ld16(trow + BN / 2 + c, u);
-        const int n = nb * OUT_N + c;
-        if (m < M && n < e.N) epi16<KIND>(e, m, n, v, u);
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + c, v);
+          float4* p = reinterpret_cast<float4*>(slot + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        tc::fence_before();
+        __threadfence();
+        named_bar(1, 128);
+        if (et == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(1) : "memory");
+      } else {
+        if (n_con > 0) {  // wait for the earlier pieces of this tile
+          if (et < n_con) {
+            int f = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flags + contrib[et]) : "memory");
+            } while (f == 0);
+          }
+          named_bar(1, 128);
+        }
+#pragma unroll 1
+        for (int c = 0; c < OUT_N; c += 16) {
+          float v[16], u[16];
+          tc::tmem_ld16(trow + c, v);
+          if constexpr (SW) tc::tmem_ld16(trow + BN / 2 + c, u);
+          if (n_con > 0) {  // fixed order: partials of ascending CTAs, then this CTA's accumulator
+            float sv[16], su[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) { sv[i] = 0.f; su[i] = 0.f; }
+            for (int j0 = 0; j0 < n_con; j0 += 4) {
+              float4 x[4][4], y[4][4];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {  // issue every load of up to 4 contributors before adding
+                if (j0 + jj < n_con) {
+                  const float* slot = part + ((size_t)contrib[j0 + jj] * BM + row) * SLOT_COLS;
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) x[jj][i] = __ldcg(reinterpret_cast<const float4*>(slot + c) + i);
+                  if constexpr (SW) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                      y[jj][i] = __ldcg(reinterpret_cast<const float4*>(slot + BN / 2 + c) + i);
+                  }
+                }
+              }
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                if (j0 + jj < n_con) {
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    sv[4 * i] += x[jj][i].x; sv[4 * i + 1] += x[jj][i].y;
+                    sv[4 * i + 2] += x[jj][i].z; sv[4 * i + 3] += x[jj][i].w;
+                    if constexpr (SW) {
+                      su[4 * i] += y[jj][i].x; su[4 * i + 1] += y[jj][i].y;
+                      su[4 * i + 2] += y[jj][i].z; su[4 * i + 3] += y[jj][i].w;
+                    }
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) { v[i] = sv[i] + v[i]; u[i] = su[i] + u[i]; }
+          }
+          const int n = nb * OUT_N + c;
+          if (m < M && n < e.N) epi16<KIND>(e, m, n, v, u);
+        }
+        if (n_con > 0) {  // release the contributors' slots for the next launch
+          named_bar(1, 128);
+          if (et < n_con) flags[contrib[et]] = 0;
+        }
       }
       tc::fence_before();
       __syncwarp();
@@ -192,7 +338,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   __syncthreads();
-  if (warp == 2) tc::tmem_dealloc(tmem_base, 512);
+  if (warp == 2) tc::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }
 
 // ---- host side --------------------------------------------------------------------------------------
@@ -213,10 +359,52 @@ struct TmKeyHash {
     return h ^ (size_t)k.box_rows;
   }
 };
+
+// Launch plan: tile width, stream-K on/off and grid, from a cost model in "MMA cycles per SM".
+struct Plan {
+  int bn, stream_k, grid;
+};
+
+Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, int force_bn) {
+  const int num_kb = (K + BK - 1) / BK;
+  const int m_tiles = (M + BM - 1) / BM;
+  Plan best{256, 0, 1};
+  double best_cost = 1e300;
+  for (int bn : {256, 128}) {
+    if (force_bn && bn != force_bn) continue;
+    const int out_n = sw ? bn / 2 : bn;
+    const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
+    const double cyc = bn == 256 ? 512.0 : 300.0;  // per k-block; BN=128 is shared-memory-read bound
+    for (int skm : {0, 1}) {
+      if (force_sched == 1 && skm) continue;
+      if (force_sched == 2 && !skm) continue;
+      double cost;
+      int grid;
+      if (!skm) {
+        grid = (int)std::min<long long>(num_sms, tiles);
+        cost = (double)((tiles + grid - 1) / grid) * num_kb * cyc;
+      } else {
+        const long long iters = tiles * num_kb;
+        grid = (int)std::max<long long>(
+            1, std::min<long long>(std::min<long long>(num_sms, tiles * MAX_SPLIT), iters / MIN_KB));
+        const long long dp = (tiles % grid == 0) ? tiles / grid : std::max<long long>(0, tiles / grid - 1);
+        const long long sk = iters - dp * grid * num_kb;
+        // partial store/read + flag round trip, and the L2-locality loss of spreading the tail
+        cost = ((double)dp * num_kb + (double)((sk + grid - 1) / grid)) * cyc + (sk > 0 ? 12000.0 : 0.0);
+        cost *= 1.15;
+      }
+      if (cost < best_cost) { best_cost = cost; best = Plan{bn, skm, grid}; }
+    }
+  }
+  return best;
+}
 }  // namespace
 
 struct TmapCache {
   std::unordered_map<TmKey, CUtensorMap, TmKeyHash> maps;
+  float* part = nullptr;  // [num_sms][BM][SLOT_COLS] fp32 stream-K partial slots
+  int* flags = nullptr;   // [num_sms]
+  int force_bn = 0;
 };
 
 static cb_status get_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
@@ -249,35 +437,55 @@ bool gemm_tc_ok(const cb_ctx* c, const void* A, int lda, const void* B, int ldb,
   return M > 0;
 }
 
-template <int KIND>
-static cb_status launch_kind(cb_ctx* c, const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int m_tiles,
-                             int n_tiles, const EpiParams& e, cudaStream_t s) {
-  const int tiles = m_tiles * n_tiles;
-  const int grid = std::min(tiles, c->num_sms);
-  gemm_tc_kernel<KIND><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ta, tb, M, K, m_tiles, n_tiles, e);
-  CB_LAUNCHED(c);
-  return CB_OK;
-}
-
-cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
-                         cudaStream_t s) {
-  const bool sw = e.kind == EPI_SWIGLU;
-  const int out_n = sw ? BN / 2 : BN;
+template <int KIND, int BN>
+static cb_status launch_kind(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
+                             const EpiParams& e, const Plan& pl, cudaStream_t s) {
+  constexpr bool sw = KIND == EPI_SWIGLU;
+  constexpr int out_n = sw ? BN / 2 : BN;
   const long long b_rows = sw ? 2LL * e.ff : (long long)e.N;
   CUtensorMap ta, tb;
   CB_TRY(get_tmap(c, A, M, K, lda, BM, &ta));
   CB_TRY(get_tmap(c, B, b_rows, K, ldb, sw ? BN / 2 : BN, &tb));
   const int m_tiles = (M + BM - 1) / BM, n_tiles = (e.N + out_n - 1) / out_n;
-  ProfScope ps_(c, PROF_GEMM, s);
+  gemm_tc_kernel<KIND, BN><<<pl.grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, M, K, m_tiles, n_tiles, e,
+                                                                       c->tmaps->part, c->tmaps->flags, pl.stream_k);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+template <int BN>
+static cb_status launch_bn(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
+                           const Plan& pl, cudaStream_t s) {
   switch (e.kind) {
-    case EPI_STORE: return launch_kind<EPI_STORE>(c, ta, tb, M, K, m_tiles, n_tiles, e, s);
-    case EPI_STORE_F32: return launch_kind<EPI_STORE_F32>(c, ta, tb, M, K, m_tiles, n_tiles, e, s);
-    case EPI_QKV: return launch_kind<EPI_QKV>(c, ta, tb, M, K, m_tiles, n_tiles, e, s);
-    case EPI_RESID: return launch_kind<EPI_RESID>(c, ta, tb, M, K, m_tiles, n_tiles, e, s);
-    case EPI_SWIGLU: return launch_kind<EPI_SWIGLU>(c, ta, tb, M, K, m_tiles, n_tiles, e, s);
+    case EPI_STORE: return launch_kind<EPI_STORE, BN>(c, A, lda, B, ldb, M, K, e, pl, s);
+    case EPI_STORE_F32: return launch_kind<EPI_STORE_F32, BN>(c, A, lda, B, ldb, M, K, e, pl, s);
+    case EPI_QKV: return launch_kind<EPI_QKV, BN>(c, A, lda, B, ldb, M, K, e, pl, s);
+    case EPI_RESID: return launch_kind<EPI_RESID, BN>(c, A, lda, B, ldb, M, K, e, pl, s);
+    case EPI_SWIGLU: return launch_kind<EPI_SWIGLU, BN>(c, A, lda, B, ldb, M, K, e, pl, s);
   }
   cb_set_error("bad epilogue kind %d", e.kind);
   return CB_E_INVALID_ARG;
+}
+
+cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
+                         cudaStream_t s) {
+  const Plan pl = plan_gemm(c->num_sms, M, e.N, e.kind == EPI_SWIGLU, K, c->gemm_sched, c->tmaps->force_bn);
+  ProfScope ps_(c, PROF_GEMM, s);
+  if (pl.bn == 256) return launch_bn<256>(c, A, lda, B, ldb, M, K, e, pl, s);
+  return launch_bn<128>(c, A, lda, B, ldb, M, K, e, pl, s);
+}
+
+void gemm_tc_force_bn(cb_ctx* c, int bn) { c->tmaps->force_bn = bn; }
+
+template <int BN> static cb_status set_attrs() {
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE_F32, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg<BN>::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_QKV, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_RESID, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_SWIGLU, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg<BN>::SMEM));
+  return CB_OK;
 }
 
 cb_status gemm_tc_init(cb_ctx* c) {
@@ -288,16 +496,20 @@ cb_status gemm_tc_init(cb_ctx* c) {
     CB_REQUIRE(q == cudaDriverEntryPointSuccess && fn != nullptr, CB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_QKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-  CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+  CB_TRY(set_attrs<256>());
+  CB_TRY(set_attrs<128>());
   c->tmaps = new TmapCache();
+  CB_CUDA(cudaMalloc(&c->tmaps->part, (size_t)c->num_sms * BM * SLOT_COLS * sizeof(float)));
+  CB_CUDA(cudaMalloc(&c->tmaps->flags, (size_t)c->num_sms * sizeof(int)));
+  CB_CUDA(cudaMemset(c->tmaps->flags, 0, (size_t)c->num_sms * sizeof(int)));
   return CB_OK;
 }
 
 void gemm_tc_destroy(cb_ctx* c) {
+  if (c->tmaps) {
+    cudaFree(c->tmaps->part);
+    cudaFree(c->tmaps->flags);
+  }
   delete c->tmaps;
   c->tmaps = nullptr;
 }

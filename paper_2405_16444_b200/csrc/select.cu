@@ -9,6 +9,17 @@
 // One warp per candidate; per-head partials are warp-reduced in a fixed tree and summed over heads
 // in index order, so the value is bitwise reproducible (and decomposes per kv head for TP).
 // ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void load4(const float* p, float (&x)[4]) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+}
+__device__ __forceinline__ void load4(const bf16* p, float (&x)[4]) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+  x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) deviation_kernel(const T* __restrict__ kn, const T* __restrict__ vn,
                                                         const T* __restrict__ kr, const T* __restrict__ vr,
@@ -22,14 +33,19 @@ __global__ void __launch_bounds__(256) deviation_kernel(const T* __restrict__ kn
   float tot = 0.f;
   for (int h = 0; h < n_kv; ++h) {
     float p = 0.f;
-    for (int e = h * hd + lane; e < (h + 1) * hd; e += 32) {
+    for (int e = h * hd + lane * 4; e < (h + 1) * hd; e += 128) {  // 4 consecutive elements per lane
+      float x[4], y[4];
       if (mode != CB_DEV_V) {
-        const float d = to_f(kn[a + e]) - to_f(kr[b + e]);
-        p += d * d;
+        load4(kn + a + e, x);
+        load4(kr + b + e, y);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p += (x[i] - y[i]) * (x[i] - y[i]);
       }
       if (mode != CB_DEV_K) {
-        const float d = to_f(vn[a + e]) - to_f(vr[b + e]);
-        p += d * d;
+        load4(vn + a + e, x);
+        load4(vr + b + e, y);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p += (x[i] - y[i]) * (x[i] - y[i]);
       }
     }
     tot += warp_sum(p);

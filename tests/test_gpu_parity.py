@@ -125,6 +125,8 @@ def test_gemm_tcgen05(P, M, N, K):
     C = P.api.op_gemm(ctx, A, B, out_f32=True, impl=2)
     ref = (A.double() @ B.double().T).cpu().numpy()
     assert rel_err(np32(C), ref) < 5e-5   # tensor-core fp32 accumulation over K up to 14336
+    # stream-K partials are reduced in a fixed order: bitwise reproducible
+    assert torch.equal(P.api.op_gemm(ctx, A, B, out_f32=True, impl=2), C)
     Cb = P.api.op_gemm(ctx, A, B, out_f32=False, impl=2)
     assert rel_err(np32(Cb), ref) < 5e-3
 

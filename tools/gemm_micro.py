@@ -1,0 +1,59 @@
+"""Micro-benchmark of the tcgen05 GEMM on the blend's projection shapes (schedule / tile experiments).
+
+python tools/gemm_micro.py [--iters 50]   (needs a B200)"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+SHAPES = [  # (name, M, N, K)
+    ("qkv_l1", 3072, 6144, 4096), ("qkv_l2", 553, 6144, 4096), ("o_l2", 547, 4096, 4096),
+    ("gu_l2", 547, 28672, 4096), ("down_l2", 547, 4096, 14336), ("o_l31", 369, 4096, 4096),
+    ("gu_l31", 369, 28672, 4096), ("down_l31", 369, 4096, 14336), ("q_l0", 3072, 4096, 4096),
+    ("gu_l0", 3072, 28672, 4096), ("down_l0", 3072, 4096, 14336),
+]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--modes", default="1,2,0")
+    ap.add_argument("--bns", default="0")
+    a = ap.parse_args()
+    from paper_2405_16444_b200.build import build
+    build()
+    import paper_2405_16444_b200 as P
+    from synth import workload as W
+    ctx = P.Context(W.MODELS["mistral-7b"], "bf16", max_tokens=8)
+    res = {}
+    for name, M, N, K in SHAPES:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        for mode, bn in [(int(m), int(b)) for m in a.modes.split(",") for b in a.bns.split(",")]:
+            ctx.set_option("gemm_sched", mode)
+            ctx.set_option("gemm_bn", bn)
+            fn = lambda: P.api.check(P.api.lib().cb_op_gemm(ctx.handle, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                                                            M, N, K, 0, 2, torch.cuda.current_stream().cuda_stream))
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(a.iters):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / a.iters * 1e3
+            tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
+            res[f"{name}/m{mode}/bn{bn}"] = (round(us, 1), round(tf, 1))
+            print(f"{name:10s} M={M:5d} N={N:6d} K={K:6d} mode={mode} bn={bn}: {us:8.1f} us  {tf:7.1f} TFLOP/s", flush=True)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
