@@ -38,7 +38,7 @@ CB_API cb_status cb_op_gemm(cb_ctx* ctx, const void* A, const void* B, void* C, 
  * index q_tok[r]) and q head h: out[r][h] = softmax_j(q.k_j / sqrt(hd)) v_j over keys j <= q_tok[r]
  * of k, v [n_keys][n_kv][hd], kv head h / (n_q / n_kv).  Token positions are strictly increasing, so
  * "key position <= query position" is "j <= q_tok[r]".  out: [n_rows][n_q * hd] (model dtype).
- * impl: 0 = auto, 1 = SIMT, 2 = tensor-core (bf16, head_dim 128). */
+ * impl: 0 = auto, 1 = SIMT, 2 = tcgen05/TMEM (bf16, head_dim 128), 3 = mma.sync (bf16, head_dim 128). */
 CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_row, const int32_t* q_tok,
                           int32_t n_rows, const void* k, const void* v, int32_t n_keys, void* out, int32_t impl,
                           void* stream);
@@ -46,7 +46,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
 /* Tuning knobs (for experiments; defaults are the tuned choices). Unknown names -> INVALID_ARG.
  *   "gemm_sched"  0 = auto (cost model picks data-parallel or data-parallel + stream-K tail),
  *                 1 = data-parallel only, 2 = data-parallel rounds + stream-K tail
- *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width */
+ *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width
+ *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM, 3 = mma.sync (legacy tensor path) */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */

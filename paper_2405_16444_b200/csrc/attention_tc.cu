@@ -241,18 +241,24 @@ __global__ void attn_merge_kernel(const float* __restrict__ opart, const float2*
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= R * n_kv) return;
   const int g = w / R, rho = w - g * R;
-  float mstar = -INFINITY;
-  for (int s = 0; s < n_splits; ++s) mstar = fmaxf(mstar, ml[((size_t)s * n_kv + g) * R + rho].x);
+  constexpr int MAXS = 16;  // launcher caps n_splits
+  // lane s holds split s's (m, l); every partial row load is issued before the weighted sum
+  const float2 my = lane < n_splits ? ml[((size_t)lane * n_kv + g) * R + rho] : make_float2(-INFINITY, 0.f);
+  const float mstar = warp_max(my.x);
+  float4 o[MAXS];
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s)
+    if (s < n_splits) o[s] = reinterpret_cast<const float4*>(opart + (((size_t)s * n_kv + g) * R + rho) * HD)[lane];
   float l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s = 0; s < n_splits; ++s) {
-    const size_t pr = ((size_t)s * n_kv + g) * R + rho;
-    const float2 m_l = ml[pr];
-    if (m_l.x == -INFINITY) continue;
-    const float f = exp2f(m_l.x - mstar);
-    l += m_l.y * f;
-    const float4 o = reinterpret_cast<const float4*>(opart + pr * HD)[lane];
-    acc.x += o.x * f; acc.y += o.y * f; acc.z += o.z * f; acc.w += o.w * f;
+#pragma unroll
+  for (int s = 0; s < MAXS; ++s) {
+    if (s >= n_splits) break;
+    const float ms = __shfl_sync(0xffffffffu, my.x, s), ls = __shfl_sync(0xffffffffu, my.y, s);
+    if (ms == -INFINITY) continue;
+    const float f = exp2f(ms - mstar);
+    l += ls * f;
+    acc.x += o[s].x * f; acc.y += o[s].y * f; acc.z += o[s].z * f; acc.w += o[s].w * f;
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
   const int r = rho / G, h = g * G + rho % G;
@@ -263,6 +269,16 @@ __global__ void attn_merge_kernel(const float* __restrict__ opart, const float2*
 }  // namespace
 
 bool attention_tc_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.head_dim == HD; }
+
+cb_status launch_attention_merge(cb_ctx* c, int R, int n_splits, void* out, cudaStream_t s) {
+  const int n_kv = c->m.n_kv_heads, G = c->m.n_q_heads / n_kv;
+  const int warps = R * n_kv;
+  ProfScope ps_(c, PROF_ATTN, s);
+  attn_merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(c->attn_part, c->attn_ml, R, n_kv, G, n_splits, (bf16*)out,
+                                                    c->m.n_q_heads * HD);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
 
 cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                               const void* v, int n_keys, void* out, cudaStream_t s) {
@@ -279,6 +295,7 @@ cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const 
   if (base < 4LL * c->num_sms && c->attn_part != nullptr) {
     n_splits = (int)std::min<long long>((6LL * c->num_sms + base - 1) / base, (max_kt + 3) / 4);
     n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
+    n_splits = std::min(n_splits, 16);
     n_splits = std::max(1, n_splits);
   }
   const int kt_per_split = (max_kt + n_splits - 1) / n_splits;
@@ -289,12 +306,7 @@ cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const 
                                          (bf16*)out, c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart,
                                          c->attn_ml);
   CB_LAUNCHED(c);
-  if (n_splits > 1) {
-    const int warps = R * n_kv;
-    attn_merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(c->attn_part, c->attn_ml, R, n_kv, G, n_splits, (bf16*)out,
-                                                      c->m.n_q_heads * HD);
-    CB_LAUNCHED(c);
-  }
+  if (n_splits > 1) CB_TRY(launch_attention_merge(c, R, n_splits, out, s));
   return CB_OK;
 }
 

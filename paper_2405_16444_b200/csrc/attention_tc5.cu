@@ -1,0 +1,384 @@
+// attention_tc5.cu — tcgen05 / TMEM / TMA sparse-query causal attention (step a6), bf16, head_dim 128.
+//
+// out[r][h] = softmax_j(q_{r,h} . k_{j,g} / sqrt(hd)) v_{j,g} over keys j <= q_tok[r]
+//
+// One CTA = one kv head g x 128 (query token, q head of g) rows (GQA packing: every K/V tile serves
+// all G q heads of the group) x one split of the key range (split-KV for the later layers' few
+// hundred queries). Warp roles:
+//   warp 0     TMA: K and V tiles (128 keys x 128, two 64-column SWIZZLE_128B boxes each) into a
+//              2-stage ring (3-D tensor map over [keys][kv heads][hd])
+//   warp 1     MMA issuer: S_t = Q K_t^T (M=128, N=128 keys, K=16) into one of two TMEM S buffers,
+//              then O += P_t V_t (A = P from shared memory, B = V MN-major) into the TMEM O buffer.
+//              S_{t+1} is issued before waiting for P_t, so QK^T overlaps the softmax of tile t.
+//   warps 2-5  softmax, one thread per query row: tcgen05.ld its S row (128 fp32), mask by original
+//              position, online softmax in the log2 domain with lazy rescaling (O is rescaled in
+//              TMEM only when the row max grows by more than 2^8), P (bf16) into shared memory in
+//              the K-major SWIZZLE_128B layout the MMA reads; finally O / l (or the split partial).
+// Key tiles past the CTA's last query token are never loaded; only tiles reaching past its first
+// query token are masked. Heaviest (latest-token) tiles are scheduled first.
+#include <cudaTypedefs.h>
+
+#include <unordered_map>
+
+#include "ctx.h"
+#include "tc_common.cuh"
+
+namespace {
+constexpr int HD = 128, BM = 128, BC = 128, NT = 192;
+constexpr int ATOM = 128 * 128;    // 128 rows x 128 B (64 bf16): one SWIZZLE_128B column block
+constexpr int TILE = 2 * ATOM;     // 128 rows x 128 bf16
+constexpr int SMEM = 6 * TILE + 1024 + 256;  // Q, K[2], V[2], P + alignment + barriers
+constexpr float RESCALE_THRESHOLD = 8.0f;    // log2 units
+
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ~2 ulp; ex2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// byte offset of 16-B chunk `ch` (0..15) of row `r` in a [2 atoms][128 rows][128 B] swizzled tile
+__device__ __forceinline__ uint32_t sw_off(int r, int ch) {
+  return (uint32_t)((ch >> 3) * ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+
+__global__ void __launch_bounds__(NT, 1)
+    attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                    const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
+                    int n_rows, int n_keys, bf16* __restrict__ out, int n_q, int n_kv, float scale_log2,
+                    int kt_per_split, float* __restrict__ opart, float2* __restrict__ ml) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + TILE;          // [2] stages
+  uint8_t* sV = smem + 3 * TILE;      // [2] stages
+  uint8_t* sP = smem + 5 * TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
+  uint64_t* kv_full = bars;           // [2]
+  uint64_t* kv_empty = bars + 2;      // [2]
+  uint64_t* s_full = bars + 4;        // [2]
+  uint64_t* s_empty = bars + 6;       // [2]
+  uint64_t* q_full = bars + 8;
+  uint64_t* p_full = bars + 9;
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.y, G = n_q / n_kv, R = n_rows * G;
+  const int rho0 = (gridDim.x - 1 - blockIdx.x) * BM;
+  const int qd = n_q * HD;
+
+  int kmax = -1, kmin = 1 << 30;
+  for (int rr = rho0 / G; rr <= min(R - 1, rho0 + BM - 1) / G; ++rr) {
+    const int t = min(__ldg(q_tok + rr), n_keys - 1);
+    kmax = max(kmax, t);
+    kmin = min(kmin, t);
+  }
+  const int n_kt = (kmax + BC) / BC;
+  const int split = blockIdx.z;
+  const int jb = split * kt_per_split, je = min(n_kt, jb + kt_per_split);
+  const size_t part_row0 = ((size_t)split * n_kv + g) * R;
+  if (jb >= je) {  // no keys for this split: neutral partial (m = -inf, l = 0)
+    if (opart != nullptr)
+      for (int i = threadIdx.x; i < BM; i += NT)
+        if (rho0 + i < R) ml[part_row0 + rho0 + i] = make_float2(-INFINITY, 0.f);
+    return;
+  }
+  const int nt = je - jb;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmK);
+    tc::tma_prefetch(&tmV);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&kv_full[b], 1);
+      tc::mbar_init(&kv_empty[b], 1);
+      tc::mbar_init(&s_full[b], 1);
+      tc::mbar_init(&s_empty[b], 4);
+    }
+    tc::mbar_init(q_full, 128);
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(pv_done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;  // S0: cols [0,128), S1: [128,256), O: [256,384)
+
+  if (warp == 0) {
+    // ===== TMA producer: K_t, V_t =====
+    if (tc::elect_one()) {
+      for (int t = 0; t < nt; ++t) {
+        const int b = t & 1;
+        if (t >= 2) tc::mbar_wait(&kv_empty[b], ((t >> 1) - 1) & 1);
+        tc::mbar_arrive_expect_tx(&kv_full[b], 2 * TILE);
+        const int key0 = (jb + t) * BC;
+        tc::tma_load_3d(sK + b * TILE, &tmK, &kv_full[b], 0, g, key0);
+        tc::tma_load_3d(sK + b * TILE + ATOM, &tmK, &kv_full[b], 64, g, key0);
+        tc::tma_load_3d(sV + b * TILE, &tmV, &kv_full[b], 0, g, key0);
+        tc::tma_load_3d(sV + b * TILE + ATOM, &tmV, &kv_full[b], 64, g, key0);
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    constexpr uint32_t IDESC_S = tc::idesc_bf16(BM, BC);
+    constexpr uint32_t IDESC_PV = tc::idesc_bf16_bmn(BM, HD);
+    const uint32_t tO = tmem + 256;
+    auto issue_s = [&](int t) {
+      const int b = t & 1;
+      tc::mbar_wait(&kv_full[b], (t >> 1) & 1);
+      if (t >= 2) tc::mbar_wait(&s_empty[b], ((t >> 1) - 1) & 1);
+      tc::fence_after();
+      if (tc::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint64_t a = tc::sdesc_sw128(sQ + (kk >> 2) * ATOM) + 2 * (kk & 3);
+          const uint64_t bd = tc::sdesc_sw128(sK + b * TILE + (kk >> 2) * ATOM) + 2 * (kk & 3);
+          tc::mma_bf16(tmem + b * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&s_full[b]);
+      }
+      __syncwarp();
+    };
+    tc::mbar_wait(q_full, 0);
+    issue_s(0);
+    for (int t = 0; t < nt; ++t) {
+      if (t + 1 < nt) issue_s(t + 1);
+      tc::mbar_wait(p_full, t & 1);
+      tc::fence_after();
+      if (tc::elect_one()) {
+        const int b = t & 1;
+#pragma unroll
+        for (int kk = 0; kk < BC / 16; ++kk) {  // 16 keys per step
+          const uint64_t a = tc::sdesc_sw128(sP + (kk >> 2) * ATOM) + 2 * (kk & 3);
+          const uint64_t bd = tc::sdesc_sw128_mn(sV + b * TILE + kk * 2048, ATOM);
+          tc::mma_bf16(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(pv_done);
+        tc::mma_commit(&kv_empty[b]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ===== softmax / correction / epilogue: thread = query row =====
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int rho = rho0 + r;
+    const bool valid = rho < R;
+    const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
+    const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
+    {  // stage this row of Q
+      const bf16* src = q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD;
+      const uint32_t dq = tc::smem_u32(sQ);
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        const int sz = valid ? 16 : 0;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dq + sw_off(r, ch)), "l"(src + ch * 8),
+                     "r"(sz)
+                     : "memory");
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      tc::fence_proxy_async();
+      tc::mbar_arrive(q_full);
+    }
+    float m_used = -INFINITY, l = 0.f;
+    const uint32_t dp = tc::smem_u32(sP);
+    for (int t = 0; t < nt; ++t) {
+      const int b = t & 1;
+      tc::mbar_wait(&s_full[b], (t >> 1) & 1);
+      tc::fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float x[32];
+        tc::tmem_ld32(tmem + lane_base + b * 128 + c * 32, x);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = x[i];
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&s_empty[b]);
+      const int key0 = (jb + t) * BC;
+      const bool need_mask = key0 + BC - 1 > kmin;
+      // row max of the raw scores (scale > 0 commutes with max); 8 independent chains for ILP
+      float mx8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+      if (need_mask) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          if (key0 + i > tok) s[i] = -INFINITY;
+          mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      }
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+      // lazy rescale: move the reference max only when it grew by more than 2^8
+      float corr = 1.f;
+      if (mx > m_used + RESCALE_THRESHOLD || (m_used == -INFINITY && mx != -INFINITY)) {
+        if (m_used != -INFINITY) corr = ex2(m_used - mx);
+        m_used = mx;
+      }
+      const float nref = m_used == -INFINITY ? 0.f : -m_used;
+      l *= corr;
+      float rs8[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rs8[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        s[i] = ex2(fmaf(s[i], scale_log2, nref));  // -inf -> 0
+        rs8[i & 7] += s[i];
+      }
+      l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      if (t >= 1) {  // PV_{t-1} done: the P buffer is free and O is stable
+        tc::mbar_wait(pv_done, (t - 1) & 1);
+        tc::fence_after();
+        if (__any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write of O
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float o[32];
+            tc::tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= corr;
+            tc::tmem_st32(tmem + lane_base + 256 + c * 32, o);
+          }
+          tc::tmem_st_wait();
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        uint4 w;
+        w.x = pack2(s[ch * 8 + 0], s[ch * 8 + 1]);
+        w.y = pack2(s[ch * 8 + 2], s[ch * 8 + 3]);
+        w.z = pack2(s[ch * 8 + 4], s[ch * 8 + 5]);
+        w.w = pack2(s[ch * 8 + 6], s[ch * 8 + 7]);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dp + sw_off(r, ch)), "r"(w.x), "r"(w.y),
+                     "r"(w.z), "r"(w.w)
+                     : "memory");
+      }
+      tc::fence_proxy_async();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_full);
+    }
+    tc::mbar_wait(pv_done, (nt - 1) & 1);
+    tc::fence_after();
+    float o[128];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float x[32];
+      tc::tmem_ld32(tmem + lane_base + 256 + c * 32, x);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[c * 32 + i] = x[i];
+    }
+    if (valid) {
+      if (opart != nullptr) {
+        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        ml[part_row0 + rho] = make_float2(m_used, l);
+      } else {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD);
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+          uint4 w;
+          w.x = pack2(o[ch * 8 + 0] * inv, o[ch * 8 + 1] * inv);
+          w.y = pack2(o[ch * 8 + 2] * inv, o[ch * 8 + 3] * inv);
+          w.z = pack2(o[ch * 8 + 4] * inv, o[ch * 8 + 5] * inv);
+          w.w = pack2(o[ch * 8 + 6] * inv, o[ch * 8 + 7] * inv);
+          dst[ch] = w;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode5 = nullptr;
+
+struct KvKey {
+  const void* p;
+  int n_keys;
+  bool operator==(const KvKey& o) const { return p == o.p && n_keys == o.n_keys; }
+};
+struct KvKeyHash {
+  size_t operator()(const KvKey& k) const { return std::hash<const void*>()(k.p) ^ ((size_t)k.n_keys * 0x9e3779b9); }
+};
+std::unordered_map<KvKey, CUtensorMap, KvKeyHash>* g_kvmaps = nullptr;
+
+cb_status kv_tmap(const cb_ctx* c, const void* p, int n_keys, CUtensorMap* out) {
+  KvKey key{p, n_keys};
+  auto it = g_kvmaps->find(key);
+  if (it != g_kvmaps->end()) { *out = it->second; return CB_OK; }
+  const int n_kv = c->m.n_kv_heads;
+  cuuint64_t dims[3] = {(cuuint64_t)HD, (cuuint64_t)n_kv, (cuuint64_t)n_keys};
+  cuuint64_t strides[2] = {(cuuint64_t)HD * 2, (cuuint64_t)n_kv * HD * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)BC};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult r = g_encode5(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(p), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CB_REQUIRE(r == CUDA_SUCCESS, CB_E_CUDA, "cuTensorMapEncodeTiled (K/V) failed (%d)", (int)r);
+  if (g_kvmaps->size() > 4096) g_kvmaps->clear();
+  g_kvmaps->emplace(key, m);
+  *out = m;
+  return CB_OK;
+}
+}  // namespace
+
+bool attention_tc5_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.head_dim == HD && g_encode5 != nullptr; }
+
+cb_status launch_attention_merge(cb_ctx* c, int R, int n_splits, void* out, cudaStream_t s);
+
+cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
+                               const void* v, int n_keys, void* out, cudaStream_t s) {
+  if (n_rows == 0) return CB_OK;
+  CB_REQUIRE(((uintptr_t)k | (uintptr_t)v) % 16 == 0, CB_E_INVALID_ARG, "K/V must be 16-byte aligned");
+  const int n_kv = c->m.n_kv_heads, G = c->m.n_q_heads / n_kv;
+  const int R = n_rows * G;
+  const int tiles = (R + BM - 1) / BM;
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  const int max_kt = (n_keys + BC - 1) / BC;
+  const long long base = (long long)tiles * n_kv;
+  int n_splits = 1;
+  if (base < 2LL * c->num_sms && c->attn_part != nullptr) {
+    n_splits = (int)std::min<long long>((3LL * c->num_sms + base - 1) / base, (max_kt + 1) / 2);
+    n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
+    n_splits = std::max(1, std::min(n_splits, 16));
+  }
+  const int kt_per_split = (max_kt + n_splits - 1) / n_splits;
+  CUtensorMap tk, tv;
+  CB_TRY(kv_tmap(c, k, n_keys, &tk));
+  CB_TRY(kv_tmap(c, v, n_keys, &tv));
+  dim3 grid(tiles, n_kv, n_splits);
+  ProfScope ps_(c, PROF_ATTN, s);
+  float* opart = n_splits > 1 ? c->attn_part : nullptr;
+  attn_tc5_kernel<<<grid, NT, SMEM, s>>>(tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
+                                         c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart, c->attn_ml);
+  CB_LAUNCHED(c);
+  if (n_splits > 1) CB_TRY(launch_attention_merge(c, R, n_splits, out, s));
+  return CB_OK;
+}
+
+cb_status attention_tc5_init() {
+  if (g_encode5 == nullptr) {
+    cudaDriverEntryPointQueryResult qr;
+    void* fn = nullptr;
+    CB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+    CB_REQUIRE(qr == cudaDriverEntryPointSuccess && fn != nullptr, CB_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    g_encode5 = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (g_kvmaps == nullptr) g_kvmaps = new std::unordered_map<KvKey, CUtensorMap, KvKeyHash>();
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  return CB_OK;
+}

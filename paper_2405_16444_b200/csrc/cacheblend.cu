@@ -20,6 +20,10 @@ cb_status launch_attention_simt(cb_ctx* c, const void* q, const int* q_row, cons
 cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
                               const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
 bool attention_tc_ok(const cb_ctx* c);
+cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
+                               const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
+bool attention_tc5_ok(const cb_ctx* c);
+cb_status attention_tc5_init();
 cb_status topk_init_attrs();
 cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
@@ -107,8 +111,13 @@ cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb,
 cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                            const void* v, int n_keys, void* out, int impl, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
-  if (impl == 2 || (impl == 0 && attention_tc_ok(c))) {
-    CB_REQUIRE(attention_tc_ok(c), CB_E_UNSUPPORTED, "tensor-core attention needs bf16 and head_dim 128");
+  if (impl == 0) impl = c->attn_impl;
+  if (impl == 2 || (impl == 0 && attention_tc5_ok(c))) {
+    CB_REQUIRE(attention_tc5_ok(c), CB_E_UNSUPPORTED, "tcgen05 attention needs bf16 and head_dim 128");
+    return launch_attention_tc5(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
+  }
+  if (impl == 3) {
+    CB_REQUIRE(attention_tc_ok(c), CB_E_UNSUPPORTED, "mma.sync attention needs bf16 and head_dim 128");
     return launch_attention_tc(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
   }
   return launch_attention_simt(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
@@ -142,6 +151,8 @@ cb_status check_model(const cb_model* m) {
   CB_REQUIRE(m->head_dim % V == 0 && m->d_model % 8 == 0 && m->d_ff % 8 == 0, CB_E_UNSUPPORTED,
              "head_dim must be a multiple of %d and d_model, d_ff multiples of 8", V);
   CB_REQUIRE(m->head_dim <= 256, CB_E_UNSUPPORTED, "head_dim > 256");
+  CB_REQUIRE(m->n_kv_heads <= 16, CB_E_UNSUPPORTED, "n_kv_heads > 16");
+  CB_REQUIRE(m->d_model <= 8192, CB_E_UNSUPPORTED, "d_model > 8192");
   CB_REQUIRE(m->max_pos >= 1, CB_E_INVALID_ARG, "max_pos must be >= 1");
   CB_REQUIRE(m->rope_theta > 0.0 && m->rms_eps >= 0.f, CB_E_INVALID_ARG, "rope_theta/rms_eps out of range");
   return CB_OK;
@@ -263,6 +274,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   cb_status st = topk_init_attrs();
   if (st == CB_OK) st = gemm_tc_init(c);
   if (st == CB_OK) st = attention_tc_init();
+  if (st == CB_OK) st = attention_tc5_init();
   if (st != CB_OK) {
     cudaFree(c->rope_tab);
     cudaFree(c->err_word);
@@ -307,6 +319,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "gemm_sched") == 0) {
     CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_sched must be 0, 1 or 2");
     c->gemm_sched = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "attn_impl") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 3, CB_E_INVALID_ARG, "attn_impl must be 0..3");
+    c->attn_impl = (int)value;
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_bn") == 0) {
@@ -368,7 +385,7 @@ extern "C" cb_status cb_op_attention(cb_ctx* c, const void* q, const int32_t* q_
                                      int32_t impl, void* st) {
   CB_REQUIRE(c && q && q_row && q_tok && k && v && out && n_rows >= 0 && n_keys >= 1, CB_E_INVALID_ARG,
              "cb_op_attention: bad arguments");
-  CB_REQUIRE(impl >= 0 && impl <= 2, CB_E_INVALID_ARG, "cb_op_attention: impl must be 0, 1 or 2");
+  CB_REQUIRE(impl >= 0 && impl <= 3, CB_E_INVALID_ARG, "cb_op_attention: impl must be 0, 1, 2 or 3");
   return launch_attention(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, impl, (cudaStream_t)st);
 }
 

@@ -50,6 +50,7 @@ struct cb_ctx {
   float2* attn_ml;      // [attn_part_rows] (m, l)
   long long attn_part_rows;
   int gemm_sched;   // cb_set_option("gemm_sched")
+  int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int* tok_d;       // [T] request-mode device copies of tokens / positions
   int* pos_d;       // [T]
   long long launches;

@@ -131,35 +131,51 @@ __device__ __forceinline__ void store4(bf16* p, float a, float b, float c, float
   *reinterpret_cast<uint2*>(p) = w;
 }
 
+// One 128-thread block per row: every 16-byte load of the row is issued before the reduction (the
+// row stays in registers, up to d = 8192), fixed-order block reduction (deterministic).
+constexpr int RMS_THREADS = 128, RMS_MAXV = 16;
 template <typename T>
-__global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
-                                                      T* __restrict__ x, int n_rows, int d, float eps) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (r >= n_rows) return;
+__global__ void __launch_bounds__(RMS_THREADS) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
+                                                              T* __restrict__ x, int d, float eps) {
+  const int r = blockIdx.x, tid = threadIdx.x;
   const float* hr = h + (size_t)r * d;
+  float4 v[RMS_MAXV];
   float ss = 0.f;
-  for (int e = lane * 4; e < d; e += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(hr + e);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) {
+    const int e = (i * RMS_THREADS + tid) * 4;
+    v[i] = e < d ? *reinterpret_cast<const float4*>(hr + e) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  __shared__ float red[RMS_THREADS / 32];
   ss = warp_sum(ss);
-  const float inv = 1.0f / sqrtf(ss / (float)d + eps);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < RMS_THREADS / 32; ++w) tot += red[w];
+  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
   T* xr = x + (size_t)r * d;
-  for (int e = lane * 4; e < d; e += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(hr + e);
-    const float4 gg = __ldg(reinterpret_cast<const float4*>(g + e));
-    store4(xr + e, v.x * inv * gg.x, v.y * inv * gg.y, v.z * inv * gg.z, v.w * inv * gg.w);
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) {
+    const int e = (i * RMS_THREADS + tid) * 4;
+    if (e < d) {
+      const float4 gg = __ldg(reinterpret_cast<const float4*>(g + e));
+      store4(xr + e, v[i].x * inv * gg.x, v[i].y * inv * gg.y, v[i].z * inv * gg.z, v[i].w * inv * gg.w);
+    }
   }
 }
 
 cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
+  CB_REQUIRE(c->m.d_model <= RMS_THREADS * RMS_MAXV * 4, CB_E_UNSUPPORTED, "rmsnorm: d_model > %d",
+             RMS_THREADS * RMS_MAXV * 4);
   ProfScope ps_(c, PROF_RMSNORM, s);
-  const int blocks = (n_rows + 7) / 8;
   if (c->m.dtype == CB_BF16)
-    rmsnorm_kernel<bf16><<<blocks, 256, 0, s>>>(h, gain, (bf16*)x, n_rows, c->m.d_model, c->m.rms_eps);
+    rmsnorm_kernel<bf16><<<n_rows, RMS_THREADS, 0, s>>>(h, gain, (bf16*)x, c->m.d_model, c->m.rms_eps);
   else
-    rmsnorm_kernel<float><<<blocks, 256, 0, s>>>(h, gain, (float*)x, n_rows, c->m.d_model, c->m.rms_eps);
+    rmsnorm_kernel<float><<<n_rows, RMS_THREADS, 0, s>>>(h, gain, (float*)x, c->m.d_model, c->m.rms_eps);
   CB_LAUNCHED(c);
   return CB_OK;
 }

@@ -30,26 +30,32 @@ __global__ void __launch_bounds__(256) deviation_kernel(const T* __restrict__ kn
   if (warp >= n_cand) return;
   const int kvd = n_kv * hd;
   const size_t a = (size_t)warp * kvd, b = (size_t)__ldg(cand_tok + warp) * kvd;
-  float tot = 0.f;
-  for (int h = 0; h < n_kv; ++h) {
-    float p = 0.f;
-    for (int e = h * hd + lane * 4; e < (h + 1) * hd; e += 128) {  // 4 consecutive elements per lane
-      float x[4], y[4];
-      if (mode != CB_DEV_V) {
+  // per-lane partial of every head first (all loads in flight together), then per-head warp sums
+  // added in head order
+  constexpr int MAXH = 16;
+  float p[MAXH];
+#pragma unroll
+  for (int h = 0; h < MAXH; ++h) {
+    p[h] = 0.f;
+    if (h < n_kv) {
+      for (int e = h * hd + lane * 4; e < (h + 1) * hd; e += 128) {  // 4 consecutive elements per lane
+        float x[4], y[4], z[4], w[4];
         load4(kn + a + e, x);
         load4(kr + b + e, y);
+        load4(vn + a + e, z);
+        load4(vr + b + e, w);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) p += (x[i] - y[i]) * (x[i] - y[i]);
-      }
-      if (mode != CB_DEV_K) {
-        load4(vn + a + e, x);
-        load4(vr + b + e, y);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) p += (x[i] - y[i]) * (x[i] - y[i]);
+        for (int i = 0; i < 4; ++i) {
+          if (mode != CB_DEV_V) p[h] += (x[i] - y[i]) * (x[i] - y[i]);
+          if (mode != CB_DEV_K) p[h] += (z[i] - w[i]) * (z[i] - w[i]);
+        }
       }
     }
-    tot += warp_sum(p);
   }
+  float tot = 0.f;
+#pragma unroll
+  for (int h = 0; h < MAXH; ++h)
+    if (h < n_kv) tot += warp_sum(p[h]);
   if (lane == 0) dev[warp] = tot;
 }
 

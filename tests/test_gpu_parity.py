@@ -151,9 +151,12 @@ def test_attention_parity(P, dtype, name):
     assert rel_err(np32(out), ref) < (1e-5 if dtype == "f32" else 1e-2)
 
 
-@pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (1000, 1000, 2), (777, 50, 1), (130, 3, 8)])
-def test_attention_tensor_core(P, T, n_sel, n_kv):
-    """mma.sync flash attention (bf16, hd 128, GQA packing, position-aware key skip) against the oracle."""
+@pytest.mark.parametrize("impl", [2, 3])
+@pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (1000, 1000, 2), (777, 50, 1), (130, 3, 8),
+                                          (4100, 900, 4)])
+def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
+    """Tensor-core flash attention (impl 2 = tcgen05/TMEM, 3 = mma.sync; bf16, hd 128, GQA packing,
+    position-aware key skip, split-KV) against the oracle."""
     s = shape("small", n_kv_heads=n_kv)
     g = lambda st, n, H: rng.values(12, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
     q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
@@ -163,7 +166,7 @@ def test_attention_tensor_core(P, T, n_sel, n_kv):
     qbuf[qrow] = q[rows]
     ctx = P.Context(s, "bf16", max_tokens=T)
     out = P.api.op_attention(ctx, to_dev(qbuf, torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
-                             to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T, impl=2)
+                             to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T, impl=impl)
     pos = np.arange(T)
     ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
     assert rel_err(np32(out), ref) < 1e-2
