@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of one CUDA graph per step")
     return ap.parse_args()
 
 
@@ -279,15 +280,24 @@ def run_ours(args):
     h_out = torch.empty(ks[-1], s.d_model, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step_eager():
         P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, k_out, v_out, ks, h_out=h_out)
 
+    l0 = ctx.launch_count()
+    step_eager()  # also warms the tensor-map caches
+    per_step_launches = ctx.launch_count() - l0
+    torch.cuda.synchronize()
+    step = step_eager
+    if not args.no_graph:  # the whole blend as one CUDA graph (static shapes: every k_i is a host integer)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_eager()
+        step = graph.replay
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    l0 = ctx.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -298,7 +308,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    launches = (ctx.launch_count() - l0) // args.steps
+    launches = per_step_launches * args.steps
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -307,7 +317,7 @@ def run_ours(args):
     value = world * N / (ms_max / 1e3)
 
     # per-kernel profile pass (same steps, per-launch CUDA events on the launching stream)
-    prof = P.api.profile_steps(ctx, step, max(3, min(args.steps, 10)))
+    prof = P.api.profile_steps(ctx, step_eager, max(3, min(args.steps, 10)))
     work = algorithmic_work(s, N, 0, ks)
     hbm, tf_burst, tf_sus, peak_src = measured_peaks()
     gemm_ms = prof.get("gemm", 0.0)
@@ -364,9 +374,20 @@ def run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args):
     cs = list(req.chunk_starts())
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step_eager():
         P.api.blend_request(ctx, mw, toks, poss, cs, 0, kh, vh, kb, vb, ks, hh)
 
+    step_eager()
+    torch.cuda.synchronize()
+    step, graphed = step_eager, False
+    if not args.no_graph:  # copy stream forks/joins inside the capture through the library's events
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step_eager()
+            step, graphed = graph.replay, True
+        except Exception:
+            torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -382,7 +403,7 @@ def run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args):
     return {"value": N / (ms / 1e3), "unit": "ctx_tok/s", "ms": ms, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h),
             "path": "cb_blend_request: pinned host chunk KV + tokens, layer-pipelined H2D on a copy stream, "
-                    "h_out D2H; KV^new stays on the GPU"}
+                    "h_out D2H; KV^new stays on the GPU" + (" (CUDA graph)" if graphed else "")}
 
 
 if __name__ == "__main__":
