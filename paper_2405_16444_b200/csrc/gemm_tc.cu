@@ -103,26 +103,39 @@ __device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const fl
 
 // Data-parallel rounds followed by an optional stream-K tail; every role walks the identical sequence.
 struct Sched {
-  int tiles, num_kb, G, b, dp_rounds, r;
+  int tiles, num_kb, G, b, dp_rounds, r, sk_ctas;
   long long sk_base, sk_iters, it, it_end;
-  __device__ void init(int tiles_, int num_kb_, int stream_k) {
-    tiles = tiles_; num_kb = num_kb_; G = gridDim.x; b = blockIdx.x; r = 0;
-    if (!stream_k) {
+  // sk_ctas_ = 0: whole tiles only (ceil(tiles/G) rounds). sk_ctas_ > 0: floor(tiles/G) whole-tile
+  // rounds, then the remaining tiles' k-blocks split evenly over the first sk_ctas_ CTAs.
+  __device__ void init(int tiles_, int num_kb_, int sk_ctas_) {
+    tiles = tiles_; num_kb = num_kb_; G = gridDim.x; b = blockIdx.x; r = 0; sk_ctas = sk_ctas_;
+    if (sk_ctas <= 0) {
       dp_rounds = (tiles + G - 1) / G;
       sk_base = sk_iters = it = it_end = 0;
+      sk_ctas = 1;
       return;
     }
-    dp_rounds = (tiles % G == 0) ? tiles / G : max(0, tiles / G - 1);
+    dp_rounds = tiles / G;
     sk_base = (long long)dp_rounds * G * num_kb;
     sk_iters = (long long)tiles * num_kb - sk_base;
-    it = sk_base + sk_start(b);
-    it_end = sk_base + sk_start(b + 1);
+    it = it_end = 0;
+    if (b < sk_ctas) {
+      it = sk_base + sk_start(b);
+      it_end = sk_base + sk_start(b + 1);
+    }
   }
-  __device__ long long sk_start(int cta) const { return (long long)cta * sk_iters / G; }
-  // Next segment: tile and k-block range [kb0, kb1). The stream-K range is walked backwards, so a
-  // CTA's only non-final piece (the head of its last tile) is computed and published first; its
-  // final pieces then wait only on partials that other CTAs also publish first (no chains).
+  __device__ long long sk_start(int cta) const { return (long long)cta * sk_iters / sk_ctas; }
+  // Next segment: tile and k-block range [kb0, kb1). Whole-tile rounds first (concurrent CTAs share
+  // weight tiles in L2), then the stream-K tail walked backwards, so a CTA's only non-final piece
+  // (the head of its last tile) is computed and published first; its final pieces then wait only
+  // on partials other CTAs also publish first (no dependency chains).
   __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (r < dp_rounds) {
+      tile = r * G + b;
+      ++r;
+      if (tile < tiles) { kb0 = 0; kb1 = num_kb; return true; }
+      r = dp_rounds;
+    }
     if (it < it_end) {
       const long long last = it_end - 1;
       tile = (int)(last / num_kb);
@@ -131,12 +144,6 @@ struct Sched {
       kb0 = (int)(s - tstart);
       kb1 = (int)(last - tstart) + 1;
       it_end = s;
-      return true;
-    }
-    if (r < dp_rounds) {
-      tile = r * G + b;
-      if (tile >= tiles) return false;
-      kb0 = 0; kb1 = num_kb; ++r;
       return true;
     }
     return false;
@@ -160,7 +167,7 @@ template <int KIND, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
                    int m_tiles, int n_tiles, EpiParams e, float* __restrict__ part, int* __restrict__ flags,
-                   int stream_k) {
+                   int sk_ctas) {
   using C = Cfg<BN>;
   constexpr bool SW = (KIND == EPI_SWIGLU);
   constexpr int OUT_N = SW ? BN / 2 : BN;  // output columns per tile
@@ -175,7 +182,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_kb = (K + BK - 1) / BK;
   Sched sch;
-  sch.init(m_tiles * n_tiles, num_kb, stream_k);
+  sch.init(m_tiles * n_tiles, num_kb, sk_ctas);
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
@@ -360,9 +367,9 @@ struct TmKeyHash {
   }
 };
 
-// Launch plan: tile width, stream-K on/off and grid, from a cost model in "MMA cycles per SM".
+// Launch plan: tile width, stream-K tail and grid, from a cost model in MMA cycles per SM.
 struct Plan {
-  int bn, stream_k, grid;
+  int bn, sk_ctas, grid;
 };
 
 Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, int force_bn) {
@@ -375,25 +382,24 @@ Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, i
     const int out_n = sw ? bn / 2 : bn;
     const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
     const double cyc = bn == 256 ? 512.0 : 300.0;  // per k-block; BN=128 is shared-memory-read bound
-    for (int skm : {0, 1}) {
-      if (force_sched == 1 && skm) continue;
-      if (force_sched == 2 && !skm) continue;
-      double cost;
-      int grid;
-      if (!skm) {
-        grid = (int)std::min<long long>(num_sms, tiles);
-        cost = (double)((tiles + grid - 1) / grid) * num_kb * cyc;
-      } else {
-        const long long iters = tiles * num_kb;
-        grid = (int)std::max<long long>(
-            1, std::min<long long>(std::min<long long>(num_sms, tiles * MAX_SPLIT), iters / MIN_KB));
-        const long long dp = (tiles % grid == 0) ? tiles / grid : std::max<long long>(0, tiles / grid - 1);
-        const long long sk = iters - dp * grid * num_kb;
-        // partial store/read + flag round trip, and the L2-locality loss of spreading the tail
-        cost = ((double)dp * num_kb + (double)((sk + grid - 1) / grid)) * cyc + (sk > 0 ? 12000.0 : 0.0);
-        cost *= 1.15;
-      }
-      if (cost < best_cost) { best_cost = cost; best = Plan{bn, skm, grid}; }
+    // (a) whole tiles only
+    if (force_sched != 2) {
+      const int grid = (int)std::min<long long>(num_sms, tiles);
+      const double cost = (double)((tiles + grid - 1) / grid) * num_kb * cyc;
+      if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, grid}; }
+    }
+    // (b) floor(tiles/G) whole-tile rounds + the remainder split over up to MAX_SPLIT CTAs per tile
+    // The stream-K tail is opt-in (gemm_sched = 2): measured on B200 its fixup costs ~15-25 us per
+    // launch at these sizes, more than the idle-SM time it recovers (tools/gemm_micro.py).
+    if (force_sched == 2 && tiles % num_sms != 0) {
+      const long long dp = tiles / num_sms, rem = tiles - dp * num_sms;
+      const long long sk_iters = rem * num_kb;
+      const int sk_ctas = (int)std::max<long long>(
+          1, std::min<long long>(std::min<long long>(num_sms, rem * MAX_SPLIT), sk_iters / MIN_KB));
+      const int grid = dp > 0 ? num_sms : sk_ctas;
+      const double fixup = 6000.0;  // partial store + flag + partial reads, in MMA-cycle units
+      const double cost = (double)dp * num_kb * cyc + (double)((sk_iters + sk_ctas - 1) / sk_ctas) * cyc + fixup;
+      if (cost < best_cost) { best_cost = cost; best = Plan{bn, sk_ctas, grid}; }
     }
   }
   return best;
@@ -448,7 +454,7 @@ static cb_status launch_kind(cb_ctx* c, const void* A, int lda, const void* B, i
   CB_TRY(get_tmap(c, B, b_rows, K, ldb, sw ? BN / 2 : BN, &tb));
   const int m_tiles = (M + BM - 1) / BM, n_tiles = (e.N + out_n - 1) / out_n;
   gemm_tc_kernel<KIND, BN><<<pl.grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, M, K, m_tiles, n_tiles, e,
-                                                                       c->tmaps->part, c->tmaps->flags, pl.stream_k);
+                                                                       c->tmaps->part, c->tmaps->flags, pl.sk_ctas);
   CB_LAUNCHED(c);
   return CB_OK;
 }
