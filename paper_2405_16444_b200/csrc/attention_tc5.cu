@@ -351,11 +351,16 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   const int max_kt = (n_keys + BC - 1) / BC;
   const long long base = (long long)tiles * n_kv;
   int n_splits = 1;
-  if (base < 2LL * c->num_sms && c->attn_part != nullptr) {
-    n_splits = (int)std::min<long long>((3LL * c->num_sms + base - 1) / base, (max_kt + 1) / 2);
-    n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
-    n_splits = std::max(1, std::min(n_splits, 16));
+  if (c->attn_splits > 0) {
+    n_splits = c->attn_splits;
+  } else if (4 * base < 3LL * c->num_sms) {
+    // only when the (tile, head) grid leaves a quarter of the SMs idle: each split costs a CTA
+    // prologue and the LSE merge re-reads fp32 partials (tools/attn_micro.py)
+    n_splits = (int)std::min<long long>((c->num_sms + base - 1) / base, (max_kt + 1) / 2);
   }
+  if (c->attn_part == nullptr) n_splits = 1;
+  n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
+  n_splits = std::max(1, std::min(n_splits, 16));
   const int kt_per_split = (max_kt + n_splits - 1) / n_splits;
   CUtensorMap tk, tv;
   CB_TRY(kv_tmap(c, k, n_keys, &tk));

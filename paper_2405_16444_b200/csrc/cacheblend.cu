@@ -321,6 +321,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     c->gemm_sched = (int)value;
     return CB_OK;
   }
+  if (std::strcmp(name, "attn_splits") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 16, CB_E_INVALID_ARG, "attn_splits must be 0..16");
+    c->attn_splits = (int)value;
+    return CB_OK;
+  }
   if (std::strcmp(name, "attn_impl") == 0) {
     CB_REQUIRE(value >= 0 && value <= 3, CB_E_INVALID_ARG, "attn_impl must be 0..3");
     c->attn_impl = (int)value;

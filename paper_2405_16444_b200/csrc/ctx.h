@@ -51,6 +51,7 @@ struct cb_ctx {
   long long attn_part_rows;
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
+  int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
   int* tok_d;       // [T] request-mode device copies of tokens / positions
   int* pos_d;       // [T]
   long long launches;
