@@ -48,7 +48,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *                 1 = data-parallel only, 2 = data-parallel rounds + stream-K tail
  *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width
  *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM, 3 = mma.sync (legacy tensor path)
- *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor of the tcgen05 attention */
+ *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor of the tcgen05 attention
+ *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */

@@ -173,6 +173,7 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->attn = cv.take<void>((size_t)T * qd * B);
   o->act = cv.take<void>((size_t)T * m->d_ff * B);
   o->dev = cv.take<float>((size_t)T * 4);
+  o->dev_part = cv.take<float>((size_t)2 * m->n_kv_heads * T * 4);
   o->row_tok[0] = cv.take<int>((size_t)T * 4);
   o->row_tok[1] = cv.take<int>((size_t)T * 4);
   o->qrow = cv.take<int>((size_t)T * 4);
@@ -319,6 +320,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "gemm_sched") == 0) {
     CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_sched must be 0, 1 or 2");
     c->gemm_sched = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "fuse_deviation") == 0) {
+    c->no_fuse_dev = value == 0;
     return CB_OK;
   }
   if (std::strcmp(name, "attn_splits") == 0) {
@@ -487,11 +492,19 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   EpiParams e{};
   e.kind = EPI_QKV; e.M = R; e.N = qd + 2 * kvd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
   e.q_out = c->q; e.k_out = c->kf; e.v_out = c->vf; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  // 2. Delta_kv against the loaded entries: fused into the tcgen05 QKV epilogue when every
+  //    k/v head lies inside one output tile, else a separate kernel
+  const bool fuse_dev = m.dtype == CB_BF16 && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e) && qd % 256 == 0 &&
+                        256 % m.head_dim == 0 && n_cand > 0 && !c->no_fuse_dev;
+  if (fuse_dev) {
+    e.k_ref = kb; e.v_ref = vb; e.dev_part = c->dev_part; e.n_cand = n_cand; e.ld_part = c->max_tokens;
+  }
   CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, R, d, e, 0, s));
-  // 2-3. Delta_kv against the loaded entries, HKVD = top-k
+  // 3. HKVD = top-k of Delta_kv (Insight 1)
   float* dev = dev_out ? dev_out : c->dev;
-  CB_TRY(launch_deviation(c, c->kf, c->vf, kb, vb, b.row_tok, n_cand, dev_mode, dev, s));
-  CB_TRY(launch_topk(c, dev, b.row_tok, n_cand, k, n_suf, N, force_sel, c->qrow, b.qtok, sel_tok, s));
+  if (!fuse_dev) CB_TRY(launch_deviation(c, c->kf, c->vf, kb, vb, b.row_tok, n_cand, dev_mode, dev, s));
+  CB_TRY(launch_topk(c, dev, b.row_tok, n_cand, k, n_suf, N, force_sel, c->qrow, b.qtok, sel_tok, s,
+                     fuse_dev ? c->dev_part : nullptr, c->max_tokens, dev_mode));
   if (Q == 0) return CB_OK;
   // 4. only the KV of the HKVD tokens (and the suffix) is updated (R3)
   CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));

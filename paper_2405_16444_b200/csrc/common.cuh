@@ -77,6 +77,9 @@ struct EpiParams {
   void* q_out; void* k_out; void* v_out;
   int col0, qd, kvd, hd;
   const int* row_tok; const int* pos; const float2* rope_tab;
+  // EPI_QKV fused Delta_kv (tcgen05 path): for candidate rows m < n_cand, per kv head h
+  // dev_part[(2h + 0) * ld_part + m] = ||k_m,h - k_ref[row_tok[m], h]||^2, [(2h + 1) ...] the same for v
+  const void* k_ref; const void* v_ref; float* dev_part; int n_cand, ld_part;
   // EPI_RESID
   float* h_out; const float* h_in; const int* res_row;
   // EPI_SWIGLU

@@ -42,6 +42,7 @@ struct cb_ctx {
   void* attn;       // [T][qd]
   void* act;        // [T][ff]
   float* dev;       // [T]
+  float* dev_part;  // [2 n_kv][T] fused-deviation partials (QKV epilogue)
   int* row_tok[2];  // [T] token index of each current row (candidates, then suffix)
   int* qrow;        // [T] row (in the current compact buffers) of each kept query
   int* iota;        // [T] 0..T-1
@@ -52,6 +53,7 @@ struct cb_ctx {
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
+  int no_fuse_dev;  // cb_set_option("fuse_deviation", 0) disables the QKV-epilogue deviation
   int* tok_d;       // [T] request-mode device copies of tokens / positions
   int* pos_d;       // [T]
   long long launches;
@@ -121,8 +123,11 @@ cb_status launch_local_pos(cb_ctx* c, const int* chunk_start_host, int n_chunks,
 cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* sel_row, cudaStream_t s);
 cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, const void* k_ref, const void* v_ref,
                            const int* cand_tok, int n_cand, int dev_mode, float* dev, cudaStream_t s);
-cb_status launch_topk(cb_ctx* c, const float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix,
-                      int N, const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s);
+// dev_part != NULL: Delta_kv is first summed from the QKV epilogue's per-(kv head, k|v) partials
+// [2 n_kv][ld_part] into dev (fixed head order, dev_mode selects K / V / both).
+cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix,
+                      int N, const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s,
+                      const float* dev_part = nullptr, int ld_part = 0, int dev_mode = CB_DEV_KV);
 // GEMM: acc = A[M][K] . B[N_b][K]^T; for SWIGLU B holds 2*ff rows and e.N = ff.
 // impl: 0 auto, 1 simt, 2 tcgen05.
 cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,

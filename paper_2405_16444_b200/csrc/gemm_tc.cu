@@ -53,10 +53,27 @@ __device__ __forceinline__ void st_bf16x16(bf16* p, const float* o) {
   reinterpret_cast<uint4*>(p)[1] = w1;
 }
 
-// Epilogue for 16 consecutive output columns n..n+15 of row m (all < N; N % 16 == 0).
+// sum over 16 columns of (x - ref)^2, ref = 16 bf16 at p (fused Delta_kv, R1)
+__device__ __forceinline__ float sqdiff16(const float* x, const bf16* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  const uint4 r0 = __ldg(q), r1 = __ldg(q + 1);
+  const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+    const float d0 = x[2 * i] - f.x, d1 = x[2 * i + 1] - f.y;
+    s += d0 * d0 + d1 * d1;
+  }
+  return s;
+}
+
+// Epilogue for 16 consecutive output columns n..n+15 of row m (all < N; N % 16 == 0). For EPI_QKV
+// with fused deviation it returns this chunk's squared distance to the cached K/V row.
 template <int KIND>
-__device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const float* v, const float* u) {
+__device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const float* v, const float* u) {
   float o[16];
+  float dev = 0.f;
   if constexpr (KIND == EPI_STORE) {
     st_bf16x16(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + n, v);
   } else if constexpr (KIND == EPI_STORE_F32) {
@@ -81,8 +98,13 @@ __device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const fl
       bf16* dst = (c < e.qd) ? reinterpret_cast<bf16*>(e.q_out) + (size_t)m * e.qd + c
                              : reinterpret_cast<bf16*>(e.k_out) + (size_t)m * e.kvd + (c - e.qd);
       st_bf16x16(dst, o);
+      if (c >= e.qd && e.dev_part != nullptr && m < e.n_cand)
+        dev = sqdiff16(o, reinterpret_cast<const bf16*>(e.k_ref) + (size_t)__ldg(e.row_tok + m) * e.kvd + (c - e.qd));
     } else {
       st_bf16x16(reinterpret_cast<bf16*>(e.v_out) + (size_t)m * e.kvd + (c - e.qd - e.kvd), v);
+      if (e.dev_part != nullptr && m < e.n_cand)
+        dev = sqdiff16(v, reinterpret_cast<const bf16*>(e.v_ref) + (size_t)__ldg(e.row_tok + m) * e.kvd +
+                              (c - e.qd - e.kvd));
     }
   } else if constexpr (KIND == EPI_RESID) {
     const int src = e.res_row ? __ldg(e.res_row + m) : m;
@@ -99,6 +121,7 @@ __device__ __forceinline__ void epi16(const EpiParams& e, int m, int n, const fl
     for (int i = 0; i < 16; ++i) o[i] = v[i] / (1.f + __expf(-v[i])) * u[i];
     st_bf16x16(reinterpret_cast<bf16*>(e.act) + (size_t)m * e.ff + n, o);
   }
+  return dev;
 }
 
 // Data-parallel rounds followed by an optional stream-K tail; every role walks the identical sequence.
@@ -260,6 +283,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m0 = (tile % m_tiles) * BM, nb = tile / m_tiles;
       const bool final_piece = (kb1 == num_kb);
       const int n_con = (final_piece && kb0 > 0) ? sch.contributors(tile, contrib) : 0;
+      float dacc = 0.f;  // fused deviation: running squared distance of the current k/v head
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const int m = m0 + row;
@@ -332,7 +356,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 16; ++i) { v[i] = sv[i] + v[i]; u[i] = su[i] + u[i]; }
           }
           const int n = nb * OUT_N + c;
-          if (m < M && n < e.N) epi16<KIND>(e, m, n, v, u);
+          if (m < M && n < e.N) {
+            const float d = epi16<KIND>(e, m, n, v, u);
+            if constexpr (KIND == EPI_QKV) {
+              // a k or v head ends at this chunk: publish its deviation partial (fixed in-thread order)
+              dacc += d;
+              const int cl = e.col0 + n;
+              if (e.dev_part != nullptr && cl >= e.qd && (cl + 16) % e.hd == 0) {
+                const int kv_col = cl - e.qd;
+                const int slot = kv_col < e.kvd ? 2 * (kv_col / e.hd) : 2 * ((kv_col - e.kvd) / e.hd) + 1;
+                if (m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc;
+                dacc = 0.f;
+              }
+            }
+          }
         }
         if (n_con > 0) {  // release the contributors' slots for the next launch
           named_bar(1, 128);

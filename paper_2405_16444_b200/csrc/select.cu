@@ -115,17 +115,32 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sm_warp, int* total) 
   return r;
 }
 
-__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float* __restrict__ dev,
+__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ dev,
                                                             const int* __restrict__ cand_tok, int n_cand, int k,
                                                             int n_suf, int N, const int* __restrict__ force_sel,
                                                             int* __restrict__ qrow, int* __restrict__ qtok,
-                                                            int* __restrict__ sel_tok, int* err) {
+                                                            int* __restrict__ sel_tok, int* err,
+                                                            const float* __restrict__ dev_part, int n_kv, int ld_part,
+                                                            int dev_mode) {
   extern __shared__ unsigned keys[];
   __shared__ int hist[256];
   __shared__ int sm_warp[32];
   __shared__ int sm_total;
   __shared__ int sm_digit, sm_rem;
   const int tid = threadIdx.x;
+
+  if (dev_part != nullptr) {  // Delta_kv from the QKV epilogue's per-(head, k|v) partials, fixed head order
+    for (int j = tid; j < n_cand; j += blockDim.x) {
+      float tot = 0.f;
+      for (int h = 0; h < n_kv; ++h) {
+        const float a = dev_mode != CB_DEV_V ? dev_part[(size_t)(2 * h) * ld_part + j] : 0.f;
+        const float b = dev_mode != CB_DEV_K ? dev_part[(size_t)(2 * h + 1) * ld_part + j] : 0.f;
+        tot += a + b;
+      }
+      dev[j] = tot;
+    }
+    __syncthreads();
+  }
 
   // suffix rows are always kept
   for (int s = tid; s < n_suf; s += blockDim.x) {
@@ -229,14 +244,15 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float* __restr
   }
 }
 
-cb_status launch_topk(cb_ctx* c, const float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix, int N,
-                      const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s) {
+cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix, int N,
+                      const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s,
+                      const float* dev_part, int ld_part, int dev_mode) {
   CB_REQUIRE(n_cand <= TOPK_MAX_CAND, CB_E_SHAPE, "top-k: n_cand %d exceeds %d", n_cand, TOPK_MAX_CAND);
-  if (k_keep + n_suffix == 0) return CB_OK;
+  if (k_keep + n_suffix == 0 && (dev_part == nullptr || n_cand == 0)) return CB_OK;
   const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
   ProfScope ps_(c, PROF_TOPK, s);
   topk_kernel<<<1, TOPK_THREADS, smem, s>>>(dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
-                                            c->err_word);
+                                            c->err_word, dev_part, c->m.n_kv_heads, ld_part, dev_mode);
   CB_LAUNCHED(c);
   return CB_OK;
 }
