@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of one CUDA graph per step")
+    ap.add_argument("--no-pdl", action="store_true", help="disable programmatic dependent launch")
     return ap.parse_args()
 
 
@@ -256,6 +257,8 @@ def run_ours(args):
     N, L, kvd = req.n_ctx, s.n_layers, s.kvd
     dev = torch.device("cuda", local)
     ctx = P.Context(s, "bf16", max_tokens=max(N, max(lens)), max_pos=max(2 * N, 4096))
+    if args.no_pdl:
+        ctx.set_option("pdl", 0)
     mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
     tok_h = req.tokens(s.vocab)
     tok = torch.from_numpy(tok_h).to(dev)

@@ -47,13 +47,19 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "gemm_sched"  0 = auto (cost model picks data-parallel or data-parallel + stream-K tail),
  *                 1 = data-parallel only, 2 = data-parallel rounds + stream-K tail
  *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width
+ *   "gemm_pair"   0 = auto, 1 = CTA-pair (cta_group::2, 256-row tiles) only, 2 = single-CTA only
  *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM, 3 = mma.sync (legacy tensor path)
  *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor of the tcgen05 attention
- *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel */
+ *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
+ *   "debug_trace" 1 = record clock64 pipeline events of one CTA of the tcgen05 attention (tuning)
+ *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */
 CB_API int64_t cb_launch_count(cb_ctx* ctx);
+
+/* Copy n (<= 2048) int64 entries of the debug_trace buffer to host memory. Blocking. */
+CB_API cb_status cb_debug_fetch(cb_ctx* ctx, int64_t* host, int32_t n);
 
 /* Per-launch profile: between begin and end every library launch is bracketed by a CUDA event pair
  * on its stream. cb_profile_end synchronises the device and writes, per kernel class

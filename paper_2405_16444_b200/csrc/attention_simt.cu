@@ -11,6 +11,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
                                                         const int* __restrict__ q_tok, int n_rows,
                                                         const T* __restrict__ k, const T* __restrict__ v, int n_keys,
                                                         T* __restrict__ out, int n_q, int n_kv, int hd, float scale) {
+  pdl_enter();
   __shared__ float qs[4][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x, h = blockIdx.y * 4 + warp;
@@ -62,19 +63,20 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const T* __restrict__ q,
 }
 
 template <typename T>
-void launch_t(const cb_model& md, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
+cb_status launch_t(cb_ctx* c, const cb_model& md, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
               const void* v, int n_keys, void* out, cudaStream_t s) {
   dim3 grid(n_rows, (md.n_q_heads + 3) / 4);
   const float scale = 1.0f / sqrtf((float)md.head_dim);
   const int dpl = (md.head_dim + 31) / 32;
 #define L_(D)                                                                                              \
-  attn_simt_kernel<T, D><<<grid, 128, 0, s>>>((const T*)q, q_row, q_tok, n_rows, (const T*)k, (const T*)v, n_keys, \
+  CB_LAUNCH(c, (attn_simt_kernel<T, D>), grid, 128, 0, s, (const T*)q, q_row, q_tok, n_rows, (const T*)k, (const T*)v, n_keys, \
                                               (T*)out, md.n_q_heads, md.n_kv_heads, md.head_dim, scale)
   if (dpl <= 1) L_(1);
   else if (dpl <= 2) L_(2);
   else if (dpl <= 4) L_(4);
   else L_(8);
 #undef L_
+  return CB_OK;
 }
 }  // namespace
 
@@ -84,9 +86,9 @@ cb_status launch_attention_simt(cb_ctx* c, const void* q, const int* q_row, cons
   CB_REQUIRE(c->m.head_dim <= 256, CB_E_UNSUPPORTED, "attention: head_dim > 256");
   ProfScope ps_(c, PROF_ATTN, s);
   if (c->m.dtype == CB_BF16)
-    launch_t<bf16>(c->m, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
+    CB_TRY(launch_t<bf16>(c, c->m, q, q_row, q_tok, n_rows, k, v, n_keys, out, s));
   else
-    launch_t<float>(c->m, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
+    CB_TRY(launch_t<float>(c, c->m, q, q_row, q_tok, n_rows, k, v, n_keys, out, s));
   CB_LAUNCHED(c);
   return CB_OK;
 }

@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
                                                       int n_keys, bf16* __restrict__ out, int n_q, int n_kv,
                                                       float scale_log2, int kt_per_split, float* __restrict__ opart,
                                                       float2* __restrict__ ml) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t sQ = (uint32_t)__cvta_generic_to_shared(sm);
   const uint32_t sK0 = sQ + BR * HD * 2;  // K[2], then V[2]
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(NT) attn_mma_kernel(const bf16* __restrict__ q
 // m* = max m_s, l* = sum l_s 2^(m_s - m*), O = sum O_s 2^(m_s - m*) / l*.
 __global__ void attn_merge_kernel(const float* __restrict__ opart, const float2* __restrict__ ml, int R, int n_kv,
                                   int G, int n_splits, bf16* __restrict__ out, int qd) {
+  pdl_enter();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= R * n_kv) return;
   const int g = w / R, rho = w - g * R;
@@ -274,7 +276,7 @@ cb_status launch_attention_merge(cb_ctx* c, int R, int n_splits, void* out, cuda
   const int n_kv = c->m.n_kv_heads, G = c->m.n_q_heads / n_kv;
   const int warps = R * n_kv;
   ProfScope ps_(c, PROF_ATTN, s);
-  attn_merge_kernel<<<(warps + 7) / 8, 256, 0, s>>>(c->attn_part, c->attn_ml, R, n_kv, G, n_splits, (bf16*)out,
+  CB_LAUNCH(c, (attn_merge_kernel), (warps + 7) / 8, 256, 0, s, c->attn_part, c->attn_ml, R, n_kv, G, n_splits, (bf16*)out,
                                                     c->m.n_q_heads * HD);
   CB_LAUNCHED(c);
   return CB_OK;
@@ -302,7 +304,7 @@ cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const 
   dim3 grid(tiles, n_kv, n_splits);
   ProfScope ps_(c, PROF_ATTN, s);
   float* opart = n_splits > 1 ? c->attn_part : nullptr;
-  attn_mma_kernel<<<grid, NT, SMEM, s>>>((const bf16*)q, q_row, q_tok, n_rows, (const bf16*)k, (const bf16*)v, n_keys,
+  CB_LAUNCH(c, (attn_mma_kernel), grid, NT, SMEM, s, (const bf16*)q, q_row, q_tok, n_rows, (const bf16*)k, (const bf16*)v, n_keys,
                                          (bf16*)out, c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart,
                                          c->attn_ml);
   CB_LAUNCHED(c);

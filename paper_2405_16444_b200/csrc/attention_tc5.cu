@@ -10,10 +10,12 @@
 //   warp 1     MMA issuer: S_t = Q K_t^T (M=128, N=128 keys, K=16) into one of two TMEM S buffers,
 //              then O += P_t V_t (A = P from shared memory, B = V MN-major) into the TMEM O buffer.
 //              S_{t+1} is issued before waiting for P_t, so QK^T overlaps the softmax of tile t.
-//   warps 2-5  softmax, one thread per query row: tcgen05.ld its S row (128 fp32), mask by original
-//              position, online softmax in the log2 domain with lazy rescaling (O is rescaled in
-//              TMEM only when the row max grows by more than 2^8), P (bf16) into shared memory in
-//              the K-major SWIZZLE_128B layout the MMA reads; finally O / l (or the split partial).
+//   warps 2-9  softmax: two warpgroups, thread = (query row, 64-key half). Each tcgen05.lds its half of
+//              the S row, masks by original position, and the two halves agree on the row max through
+//              shared memory; online softmax in the log2 domain with lazy rescaling (O is rescaled in
+//              TMEM only when the row max grows by more than 2^8); P (bf16) goes to shared memory in
+//              the K-major SWIZZLE_128B layout the MMA reads (one column block per half); finally
+//              O / l (or the split partial), each half writing its 64 output columns.
 // Key tiles past the CTA's last query token are never loaded; only tiles reaching past its first
 // query token are masked. Heaviest (latest-token) tiles are scheduled first.
 #include <cudaTypedefs.h>
@@ -24,12 +26,15 @@
 #include "tc_common.cuh"
 
 namespace {
-constexpr int HD = 128, BM = 128, BC = 128, NT = 192;
+constexpr int HD = 128, BM = 128, BC = 128, NT = 320;
 constexpr int ATOM = 128 * 128;    // 128 rows x 128 B (64 bf16): one SWIZZLE_128B column block
 constexpr int TILE = 2 * ATOM;     // 128 rows x 128 bf16
-constexpr int SMEM = 6 * TILE + 1024 + 256;  // Q, K[2], V[2], P + alignment + barriers
+constexpr int SMEM = 6 * TILE + 1024 + 256 + 3072;  // Q, K[2], V[2], P + alignment + barriers + exchange
 constexpr float RESCALE_THRESHOLD = 8.0f;    // log2 units
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ~2 ulp; ex2(-inf) = 0
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -48,7 +53,10 @@ __global__ void __launch_bounds__(NT, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
                     int n_rows, int n_keys, bf16* __restrict__ out, int n_q, int n_kv, float scale_log2,
-                    int kt_per_split, float* __restrict__ opart, float2* __restrict__ ml) {
+                    int kt_per_split, float* __restrict__ opart, float2* __restrict__ ml, long long* __restrict__ dbg) {
+  pdl_enter();
+  const bool dbg_on = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#define DBG(i) do { if (dbg_on && (i) < 2048) dbg[i] = clock64(); } while (0)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -56,14 +64,16 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sV = smem + 3 * TILE;      // [2] stages
   uint8_t* sP = smem + 5 * TILE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
-  uint64_t* kv_full = bars;           // [2]
-  uint64_t* kv_empty = bars + 2;      // [2]
+  uint64_t* k_full = bars;            // [2]  K tile landed
+  uint64_t* k_empty = bars + 2;       // [2]  S MMAs done reading the K stage
+  uint64_t* v_full = bars + 11;       // [2]  V tile landed
+  uint64_t* v_empty = bars + 13;      // [2]  PV MMAs done reading the V stage
   uint64_t* s_full = bars + 4;        // [2]
   uint64_t* s_empty = bars + 6;       // [2]
   uint64_t* q_full = bars + 8;
   uint64_t* p_full = bars + 9;
   uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.y, G = n_q / n_kv, R = n_rows * G;
@@ -92,13 +102,15 @@ __global__ void __launch_bounds__(NT, 1)
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
     for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&kv_full[b], 1);
-      tc::mbar_init(&kv_empty[b], 1);
+      tc::mbar_init(&k_full[b], 1);
+      tc::mbar_init(&k_empty[b], 1);
+      tc::mbar_init(&v_full[b], 1);
+      tc::mbar_init(&v_empty[b], 1);
       tc::mbar_init(&s_full[b], 1);
-      tc::mbar_init(&s_empty[b], 4);
+      tc::mbar_init(&s_empty[b], 8);
     }
-    tc::mbar_init(q_full, 128);
-    tc::mbar_init(p_full, 4);
+    tc::mbar_init(q_full, 256);
+    tc::mbar_init(p_full, 8);
     tc::mbar_init(pv_done, 1);
     tc::fence_barrier_init();
   }
@@ -106,20 +118,26 @@ __global__ void __launch_bounds__(NT, 1)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  DBG(1200);
   const uint32_t tmem = *tmem_slot;  // S0: cols [0,128), S1: [128,256), O: [256,384)
 
   if (warp == 0) {
-    // ===== TMA producer: K_t, V_t =====
+    // ===== TMA producer: K_t as soon as S_{t-2} released its stage, V_t once PV_{t-2} did, so K runs
+    // about one tile ahead of V (S_t needs K_t long before PV_t needs V_t) =====
     if (tc::elect_one()) {
+      auto load = [&](uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int key0) {
+        tc::mbar_arrive_expect_tx(bar, TILE);
+        tc::tma_load_3d(dst, m, bar, 0, g, key0);
+        tc::tma_load_3d(dst + ATOM, m, bar, 64, g, key0);
+      };
       for (int t = 0; t < nt; ++t) {
-        const int b = t & 1;
-        if (t >= 2) tc::mbar_wait(&kv_empty[b], ((t >> 1) - 1) & 1);
-        tc::mbar_arrive_expect_tx(&kv_full[b], 2 * TILE);
-        const int key0 = (jb + t) * BC;
-        tc::tma_load_3d(sK + b * TILE, &tmK, &kv_full[b], 0, g, key0);
-        tc::tma_load_3d(sK + b * TILE + ATOM, &tmK, &kv_full[b], 64, g, key0);
-        tc::tma_load_3d(sV + b * TILE, &tmV, &kv_full[b], 0, g, key0);
-        tc::tma_load_3d(sV + b * TILE + ATOM, &tmV, &kv_full[b], 64, g, key0);
+        const int b = t & 1, key0 = (jb + t) * BC;
+        if (t >= 2) tc::mbar_wait(&k_empty[b], ((t >> 1) - 1) & 1);
+        DBG(4 * t);
+        load(sK + b * TILE, &tmK, &k_full[b], key0);
+        if (t >= 2) tc::mbar_wait(&v_empty[b], ((t >> 1) - 1) & 1);
+        DBG(4 * t + 1);
+        load(sV + b * TILE, &tmV, &v_full[b], key0);
       }
     }
   } else if (warp == 1) {
@@ -129,8 +147,9 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t tO = tmem + 256;
     auto issue_s = [&](int t) {
       const int b = t & 1;
-      tc::mbar_wait(&kv_full[b], (t >> 1) & 1);
+      tc::mbar_wait(&k_full[b], (t >> 1) & 1);
       if (t >= 2) tc::mbar_wait(&s_empty[b], ((t >> 1) - 1) & 1);
+      if (lane == 0) DBG(400 + 4 * t);
       tc::fence_after();
       if (tc::elect_one()) {
 #pragma unroll
@@ -140,6 +159,7 @@ __global__ void __launch_bounds__(NT, 1)
           tc::mma_bf16(tmem + b * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
         }
         tc::mma_commit(&s_full[b]);
+        tc::mma_commit(&k_empty[b]);
       }
       __syncwarp();
     };
@@ -148,6 +168,8 @@ __global__ void __launch_bounds__(NT, 1)
     for (int t = 0; t < nt; ++t) {
       if (t + 1 < nt) issue_s(t + 1);
       tc::mbar_wait(p_full, t & 1);
+      tc::mbar_wait(&v_full[t & 1], (t >> 1) & 1);
+      if (lane == 0) DBG(400 + 4 * t + 1);
       tc::fence_after();
       if (tc::elect_one()) {
         const int b = t & 1;
@@ -158,23 +180,29 @@ __global__ void __launch_bounds__(NT, 1)
           tc::mma_bf16(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(pv_done);
-        tc::mma_commit(&kv_empty[b]);
+        tc::mma_commit(&v_empty[b]);
       }
       __syncwarp();
     }
   } else {
-    // ===== softmax / correction / epilogue: thread = query row =====
+    // ===== softmax / correction / epilogue: two warpgroups, each owns one 64-key half of every row
+    // (thread = (row, half)); the halves agree on the row max through shared memory every tile =====
+    const int wg = (warp - 2) >> 2;              // 0: keys / O columns 0..63, 1: 64..127
     const int r = (warp & 3) * 32 + lane;
+    const int et = threadIdx.x - 64;             // 0..255 among softmax threads
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int rho = rho0 + r;
     const bool valid = rho < R;
     const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
     const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
-    {  // stage this row of Q
+    float* xmax = reinterpret_cast<float*>(bars + 16);  // [2 parity][2 wg][128 rows], then l [2][128]
+    float* xl = xmax + 512;
+    {  // stage this row's half of Q (one SWIZZLE_128B column block)
       const bf16* src = q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD;
       const uint32_t dq = tc::smem_u32(sQ);
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const int ch = wg * 8 + c8;
         const int sz = valid ? 16 : 0;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dq + sw_off(r, ch)), "l"(src + ch * 8),
                      "r"(sz)
@@ -183,43 +211,50 @@ __global__ void __launch_bounds__(NT, 1)
       asm volatile("cp.async.wait_all;" ::: "memory");
       tc::fence_proxy_async();
       tc::mbar_arrive(q_full);
+      if (et == 0) DBG(1201);
     }
     float m_used = -INFINITY, l = 0.f;
     const uint32_t dp = tc::smem_u32(sP);
     for (int t = 0; t < nt; ++t) {
       const int b = t & 1;
       tc::mbar_wait(&s_full[b], (t >> 1) & 1);
+      if (et == 0) DBG(800 + 4 * t);
       tc::fence_after();
-      float s[128];
+      float s[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float x[32];
-        tc::tmem_ld32(tmem + lane_base + b * 128 + c * 32, x);
+        tc::tmem_ld32(tmem + lane_base + b * 128 + wg * 64 + c * 32, x);
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = x[i];
       }
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&s_empty[b]);
-      const int key0 = (jb + t) * BC;
-      const bool need_mask = key0 + BC - 1 > kmin;
-      // row max of the raw scores (scale > 0 commutes with max); 8 independent chains for ILP
+      const int key0 = (jb + t) * BC + wg * 64;
+      const bool need_mask = key0 + 63 > kmin;
+      // half-row max of the raw scores (scale > 0 commutes with max); 8 chains for ILP
       float mx8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
       if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
+        for (int i = 0; i < 64; ++i) {
           if (key0 + i > tok) s[i] = -INFINITY;
           mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+        for (int i = 0; i < 64; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
       }
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
-      // lazy rescale: move the reference max only when it grew by more than 2^8
+      const float hmx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      xmax[(b * 2 + wg) * 128 + r] = hmx;
+      named_bar_sync(1, 256);
+      const float mx = fmaxf(hmx, xmax[(b * 2 + (wg ^ 1)) * 128 + r]) * scale_log2;
+      if (et == 0) DBG(800 + 4 * t + 1);
+      // lazy rescale (identical decision in both halves): move the reference max only when it grew
+      // by more than 2^8
       float corr = 1.f;
       if (mx > m_used + RESCALE_THRESHOLD || (m_used == -INFINITY && mx != -INFINITY)) {
         if (m_used != -INFINITY) corr = ex2(m_used - mx);
@@ -231,75 +266,84 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) rs8[i] = 0.f;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
+      for (int i = 0; i < 64; ++i) {
         s[i] = ex2(fmaf(s[i], scale_log2, nref));  // -inf -> 0
         rs8[i & 7] += s[i];
       }
       l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
       if (t >= 1) {  // PV_{t-1} done: the P buffer is free and O is stable
         tc::mbar_wait(pv_done, (t - 1) & 1);
+        if (et == 0) DBG(800 + 4 * t + 2);
         tc::fence_after();
         if (__any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write of O
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             float o[32];
-            tc::tmem_ld32(tmem + lane_base + 256 + c * 32, o);
+            tc::tmem_ld32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] *= corr;
-            tc::tmem_st32(tmem + lane_base + 256 + c * 32, o);
+            tc::tmem_st32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
           }
           tc::tmem_st_wait();
         }
       }
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
+      for (int c8 = 0; c8 < 8; ++c8) {
         uint4 w;
-        w.x = pack2(s[ch * 8 + 0], s[ch * 8 + 1]);
-        w.y = pack2(s[ch * 8 + 2], s[ch * 8 + 3]);
-        w.z = pack2(s[ch * 8 + 4], s[ch * 8 + 5]);
-        w.w = pack2(s[ch * 8 + 6], s[ch * 8 + 7]);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dp + sw_off(r, ch)), "r"(w.x), "r"(w.y),
-                     "r"(w.z), "r"(w.w)
+        w.x = pack2(s[c8 * 8 + 0], s[c8 * 8 + 1]);
+        w.y = pack2(s[c8 * 8 + 2], s[c8 * 8 + 3]);
+        w.z = pack2(s[c8 * 8 + 4], s[c8 * 8 + 5]);
+        w.w = pack2(s[c8 * 8 + 6], s[c8 * 8 + 7]);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dp + sw_off(r, wg * 8 + c8)), "r"(w.x),
+                     "r"(w.y), "r"(w.z), "r"(w.w)
                      : "memory");
       }
       tc::fence_proxy_async();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full);
+      if (et == 0) DBG(800 + 4 * t + 3);
     }
+    // total row sum = both halves (same reference max)
+    xl[wg * 128 + r] = l;
+    named_bar_sync(1, 256);
+    l += xl[(wg ^ 1) * 128 + r];
     tc::mbar_wait(pv_done, (nt - 1) & 1);
     tc::fence_after();
-    float o[128];
+    float o[64];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       float x[32];
-      tc::tmem_ld32(tmem + lane_base + 256 + c * 32, x);
+      tc::tmem_ld32(tmem + lane_base + 256 + wg * 64 + c * 32, x);
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[c * 32 + i] = x[i];
     }
     if (valid) {
       if (opart != nullptr) {
-        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD);
+        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD + wg * 64);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-        ml[part_row0 + rho] = make_float2(m_used, l);
+        for (int i = 0; i < 16; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        if (wg == 0) ml[part_row0 + rho] = make_float2(m_used, l);
       } else {
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD);
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD + wg * 64);
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
+        for (int c8 = 0; c8 < 8; ++c8) {
           uint4 w;
-          w.x = pack2(o[ch * 8 + 0] * inv, o[ch * 8 + 1] * inv);
-          w.y = pack2(o[ch * 8 + 2] * inv, o[ch * 8 + 3] * inv);
-          w.z = pack2(o[ch * 8 + 4] * inv, o[ch * 8 + 5] * inv);
-          w.w = pack2(o[ch * 8 + 6] * inv, o[ch * 8 + 7] * inv);
-          dst[ch] = w;
+          w.x = pack2(o[c8 * 8 + 0] * inv, o[c8 * 8 + 1] * inv);
+          w.y = pack2(o[c8 * 8 + 2] * inv, o[c8 * 8 + 3] * inv);
+          w.z = pack2(o[c8 * 8 + 4] * inv, o[c8 * 8 + 5] * inv);
+          w.w = pack2(o[c8 * 8 + 6] * inv, o[c8 * 8 + 7] * inv);
+          dst[c8] = w;
         }
       }
     }
+    (void)et;
   }
   tc::fence_before();
   __syncthreads();
+  DBG(1202);
+#undef DBG
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
@@ -368,8 +412,9 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   dim3 grid(tiles, n_kv, n_splits);
   ProfScope ps_(c, PROF_ATTN, s);
   float* opart = n_splits > 1 ? c->attn_part : nullptr;
-  attn_tc5_kernel<<<grid, NT, SMEM, s>>>(tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
-                                         c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart, c->attn_ml);
+  CB_LAUNCH(c, (attn_tc5_kernel), grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
+                                         c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart, c->attn_ml,
+                                         c->dbg_buf);
   CB_LAUNCHED(c);
   if (n_splits > 1) CB_TRY(launch_attention_merge(c, R, n_splits, out, s));
   return CB_OK;

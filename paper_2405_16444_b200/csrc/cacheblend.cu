@@ -28,6 +28,7 @@ cb_status topk_init_attrs();
 cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
 void gemm_tc_force_bn(cb_ctx* c, int bn);
+void gemm_tc_force_pair(cb_ctx* c, int v);
 cb_status attention_tc_init();
 
 // ---- error reporting ------------------------------------------------------------------------------
@@ -194,6 +195,7 @@ __global__ void iota_kernel(int* p, int n) {
 
 // row_tok = [cand_tok..., N, N+1, ..., N+n_suf-1]
 __global__ void make_rows_kernel(const int* __restrict__ cand, int n_cand, int n_suf, int N, int* __restrict__ rows) {
+  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_cand + n_suf; i += gridDim.x * blockDim.x)
     rows[i] = i < n_cand ? cand[i] : N + (i - n_cand);
 }
@@ -217,6 +219,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   cb_ctx* c = new cb_ctx();  // value-initialised: pointers null, counters zero
   c->m = *model;
   c->max_tokens = max_tokens;
+  c->pdl = 1;
   cudaError_t e = cudaGetDevice(&c->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   int cc_major = 0, cc_minor = 0;
@@ -295,6 +298,7 @@ extern "C" cb_status cb_destroy(cb_ctx* c) {
   for (auto ev : c->layer_ev) if (ev) cudaEventDestroy(ev);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->dbg_buf) cudaFree(c->dbg_buf);
   gemm_tc_destroy(c);
   cudaFree(c->rope_tab);
   cudaFree(c->err_word);
@@ -315,11 +319,32 @@ extern "C" cb_status cb_check_device_errors(cb_ctx* c) {
 
 extern "C" int64_t cb_launch_count(cb_ctx* c) { return c ? c->launches : 0; }
 
+extern "C" cb_status cb_debug_fetch(cb_ctx* c, int64_t* host, int32_t n) {
+  CB_REQUIRE(c && host && n >= 0 && n <= 2048, CB_E_INVALID_ARG, "cb_debug_fetch: bad arguments");
+  CB_REQUIRE(c->dbg_buf != nullptr, CB_E_INVALID_ARG, "debug_trace is off");
+  CB_CUDA(cudaMemcpy(host, c->dbg_buf, (size_t)n * sizeof(long long), cudaMemcpyDeviceToHost));
+  return CB_OK;
+}
+
 extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   CB_REQUIRE(c != nullptr && name != nullptr, CB_E_INVALID_ARG, "ctx / name is NULL");
   if (std::strcmp(name, "gemm_sched") == 0) {
     CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_sched must be 0, 1 or 2");
     c->gemm_sched = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "pdl") == 0) {
+    c->pdl = value != 0;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "debug_trace") == 0) {
+    if (value && !c->dbg_buf) {
+      CB_CUDA(cudaMalloc(&c->dbg_buf, 2048 * sizeof(long long)));
+      CB_CUDA(cudaMemset(c->dbg_buf, 0, 2048 * sizeof(long long)));
+    } else if (!value && c->dbg_buf) {
+      cudaFree(c->dbg_buf);
+      c->dbg_buf = nullptr;
+    }
     return CB_OK;
   }
   if (std::strcmp(name, "fuse_deviation") == 0) {
@@ -334,6 +359,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "attn_impl") == 0) {
     CB_REQUIRE(value >= 0 && value <= 3, CB_E_INVALID_ARG, "attn_impl must be 0..3");
     c->attn_impl = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_pair") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_pair must be 0, 1 or 2");
+    gemm_tc_force_pair(c, (int)value);
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_bn") == 0) {
@@ -549,7 +579,7 @@ extern "C" cb_status cb_blend_layer(cb_ctx* c, int32_t layer, const cb_layer_w* 
   const int rows = n_cand + n_suffix;
   if (rows > 0) {
     ProfScope ps_(c, PROF_MISC, s);
-    make_rows_kernel<<<std::min(256, (rows + 255) / 256), 256, 0, s>>>(cand_tok, n_cand, n_suffix, N, c->row_tok[0]);
+    CB_LAUNCH(c, (make_rows_kernel), std::min(256, (rows + 255) / 256), 256, 0, s, cand_tok, n_cand, n_suffix, N, c->row_tok[0]);
     CB_LAUNCHED(c);
   }
   const size_t d = c->m.d_model;

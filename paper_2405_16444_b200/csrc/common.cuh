@@ -56,6 +56,19 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// ---- programmatic dependent launch -------------------------------------------------------------
+// Every library kernel is launched with programmatic stream serialization. pdl_wait() blocks until the
+// preceding kernel has completed and its memory is visible; pdl_trigger() lets the next kernel's CTAs
+// be scheduled (its prologue then overlaps this kernel's tail). Triggering once every CTA of this grid
+// is running cannot deadlock: the dependent grid launches only after all of this grid's CTAs executed
+// the trigger, i.e. are resident.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
 // Device-side error word bits (cb_check_device_errors).
 enum : int { CB_DEVERR_FORCE_SEL = 1, CB_DEVERR_POS_RANGE = 2 };
 

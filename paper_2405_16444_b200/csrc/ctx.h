@@ -54,6 +54,8 @@ struct cb_ctx {
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
   int no_fuse_dev;  // cb_set_option("fuse_deviation", 0) disables the QKV-epilogue deviation
+  long long* dbg_buf;  // cb_set_option("debug_trace", 1): per-event clock64 trace of one CTA (tuning)
+  int pdl;          // programmatic dependent launch between library kernels (cb_set_option("pdl"))
   int* tok_d;       // [T] request-mode device copies of tokens / positions
   int* pos_d;       // [T]
   long long launches;
@@ -110,6 +112,38 @@ void cb_set_error(const char* fmt, ...);
   } while (0)
 
 static inline size_t dtype_bytes(int dt) { return dt == CB_BF16 ? 2 : 4; }
+
+// Launch `kern` with programmatic stream serialization (PDL, when the context enables it) and an
+// optional cluster size. Every kernel launched this way must begin with pdl_wait()/pdl_enter().
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_k(const cb_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                   cudaStream_t s, int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (c->pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define CB_LAUNCH(ctx, kern, grid, block, smem, stream, ...) \
+  CB_CUDA(launch_k((ctx), kern, dim3(grid), dim3(block), (smem), (stream), 1, __VA_ARGS__))
 
 // ---- internal launchers (implemented per .cu file) ------------------------------------------
 cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out, const void* v_src,

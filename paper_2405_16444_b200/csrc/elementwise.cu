@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(256) realign_kernel(T* __restrict__ k_out, con
                                                       int n_slices, int n_tok, long long out_stride,
                                                       long long src_stride, int kvd, int hd,
                                                       const float2* __restrict__ tab, int max_pos, int* err) {
+  pdl_enter();
   constexpr int V = Vec16<T>::N;  // elements per vector
   const int nvec = kvd / V;
   const long long total = (long long)n_tok * nvec;
@@ -78,11 +79,11 @@ cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out,
   const int grid = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c->num_sms * 8));
   ProfScope ps_(c, PROF_REALIGN, s);
   if (c->m.dtype == CB_BF16)
-    realign_kernel<bf16, 4><<<grid, 256, 0, s>>>((bf16*)k_out, (const bf16*)k_src, (bf16*)v_out, (const bf16*)v_src,
+    CB_LAUNCH(c, (realign_kernel<bf16, 4>), grid, 256, 0, s, (bf16*)k_out, (const bf16*)k_src, (bf16*)v_out, (const bf16*)v_src,
                                                  src_pos, dst_pos, n_slices, n_tok, out_stride, src_stride, kvd,
                                                  c->m.head_dim, c->rope_tab, c->m.max_pos, c->err_word);
   else
-    realign_kernel<float, 4><<<grid, 256, 0, s>>>((float*)k_out, (const float*)k_src, (float*)v_out,
+    CB_LAUNCH(c, (realign_kernel<float, 4>), grid, 256, 0, s, (float*)k_out, (const float*)k_src, (float*)v_out,
                                                   (const float*)v_src, src_pos, dst_pos, n_slices, n_tok, out_stride,
                                                   src_stride, kvd, c->m.head_dim, c->rope_tab, c->m.max_pos,
                                                   c->err_word);
@@ -95,6 +96,7 @@ cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out,
 // ---------------------------------------------------------------------------------------------
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ tok, float* __restrict__ h, int d) {
+  pdl_enter();
   const int t = blockIdx.x;
   const T* src = emb + (size_t)__ldg(tok + t) * d;
   float* dst = h + (size_t)t * d;
@@ -109,9 +111,9 @@ cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, floa
   if (n == 0) return CB_OK;
   ProfScope ps_(c, PROF_EMBED, s);
   if (c->m.dtype == CB_BF16)
-    embed_kernel<bf16><<<n, 128, 0, s>>>((const bf16*)embed, tok, h, c->m.d_model);
+    CB_LAUNCH(c, (embed_kernel<bf16>), n, 128, 0, s, (const bf16*)embed, tok, h, c->m.d_model);
   else
-    embed_kernel<float><<<n, 128, 0, s>>>((const float*)embed, tok, h, c->m.d_model);
+    CB_LAUNCH(c, (embed_kernel<float>), n, 128, 0, s, (const float*)embed, tok, h, c->m.d_model);
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -137,6 +139,7 @@ constexpr int RMS_THREADS = 128, RMS_MAXV = 16;
 template <typename T>
 __global__ void __launch_bounds__(RMS_THREADS) rmsnorm_kernel(const float* __restrict__ h, const float* __restrict__ g,
                                                               T* __restrict__ x, int d, float eps) {
+  pdl_enter();
   const int r = blockIdx.x, tid = threadIdx.x;
   const float* hr = h + (size_t)r * d;
   float4 v[RMS_MAXV];
@@ -173,9 +176,9 @@ cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_row
              RMS_THREADS * RMS_MAXV * 4);
   ProfScope ps_(c, PROF_RMSNORM, s);
   if (c->m.dtype == CB_BF16)
-    rmsnorm_kernel<bf16><<<n_rows, RMS_THREADS, 0, s>>>(h, gain, (bf16*)x, c->m.d_model, c->m.rms_eps);
+    CB_LAUNCH(c, (rmsnorm_kernel<bf16>), n_rows, RMS_THREADS, 0, s, h, gain, (bf16*)x, c->m.d_model, c->m.rms_eps);
   else
-    rmsnorm_kernel<float><<<n_rows, RMS_THREADS, 0, s>>>(h, gain, (float*)x, c->m.d_model, c->m.rms_eps);
+    CB_LAUNCH(c, (rmsnorm_kernel<float>), n_rows, RMS_THREADS, 0, s, h, gain, (float*)x, c->m.d_model, c->m.rms_eps);
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -186,6 +189,7 @@ cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_row
 template <typename T>
 __global__ void scatter_kv_kernel(const T* __restrict__ kf, const T* __restrict__ vf, const int* __restrict__ qrow,
                                   const int* __restrict__ qtok, T* __restrict__ kb, T* __restrict__ vb, int kvd) {
+  pdl_enter();
   const int r = blockIdx.x;
   const size_t src = (size_t)__ldg(qrow + r) * kvd, dst = (size_t)__ldg(qtok + r) * kvd;
   for (int e = threadIdx.x * Vec16<T>::N; e < kvd; e += blockDim.x * Vec16<T>::N) {
@@ -200,9 +204,9 @@ cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int
   const int kvd = c->m.n_kv_heads * c->m.head_dim;
   ProfScope ps_(c, PROF_SCATTER, s);
   if (c->m.dtype == CB_BF16)
-    scatter_kv_kernel<bf16><<<n, 128, 0, s>>>((const bf16*)kf, (const bf16*)vf, qrow, qtok, (bf16*)kb, (bf16*)vb, kvd);
+    CB_LAUNCH(c, (scatter_kv_kernel<bf16>), n, 128, 0, s, (const bf16*)kf, (const bf16*)vf, qrow, qtok, (bf16*)kb, (bf16*)vb, kvd);
   else
-    scatter_kv_kernel<float><<<n, 128, 0, s>>>((const float*)kf, (const float*)vf, qrow, qtok, (float*)kb, (float*)vb,
+    CB_LAUNCH(c, (scatter_kv_kernel<float>), n, 128, 0, s, (const float*)kf, (const float*)vf, qrow, qtok, (float*)kb, (float*)vb,
                                                kvd);
   CB_LAUNCHED(c);
   return CB_OK;
@@ -217,6 +221,7 @@ struct ChunkTable {
 };
 
 __global__ void local_pos_kernel(ChunkTable ct, int base_chunk, int* __restrict__ src_pos) {
+  pdl_enter();
   const int t0 = ct.start[0], t1 = ct.start[ct.n];
   for (int t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
     int lo = 0, hi = ct.n - 1;  // largest c with start[c] <= t
@@ -237,13 +242,14 @@ cb_status launch_local_pos(cb_ctx* c, const int* cs, int n_chunks, int* src_pos,
     const int len = ct.start[ct.n] - ct.start[0];
     if (len <= 0) continue;
     ProfScope ps_(c, PROF_MISC, s);
-    local_pos_kernel<<<std::min(1024, (len + 255) / 256), 256, 0, s>>>(ct, b, src_pos);
+    CB_LAUNCH(c, (local_pos_kernel), std::min(1024, (len + 255) / 256), 256, 0, s, ct, b, src_pos);
     CB_LAUNCHED(c);
   }
   return CB_OK;
 }
 
 __global__ void sel_out_kernel(const int* __restrict__ qtok, int k, int N, int* __restrict__ row) {
+  pdl_enter();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x)
     row[j] = j < k ? qtok[j] : -1;
 }
@@ -251,7 +257,7 @@ __global__ void sel_out_kernel(const int* __restrict__ qtok, int k, int N, int* 
 cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* row, cudaStream_t s) {
   if (N == 0) return CB_OK;
   ProfScope ps_(c, PROF_MISC, s);
-  sel_out_kernel<<<std::min(256, (N + 255) / 256), 256, 0, s>>>(qtok, k, N, row);
+  CB_LAUNCH(c, (sel_out_kernel), std::min(256, (N + 255) / 256), 256, 0, s, qtok, k, N, row);
   CB_LAUNCHED(c);
   return CB_OK;
 }

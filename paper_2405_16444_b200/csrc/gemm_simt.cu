@@ -8,6 +8,7 @@ constexpr int BM = 64, BN = 64, BK = 16;
 template <typename T, bool SWIGLU>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A, int lda, const T* __restrict__ B,
                                                         int ldb, int M, int K, EpiParams e) {
+  pdl_enter();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   __shared__ float Bu[SWIGLU ? BK : 1][BN + 4];
@@ -67,11 +68,11 @@ cb_status launch_gemm_simt(cb_ctx* c, const void* A, int lda, const void* B, int
   const bool sw = e.kind == EPI_SWIGLU;
   ProfScope ps_(c, PROF_GEMM, s);
   if (c->m.dtype == CB_BF16) {
-    if (sw) gemm_simt_kernel<bf16, true><<<grid, 256, 0, s>>>((const bf16*)A, lda, (const bf16*)B, ldb, M, K, e);
-    else gemm_simt_kernel<bf16, false><<<grid, 256, 0, s>>>((const bf16*)A, lda, (const bf16*)B, ldb, M, K, e);
+    if (sw) CB_LAUNCH(c, (gemm_simt_kernel<bf16, true>), grid, 256, 0, s, (const bf16*)A, lda, (const bf16*)B, ldb, M, K, e);
+    else CB_LAUNCH(c, (gemm_simt_kernel<bf16, false>), grid, 256, 0, s, (const bf16*)A, lda, (const bf16*)B, ldb, M, K, e);
   } else {
-    if (sw) gemm_simt_kernel<float, true><<<grid, 256, 0, s>>>((const float*)A, lda, (const float*)B, ldb, M, K, e);
-    else gemm_simt_kernel<float, false><<<grid, 256, 0, s>>>((const float*)A, lda, (const float*)B, ldb, M, K, e);
+    if (sw) CB_LAUNCH(c, (gemm_simt_kernel<float, true>), grid, 256, 0, s, (const float*)A, lda, (const float*)B, ldb, M, K, e);
+    else CB_LAUNCH(c, (gemm_simt_kernel<float, false>), grid, 256, 0, s, (const float*)A, lda, (const float*)B, ldb, M, K, e);
   }
   CB_LAUNCHED(c);
   return CB_OK;

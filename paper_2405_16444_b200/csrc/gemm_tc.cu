@@ -23,6 +23,7 @@
 
 #include "ctx.h"
 #include "tc_common.cuh"
+#include "gemm_epi.cuh"
 
 namespace {
 constexpr int BM = 128, BK = 64, NUM_THREADS = 192;
@@ -39,90 +40,6 @@ template <int BN> struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN;
 };
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ void st_bf16x16(bf16* p, const float* o) {
-  uint4 w0, w1;
-  w0.x = pack_bf16(o[0], o[1]); w0.y = pack_bf16(o[2], o[3]); w0.z = pack_bf16(o[4], o[5]); w0.w = pack_bf16(o[6], o[7]);
-  w1.x = pack_bf16(o[8], o[9]); w1.y = pack_bf16(o[10], o[11]); w1.z = pack_bf16(o[12], o[13]);
-  w1.w = pack_bf16(o[14], o[15]);
-  reinterpret_cast<uint4*>(p)[0] = w0;
-  reinterpret_cast<uint4*>(p)[1] = w1;
-}
-
-// sum over 16 columns of (x - ref)^2, ref = 16 bf16 at p (fused Delta_kv, R1)
-__device__ __forceinline__ float sqdiff16(const float* x, const bf16* p) {
-  const uint4* q = reinterpret_cast<const uint4*>(p);
-  const uint4 r0 = __ldg(q), r1 = __ldg(q + 1);
-  const uint32_t w[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
-    const float d0 = x[2 * i] - f.x, d1 = x[2 * i + 1] - f.y;
-    s += d0 * d0 + d1 * d1;
-  }
-  return s;
-}
-
-// Epilogue for 16 consecutive output columns n..n+15 of row m (all < N; N % 16 == 0). For EPI_QKV
-// with fused deviation it returns this chunk's squared distance to the cached K/V row.
-template <int KIND>
-__device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const float* v, const float* u) {
-  float o[16];
-  float dev = 0.f;
-  if constexpr (KIND == EPI_STORE) {
-    st_bf16x16(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + n, v);
-  } else if constexpr (KIND == EPI_STORE_F32) {
-    float4* p = reinterpret_cast<float4*>(e.outf + (size_t)m * e.ldo + n);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-  } else if constexpr (KIND == EPI_QKV) {
-    const int c = e.col0 + n;
-    if (c < e.qd + e.kvd) {  // q or k head: rotate pairs (2i, 2i+1) at the row's global position
-      const int dim = (c < e.qd ? c : c - e.qd) % e.hd;
-      const int p = __ldg(e.pos + __ldg(e.row_tok + m));
-      const float4* cs = reinterpret_cast<const float4*>(e.rope_tab + (size_t)p * (e.hd >> 1) + (dim >> 1));
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float4 t = __ldg(cs + i);  // (cos, sin) of pairs 2i, 2i+1
-        const float a0 = v[4 * i], a1 = v[4 * i + 1], b0 = v[4 * i + 2], b1 = v[4 * i + 3];
-        o[4 * i] = t.x * a0 - t.y * a1;
-        o[4 * i + 1] = t.y * a0 + t.x * a1;
-        o[4 * i + 2] = t.z * b0 - t.w * b1;
-        o[4 * i + 3] = t.w * b0 + t.z * b1;
-      }
-      bf16* dst = (c < e.qd) ? reinterpret_cast<bf16*>(e.q_out) + (size_t)m * e.qd + c
-                             : reinterpret_cast<bf16*>(e.k_out) + (size_t)m * e.kvd + (c - e.qd);
-      st_bf16x16(dst, o);
-      if (c >= e.qd && e.dev_part != nullptr && m < e.n_cand)
-        dev = sqdiff16(o, reinterpret_cast<const bf16*>(e.k_ref) + (size_t)__ldg(e.row_tok + m) * e.kvd + (c - e.qd));
-    } else {
-      st_bf16x16(reinterpret_cast<bf16*>(e.v_out) + (size_t)m * e.kvd + (c - e.qd - e.kvd), v);
-      if (e.dev_part != nullptr && m < e.n_cand)
-        dev = sqdiff16(v, reinterpret_cast<const bf16*>(e.v_ref) + (size_t)__ldg(e.row_tok + m) * e.kvd +
-                              (c - e.qd - e.kvd));
-    }
-  } else if constexpr (KIND == EPI_RESID) {
-    const int src = e.res_row ? __ldg(e.res_row + m) : m;
-    const float4* hi = reinterpret_cast<const float4*>(e.h_in + (size_t)src * e.ldo + n);
-    float4* ho = reinterpret_cast<float4*>(e.h_out + (size_t)m * e.ldo + n);
-    float4 hv[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) hv[i] = hi[i];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      ho[i] = make_float4(hv[i].x + v[4 * i], hv[i].y + v[4 * i + 1], hv[i].z + v[4 * i + 2], hv[i].w + v[4 * i + 3]);
-  } else if constexpr (KIND == EPI_SWIGLU) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) o[i] = v[i] / (1.f + __expf(-v[i])) * u[i];
-    st_bf16x16(reinterpret_cast<bf16*>(e.act) + (size_t)m * e.ff + n, o);
-  }
-  return dev;
-}
 
 // Data-parallel rounds followed by an optional stream-K tail; every role walks the identical sequence.
 struct Sched {
@@ -219,6 +136,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // prologue above overlapped the previous kernel; its outputs are visible from here
   int tile, kb0, kb1;
 
   if (warp == 0) {
@@ -357,7 +275,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           const int n = nb * OUT_N + c;
           if (m < M && n < e.N) {
-            const float d = epi16<KIND>(e, m, n, v, u);
+            const float d = gepi::epi16<KIND>(e, m, n, v, u);
             if constexpr (KIND == EPI_QKV) {
               // a k or v head ends at this chunk: publish its deviation partial (fixed in-thread order)
               dacc += d;
@@ -404,27 +322,37 @@ struct TmKeyHash {
   }
 };
 
-// Launch plan: tile width, stream-K tail and grid, from a cost model in MMA cycles per SM.
+// Launch plan: CTA pair or single CTA, tile width, stream-K tail and grid, from a cost model in
+// cycles per SM. Per-k-block costs are the floor divided by the measured tensor-pipe efficiency
+// (single CTA 128x256: shared-memory bound at ~65 %; 128x128: ~57 % of its half-size floor;
+// pair 256x256 / 256x128: ~90 % / ~65 %).
 struct Plan {
-  int bn, sk_ctas, grid;
+  int bn, sk_ctas, grid, pair;
 };
 
-Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, int force_bn) {
+Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, int force_bn, int force_pair) {
   const int num_kb = (K + BK - 1) / BK;
-  const int m_tiles = (M + BM - 1) / BM;
-  Plan best{256, 0, 1};
+  Plan best{256, 0, 1, 0};
   double best_cost = 1e300;
-  for (int bn : {256, 128}) {
-    if (force_bn && bn != force_bn) continue;
-    const int out_n = sw ? bn / 2 : bn;
-    const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
-    const double cyc = bn == 256 ? 512.0 : 300.0;  // per k-block; BN=128 is shared-memory-read bound
-    // (a) whole tiles only
-    if (force_sched != 2) {
-      const int grid = (int)std::min<long long>(num_sms, tiles);
-      const double cost = (double)((tiles + grid - 1) / grid) * num_kb * cyc;
-      if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, grid}; }
-    }
+  for (int pair : {1, 0}) {
+    if (force_pair == 1 && !pair) continue;   // 1: pairs only, 2: single CTAs only
+    if (force_pair == 2 && pair) continue;
+    if (pair && force_sched == 2) continue;   // the stream-K tail exists for single CTAs only
+    const int tile_m = pair ? 256 : BM;
+    const int m_tiles = (M + tile_m - 1) / tile_m;
+    for (int bn : {256, 128}) {
+      if (force_bn && bn != force_bn) continue;
+      const int out_n = sw ? bn / 2 : bn;
+      const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
+      const double cyc = pair ? (bn == 256 ? 570.0 : 390.0) : (bn == 256 ? 790.0 : 450.0);
+      const int units = pair ? num_sms / 2 : num_sms;
+      // (a) whole tiles only
+      if (force_sched != 2) {
+        const int grid = (int)std::min<long long>(units, tiles);
+        const double cost = (double)((tiles + grid - 1) / grid) * num_kb * cyc;
+        if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, pair ? 2 * grid : grid, pair}; }
+      }
+      if (pair) continue;
     // (b) floor(tiles/G) whole-tile rounds + the remainder split over up to MAX_SPLIT CTAs per tile
     // The stream-K tail is opt-in (gemm_sched = 2): measured on B200 its fixup costs ~15-25 us per
     // launch at these sizes, more than the idle-SM time it recovers (tools/gemm_micro.py).
@@ -436,7 +364,8 @@ Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, i
       const int grid = dp > 0 ? num_sms : sk_ctas;
       const double fixup = 6000.0;  // partial store + flag + partial reads, in MMA-cycle units
       const double cost = (double)dp * num_kb * cyc + (double)((sk_iters + sk_ctas - 1) / sk_ctas) * cyc + fixup;
-      if (cost < best_cost) { best_cost = cost; best = Plan{bn, sk_ctas, grid}; }
+      if (cost < best_cost) { best_cost = cost; best = Plan{bn, sk_ctas, grid, 0}; }
+    }
     }
   }
   return best;
@@ -448,9 +377,21 @@ struct TmapCache {
   float* part = nullptr;  // [num_sms][BM][SLOT_COLS] fp32 stream-K partial slots
   int* flags = nullptr;   // [num_sms]
   int force_bn = 0;
+  int force_pair = 0;     // 0 auto, 1 CTA pairs only, 2 single CTAs only
 };
 
+cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
+                          int bn, int n_pairs, cudaStream_t s);
+cb_status gemm_tc2_init();
+
+cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
+                    CUtensorMap* out);
 static cb_status get_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
+                          CUtensorMap* out) {
+  return gemm_tmap(c, p, rows, k, ld, box_rows, out);
+}
+
+cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
                           CUtensorMap* out) {
   TmKey key{p, rows, k, ld, box_rows};
   auto it = c->tmaps->maps.find(key);
@@ -490,8 +431,8 @@ static cb_status launch_kind(cb_ctx* c, const void* A, int lda, const void* B, i
   CB_TRY(get_tmap(c, A, M, K, lda, BM, &ta));
   CB_TRY(get_tmap(c, B, b_rows, K, ldb, sw ? BN / 2 : BN, &tb));
   const int m_tiles = (M + BM - 1) / BM, n_tiles = (e.N + out_n - 1) / out_n;
-  gemm_tc_kernel<KIND, BN><<<pl.grid, NUM_THREADS, Cfg<BN>::SMEM, s>>>(ta, tb, M, K, m_tiles, n_tiles, e,
-                                                                       c->tmaps->part, c->tmaps->flags, pl.sk_ctas);
+  CB_CUDA(launch_k(c, gemm_tc_kernel<KIND, BN>, dim3(pl.grid), dim3(NUM_THREADS), Cfg<BN>::SMEM, s, 1, ta, tb, M, K,
+                    m_tiles, n_tiles, e, c->tmaps->part, c->tmaps->flags, pl.sk_ctas));
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -512,13 +453,16 @@ static cb_status launch_bn(cb_ctx* c, const void* A, int lda, const void* B, int
 
 cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
                          cudaStream_t s) {
-  const Plan pl = plan_gemm(c->num_sms, M, e.N, e.kind == EPI_SWIGLU, K, c->gemm_sched, c->tmaps->force_bn);
+  const Plan pl = plan_gemm(c->num_sms, M, e.N, e.kind == EPI_SWIGLU, K, c->gemm_sched, c->tmaps->force_bn,
+                            c->tmaps->force_pair);
+  if (pl.pair) return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, s);
   ProfScope ps_(c, PROF_GEMM, s);
   if (pl.bn == 256) return launch_bn<256>(c, A, lda, B, ldb, M, K, e, pl, s);
   return launch_bn<128>(c, A, lda, B, ldb, M, K, e, pl, s);
 }
 
 void gemm_tc_force_bn(cb_ctx* c, int bn) { c->tmaps->force_bn = bn; }
+void gemm_tc_force_pair(cb_ctx* c, int v) { c->tmaps->force_pair = v; }
 
 template <int BN> static cb_status set_attrs() {
   CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
@@ -541,6 +485,7 @@ cb_status gemm_tc_init(cb_ctx* c) {
   }
   CB_TRY(set_attrs<256>());
   CB_TRY(set_attrs<128>());
+  CB_TRY(gemm_tc2_init());
   c->tmaps = new TmapCache();
   CB_CUDA(cudaMalloc(&c->tmaps->part, (size_t)c->num_sms * BM * SLOT_COLS * sizeof(float)));
   CB_CUDA(cudaMalloc(&c->tmaps->flags, (size_t)c->num_sms * sizeof(int)));

@@ -1,0 +1,215 @@
+// gemm_tc2.cu — CTA-pair (cta_group::2) tcgen05 GEMM: one 256 x BN tile per 2-SM cluster.
+//
+// Why: with one CTA per 128 x 256 tile the SM's shared memory must feed 12 KB of A/B operands per
+// 128-cycle MMA plus 48 KB of TMA writes per k-block — about 1.5x the ~128 B/clk it delivers, which
+// caps the tensor pipe near 65 % (ncu: tensor pipe active 60-66 %, profiles/r01_gemm_ncu_full.txt).
+// A CTA pair computes M = 256 with each SM holding its own 128 A rows and half of the B rows, so each
+// SM moves half the B bytes per FLOP: ~64 B/clk of MMA reads + ~64 B/clk of TMA writes.
+//
+// Roles per CTA (6 warps): warp 0 TMA producer (both CTAs load their halves; the transaction bytes
+// complete on the leader's barrier), warp 1 MMA issuer (leader CTA only: tcgen05.mma.cta_group::2,
+// commits multicast to both CTAs' barriers), warps 2-5 epilogue on the CTA's own 128 accumulator
+// rows (arrivals on the leader's TMEM-empty barrier). Same fused epilogues as gemm_tc.cu.
+#include <cudaTypedefs.h>
+
+#include "ctx.h"
+#include "gemm_epi.cuh"
+#include "tc_common.cuh"
+
+namespace {
+constexpr int BK = 64, NUM_THREADS = 192;
+constexpr int A_BYTES = 128 * BK * 2;  // this CTA's 128 A rows
+
+template <int BN> struct Cfg2 {
+  static constexpr int B_HALF = BN / 2;
+  static constexpr int B_BYTES = B_HALF * BK * 2;  // this CTA's half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int KIND, int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
+                    int m_tiles, int n_tiles, EpiParams e) {
+  using C = Cfg2<BN>;
+  constexpr bool SW = (KIND == EPI_SWIGLU);
+  constexpr int OUT_N = SW ? BN / 2 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int num_kb = (K + BK - 1) / BK;
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int tiles = m_tiles * n_tiles;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmA);
+    tc::tma_prefetch(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc_2sm(tmem_slot, C::TMEM_COLS);
+  tc::fence_before();
+  tc::cluster_sync();  // barriers of both CTAs initialised before any remote arrive / transaction
+  tc::fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // prologue above overlapped the previous kernel; its outputs are visible from here
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs) =====
+    if (tc::elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < tiles; t += n_pairs) {
+        const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
+        const int b_row = SW ? (rank == 0 ? nb * OUT_N : e.ff + nb * OUT_N) : nb * BN + (int)rank * C::B_HALF;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
+          tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA) =====
+    if (leader) {
+      constexpr uint32_t IDESC = tc::idesc_bf16(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = pair; t < tiles; t += n_pairs, ++it) {
+        const int acc = it & 1;
+        tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::fence_after();
+          if (tc::elect_one()) {
+            const uint8_t* sa = smem + stage * C::STAGE_BYTES;
+            const uint64_t adesc = tc::sdesc_sw128(sa), bdesc = tc::sdesc_sw128(sa + A_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc::mma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+            tc::mma_commit_2sm(&empty[stage]);
+            if (kb == num_kb - 1) tc::mma_commit_2sm(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ===== epilogue (warps 2..5, each CTA its own 128 rows) =====
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int it = 0;
+    for (int t = pair; t < tiles; t += n_pairs, ++it) {
+      const int acc = it & 1;
+      const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
+      tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc::fence_after();
+      const int m = m0 + row;
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      float dacc = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < OUT_N; c += 16) {
+        float v[16], u[16];
+        tc::tmem_ld16(trow + c, v);
+        if constexpr (SW) tc::tmem_ld16(trow + BN / 2 + c, u);
+        const int n = nb * OUT_N + c;
+        if (m < M && n < e.N) {
+          const float d = gepi::epi16<KIND>(e, m, n, v, u);
+          if constexpr (KIND == EPI_QKV) {
+            dacc += d;
+            const int cl = e.col0 + n;
+            if (e.dev_part != nullptr && cl >= e.qd && (cl + 16) % e.hd == 0) {
+              const int kv_col = cl - e.qd;
+              const int slot = kv_col < e.kvd ? 2 * (kv_col / e.hd) : 2 * ((kv_col - e.kvd) / e.hd) + 1;
+              if (m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc;
+              dacc = 0.f;
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive_rank0(&tempty[acc]);
+    }
+  }
+  tc::fence_before();
+  tc::cluster_sync();  // no multicast commit or remote arrive may target an exited CTA
+  if (warp == 2) tc::tmem_dealloc_2sm(tmem_base, C::TMEM_COLS);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode2 = nullptr;
+}  // namespace
+
+cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
+                    CUtensorMap* out);  // gemm_tc.cu (shared tensor-map cache)
+
+template <int KIND, int BN>
+static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
+                              const EpiParams& e, int n_pairs, cudaStream_t s) {
+  using C = Cfg2<BN>;
+  constexpr bool sw = KIND == EPI_SWIGLU;
+  constexpr int out_n = sw ? BN / 2 : BN;
+  const long long b_rows = sw ? 2LL * e.ff : (long long)e.N;
+  CUtensorMap ta, tb;
+  CB_TRY(gemm_tmap(c, A, M, K, lda, 128, &ta));
+  CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, C::B_HALF, &tb));
+  const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
+  CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
+                    m_tiles, n_tiles, e));
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// Pair tiles of 256 x BN; n_pairs CTA pairs (grid = 2 * n_pairs).
+cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
+                          int bn, int n_pairs, cudaStream_t s) {
+  ProfScope ps_(c, PROF_GEMM, s);
+#define L2_(KIND_)                                                                                      \
+  return bn == 256 ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, s)                  \
+                   : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, s)
+  switch (e.kind) {
+    case EPI_STORE: L2_(EPI_STORE);
+    case EPI_STORE_F32: L2_(EPI_STORE_F32);
+    case EPI_QKV: L2_(EPI_QKV);
+    case EPI_RESID: L2_(EPI_RESID);
+    case EPI_SWIGLU: L2_(EPI_SWIGLU);
+  }
+#undef L2_
+  cb_set_error("bad epilogue kind %d", e.kind);
+  return CB_E_INVALID_ARG;
+}
+
+template <int BN> static cb_status set_attrs2() {
+  using C = Cfg2<BN>;
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<EPI_STORE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<EPI_STORE_F32, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<EPI_QKV, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<EPI_RESID, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<EPI_SWIGLU, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  return CB_OK;
+}
+
+cb_status gemm_tc2_init() {
+  CB_TRY(set_attrs2<256>());
+  CB_TRY(set_attrs2<128>());
+  return CB_OK;
+}

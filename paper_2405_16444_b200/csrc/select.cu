@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) deviation_kernel(const T* __restrict__ kn
                                                         const T* __restrict__ kr, const T* __restrict__ vr,
                                                         const int* __restrict__ cand_tok, int n_cand, int n_kv,
                                                         int hd, int mode, float* __restrict__ dev) {
+  pdl_enter();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_cand) return;
@@ -65,11 +66,11 @@ cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, cons
   const int grid = (n_cand + 7) / 8;
   ProfScope ps_(c, PROF_DEVIATION, s);
   if (c->m.dtype == CB_BF16)
-    deviation_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)k_new, (const bf16*)v_new, (const bf16*)k_ref,
+    CB_LAUNCH(c, (deviation_kernel<bf16>), grid, 256, 0, s, (const bf16*)k_new, (const bf16*)v_new, (const bf16*)k_ref,
                                                 (const bf16*)v_ref, cand_tok, n_cand, c->m.n_kv_heads,
                                                 c->m.head_dim, dev_mode, dev);
   else
-    deviation_kernel<float><<<grid, 256, 0, s>>>((const float*)k_new, (const float*)v_new, (const float*)k_ref,
+    CB_LAUNCH(c, (deviation_kernel<float>), grid, 256, 0, s, (const float*)k_new, (const float*)v_new, (const float*)k_ref,
                                                  (const float*)v_ref, cand_tok, n_cand, c->m.n_kv_heads,
                                                  c->m.head_dim, dev_mode, dev);
   CB_LAUNCHED(c);
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
                                                             int* __restrict__ sel_tok, int* err,
                                                             const float* __restrict__ dev_part, int n_kv, int ld_part,
                                                             int dev_mode) {
+  pdl_enter();
   extern __shared__ unsigned keys[];
   __shared__ int hist[256];
   __shared__ int sm_warp[32];
@@ -251,7 +253,7 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   if (k_keep + n_suffix == 0 && (dev_part == nullptr || n_cand == 0)) return CB_OK;
   const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
   ProfScope ps_(c, PROF_TOPK, s);
-  topk_kernel<<<1, TOPK_THREADS, smem, s>>>(dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
+  CB_LAUNCH(c, (topk_kernel), 1, TOPK_THREADS, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
                                             c->err_word, dev_part, c->m.n_kv_heads, ld_part, dev_mode);
   CB_LAUNCHED(c);
   return CB_OK;

@@ -116,9 +116,12 @@ def test_gemm_simt(P, dtype, M, N, K):
 
 @pytest.mark.parametrize("M,N,K", [(1, 256, 64), (100, 512, 200), (128, 256, 4096), (553, 6144, 4096),
                                    (300, 48, 1024), (3072, 4096, 4096), (369, 4096, 14336), (129, 1040, 136)])
-def test_gemm_tcgen05(P, M, N, K):
-    """tcgen05/TMEM/TMA GEMM against an fp64 torch matmul of the same bf16 operands (ragged M, N, K tails)."""
+@pytest.mark.parametrize("pair", [2, 1])
+def test_gemm_tcgen05(P, M, N, K, pair):
+    """tcgen05/TMEM/TMA GEMM against an fp64 torch matmul of the same bf16 operands (ragged M, N, K tails);
+    pair = 2: single-CTA kernel, 1: CTA-pair (cta_group::2) kernel."""
     ctx = P.Context(shape("small"), "bf16", max_tokens=8)
+    ctx.set_option("gemm_pair", pair)
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N)
     A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
     B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)

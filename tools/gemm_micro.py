@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--modes", default="1,2,0")
     ap.add_argument("--bns", default="0")
+    ap.add_argument("--pairs", default="0")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -34,9 +35,11 @@ def main():
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        for mode, bn in [(int(m), int(b)) for m in a.modes.split(",") for b in a.bns.split(",")]:
+        for mode, bn, pr in [(int(m), int(b), int(p)) for m in a.modes.split(",") for b in a.bns.split(",")
+                             for p in a.pairs.split(",")]:
             ctx.set_option("gemm_sched", mode)
             ctx.set_option("gemm_bn", bn)
+            ctx.set_option("gemm_pair", pr)
             fn = lambda: P.api.check(P.api.lib().cb_op_gemm(ctx.handle, A.data_ptr(), B.data_ptr(), C.data_ptr(),
                                                             M, N, K, 0, 2, torch.cuda.current_stream().cuda_stream))
             for _ in range(3):
@@ -50,8 +53,8 @@ def main():
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.iters * 1e3
             tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
-            res[f"{name}/m{mode}/bn{bn}"] = (round(us, 1), round(tf, 1))
-            print(f"{name:10s} M={M:5d} N={N:6d} K={K:6d} mode={mode} bn={bn}: {us:8.1f} us  {tf:7.1f} TFLOP/s", flush=True)
+            res[f"{name}/m{mode}/bn{bn}/p{pr}"] = (round(us, 1), round(tf, 1))
+            print(f"{name:10s} M={M:5d} N={N:6d} K={K:6d} mode={mode} bn={bn} pair={pr}: {us:8.1f} us  {tf:7.1f} TFLOP/s", flush=True)
     print(json.dumps(res))
 
 
