@@ -302,13 +302,18 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof_range = os.environ.get("CB_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: timed steps only
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.cudart().cudaProfilerStart()
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        if prof_range:
+            torch.cuda.cudart().cudaProfilerStop()
     if world > 1:
         dist.barrier()
     launches = per_step_launches * args.steps

@@ -29,8 +29,9 @@ CB_API cb_status cb_op_embed(cb_ctx* ctx, const void* embed, const int32_t* tok,
 /* x[r] = h[r] / sqrt(mean(h[r]^2) + eps) * gain   (x in the model dtype). */
 CB_API cb_status cb_op_rmsnorm(cb_ctx* ctx, const float* h, const float* gain, int32_t n_rows, void* x, void* stream);
 
-/* C[M][N] = A[M][K] . B[N][K]^T with fp32 accumulation; C is fp32 when out_f32 != 0, else the model
- * dtype. impl: 0 = auto (tcgen05 for bf16), 1 = SIMT, 2 = tcgen05 (bf16 only; K % 8 == 0). */
+/* C[M][N] = A[M][K] . B[N][K]^T with fp32 accumulation; C is fp32 when out_f32 == 1, else the model
+ * dtype. out_f32 == 2: residual form C[M][N] += A . B^T on an fp32 C (the o-/down-projection epilogue).
+ * impl: 0 = auto (tcgen05 for bf16), 1 = SIMT, 2 = tcgen05 (bf16 only; K % 8 == 0). */
 CB_API cb_status cb_op_gemm(cb_ctx* ctx, const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                      int32_t out_f32, int32_t impl, void* stream);
 
@@ -48,12 +49,17 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *                 1 = data-parallel only, 2 = data-parallel rounds + stream-K tail
  *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width
  *   "gemm_pair"   0 = auto, 1 = CTA-pair (cta_group::2, 256-row tiles) only, 2 = single-CTA only
+ *   "gemm_ksplit" 0 = auto, 1..4 = force the k-split chain of pair residual GEMMs (when it fits one wave)
  *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM, 3 = mma.sync (legacy tensor path)
  *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor of the tcgen05 attention
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
  *   "debug_trace" 1 = record clock64 pipeline events of one CTA of the tcgen05 attention (tuning)
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
+
+/* Read-only facts about the context: "num_sms", "gemm_max_pairs" (co-resident 2-CTA clusters of the
+ * CTA-pair GEMM, from cudaOccupancyMaxActiveClusters). Unknown names -> INVALID_ARG. */
+CB_API cb_status cb_get_info(cb_ctx* ctx, const char* name, int64_t* value);
 
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */
 CB_API int64_t cb_launch_count(cb_ctx* ctx);

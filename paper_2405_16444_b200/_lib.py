@@ -51,6 +51,7 @@ _SIGS = {
     "cb_blend_request": (c_i32, [c_vp, ctypes.POINTER(CbLayerW), c_vp, c_vp, c_vp, c_i32, c_i32, c_i32p, c_i32,
                                  c_vp, c_vp, c_vp, c_vp, c_i32p, c_vp, c_vp, c_vp]),
     "cb_set_option": (c_i32, [c_vp, ctypes.c_char_p, c_i64]),
+    "cb_get_info": (c_i32, [c_vp, ctypes.c_char_p, ctypes.POINTER(c_i64)]),
     "cb_debug_fetch": (c_i32, [c_vp, ctypes.POINTER(c_i64), c_i32]),
     "cb_profile_begin": (c_i32, [c_vp]),
     "cb_profile_end": (c_i32, [c_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),

@@ -70,6 +70,11 @@ class Context:
     def set_option(self, name: str, value: int):
         check(lib().cb_set_option(self.handle, name.encode(), int(value)))
 
+    def info(self, name: str) -> int:
+        v = ctypes.c_int64(0)
+        check(lib().cb_get_info(self.handle, name.encode(), ctypes.byref(v)))
+        return v.value
+
 
 class ModelWeights:
     """Device weights in the C-ABI layouts (cacheblend.h cb_layer_w)."""
@@ -230,6 +235,15 @@ def op_gemm(ctx: Context, A: torch.Tensor, B: torch.Tensor, out_f32: bool = Fals
     N = B.shape[0]
     C = A.new_empty(M, N, dtype=torch.float32 if out_f32 else A.dtype)
     check(lib().cb_op_gemm(ctx.handle, _p(A), _p(B), _p(C), M, N, K, int(out_f32), impl, _stream(stream)))
+    return C
+
+
+def op_gemm_resid(ctx: Context, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, impl: int = 0, stream=None):
+    """In place C += A . B^T on an fp32 C (the residual epilogue of the o-/down-projections)."""
+    M, K = A.shape
+    N = B.shape[0]
+    assert C.dtype == torch.float32 and C.shape == (M, N) and C.is_contiguous()
+    check(lib().cb_op_gemm(ctx.handle, _p(A), _p(B), _p(C), M, N, K, 2, impl, _stream(stream)))
     return C
 
 

@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
          "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+# tuning experiments only (e.g. CB_EXTRA_NVCC=-DCB_EPI_EXP=1 ... build --force)
+FLAGS += os.environ.get("CB_EXTRA_NVCC", "").split()
 
 
 def sources():

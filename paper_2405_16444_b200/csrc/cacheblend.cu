@@ -28,7 +28,9 @@ cb_status topk_init_attrs();
 cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
 void gemm_tc_force_bn(cb_ctx* c, int bn);
+void gemm_tc_force_ksplit(cb_ctx* c, int v);
 void gemm_tc_force_pair(cb_ctx* c, int v);
+int gemm_tc_max_pairs(const cb_ctx* c);
 cb_status attention_tc_init();
 
 // ---- error reporting ------------------------------------------------------------------------------
@@ -326,6 +328,14 @@ extern "C" cb_status cb_debug_fetch(cb_ctx* c, int64_t* host, int32_t n) {
   return CB_OK;
 }
 
+extern "C" cb_status cb_get_info(cb_ctx* c, const char* name, int64_t* value) {
+  CB_REQUIRE(c && name && value, CB_E_INVALID_ARG, "cb_get_info: NULL argument");
+  if (std::strcmp(name, "num_sms") == 0) { *value = c->num_sms; return CB_OK; }
+  if (std::strcmp(name, "gemm_max_pairs") == 0) { *value = gemm_tc_max_pairs(c); return CB_OK; }
+  cb_set_error("unknown info '%s'", name);
+  return CB_E_INVALID_ARG;
+}
+
 extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   CB_REQUIRE(c != nullptr && name != nullptr, CB_E_INVALID_ARG, "ctx / name is NULL");
   if (std::strcmp(name, "gemm_sched") == 0) {
@@ -364,6 +374,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "gemm_pair") == 0) {
     CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_pair must be 0, 1 or 2");
     gemm_tc_force_pair(c, (int)value);
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_ksplit") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 4, CB_E_INVALID_ARG, "gemm_ksplit must be 0..4");
+    gemm_tc_force_ksplit(c, (int)value);
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_bn") == 0) {
@@ -413,10 +428,12 @@ extern "C" cb_status cb_op_gemm(cb_ctx* c, const void* A, const void* B, void* C
   CB_REQUIRE(c && A && B && C && M >= 0 && N >= 0 && K >= 1, CB_E_INVALID_ARG, "cb_op_gemm: bad arguments");
   CB_REQUIRE(impl >= 0 && impl <= 2, CB_E_INVALID_ARG, "cb_op_gemm: impl must be 0, 1 or 2");
   CB_REQUIRE(N % 2 == 0 && K % 8 == 0, CB_E_SHAPE, "cb_op_gemm: N must be even and K a multiple of 8");
+  CB_REQUIRE(out_f32 >= 0 && out_f32 <= 2, CB_E_INVALID_ARG, "cb_op_gemm: out_f32 must be 0, 1 or 2");
   EpiParams e{};
-  e.kind = out_f32 ? EPI_STORE_F32 : EPI_STORE;
+  e.kind = out_f32 == 2 ? EPI_RESID : out_f32 ? EPI_STORE_F32 : EPI_STORE;
   e.M = M; e.N = N; e.ldo = N;
   e.out = C; e.outf = (float*)C;
+  e.h_out = (float*)C; e.h_in = (const float*)C; e.res_row = nullptr;
   return launch_gemm(c, A, K, B, K, M, K, e, impl, (cudaStream_t)st);
 }
 

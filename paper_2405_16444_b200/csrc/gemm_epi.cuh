@@ -2,6 +2,7 @@
 #pragma once
 
 #include "ctx.h"
+#include "tc_common.cuh"
 
 namespace gepi {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -86,6 +87,176 @@ __device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const f
     st_bf16x16(reinterpret_cast<bf16*>(e.act) + (size_t)m * e.ff + n, o);
   }
   return dev;
+}
+
+// ---- coalesced tile epilogue ------------------------------------------------------------------------
+// tcgen05.ld 32x32b hands each lane one accumulator row, so storing straight from registers makes every
+// warp instruction touch 32 rows (32 L1 wavefronts). Instead each warp stages 32 rows x 32 fp32 columns
+// in shared memory and re-reads them 4 rows per instruction (8 lanes x 16 B = 128 B of one row), so
+// global loads and stores of the epilogue are row-contiguous. Float4 slots are XOR-swizzled by row:
+// both the row-per-lane writes and the 4-rows-per-instruction reads are bank-conflict free.
+constexpr int EPI_WARP_F4 = 32 * 8;  // float4 slots per warp buffer (4 KB)
+
+__device__ __forceinline__ void stage_put(float4* buf, int lane, const float* v) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) buf[lane * 8 + (j ^ (lane & 7))] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+__device__ __forceinline__ float4 stage_get(const float4* buf, int r, int j) { return buf[r * 8 + (j ^ (r & 7))]; }
+
+__device__ __forceinline__ uint2 pack4_bf16(float4 a) { return make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w)); }
+
+// Epilogue of one warp's 32 accumulator rows (tile rows m_base .. m_base + 31, TMEM address trow) over
+// the tile's output columns n0 .. n0 + OUT_N. Lane L owns, in pass it = 0..7, row it * 4 + L / 8 and
+// columns 4 * (L % 8) .. +3 of each 32-column chunk. cont (EPI_RESID only): a later split-K piece,
+// h_out += acc. EPI_QKV needs hd % 32 == 0 (a chunk lies in one head); per-head deviation partials
+// are summed per row over the head's chunks in order (each chunk: 4 terms per lane, then a fixed
+// xor-shuffle tree over the row's 8 lanes).
+template <int KIND, int BN>
+__device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_base, int n0, uint32_t trow,
+                                              float4* buf, int lane, bool cont, long long* dbg = nullptr) {
+  constexpr bool SW = KIND == EPI_SWIGLU;
+  constexpr int OUT_N = SW ? BN / 2 : BN;
+  const int j = lane & 7, r0 = lane >> 3;
+  const int my_m = m_base + lane;
+  const bool my_ok = my_m < M;
+  int my_a = 0, my_b = 0;  // per-row operands of the lane's own row, broadcast below
+  if constexpr (KIND == EPI_RESID) {
+    if (my_ok) my_a = cont ? my_m : (e.res_row ? __ldg(e.res_row + my_m) : my_m);
+  }
+  if constexpr (KIND == EPI_QKV) {
+    if (my_ok) { my_a = __ldg(e.row_tok + my_m); my_b = __ldg(e.pos + my_a); }
+  }
+  int ra[8], rb[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    ra[it] = __shfl_sync(0xffffffffu, my_a, it * 4 + r0);
+    rb[it] = __shfl_sync(0xffffffffu, my_b, it * 4 + r0);
+  }
+  float dacc[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) dacc[it] = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < OUT_N; c += 32) {
+    const int n = n0 + c;
+    if (n >= e.N) break;  // warp-uniform
+    const int col = n + 4 * j;
+    const bool col_ok = col < e.N;
+    // 1. global operands first (their latency overlaps the TMEM read)
+    float4 pre[8];
+    uint2 ref[8];
+    [[maybe_unused]] bool is_q = false, is_v = false, dev_on = false;
+    [[maybe_unused]] int qc = 0, kv_c = 0;
+    if constexpr (KIND == EPI_RESID) {
+      const float* base = cont ? e.h_out : e.h_in;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int m = m_base + it * 4 + r0;
+        pre[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m < M && col_ok) {
+          const float4* p = reinterpret_cast<const float4*>(base + (size_t)ra[it] * e.ldo + col);
+          pre[it] = cont ? __ldcg(p) : *p;
+        }
+      }
+    }
+    if constexpr (KIND == EPI_QKV) {
+      qc = e.col0 + n;  // column of the fused [q | k | v] output
+      is_q = qc < e.qd;
+      is_v = qc >= e.qd + e.kvd;
+      kv_c = is_q ? 0 : (is_v ? qc - e.qd - e.kvd : qc - e.qd);
+      dev_on = !is_q && e.dev_part != nullptr;
+      const int dim = ((is_q ? qc : qc - e.qd) % e.hd) + 4 * j;  // even: pairs (dim, dim+1), (dim+2, dim+3)
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int m = m_base + it * 4 + r0;
+        if (m < M && col_ok) {
+          if (!is_v) pre[it] = __ldg(reinterpret_cast<const float4*>(e.rope_tab + (size_t)rb[it] * (e.hd >> 1) + (dim >> 1)));
+          if (dev_on && m < e.n_cand)
+            ref[it] = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const bf16*>(is_v ? e.v_ref : e.k_ref) +
+                                                           (size_t)ra[it] * e.kvd + kv_c + 4 * j));
+        }
+      }
+    }
+    // 2. TMEM -> registers (fused SwiGLU) -> staging buffer
+    {
+      float v[32];
+#if defined(CB_EPI_EXP) && (CB_EPI_EXP & 1)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = (float)i;
+#else
+      tc::tmem_ld32(trow + c, v);
+#endif
+      if constexpr (SW) {
+        float u[32];
+        tc::tmem_ld32(trow + BN / 2 + c, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = v[i] / (1.f + __expf(-v[i])) * u[i];
+      }
+#if defined(CB_EPI_EXP) && (CB_EPI_EXP & 2)
+      if (v[0] == 12345.f) stage_put(buf, lane, v);
+#else
+      stage_put(buf, lane, v);
+#endif
+    }
+    __syncwarp();
+    // 3. row-contiguous global traffic
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int r = it * 4 + r0, m = m_base + r;
+#if defined(CB_EPI_EXP) && (CB_EPI_EXP & 4)
+      const bool ok = false;
+#else
+      const bool ok = m < M && col_ok;
+#endif
+      float4 a = stage_get(buf, r, j);
+      if constexpr (KIND == EPI_STORE) {
+        if (ok) *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + col) = pack4_bf16(a);
+      } else if constexpr (KIND == EPI_STORE_F32) {
+        if (ok) *reinterpret_cast<float4*>(e.outf + (size_t)m * e.ldo + col) = a;
+      } else if constexpr (KIND == EPI_SWIGLU) {
+        if (ok) *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.act) + (size_t)m * e.ff + col) = pack4_bf16(a);
+      } else if constexpr (KIND == EPI_RESID) {
+        if (ok)
+          *reinterpret_cast<float4*>(e.h_out + (size_t)m * e.ldo + col) =
+              make_float4(pre[it].x + a.x, pre[it].y + a.y, pre[it].z + a.z, pre[it].w + a.w);
+      } else if constexpr (KIND == EPI_QKV) {
+        if (ok && !is_v) {  // rotate pairs (dim, dim+1), (dim+2, dim+3) at the row's global position
+          const float4 t = pre[it];
+          a = make_float4(t.x * a.x - t.y * a.y, t.y * a.x + t.x * a.y, t.z * a.z - t.w * a.w, t.w * a.z + t.z * a.w);
+        }
+        if (ok) {
+          bf16* dst = is_q ? reinterpret_cast<bf16*>(e.q_out) + (size_t)m * e.qd + qc + 4 * j
+                           : reinterpret_cast<bf16*>(is_v ? e.v_out : e.k_out) + (size_t)m * e.kvd + kv_c + 4 * j;
+          *reinterpret_cast<uint2*>(dst) = pack4_bf16(a);
+        }
+        if (dev_on) {  // warp-uniform
+          float d = 0.f;
+          if (ok && m < e.n_cand) {
+            const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ref[it].x));
+            const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ref[it].y));
+            const float d0 = a.x - f0.x, d1 = a.y - f0.y, d2 = a.z - f1.x, d3 = a.w - f1.y;
+            d = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+          }
+          d += __shfl_xor_sync(0xffffffffu, d, 1);
+          d += __shfl_xor_sync(0xffffffffu, d, 2);
+          d += __shfl_xor_sync(0xffffffffu, d, 4);
+          dacc[it] += d;
+        }
+      }
+    }
+    if constexpr (KIND == EPI_QKV) {
+      if (dev_on && (qc + 32) % e.hd == 0) {  // a k or v head ends with this chunk: publish its partials
+        const int slot = !is_v ? 2 * (kv_c / e.hd) : 2 * (kv_c / e.hd) + 1;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int m = m_base + it * 4 + r0;
+          if (j == 0 && m < M && m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc[it];
+          dacc[it] = 0.f;
+        }
+      }
+    }
+    __syncwarp();  // buffer reused by the next chunk
+    if (dbg != nullptr && lane == 0 && c / 32 < 8) dbg[c / 32] = tc::globaltimer();
+  }
 }
 
 }  // namespace gepi

@@ -37,7 +37,8 @@ template <int BN> struct Cfg {
   static constexpr int STAGES = BN == 256 ? 4 : 6;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = 4 * gepi::EPI_WARP_F4 * 16;  // epilogue staging, 4 KB per warp
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -113,7 +114,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int OUT_N = SW ? BN / 2 : BN;  // output columns per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  float4* ebuf = reinterpret_cast<float4*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -231,6 +233,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           named_bar(1, 128);
         }
+        if (n_con == 0 && (KIND == EPI_RESID || KIND == EPI_STORE || KIND == EPI_STORE_F32)) {
+          gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4,
+                                        lane, false);
+        } else
 #pragma unroll 1
         for (int c = 0; c < OUT_N; c += 16) {
           float v[16], u[16];
@@ -326,13 +332,19 @@ struct TmKeyHash {
 // cycles per SM. Per-k-block costs are the floor divided by the measured tensor-pipe efficiency
 // (single CTA 128x256: shared-memory bound at ~65 %; 128x128: ~57 % of its half-size floor;
 // pair 256x256 / 256x128: ~90 % / ~65 %).
+// Pair RESID GEMMs (o-proj, down-proj: N = d_model, few tiles at blend sizes) may also split K into a
+// chain of ksplit pieces per tile, each adding onto h_out after the previous one (fixed order).
 struct Plan {
-  int bn, sk_ctas, grid, pair;
+  int bn, sk_ctas, grid, pair, ksplit;
 };
 
-Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, int force_bn, int force_pair) {
+constexpr int MAX_KSPLIT = 4;
+constexpr double KSPLIT_EPI_CYC = 3000.0;  // one more serialised fp32 read-modify-write epilogue
+
+Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid, int K, int force_sched, int force_bn, int force_pair,
+               int force_ksplit) {
   const int num_kb = (K + BK - 1) / BK;
-  Plan best{256, 0, 1, 0};
+  Plan best{256, 0, 1, 0, 1};
   double best_cost = 1e300;
   for (int pair : {1, 0}) {
     if (force_pair == 1 && !pair) continue;   // 1: pairs only, 2: single CTAs only
@@ -345,12 +357,21 @@ Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, i
       const int out_n = sw ? bn / 2 : bn;
       const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
       const double cyc = pair ? (bn == 256 ? 570.0 : 390.0) : (bn == 256 ? 790.0 : 450.0);
-      const int units = pair ? num_sms / 2 : num_sms;
-      // (a) whole tiles only
+      const int units = pair ? max_pairs : num_sms;
+      // (a) whole tiles only (pairs: optionally a k-split chain for RESID)
       if (force_sched != 2) {
-        const int grid = (int)std::min<long long>(units, tiles);
-        const double cost = (double)((tiles + grid - 1) / grid) * num_kb * cyc;
-        if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, pair ? 2 * grid : grid, pair}; }
+        const auto fits = [&](int ks) { return ks == 1 || (tiles * ks <= units && num_kb / ks >= 4); };
+        // k-split chains are opt-in (gemm_ksplit): measured slower at blend sizes, the second piece's
+        // residual read-modify-write is serialised behind the first (tools/gemm_trace.py)
+        for (int ks = 1; ks <= (pair && resid && force_ksplit > 1 ? MAX_KSPLIT : 1); ++ks) {
+          if (!fits(ks)) continue;
+          // forced: that split when it fits, else no split
+          if (pair && resid && force_ksplit && ks != (fits(force_ksplit) ? force_ksplit : 1)) continue;
+          const int grid = (int)std::min<long long>(units, tiles * ks);
+          const double cost =
+              (double)((tiles * ks + grid - 1) / grid) * ((num_kb + ks - 1) / ks) * cyc + (ks - 1) * KSPLIT_EPI_CYC;
+          if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, pair ? 2 * grid : grid, pair, ks}; }
+        }
       }
       if (pair) continue;
     // (b) floor(tiles/G) whole-tile rounds + the remainder split over up to MAX_SPLIT CTAs per tile
@@ -364,7 +385,7 @@ Plan plan_gemm(int num_sms, int M, int N_out, bool sw, int K, int force_sched, i
       const int grid = dp > 0 ? num_sms : sk_ctas;
       const double fixup = 6000.0;  // partial store + flag + partial reads, in MMA-cycle units
       const double cost = (double)dp * num_kb * cyc + (double)((sk_iters + sk_ctas - 1) / sk_ctas) * cyc + fixup;
-      if (cost < best_cost) { best_cost = cost; best = Plan{bn, sk_ctas, grid, 0}; }
+      if (cost < best_cost) { best_cost = cost; best = Plan{bn, sk_ctas, grid, 0, 1}; }
     }
     }
   }
@@ -376,13 +397,17 @@ struct TmapCache {
   std::unordered_map<TmKey, CUtensorMap, TmKeyHash> maps;
   float* part = nullptr;  // [num_sms][BM][SLOT_COLS] fp32 stream-K partial slots
   int* flags = nullptr;   // [num_sms]
+  int* kflags = nullptr;  // [KFLAGS] split-K chain counters of the pair kernel (zero between launches)
   int force_bn = 0;
+  int max_pairs = 0;      // co-resident 2-CTA clusters of the pair kernel
+  int force_ksplit = 0;   // 0 auto, else force this k-split for pair RESID GEMMs (when it fits)
   int force_pair = 0;     // 0 auto, 1 CTA pairs only, 2 single CTAs only
 };
 
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
-                          int bn, int n_pairs, cudaStream_t s);
-cb_status gemm_tc2_init();
+                          int bn, int n_pairs, int ksplit, int* kflags, cudaStream_t s);
+cb_status gemm_tc2_init(int num_sms, int* max_pairs);
+constexpr int KFLAGS = 4096;  // >= 8 per tile for every tile of a split-K launch (tiles * ksplit <= 74 pairs)
 
 cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
                     CUtensorMap* out);
@@ -451,11 +476,11 @@ static cb_status launch_bn(cb_ctx* c, const void* A, int lda, const void* B, int
   return CB_E_INVALID_ARG;
 }
 
-cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
-                         cudaStream_t s) {
-  const Plan pl = plan_gemm(c->num_sms, M, e.N, e.kind == EPI_SWIGLU, K, c->gemm_sched, c->tmaps->force_bn,
-                            c->tmaps->force_pair);
-  if (pl.pair) return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, s);
+cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
+                         const EpiParams& e, cudaStream_t s) {
+  const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, c->gemm_sched,
+                            c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit);
+  if (pl.pair) return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, s);
   ProfScope ps_(c, PROF_GEMM, s);
   if (pl.bn == 256) return launch_bn<256>(c, A, lda, B, ldb, M, K, e, pl, s);
   return launch_bn<128>(c, A, lda, B, ldb, M, K, e, pl, s);
@@ -463,6 +488,8 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
 
 void gemm_tc_force_bn(cb_ctx* c, int bn) { c->tmaps->force_bn = bn; }
 void gemm_tc_force_pair(cb_ctx* c, int v) { c->tmaps->force_pair = v; }
+void gemm_tc_force_ksplit(cb_ctx* c, int v) { c->tmaps->force_ksplit = v; }
+int gemm_tc_max_pairs(const cb_ctx* c) { return c->tmaps ? c->tmaps->max_pairs : 0; }
 
 template <int BN> static cb_status set_attrs() {
   CB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<EPI_STORE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
@@ -485,11 +512,13 @@ cb_status gemm_tc_init(cb_ctx* c) {
   }
   CB_TRY(set_attrs<256>());
   CB_TRY(set_attrs<128>());
-  CB_TRY(gemm_tc2_init());
   c->tmaps = new TmapCache();
+  CB_TRY(gemm_tc2_init(c->num_sms, &c->tmaps->max_pairs));
   CB_CUDA(cudaMalloc(&c->tmaps->part, (size_t)c->num_sms * BM * SLOT_COLS * sizeof(float)));
   CB_CUDA(cudaMalloc(&c->tmaps->flags, (size_t)c->num_sms * sizeof(int)));
   CB_CUDA(cudaMemset(c->tmaps->flags, 0, (size_t)c->num_sms * sizeof(int)));
+  CB_CUDA(cudaMalloc(&c->tmaps->kflags, KFLAGS * sizeof(int)));
+  CB_CUDA(cudaMemset(c->tmaps->kflags, 0, KFLAGS * sizeof(int)));
   return CB_OK;
 }
 
@@ -497,6 +526,7 @@ void gemm_tc_destroy(cb_ctx* c) {
   if (c->tmaps) {
     cudaFree(c->tmaps->part);
     cudaFree(c->tmaps->flags);
+    cudaFree(c->tmaps->kflags);
   }
   delete c->tmaps;
   c->tmaps = nullptr;

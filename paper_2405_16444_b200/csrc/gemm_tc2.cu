@@ -25,20 +25,25 @@ template <int BN> struct Cfg2 {
   static constexpr int B_BYTES = B_HALF * BK * 2;  // this CTA's half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = 4 * gepi::EPI_WARP_F4 * 16;  // epilogue staging, 4 KB per warp
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
 template <int KIND, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
-                    int m_tiles, int n_tiles, EpiParams e) {
+                    int m_tiles, int n_tiles, EpiParams e, int ksplit, int* __restrict__ kflags,
+                    long long* __restrict__ dbg) {
+  // debug_trace: globaltimer (ns) events of each CTA's first work item at dbg[blockIdx.x * 8 + event]
+#define DBG2(ev) do { if (dbg != nullptr && blockIdx.x < 256) dbg[blockIdx.x * 8 + (ev)] = tc::globaltimer(); } while (0)
   using C = Cfg2<BN>;
   constexpr bool SW = (KIND == EPI_SWIGLU);
   constexpr int OUT_N = SW ? BN / 2 : BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  float4* ebuf = reinterpret_cast<float4*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + C::EPI_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -50,6 +55,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_kb = (K + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int tiles = m_tiles * n_tiles;
+  const int items = tiles * ksplit;  // work item i: tile i % tiles, k-split i / tiles
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
@@ -64,16 +70,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_enter();  // prologue above overlapped the previous kernel; its outputs are visible from here
+  if (threadIdx.x == 0) DBG2(0);
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs) =====
     if (tc::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < tiles; t += n_pairs) {
+      for (int i = pair; i < items; i += n_pairs) {
+        const int t = i % tiles, sp = i / tiles;
         const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
         const int b_row = SW ? (rank == 0 ? nb * OUT_N : e.ff + nb * OUT_N) : nb * BN + (int)rank * C::B_HALF;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb1 = (sp + 1) * num_kb / ksplit;
+        for (int kb = sp * num_kb / ksplit; kb < kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -81,6 +90,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        if (i == pair) DBG2(1);
       }
     }
   } else if (warp == 1) {
@@ -90,12 +100,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair; t < tiles; t += n_pairs, ++it) {
+      for (int i = pair; i < items; i += n_pairs, ++it) {
+        const int sp = i / tiles;
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = sp * num_kb / ksplit, kb1 = (sp + 1) * num_kb / ksplit;
+        for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::fence_after();
           if (tc::elect_one()) {
@@ -103,13 +115,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t adesc = tc::sdesc_sw128(sa), bdesc = tc::sdesc_sw128(sa + A_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              tc::mma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > 0 || k > 0) ? 1u : 0u);
+              tc::mma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
             tc::mma_commit_2sm(&empty[stage]);
-            if (kb == num_kb - 1) tc::mma_commit_2sm(&tfull[acc]);
+            if (kb == kb1 - 1) tc::mma_commit_2sm(&tfull[acc]);
           }
           __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
+        if (it == 0 && lane == 0) DBG2(2);
       }
     }
   } else {
@@ -117,14 +130,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     int it = 0;
-    for (int t = pair; t < tiles; t += n_pairs, ++it) {
+    for (int i = pair; i < items; i += n_pairs, ++it) {
+      const int t = i % tiles, sp = i / tiles;
       const int acc = it & 1;
       const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
+      // split-K chain (RESID only): split sp adds onto h_out after split sp - 1 of the same 32 rows
+      // published it — a fixed order, so the sum is deterministic. flag = number of splits done.
+      int* flag = kflags + ((size_t)t * 2 + rank) * 4 + q;
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after();
+      if (it == 0 && warp == 2 && lane == 0) DBG2(3);
+      if constexpr (KIND == EPI_RESID) {
+        if (sp > 0) {
+          if (lane == 0) {
+            int f;
+            while (true) {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+              if (f >= sp) break;
+              __nanosleep(100);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      if (it == 0 && warp == 2 && lane == 0) DBG2(4);
       const int m = m0 + row;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       float dacc = 0.f;
+      if (KIND == EPI_RESID || KIND == EPI_STORE || KIND == EPI_STORE_F32) {  // staged, row-contiguous
+        gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane,
+                                      sp > 0,
+                                      (dbg != nullptr && it == 0 && warp == 2 && blockIdx.x < 128)
+                                          ? dbg + 1024 + blockIdx.x * 8 : nullptr);
+      } else {
 #pragma unroll 1
       for (int c = 0; c < OUT_N; c += 16) {
         float v[16], u[16];
@@ -145,17 +183,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      }
+      if constexpr (KIND == EPI_RESID) {
+        if (ksplit > 1) {
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) {  // publish (or, after the last split, reset for the next launch)
+            const int nf = sp + 1 < ksplit ? sp + 1 : 0;
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(nf) : "memory");
+          }
+        }
+      }
+      if (it == 0 && warp == 2 && lane == 0) DBG2(5);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_rank0(&tempty[acc]);
     }
   }
+  if (threadIdx.x == 0) DBG2(6);
   tc::fence_before();
   tc::cluster_sync();  // no multicast commit or remote arrive may target an exited CTA
   if (warp == 2) tc::tmem_dealloc_2sm(tmem_base, C::TMEM_COLS);
+  if (threadIdx.x == 0) DBG2(7);
+#undef DBG2
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 g_encode2 = nullptr;
 }  // namespace
 
 cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
@@ -163,7 +215,7 @@ cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long 
 
 template <int KIND, int BN>
 static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
-                              const EpiParams& e, int n_pairs, cudaStream_t s) {
+                              const EpiParams& e, int n_pairs, int ksplit, int* kflags, cudaStream_t s) {
   using C = Cfg2<BN>;
   constexpr bool sw = KIND == EPI_SWIGLU;
   constexpr int out_n = sw ? BN / 2 : BN;
@@ -173,18 +225,19 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, C::B_HALF, &tb));
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
   CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
-                    m_tiles, n_tiles, e));
+                    m_tiles, n_tiles, e, ksplit, kflags, c->dbg_buf));
   CB_LAUNCHED(c);
   return CB_OK;
 }
 
 // Pair tiles of 256 x BN; n_pairs CTA pairs (grid = 2 * n_pairs).
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
-                          int bn, int n_pairs, cudaStream_t s) {
+                          int bn, int n_pairs, int ksplit, int* kflags, cudaStream_t s) {
   ProfScope ps_(c, PROF_GEMM, s);
+  if (e.kind != EPI_RESID) ksplit = 1;
 #define L2_(KIND_)                                                                                      \
-  return bn == 256 ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, s)                  \
-                   : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, s)
+  return bn == 256 ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, s)  \
+                   : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, s)
   switch (e.kind) {
     case EPI_STORE: L2_(EPI_STORE);
     case EPI_STORE_F32: L2_(EPI_STORE_F32);
@@ -208,8 +261,31 @@ template <int BN> static cb_status set_attrs2() {
   return CB_OK;
 }
 
-cb_status gemm_tc2_init() {
+// How many 2-CTA clusters of the kernel can be co-resident (GPC boundaries can leave fewer than SMs / 2).
+template <int BN> static cb_status max_pairs2(int num_sms, int* out) {
+  using C = Cfg2<BN>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  CB_CUDA(cudaOccupancyMaxActiveClusters(&n, gemm_tc2_kernel<EPI_RESID, BN>, &cfg));
+  *out = n;
+  return CB_OK;
+}
+
+cb_status gemm_tc2_init(int num_sms, int* max_pairs) {
   CB_TRY(set_attrs2<256>());
   CB_TRY(set_attrs2<128>());
+  int a = 0, b = 0;
+  CB_TRY(max_pairs2<256>(num_sms, &a));
+  CB_TRY(max_pairs2<128>(num_sms, &b));
+  *max_pairs = a < b ? a : b;
+  CB_REQUIRE(*max_pairs >= 1, CB_E_CUDA, "no CTA pair of the tcgen05 GEMM fits on this device");
   return CB_OK;
 }

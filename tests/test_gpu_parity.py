@@ -134,6 +134,25 @@ def test_gemm_tcgen05(P, M, N, K, pair):
     assert rel_err(np32(Cb), ref) < 5e-3
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 1024, 1000), (461, 4096, 14336), (1000, 512, 4096)])
+@pytest.mark.parametrize("ksplit", [1, 2, 3, 4])
+def test_gemm_resid_ksplit(P, M, N, K, ksplit):
+    """Residual-epilogue GEMM C += A.B^T (o-/down-projection form) with the CTA-pair kernel's k-split
+    chain forced to 1..4 pieces: fp64 reference, and bitwise reproducible (fixed chain order)."""
+    ctx = P.Context(shape("small"), "bf16", max_tokens=8)
+    ctx.set_option("gemm_pair", 1)
+    ctx.set_option("gemm_ksplit", ksplit)
+    g = torch.Generator(device=DEV).manual_seed(M + 3 * N + ksplit)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)
+    C0 = torch.randn(M, N, device=DEV, generator=g) * 30.0
+    C = P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2)
+    ref = (C0.double() + A.double() @ B.double().T).cpu().numpy()
+    assert rel_err(np32(C), ref) < 5e-5
+    for _ in range(2):  # flags reset between launches; same order -> same bits
+        assert torch.equal(P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2), C)
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("name", ["tiny", "small"])
 def test_attention_parity(P, dtype, name):

@@ -21,9 +21,13 @@ SHAPES = [  # (name, M, N, K)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
-    ap.add_argument("--modes", default="1,2,0")
+    ap.add_argument("--modes", default="0")
     ap.add_argument("--bns", default="0")
     ap.add_argument("--pairs", default="0")
+    ap.add_argument("--ksplits", default="0")
+    ap.add_argument("--resid", action="store_true", help="residual epilogue C += A.B^T (fp32 C)")
+    ap.add_argument("--only", default="", help="comma list of shape names")
+    ap.add_argument("--pdl", type=int, default=1)
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -31,17 +35,24 @@ def main():
     from synth import workload as W
     ctx = P.Context(W.MODELS["mistral-7b"], "bf16", max_tokens=8)
     res = {}
+    ctx.set_option("pdl", a.pdl)
+    print("num_sms", ctx.info("num_sms"), "gemm_max_pairs", ctx.info("gemm_max_pairs"), flush=True)
+    only = set(a.only.split(",")) if a.only else None
     for name, M, N, K in SHAPES:
+        if only and name not in only:
+            continue
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
-        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        for mode, bn, pr in [(int(m), int(b), int(p)) for m in a.modes.split(",") for b in a.bns.split(",")
-                             for p in a.pairs.split(",")]:
+        C = torch.zeros(M, N, device="cuda", dtype=torch.float32 if a.resid else torch.bfloat16)
+        for mode, bn, pr, ks in [(int(m), int(b), int(p), int(k)) for m in a.modes.split(",")
+                                 for b in a.bns.split(",") for p in a.pairs.split(",") for k in a.ksplits.split(",")]:
             ctx.set_option("gemm_sched", mode)
             ctx.set_option("gemm_bn", bn)
             ctx.set_option("gemm_pair", pr)
+            ctx.set_option("gemm_ksplit", ks)
             fn = lambda: P.api.check(P.api.lib().cb_op_gemm(ctx.handle, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                                                            M, N, K, 0, 2, torch.cuda.current_stream().cuda_stream))
+                                                            M, N, K, 2 if a.resid else 0, 2,
+                                                            torch.cuda.current_stream().cuda_stream))
             for _ in range(3):
                 fn()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -53,8 +64,9 @@ def main():
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.iters * 1e3
             tf = 2.0 * M * N * K / (us * 1e-6) / 1e12
-            res[f"{name}/m{mode}/bn{bn}/p{pr}"] = (round(us, 1), round(tf, 1))
-            print(f"{name:10s} M={M:5d} N={N:6d} K={K:6d} mode={mode} bn={bn} pair={pr}: {us:8.1f} us  {tf:7.1f} TFLOP/s", flush=True)
+            res[f"{name}/m{mode}/bn{bn}/p{pr}/k{ks}"] = (round(us, 1), round(tf, 1))
+            print(f"{name:10s} M={M:5d} N={N:6d} K={K:6d} mode={mode} bn={bn} pair={pr} ks={ks}: {us:8.1f} us "
+                  f"{tf:7.1f} TFLOP/s", flush=True)
     print(json.dumps(res))
 
 
