@@ -324,6 +324,16 @@ def run_ours(args):
     ms_max = float(t.item())
     value = world * N / (ms_max / 1e3)
 
+    if os.environ.get("CB_TRACE_SEL"):  # tuning: per-CTA event trace of the last matching launch of a step
+        ctx.set_option("debug_trace", int(os.environ["CB_TRACE_SEL"]))
+        step_eager()
+        torch.cuda.synchronize()
+        import ctypes
+        raw = (ctypes.c_int64 * 2048)()
+        P.api.check(P.api.lib().cb_debug_fetch(ctx.handle, raw, 2048))
+        np.save(os.environ.get("CB_TRACE_OUT", "gpurun_out/trace.npy"), np.array(raw[:], dtype=np.int64))
+        ctx.set_option("debug_trace", 0)
+
     # per-kernel profile pass (same steps, per-launch CUDA events on the launching stream)
     prof = P.api.profile_steps(ctx, step_eager, max(3, min(args.steps, 10)))
     work = algorithmic_work(s, N, 0, ks)

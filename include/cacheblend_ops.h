@@ -53,7 +53,9 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM, 3 = mma.sync (legacy tensor path)
  *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor of the tcgen05 attention
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
- *   "debug_trace" 1 = record clock64 pipeline events of one CTA of the tcgen05 attention (tuning)
+ *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
+ *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue
+ *                 kind k (0 store, 1 store_f32, 2 qkv, 3 residual, 4 swiglu)
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 

@@ -414,7 +414,7 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   float* opart = n_splits > 1 ? c->attn_part : nullptr;
   CB_LAUNCH(c, (attn_tc5_kernel), grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
                                          c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart, c->attn_ml,
-                                         c->dbg_buf);
+                                         c->dbg_sel == 1 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
   if (n_splits > 1) CB_TRY(launch_attention_merge(c, R, n_splits, out, s));
   return CB_OK;

@@ -348,6 +348,7 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     return CB_OK;
   }
   if (std::strcmp(name, "debug_trace") == 0) {
+    c->dbg_sel = (int)value;
     if (value && !c->dbg_buf) {
       CB_CUDA(cudaMalloc(&c->dbg_buf, 2048 * sizeof(long long)));
       CB_CUDA(cudaMemset(c->dbg_buf, 0, 2048 * sizeof(long long)));

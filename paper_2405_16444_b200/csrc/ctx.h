@@ -54,6 +54,7 @@ struct cb_ctx {
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
   int no_fuse_dev;  // cb_set_option("fuse_deviation", 0) disables the QKV-epilogue deviation
+  int dbg_sel;         // debug_trace value: 1 = attention + every CTA-pair GEMM, 100 + k = pair GEMMs of kind k only
   long long* dbg_buf;  // cb_set_option("debug_trace", 1): per-event clock64 trace of one CTA (tuning)
   int pdl;          // programmatic dependent launch between library kernels (cb_set_option("pdl"))
   int* tok_d;       // [T] request-mode device copies of tokens / positions

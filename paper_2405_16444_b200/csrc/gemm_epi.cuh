@@ -96,6 +96,11 @@ __device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const f
 // global loads and stores of the epilogue are row-contiguous. Float4 slots are XOR-swizzled by row:
 // both the row-per-lane writes and the 4-rows-per-instruction reads are bank-conflict free.
 constexpr int EPI_WARP_F4 = 32 * 8;  // float4 slots per warp buffer (4 KB)
+#ifndef CB_STAGED_KINDS
+#define CB_STAGED_KINDS ((1 << EPI_STORE) | (1 << EPI_STORE_F32) | (1 << EPI_RESID))
+#endif
+// epilogue kinds that take the staged (row-contiguous) path
+template <int KIND> constexpr bool staged_kind() { return (CB_STAGED_KINDS >> KIND) & 1; }
 
 __device__ __forceinline__ void stage_put(float4* buf, int lane, const float* v) {
 #pragma unroll
@@ -256,6 +261,125 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
     }
     __syncwarp();  // buffer reused by the next chunk
     if (dbg != nullptr && lane == 0 && c / 32 < 8) dbg[c / 32] = tc::globaltimer();
+  }
+}
+
+// ---- row-per-lane QKV epilogue with operands issued early -----------------------------------------
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {  // bulk L2 prefetch (16 B multiple)
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Called by each epilogue lane for its own tile row before the accumulator is ready (the mainloop is
+// still running): pulls the row's cached K/V reference segment and RoPE table row into L2.
+__device__ __forceinline__ void qkv_prefetch(const EpiParams& e, int m, bool row_ok, int n0, int out_n) {
+  if (!row_ok) return;
+  const int tok = __ldg(e.row_tok + m);
+  const int c0 = e.col0 + n0;
+  const int c1 = min(e.col0 + e.N, c0 + out_n);  // exclusive
+  if (c0 < e.qd + e.kvd) {  // rope row (cos, sin of all pairs) at the row's position
+    const int p = __ldg(e.pos + tok);
+    prefetch_l2(e.rope_tab + (size_t)p * (e.hd >> 1), (uint32_t)(e.hd >> 1) * 8u);
+  }
+  if (e.dev_part != nullptr && m < e.n_cand && c1 > e.qd) {
+    const int a = max(c0, e.qd);
+    if (a < e.qd + e.kvd) {
+      const int b = min(c1, e.qd + e.kvd);
+      prefetch_l2(reinterpret_cast<const bf16*>(e.k_ref) + (size_t)tok * e.kvd + (a - e.qd), (uint32_t)(b - a) * 2u);
+    }
+    const int av = max(c0, e.qd + e.kvd);
+    if (av < c1)
+      prefetch_l2(reinterpret_cast<const bf16*>(e.v_ref) + (size_t)tok * e.kvd + (av - e.qd - e.kvd),
+                  (uint32_t)(c1 - av) * 2u);
+  }
+}
+
+// EPI_RESID: pull the row's residual segment into L2 while the mainloop runs.
+__device__ __forceinline__ void resid_prefetch(const EpiParams& e, int m, bool row_ok, int n0, int out_n) {
+  if (!row_ok) return;
+  const int src = e.res_row ? __ldg(e.res_row + m) : m;
+  const int w = min(out_n, e.N - n0);
+  if (w > 0) prefetch_l2(e.h_in + (size_t)src * e.ldo + n0, (uint32_t)w * 4u);
+}
+
+// EPI_QKV on 64 accumulator columns [n, n + 64) of row m (hd % 64 == 0: the chunk lies in one q, k or
+// v head). Warp-collective. RoPE (cos, sin) and the cached K/V reference are loaded before the TMEM
+// read, so one (L2) latency is exposed per 64 columns. Returns the chunk's squared distance to the
+// reference (0 for q columns and non-candidates). tok = row_tok[m], p = pos[tok].
+__device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool row_ok, uint32_t taddr, int tok, int p) {
+  const int c = e.col0 + n;
+  const bool is_q = c < e.qd, is_v = c >= e.qd + e.kvd;
+  const bool dev_on = row_ok && !is_q && e.dev_part != nullptr && m < e.n_cand;
+  const int kv_c = is_q ? 0 : (is_v ? c - e.qd - e.kvd : c - e.qd);
+  float4 cs[16];
+  uint4 ref[8];
+  if (row_ok && !is_v) {
+    const int dim = (is_q ? c : c - e.qd) % e.hd;
+    const float4* t = reinterpret_cast<const float4*>(e.rope_tab + (size_t)p * (e.hd >> 1) + (dim >> 1));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cs[i] = __ldg(t + i);  // (cos, sin) of pairs 2i, 2i+1
+  }
+  if (dev_on) {
+    const uint4* r = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(is_v ? e.v_ref : e.k_ref) +
+                                                    (size_t)tok * e.kvd + kv_c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ref[i] = __ldg(r + i);
+  }
+  float x[64];
+  tc::tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(x));
+  tc::tmem_ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+  if (!row_ok) return 0.f;
+  if (!is_v) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float a0 = x[4 * i], a1 = x[4 * i + 1], b0 = x[4 * i + 2], b1 = x[4 * i + 3];
+      x[4 * i] = cs[i].x * a0 - cs[i].y * a1;
+      x[4 * i + 1] = cs[i].y * a0 + cs[i].x * a1;
+      x[4 * i + 2] = cs[i].z * b0 - cs[i].w * b1;
+      x[4 * i + 3] = cs[i].w * b0 + cs[i].z * b1;
+    }
+  }
+  float dev = 0.f;
+  if (dev_on) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t wv[4] = {ref[i].x, ref[i].y, ref[i].z, ref[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[j]));
+        const float d0 = x[8 * i + 2 * j] - f.x, d1 = x[8 * i + 2 * j + 1] - f.y;
+        dev += d0 * d0 + d1 * d1;
+      }
+    }
+  }
+  bf16* dst = is_q ? reinterpret_cast<bf16*>(e.q_out) + (size_t)m * e.qd + c
+                   : reinterpret_cast<bf16*>(is_v ? e.v_out : e.k_out) + (size_t)m * e.kvd + kv_c;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) st_bf16x16(dst + 16 * g, x + 16 * g);
+  return dev;
+}
+
+// Whole-row QKV epilogue over OUT_N accumulator columns from output column n0 (hd % 64 == 0):
+// 64-column chunks; a k/v head's deviation partial is published when the head ends (fixed order).
+template <int OUT_N>
+__device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, int n0, uint32_t trow) {
+  int tok = 0, p = 0;
+  if (row_ok) {
+    tok = __ldg(e.row_tok + m);
+    p = __ldg(e.pos + tok);
+  }
+  float dacc = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < OUT_N; c += 64) {
+    const int n = n0 + c;
+    if (n >= e.N) break;  // warp-uniform
+    dacc += qkv64(e, m, n, row_ok, trow + c, tok, p);
+    const int cl = e.col0 + n;
+    if (e.dev_part != nullptr && cl >= e.qd && (cl + 64) % e.hd == 0) {
+      const int kv_col = cl - e.qd;
+      const int slot = kv_col < e.kvd ? 2 * (kv_col / e.hd) : 2 * ((kv_col - e.kvd) / e.hd) + 1;
+      if (row_ok && m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc;
+      dacc = 0.f;
+    }
   }
 }
 

@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool final_piece = (kb1 == num_kb);
       const int n_con = (final_piece && kb0 > 0) ? sch.contributors(tile, contrib) : 0;
       float dacc = 0.f;  // fused deviation: running squared distance of the current k/v head
+      if constexpr (KIND == EPI_QKV) gepi::qkv_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
+      if constexpr (KIND == EPI_RESID) gepi::resid_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const int m = m0 + row;
@@ -233,7 +235,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           named_bar(1, 128);
         }
-        if (n_con == 0 && (KIND == EPI_RESID || KIND == EPI_STORE || KIND == EPI_STORE_F32)) {
+        if (KIND == EPI_QKV && n_con == 0 && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
+          gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow);
+        } else if (n_con == 0 && gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {
           gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4,
                                         lane, false);
         } else

@@ -137,6 +137,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // split-K chain (RESID only): split sp adds onto h_out after split sp - 1 of the same 32 rows
       // published it — a fixed order, so the sum is deterministic. flag = number of splits done.
       int* flag = kflags + ((size_t)t * 2 + rank) * 4 + q;
+      if constexpr (KIND == EPI_QKV) gepi::qkv_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
+      if constexpr (KIND == EPI_RESID) {
+        if (sp == 0) gepi::resid_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
+      }
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after();
       if (it == 0 && warp == 2 && lane == 0) DBG2(3);
@@ -157,7 +161,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m = m0 + row;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       float dacc = 0.f;
-      if (KIND == EPI_RESID || KIND == EPI_STORE || KIND == EPI_STORE_F32) {  // staged, row-contiguous
+      if (KIND == EPI_QKV && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
+        gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow);
+      } else if (gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {  // staged, row-contiguous
         gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane,
                                       sp > 0,
                                       (dbg != nullptr && it == 0 && warp == 2 && blockIdx.x < 128)
@@ -225,7 +231,8 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, C::B_HALF, &tb));
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
   CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
-                    m_tiles, n_tiles, e, ksplit, kflags, c->dbg_buf));
+                    m_tiles, n_tiles, e, ksplit, kflags,
+                    (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr));
   CB_LAUNCHED(c);
   return CB_OK;
 }
