@@ -259,6 +259,9 @@ def run_ours(args):
     ctx = P.Context(s, "bf16", max_tokens=max(N, max(lens)), max_pos=max(2 * N, 4096))
     if args.no_pdl:
         ctx.set_option("pdl", 0)
+    for kv in filter(None, os.environ.get("CB_OPTS", "").split(",")):  # tuning: CB_OPTS=name=value,...
+        k_, v_ = kv.split("=")
+        ctx.set_option(k_, int(v_))
     mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
     tok_h = req.tokens(s.vocab)
     tok = torch.from_numpy(tok_h).to(dev)

@@ -108,6 +108,8 @@ cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb,
     if (gemm_tc_ok(c, A, lda, B, ldb, M, K, e)) return launch_gemm_tc(c, A, lda, B, ldb, M, K, e, s);
     CB_REQUIRE(impl != 2, CB_E_UNSUPPORTED, "tcgen05 GEMM does not take this shape (M=%d N=%d K=%d)", M, e.N, K);
   }
+  CB_REQUIRE(e.norm_gain == nullptr && e.ss_in == nullptr, CB_E_UNSUPPORTED,
+             "fused RMSNorm requested on a GEMM outside the tcgen05 path");
   return launch_gemm_simt(c, A, lda, B, ldb, M, K, e, s);
 }
 
@@ -177,6 +179,7 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->act = cv.take<void>((size_t)T * m->d_ff * B);
   o->dev = cv.take<float>((size_t)T * 4);
   o->dev_part = cv.take<float>((size_t)2 * m->n_kv_heads * T * 4);
+  o->ss = cv.take<float>((size_t)T * ((d + 127) / 128) * 4);
   o->row_tok[0] = cv.take<int>((size_t)T * 4);
   o->row_tok[1] = cv.take<int>((size_t)T * 4);
   o->qrow = cv.take<int>((size_t)T * 4);
@@ -358,6 +361,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     }
     return CB_OK;
   }
+  if (std::strcmp(name, "fuse_norm") == 0) {
+    c->no_fuse_norm = value == 0;
+    return CB_OK;
+  }
   if (std::strcmp(name, "fuse_deviation") == 0) {
     c->no_fuse_dev = value == 0;
     return CB_OK;
@@ -490,7 +497,57 @@ struct LayerBufs {
   float* h_out;        // [k + n_suf][d]
   const int* row_tok;  // [n_cand + n_suf]
   int* qtok;           // [k + n_suf] out
+  bool x_ready = false;                 // c->x / c->ss already hold this layer's fused attention RMSNorm
+  const void* next_attn_norm = nullptr;  // next layer's attention-norm gain: fuse it into the down projection
+  bool* next_ready = nullptr;           // out: set when the down projection produced the next layer's norm
 };
+
+// RMSNorm fusion (R12): the residual GEMM writes y = bf16(h * gain) plus 128-column sums of h^2 and the
+// next projection scales its accumulator rows by 1/rms. Needs the tcgen05 path on both GEMMs.
+bool norm_fusable(const cb_ctx* c) { return !c->no_fuse_norm && c->m.dtype == CB_BF16 && c->m.d_model % 512 == 0; }
+
+void set_norm_producer(const cb_ctx* c, EpiParams& e, const void* gain) {
+  e.norm_gain = (const float*)gain; e.y_out = c->x; e.ss_out = c->ss; e.ld_ss = c->m.d_model / 128;
+}
+void set_norm_consumer(const cb_ctx* c, EpiParams& e) {
+  e.ss_in = c->ss; e.ld_ss = c->m.d_model / 128; e.norm_d = c->m.d_model; e.norm_eps = c->m.rms_eps;
+}
+
+// Both GEMMs of a fused RMSNorm take the tcgen05 path (otherwise the classic kernel runs).
+bool norm_pair_ok(cb_ctx* c, const void* A1, int lda1, const void* B1, int M1, int K1, const EpiParams& e1,
+                  const void* B2, int K2, const EpiParams& e2) {
+  return norm_fusable(c) && gemm_tc_ok(c, A1, lda1, B1, lda1, M1, K1, e1) &&
+         gemm_tc_ok(c, c->x, c->m.d_model, B2, c->m.d_model, M1, K2, e2);
+}
+
+// Rows 0..Q-1 after attention: W_o + residual (gathered through res_row), RMSNorm, SwiGLU MLP +
+// residual. The RMSNorms are fused into the residual epilogues when both GEMMs allow it, and
+// the down projection also prepares the next layer's attention RMSNorm (b.next_attn_norm).
+cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, const int* res_row, cudaStream_t s) {
+  const cb_model& m = c->m;
+  const int d = m.d_model, qd = m.n_q_heads * m.head_dim;
+  EpiParams eo{};
+  eo.kind = EPI_RESID; eo.M = Q; eo.N = d; eo.ldo = d; eo.h_in = b.h_in; eo.h_out = b.h_out; eo.res_row = res_row;
+  EpiParams eg{};
+  eg.kind = EPI_SWIGLU; eg.M = Q; eg.N = m.d_ff; eg.ff = m.d_ff; eg.act = c->act;
+  const bool fuse_mlp = norm_pair_ok(c, c->attn, qd, w.w_o, Q, qd, eo, w.w_gate_up, d, eg);
+  if (fuse_mlp) {
+    set_norm_producer(c, eo, w.mlp_norm);
+    set_norm_consumer(c, eg);
+  }
+  CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, Q, qd, eo, 0, s));
+  if (!fuse_mlp) CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, Q, c->x, s));
+  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
+  EpiParams ed{};
+  ed.kind = EPI_RESID; ed.M = Q; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
+  if (b.next_attn_norm != nullptr && norm_fusable(c) &&
+      gemm_tc_ok(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed)) {
+    set_norm_producer(c, ed, b.next_attn_norm);
+    if (b.next_ready) *b.next_ready = true;
+  }
+  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
+  return CB_OK;
+}
 
 // Layer 0, the full layer (R2): every row is a query; context rows keep the realigned cache
 // (P:1750), suffix rows write fresh K,V.
@@ -499,10 +556,11 @@ cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, 
   const cb_model& m = c->m;
   const int T = N + n_suf, d = m.d_model, qd = m.n_q_heads * m.head_dim, kvd = m.n_kv_heads * m.head_dim;
   const size_t B = dtype_bytes(m.dtype);
-  CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, T, c->x, s));
   EpiParams e{};
   e.kind = EPI_QKV; e.M = T; e.N = qd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
   e.q_out = c->q; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  if (b.x_ready && gemm_tc_ok(c, c->x, d, w.w_qkv, d, T, d, e)) set_norm_consumer(c, e);
+  else CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, T, c->x, s));
   CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, T, d, e, 0, s));
   if (n_suf > 0) {
     EpiParams ek = e;
@@ -510,21 +568,12 @@ cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, 
     ek.k_out = (char*)kb + (size_t)N * kvd * B;
     ek.v_out = (char*)vb + (size_t)N * kvd * B;
     ek.row_tok = b.row_tok + N;
+    if (ek.ss_in) ek.ss_in += (size_t)N * ek.ld_ss;
     CB_TRY(launch_gemm(c, (const char*)c->x + (size_t)N * d * B, d, (const char*)w.w_qkv + (size_t)qd * d * B, d,
                        n_suf, d, ek, 0, s));
   }
   CB_TRY(launch_attention(c, c->q, c->iota, b.row_tok, T, kb, vb, T, c->attn, 0, s));
-  EpiParams eo{};
-  eo.kind = EPI_RESID; eo.M = T; eo.N = d; eo.ldo = d; eo.h_in = b.h_in; eo.h_out = b.h_out; eo.res_row = nullptr;
-  CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, T, qd, eo, 0, s));
-  CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, T, c->x, s));
-  EpiParams eg{};
-  eg.kind = EPI_SWIGLU; eg.M = T; eg.N = m.d_ff; eg.ff = m.d_ff; eg.act = c->act;
-  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, T, d, eg, 0, s));
-  EpiParams ed{};
-  ed.kind = EPI_RESID; ed.M = T; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
-  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, T, m.d_ff, ed, 0, s));
-  return CB_OK;
+  return mlp_block(c, w, b, T, nullptr, s);
 }
 
 // Layers i >= 1: selective recompute with HKVD selection.
@@ -536,10 +585,11 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   const int d = m.d_model, qd = m.n_q_heads * m.head_dim, kvd = m.n_kv_heads * m.head_dim;
   if (R == 0) return CB_OK;
   // 1. mask the input to the candidate rows and transform them into Q, K, V
-  CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, R, c->x, s));
   EpiParams e{};
   e.kind = EPI_QKV; e.M = R; e.N = qd + 2 * kvd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
   e.q_out = c->q; e.k_out = c->kf; e.v_out = c->vf; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  if (b.x_ready && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e)) set_norm_consumer(c, e);
+  else CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, R, c->x, s));
   // 2. Delta_kv against the loaded entries: fused into the tcgen05 QKV epilogue when every
   //    k/v head lies inside one output tile, else a separate kernel
   const bool fuse_dev = m.dtype == CB_BF16 && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e) && qd % 256 == 0 &&
@@ -558,17 +608,7 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));
   // 5. attention of the selected queries over all tokens, then W_o + residual, MLP + residual
   CB_TRY(launch_attention(c, c->q, c->qrow, b.qtok, Q, kb, vb, N + n_suf, c->attn, 0, s));
-  EpiParams eo{};
-  eo.kind = EPI_RESID; eo.M = Q; eo.N = d; eo.ldo = d; eo.h_in = b.h_in; eo.h_out = b.h_out; eo.res_row = c->qrow;
-  CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, Q, qd, eo, 0, s));
-  CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, Q, c->x, s));
-  EpiParams eg{};
-  eg.kind = EPI_SWIGLU; eg.M = Q; eg.N = m.d_ff; eg.ff = m.d_ff; eg.act = c->act;
-  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
-  EpiParams ed{};
-  ed.kind = EPI_RESID; ed.M = Q; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
-  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
-  return CB_OK;
+  return mlp_block(c, w, b, Q, c->qrow, s);
 }
 
 cb_status check_weights(const cb_layer_w* w) {
@@ -666,7 +706,10 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
   // (a2) layer 0 in full
   CB_TRY(launch_embed(c, embed, tok, T, c->h[0], s));
   CB_TRY(realign_layer(0));
+  bool ready = false;  // the previous down projection prepared this layer's attention RMSNorm
   LayerBufs b0{c->h[0], c->h[1], c->iota, nullptr};
+  b0.next_attn_norm = L > 1 ? w[1].attn_norm : nullptr;
+  b0.next_ready = &ready;
   CB_TRY(layer_full(c, w[0], b0, N, n_suffix, k_blend, v_blend, pos, s));
   if (sel_out) CB_TRY(launch_sel_out(c, c->iota, N, N, sel_out, s));
   // (a3-a8) layers 1..L-1 with gradual filtering: C_1 = all context tokens, C_{i+1} = S_i
@@ -676,6 +719,10 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
     const int k = k_sched[i];
     CB_TRY(realign_layer(i));
     LayerBufs b{c->h[cur], c->h[cur ^ 1], rows, c->row_tok[rt]};
+    b.x_ready = ready;
+    ready = false;
+    b.next_attn_norm = i + 1 < L ? w[i + 1].attn_norm : nullptr;
+    b.next_ready = &ready;
     char* kb = (char*)k_blend + (size_t)i * layer_stride * B;
     char* vb = (char*)v_blend + (size_t)i * layer_stride * B;
     CB_TRY(layer_blend(c, w[i], b, n_cand, k, n_suffix, N, kb, vb, pos, force_sel ? force_sel + (size_t)i * N : nullptr,

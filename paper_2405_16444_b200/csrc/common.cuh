@@ -97,6 +97,13 @@ struct EpiParams {
   float* h_out; const float* h_in; const int* res_row;
   // EPI_SWIGLU
   int ff; void* act;
+  // Fused RMSNorm (tcgen05 path; R12). Producer (EPI_RESID with norm_gain set): besides h_out it writes
+  // y[m][n] = bf16(h_out[m][n] * norm_gain[n]) and ss_out[m * ld_ss + n / 128] = the sum of h_out[m][n]^2
+  // over each 128-column block. Consumer (EPI_QKV / EPI_SWIGLU with ss_in set, A operand = y): every
+  // accumulator of row m is scaled by rs_m = 1 / sqrt(sum_b ss_in[m * ld_ss + b] / norm_d + norm_eps)
+  // (blocks summed in order) -- RMSNorm's per-row factor taken out of the projection.
+  const float* norm_gain; void* y_out; float* ss_out;
+  const float* ss_in; int ld_ss, norm_d; float norm_eps;
 };
 
 // Apply the epilogue to the adjacent column pair (n, n+1), n even. For SWIGLU a0/a1 are the gate

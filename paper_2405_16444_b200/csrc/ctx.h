@@ -43,6 +43,7 @@ struct cb_ctx {
   void* act;        // [T][ff]
   float* dev;       // [T]
   float* dev_part;  // [2 n_kv][T] fused-deviation partials (QKV epilogue)
+  float* ss;        // [T][d / 128] fused-RMSNorm sum-of-squares blocks (residual GEMM epilogue -> next GEMM)
   int* row_tok[2];  // [T] token index of each current row (candidates, then suffix)
   int* qrow;        // [T] row (in the current compact buffers) of each kept query
   int* iota;        // [T] 0..T-1
@@ -53,6 +54,7 @@ struct cb_ctx {
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
+  int no_fuse_norm;  // cb_set_option("fuse_norm", 0): separate RMSNorm kernels between the projections
   int no_fuse_dev;  // cb_set_option("fuse_deviation", 0) disables the QKV-epilogue deviation
   int dbg_sel;         // debug_trace value: 1 = attention + every CTA-pair GEMM, 100 + k = pair GEMMs of kind k only
   long long* dbg_buf;  // cb_set_option("debug_trace", 1): per-event clock64 trace of one CTA (tuning)

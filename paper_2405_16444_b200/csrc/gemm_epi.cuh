@@ -33,6 +33,19 @@ __device__ __forceinline__ float sqdiff16(const float* x, const bf16* p) {
   return s;
 }
 
+// Fused RMSNorm consumer: the per-row factor 1 / sqrt(mean(h^2) + eps) from the producer's 128-column
+// sum-of-squares blocks, summed in block order (1 when the fusion is off).
+__device__ __forceinline__ float row_rs(const EpiParams& e, int m, bool row_ok) {
+  if (e.ss_in == nullptr || !row_ok) return 1.f;
+  const float4* p = reinterpret_cast<const float4*>(e.ss_in + (size_t)m * e.ld_ss);
+  float s = 0.f;
+  for (int b = 0; b < e.ld_ss / 4; ++b) {
+    const float4 v = p[b];
+    s += v.x; s += v.y; s += v.z; s += v.w;
+  }
+  return 1.0f / sqrtf(s / (float)e.norm_d + e.norm_eps);
+}
+
 // Epilogue for 16 consecutive output columns n..n+15 of row m (all < N; N % 16 == 0). For EPI_QKV
 // with fused deviation it returns this chunk's squared distance to the cached K/V row.
 template <int KIND>
@@ -118,12 +131,16 @@ __device__ __forceinline__ uint2 pack4_bf16(float4 a) { return make_uint2(pack_b
 // xor-shuffle tree over the row's 8 lanes).
 template <int KIND, int BN>
 __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_base, int n0, uint32_t trow,
-                                              float4* buf, int lane, bool cont, long long* dbg = nullptr) {
+                                              float4* buf, int lane, bool cont, bool last = true,
+                                              long long* dbg = nullptr) {
   constexpr bool SW = KIND == EPI_SWIGLU;
   constexpr int OUT_N = SW ? BN / 2 : BN;
   const int j = lane & 7, r0 = lane >> 3;
   const int my_m = m_base + lane;
   const bool my_ok = my_m < M;
+  const float my_rs = (KIND == EPI_QKV || KIND == EPI_SWIGLU) ? row_rs(e, my_m, my_ok) : 1.f;
+  // fused RMSNorm producer (EPI_RESID, final split only): y = bf16(h_out * gain), 128-column sums of h_out^2
+  [[maybe_unused]] const bool norm_on = KIND == EPI_RESID && e.norm_gain != nullptr && last;
   int my_a = 0, my_b = 0;  // per-row operands of the lane's own row, broadcast below
   if constexpr (KIND == EPI_RESID) {
     if (my_ok) my_a = cont ? my_m : (e.res_row ? __ldg(e.res_row + my_m) : my_m);
@@ -137,7 +154,7 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
     ra[it] = __shfl_sync(0xffffffffu, my_a, it * 4 + r0);
     rb[it] = __shfl_sync(0xffffffffu, my_b, it * 4 + r0);
   }
-  float dacc[8];
+  float dacc[8];  // EPI_QKV: per-row deviation of the current head; EPI_RESID + norm: sum of squares
 #pragma unroll
   for (int it = 0; it < 8; ++it) dacc[it] = 0.f;
 #pragma unroll 1
@@ -190,11 +207,18 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
 #else
       tc::tmem_ld32(trow + c, v);
 #endif
+      if constexpr (KIND == EPI_QKV) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] *= my_rs;
+      }
       if constexpr (SW) {
         float u[32];
         tc::tmem_ld32(trow + BN / 2 + c, u);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = v[i] / (1.f + __expf(-v[i])) * u[i];
+        for (int i = 0; i < 32; ++i) {
+          const float g = v[i] * my_rs;
+          v[i] = g / (1.f + __expf(-g)) * (u[i] * my_rs);
+        }
       }
 #if defined(CB_EPI_EXP) && (CB_EPI_EXP & 2)
       if (v[0] == 12345.f) stage_put(buf, lane, v);
@@ -204,6 +228,10 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
     }
     __syncwarp();
     // 3. row-contiguous global traffic
+    [[maybe_unused]] float4 gain = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (KIND == EPI_RESID) {
+      if (norm_on && col_ok) gain = __ldg(reinterpret_cast<const float4*>(e.norm_gain + col));
+    }
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int r = it * 4 + r0, m = m_base + r;
@@ -220,9 +248,13 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
       } else if constexpr (KIND == EPI_SWIGLU) {
         if (ok) *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.act) + (size_t)m * e.ff + col) = pack4_bf16(a);
       } else if constexpr (KIND == EPI_RESID) {
-        if (ok)
-          *reinterpret_cast<float4*>(e.h_out + (size_t)m * e.ldo + col) =
-              make_float4(pre[it].x + a.x, pre[it].y + a.y, pre[it].z + a.z, pre[it].w + a.w);
+        const float4 o = make_float4(pre[it].x + a.x, pre[it].y + a.y, pre[it].z + a.z, pre[it].w + a.w);
+        if (ok) *reinterpret_cast<float4*>(e.h_out + (size_t)m * e.ldo + col) = o;
+        if (norm_on && ok) {  // lane-local sum of squares; reduced over the row's 8 lanes at the block end
+          *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.y_out) + (size_t)m * e.ldo + col) =
+              pack4_bf16(make_float4(o.x * gain.x, o.y * gain.y, o.z * gain.z, o.w * gain.w));
+          dacc[it] += (o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w);
+        }
       } else if constexpr (KIND == EPI_QKV) {
         if (ok && !is_v) {  // rotate pairs (dim, dim+1), (dim+2, dim+3) at the row's global position
           const float4 t = pre[it];
@@ -245,6 +277,20 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
           d += __shfl_xor_sync(0xffffffffu, d, 2);
           d += __shfl_xor_sync(0xffffffffu, d, 4);
           dacc[it] += d;
+        }
+      }
+    }
+    if constexpr (KIND == EPI_RESID) {
+      if (norm_on && ((n + 32) % 128 == 0 || c + 32 >= OUT_N)) {  // a 128-column block ends: publish
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          float sq = dacc[it];  // fixed xor tree over the row's 8 lanes
+          sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+          sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+          sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+          const int m = m_base + it * 4 + r0;
+          if (j == 0 && m < M) e.ss_out[(size_t)m * e.ld_ss + n / 128] = sq;
+          dacc[it] = 0.f;
         }
       }
     }
@@ -305,7 +351,8 @@ __device__ __forceinline__ void resid_prefetch(const EpiParams& e, int m, bool r
 // v head). Warp-collective. RoPE (cos, sin) and the cached K/V reference are loaded before the TMEM
 // read, so one (L2) latency is exposed per 64 columns. Returns the chunk's squared distance to the
 // reference (0 for q columns and non-candidates). tok = row_tok[m], p = pos[tok].
-__device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool row_ok, uint32_t taddr, int tok, int p) {
+__device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool row_ok, uint32_t taddr, int tok, int p,
+                                       float rs) {
   const int c = e.col0 + n;
   const bool is_q = c < e.qd, is_v = c >= e.qd + e.kvd;
   const bool dev_on = row_ok && !is_q && e.dev_part != nullptr && m < e.n_cand;
@@ -328,6 +375,8 @@ __device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool ro
   tc::tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(x));
   tc::tmem_ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(x + 32));
   if (!row_ok) return 0.f;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) x[i] *= rs;
   if (!is_v) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -361,7 +410,7 @@ __device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool ro
 // Whole-row QKV epilogue over OUT_N accumulator columns from output column n0 (hd % 64 == 0):
 // 64-column chunks; a k/v head's deviation partial is published when the head ends (fixed order).
 template <int OUT_N>
-__device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, int n0, uint32_t trow) {
+__device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, int n0, uint32_t trow, float rs) {
   int tok = 0, p = 0;
   if (row_ok) {
     tok = __ldg(e.row_tok + m);
@@ -372,7 +421,7 @@ __device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, 
   for (int c = 0; c < OUT_N; c += 64) {
     const int n = n0 + c;
     if (n >= e.N) break;  // warp-uniform
-    dacc += qkv64(e, m, n, row_ok, trow + c, tok, p);
+    dacc += qkv64(e, m, n, row_ok, trow + c, tok, p, rs);
     const int cl = e.col0 + n;
     if (e.dev_part != nullptr && cl >= e.qd && (cl + 64) % e.hd == 0) {
       const int kv_col = cl - e.qd;

@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool final_piece = (kb1 == num_kb);
       const int n_con = (final_piece && kb0 > 0) ? sch.contributors(tile, contrib) : 0;
       float dacc = 0.f;  // fused deviation: running squared distance of the current k/v head
+      [[maybe_unused]] const float rs = gepi::row_rs(e, m0 + row, m0 + row < M);  // fused RMSNorm consumer
       if constexpr (KIND == EPI_QKV) gepi::qkv_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
       if constexpr (KIND == EPI_RESID) gepi::resid_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
       tc::mbar_wait(&tfull[acc], acc_phase);
@@ -236,10 +237,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           named_bar(1, 128);
         }
         if (KIND == EPI_QKV && n_con == 0 && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
-          gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow);
+          gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow, rs);
         } else if (n_con == 0 && gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {
           gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4,
-                                        lane, false);
+                                        lane, false, true);
         } else
 #pragma unroll 1
         for (int c = 0; c < OUT_N; c += 16) {
@@ -283,6 +284,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) { v[i] = sv[i] + v[i]; u[i] = su[i] + u[i]; }
           }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) { v[i] *= rs; u[i] *= rs; }
           const int n = nb * OUT_N + c;
           if (m < M && n < e.N) {
             const float d = gepi::epi16<KIND>(e, m, n, v, u);
@@ -482,7 +485,9 @@ static cb_status launch_bn(cb_ctx* c, const void* A, int lda, const void* B, int
 
 cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
                          const EpiParams& e, cudaStream_t s) {
-  const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, c->gemm_sched,
+  // the stream-K fixup path has no fused-RMSNorm producer: plain data-parallel then
+  const int sched = (e.norm_gain != nullptr && c->gemm_sched == 2) ? 1 : c->gemm_sched;
+  const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit);
   if (pl.pair) return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, s);
   ProfScope ps_(c, PROF_GEMM, s);

@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // published it — a fixed order, so the sum is deterministic. flag = number of splits done.
       int* flag = kflags + ((size_t)t * 2 + rank) * 4 + q;
       if constexpr (KIND == EPI_QKV) gepi::qkv_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
+      // fused RMSNorm consumer: the row factor is ready before the accumulator (1 if off)
+      [[maybe_unused]] const float rs = gepi::row_rs(e, m0 + row, m0 + row < M);
       if constexpr (KIND == EPI_RESID) {
         if (sp == 0) gepi::resid_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
       }
@@ -162,10 +164,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       float dacc = 0.f;
       if (KIND == EPI_QKV && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
-        gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow);
+        gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow, rs);
       } else if (gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {  // staged, row-contiguous
         gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane,
-                                      sp > 0,
+                                      sp > 0, sp == ksplit - 1,
                                       (dbg != nullptr && it == 0 && warp == 2 && blockIdx.x < 128)
                                           ? dbg + 1024 + blockIdx.x * 8 : nullptr);
       } else {
@@ -174,6 +176,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float v[16], u[16];
         tc::tmem_ld16(trow + c, v);
         if constexpr (SW) tc::tmem_ld16(trow + BN / 2 + c, u);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) { v[i] *= rs; u[i] *= rs; }
         const int n = nb * OUT_N + c;
         if (m < M && n < e.N) {
           const float d = gepi::epi16<KIND>(e, m, n, v, u);
