@@ -345,8 +345,15 @@ def run_ours(args):
     roof = None
     if gemm_ms > 0:
         achieved = work["gemm_flops"] / (gemm_ms / 1e3) / 1e12
+        traffic, tnote = None, None
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01b_traffic.json")
+        if os.path.exists(tpath):  # committed ncu measurement of the largest GEMM launch (bytes per launch)
+            tj = json.load(open(tpath))
+            traffic = tj["dram_bytes"]
+            tnote = (f"{tj['kernel']}: DRAM {tj['dram_bytes']} B vs algorithmic {tj['algorithmic_bytes']} B "
+                     f"per launch ({tj['source']})")
         roof = {"bound": "tensor", "kernel": "gemm (all projections)", "achieved": achieved, "peak": tf_sus,
-                "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": traffic, "traffic_note": tnote,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
                 "share_of_step": gemm_ms / ms}
     # end to end through the public API: chunk caches + tokens from pinned host memory, h_out back
