@@ -17,7 +17,12 @@
 //              the K-major SWIZZLE_128B layout the MMA reads (one column block per half); finally
 //              O / l (or the split partial), each half writing its 64 output columns.
 // Key tiles past the CTA's last query token are never loaded; only tiles reaching past its first
-// query token are masked. Heaviest (latest-token) tiles are scheduled first.
+// query token are masked.
+// Load balance: the rows are in token order, so the last row tiles see the most keys. Every row tile
+// gets n_splits CTAs over fixed key ranges of kt_per_split tiles (empty ranges exit at once), launched
+// heaviest first. When a row tile has more than one non-empty range, each CTA writes an fp32 partial
+// (O, m, l) and bumps the tile's counter; the last one to arrive merges all partials in split order
+// (deterministic) and writes the output -- no separate merge launch.
 #include <cudaTypedefs.h>
 
 #include <unordered_map>
@@ -53,10 +58,15 @@ __global__ void __launch_bounds__(NT, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
                     int n_rows, int n_keys, bf16* __restrict__ out, int n_q, int n_kv, float scale_log2,
-                    int kt_per_split, float* __restrict__ opart, float2* __restrict__ ml, long long* __restrict__ dbg) {
+                    int kt_per_split, int n_splits, float* __restrict__ opart, float2* __restrict__ ml,
+                    int* __restrict__ tile_cnt, long long* __restrict__ dbg) {
   pdl_enter();
-  const bool dbg_on = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+#ifdef CB_ATTN_TRACE  // tools/attn_trace.py: clock64 pipeline events of CTA 0 (build with -DCB_ATTN_TRACE)
+  const bool dbg_on = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
 #define DBG(i) do { if (dbg_on && (i) < 2048) dbg[i] = clock64(); } while (0)
+#else
+#define DBG(i) do { } while (0)
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -77,7 +87,10 @@ __global__ void __launch_bounds__(NT, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.y, G = n_q / n_kv, R = n_rows * G;
-  const int rho0 = (gridDim.x - 1 - blockIdx.x) * BM;
+  const int tiles = gridDim.x / n_splits;
+  const int tile = tiles - 1 - (int)blockIdx.x / n_splits;  // heaviest (latest rows) first
+  const int split = (int)blockIdx.x % n_splits;
+  const int rho0 = tile * BM;
   const int qd = n_q * HD;
 
   int kmax = -1, kmin = 1 << 30;
@@ -87,15 +100,11 @@ __global__ void __launch_bounds__(NT, 1)
     kmin = min(kmin, t);
   }
   const int n_kt = (kmax + BC) / BC;
-  const int split = blockIdx.z;
+  const int n_active = (n_kt + kt_per_split - 1) / kt_per_split;  // non-empty key ranges of this row tile
   const int jb = split * kt_per_split, je = min(n_kt, jb + kt_per_split);
+  if (jb >= je) return;  // nothing for this range (the tile's other CTAs do not count it)
+  const bool partial = n_active > 1;
   const size_t part_row0 = ((size_t)split * n_kv + g) * R;
-  if (jb >= je) {  // no keys for this split: neutral partial (m = -inf, l = 0)
-    if (opart != nullptr)
-      for (int i = threadIdx.x; i < BM; i += NT)
-        if (rho0 + i < R) ml[part_row0 + rho0 + i] = make_float2(-INFINITY, 0.f);
-    return;
-  }
   const int nt = je - jb;
 
   if (warp == 0 && lane == 0) {
@@ -318,24 +327,60 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[c * 32 + i] = x[i];
     }
-    if (valid) {
-      if (opart != nullptr) {
+    bool write_out = !partial;
+    if (partial) {
+      if (valid) {
         float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD + wg * 64);
 #pragma unroll
         for (int i = 0; i < 16; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         if (wg == 0) ml[part_row0 + rho] = make_float2(m_used, l);
-      } else {
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD + wg * 64);
+      }
+      __threadfence();  // partials visible device-wide before the arrival is counted
+      named_bar_sync(1, 256);
+      int* flag = reinterpret_cast<int*>(xl + 256);
+      if (et == 0) {
+        const int old = atomicAdd(tile_cnt + (size_t)tile * n_kv + g, 1);
+        const int last = old == n_active - 1;
+        if (last) tile_cnt[(size_t)tile * n_kv + g] = 0;  // reset for the next launch
+        *flag = last;
+      }
+      named_bar_sync(1, 256);
+      write_out = *flag != 0;
+      if (write_out) {  // last arrival: merge every range's partial in split order
+        __threadfence();
+        float mstar = -INFINITY;
+        for (int sp = 0; sp < n_active; ++sp)
+          if (valid) mstar = fmaxf(mstar, __ldcg(&ml[((size_t)sp * n_kv + g) * R + rho].x));
+        float lt = 0.f;
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
-          uint4 w;
-          w.x = pack2(o[c8 * 8 + 0] * inv, o[c8 * 8 + 1] * inv);
-          w.y = pack2(o[c8 * 8 + 2] * inv, o[c8 * 8 + 3] * inv);
-          w.z = pack2(o[c8 * 8 + 4] * inv, o[c8 * 8 + 5] * inv);
-          w.w = pack2(o[c8 * 8 + 6] * inv, o[c8 * 8 + 7] * inv);
-          dst[c8] = w;
+        for (int i = 0; i < 64; ++i) o[i] = 0.f;
+        for (int sp = 0; sp < n_active && valid; ++sp) {
+          const size_t prow = ((size_t)sp * n_kv + g) * R + rho;
+          const float2 ms = __ldcg(&ml[prow]);
+          if (ms.x == -INFINITY) continue;
+          const float f = ex2(ms.x - mstar);
+          lt += ms.y * f;
+          const float4* src = reinterpret_cast<const float4*>(opart + prow * HD + wg * 64);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float4 x = __ldcg(src + i);
+            o[4 * i] += x.x * f; o[4 * i + 1] += x.y * f; o[4 * i + 2] += x.z * f; o[4 * i + 3] += x.w * f;
+          }
         }
+        l = lt;
+      }
+    }
+    if (valid && write_out) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD + wg * 64);
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        uint4 w;
+        w.x = pack2(o[c8 * 8 + 0] * inv, o[c8 * 8 + 1] * inv);
+        w.y = pack2(o[c8 * 8 + 2] * inv, o[c8 * 8 + 3] * inv);
+        w.z = pack2(o[c8 * 8 + 4] * inv, o[c8 * 8 + 5] * inv);
+        w.w = pack2(o[c8 * 8 + 6] * inv, o[c8 * 8 + 7] * inv);
+        dst[c8] = w;
       }
     }
     (void)et;
@@ -382,8 +427,6 @@ cb_status kv_tmap(const cb_ctx* c, const void* p, int n_keys, CUtensorMap* out) 
 
 bool attention_tc5_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.head_dim == HD && g_encode5 != nullptr; }
 
-cb_status launch_attention_merge(cb_ctx* c, int R, int n_splits, void* out, cudaStream_t s);
-
 cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                                const void* v, int n_keys, void* out, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
@@ -397,26 +440,24 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   int n_splits = 1;
   if (c->attn_splits > 0) {
     n_splits = c->attn_splits;
-  } else if (4 * base < 3LL * c->num_sms) {
-    // only when the (tile, head) grid leaves a quarter of the SMs idle: each split costs a CTA
-    // prologue and the LSE merge re-reads fp32 partials (tools/attn_micro.py)
-    n_splits = (int)std::min<long long>((c->num_sms + base - 1) / base, (max_kt + 1) / 2);
+  } else if (2 * base < (long long)c->num_sms) {
+    // measured (tools/attn_micro.py): extra CTAs only pay off when the (row tile, head) grid leaves
+    // more than half of the SMs idle -- split CTAs run as extra waves with their own prologues
+    n_splits = (int)std::min<long long>((c->num_sms + base - 1) / base, (max_kt + 3) / 4);
   }
-  if (c->attn_part == nullptr) n_splits = 1;
   n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
   n_splits = std::max(1, std::min(n_splits, 16));
   const int kt_per_split = (max_kt + n_splits - 1) / n_splits;
+  CB_REQUIRE(base <= c->attn_cnt_n, CB_E_SHAPE, "attention: %lld row tiles exceed the counter array", base);
   CUtensorMap tk, tv;
   CB_TRY(kv_tmap(c, k, n_keys, &tk));
   CB_TRY(kv_tmap(c, v, n_keys, &tv));
-  dim3 grid(tiles, n_kv, n_splits);
+  dim3 grid(tiles * n_splits, n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
-  float* opart = n_splits > 1 ? c->attn_part : nullptr;
   CB_LAUNCH(c, (attn_tc5_kernel), grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
-                                         c->m.n_q_heads, n_kv, scale_log2, kt_per_split, opart, c->attn_ml,
-                                         c->dbg_sel == 1 ? c->dbg_buf : nullptr);
+                                         c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
+                                         c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
-  if (n_splits > 1) CB_TRY(launch_attention_merge(c, R, n_splits, out, s));
   return CB_OK;
 }
 

@@ -191,6 +191,8 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->attn_part_rows = 2LL * T * m->n_q_heads;
   o->attn_part = cv.take<float>((size_t)o->attn_part_rows * m->head_dim * 4);
   o->attn_ml = cv.take<float2>((size_t)o->attn_part_rows * 8);
+  o->attn_cnt_n = (int)(((long long)T * m->n_q_heads + 127) / 128 + m->n_kv_heads);
+  o->attn_cnt = cv.take<int>((size_t)o->attn_cnt_n * 4);
   return cv.off + kAlign;
 }
 
@@ -272,6 +274,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
     return fail(e);
   if ((e = cudaMalloc(&c->err_word, sizeof(int))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(c->err_word, 0, sizeof(int))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(c->attn_cnt, 0, (size_t)c->attn_cnt_n * sizeof(int))) != cudaSuccess) return fail(e);
   iota_kernel<<<std::min(1024, (max_tokens + 255) / 256), 256>>>(c->iota, max_tokens);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);

@@ -50,6 +50,8 @@ struct cb_ctx {
   int* src_pos;     // [T] chunk-local positions (blend_forward)
   float* attn_part;     // split-KV attention partials [attn_part_rows][head_dim] fp32
   float2* attn_ml;      // [attn_part_rows] (m, l)
+  int* attn_cnt;        // [T * n_q / 128 + n_kv] split arrival counters of the tcgen05 attention (zero between launches)
+  int attn_cnt_n;
   long long attn_part_rows;
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync

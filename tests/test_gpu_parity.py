@@ -194,6 +194,28 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     assert rel_err(np32(out), ref) < 1e-2
 
 
+@pytest.mark.parametrize("splits", [1, 2, 5, 16])
+def test_attention_tc5_split_merge(P, splits):
+    """tcgen05 attention with the key range of every row tile cut into `splits` pieces and merged
+    in-kernel by the last-arriving CTA (split order, deterministic): oracle parity and bitwise
+    reproducibility across launches (the arrival counters reset themselves)."""
+    T, n_sel = 2000, 300
+    s = shape("small", n_kv_heads=2)
+    g = lambda st, n, H: rng.values(13, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
+    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
+    rows = np.sort(np.random.default_rng(5).choice(T, n_sel, replace=False)).astype(np.int32)
+    qrow = np.arange(n_sel, dtype=np.int32)
+    ctx = P.Context(s, "bf16", max_tokens=T)
+    ctx.set_option("attn_splits", splits)
+    args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
+            to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
+    out = P.api.op_attention(ctx, *args, impl=2)
+    ref = O.causal_attention(q[rows], np.arange(T)[rows], k, v, np.arange(T))
+    assert rel_err(np32(out), ref) < 1e-2
+    for _ in range(2):
+        assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
+
+
 # ---- (c) the whole blend ------------------------------------------------------------------------
 def _oracle_case(name, seed, lens, n_suf, dtype, ratio, **over):
     s = shape(name, **over)

@@ -1,5 +1,6 @@
 """Pipeline timeline of one CTA (the heaviest: latest query tokens) of the tcgen05 attention kernel, from
-the library's debug_trace clock64 events. python tools/attn_trace.py [n_sel] [T]"""
+the library's debug_trace clock64 events (build with CB_EXTRA_NVCC=-DCB_ATTN_TRACE ... build --force).
+python tools/attn_trace.py [n_sel] [T]"""
 import ctypes
 import os
 import sys
