@@ -39,7 +39,9 @@ CB_API cb_status cb_op_gemm(cb_ctx* ctx, const void* A, const void* B, void* C, 
  * index q_tok[r]) and q head h: out[r][h] = softmax_j(q.k_j / sqrt(hd)) v_j over keys j <= q_tok[r]
  * of k, v [n_keys][n_kv][hd], kv head h / (n_q / n_kv).  Token positions are strictly increasing, so
  * "key position <= query position" is "j <= q_tok[r]".  out: [n_rows][n_q * hd] (model dtype).
- * impl: 0 = auto, 1 = SIMT, 2 = tcgen05/TMEM (bf16, head_dim 128), 3 = mma.sync (bf16, head_dim 128). */
+ * impl: 0 = auto (2 for bf16 / head_dim 128), 1 = SIMT, 2 = tcgen05/TMEM one CTA per row tile, 3 = mma.sync,
+ * 4 = experimental persistent tcgen05 (LPT queue of (row tile, kv head, key chunk) items, two key streams
+ * per item with P in TMEM, in-kernel chunk merge); 2-4 need bf16, head_dim 128. */
 CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_row, const int32_t* q_tok,
                           int32_t n_rows, const void* k, const void* v, int32_t n_keys, void* out, int32_t impl,
                           void* stream);
@@ -50,8 +52,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width
  *   "gemm_pair"   0 = auto, 1 = CTA-pair (cta_group::2, 256-row tiles) only, 2 = single-CTA only
  *   "gemm_ksplit" 0 = auto, 1..4 = force the k-split chain of pair residual GEMMs (when it fits one wave)
- *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM, 3 = mma.sync (legacy tensor path)
- *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor of the tcgen05 attention
+ *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM per tile, 3 = mma.sync, 4 = persistent tcgen05
+ *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor (impl 4: key chunks per row tile)
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
  *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
  *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue

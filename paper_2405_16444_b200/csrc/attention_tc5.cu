@@ -425,6 +425,8 @@ cb_status kv_tmap(const cb_ctx* c, const void* p, int n_keys, CUtensorMap* out) 
 }
 }  // namespace
 
+cb_status kv_tmap5(const cb_ctx* c, const void* p, int n_keys, CUtensorMap* out) { return kv_tmap(c, p, n_keys, out); }
+
 bool attention_tc5_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.head_dim == HD && g_encode5 != nullptr; }
 
 cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,

@@ -24,6 +24,10 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
                                const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
 bool attention_tc5_ok(const cb_ctx* c);
 cb_status attention_tc5_init();
+cb_status launch_attention_tc6(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
+                               const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
+bool attention_tc6_ok(const cb_ctx* c, int n_rows);
+cb_status attention_tc6_init();
 cb_status topk_init_attrs();
 cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
@@ -117,6 +121,11 @@ cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int
                            const void* v, int n_keys, void* out, int impl, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
   if (impl == 0) impl = c->attn_impl;
+  if (impl == 4) {  // experimental (not the default): slower than impl 2 at blend sizes, see DESIGN.md
+    CB_REQUIRE(attention_tc6_ok(c, n_rows), CB_E_UNSUPPORTED,
+               "persistent tcgen05 attention needs bf16, head_dim 128 and <= 512 row tiles");
+    return launch_attention_tc6(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
+  }
   if (impl == 2 || (impl == 0 && attention_tc5_ok(c))) {
     CB_REQUIRE(attention_tc5_ok(c), CB_E_UNSUPPORTED, "tcgen05 attention needs bf16 and head_dim 128");
     return launch_attention_tc5(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
@@ -193,6 +202,7 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->attn_ml = cv.take<float2>((size_t)o->attn_part_rows * 8);
   o->attn_cnt_n = (int)(((long long)T * m->n_q_heads + 127) / 128 + m->n_kv_heads);
   o->attn_cnt = cv.take<int>((size_t)o->attn_cnt_n * 4);
+  o->attn_work = cv.take<int>(64);
   return cv.off + kAlign;
 }
 
@@ -275,6 +285,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if ((e = cudaMalloc(&c->err_word, sizeof(int))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(c->err_word, 0, sizeof(int))) != cudaSuccess) return fail(e);
   if ((e = cudaMemset(c->attn_cnt, 0, (size_t)c->attn_cnt_n * sizeof(int))) != cudaSuccess) return fail(e);
+  if ((e = cudaMemset(c->attn_work, 0, 64)) != cudaSuccess) return fail(e);
   iota_kernel<<<std::min(1024, (max_tokens + 255) / 256), 256>>>(c->iota, max_tokens);
   if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
@@ -287,6 +298,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = gemm_tc_init(c);
   if (st == CB_OK) st = attention_tc_init();
   if (st == CB_OK) st = attention_tc5_init();
+  if (st == CB_OK) st = attention_tc6_init();
   if (st != CB_OK) {
     cudaFree(c->rope_tab);
     cudaFree(c->err_word);
@@ -378,7 +390,7 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     return CB_OK;
   }
   if (std::strcmp(name, "attn_impl") == 0) {
-    CB_REQUIRE(value >= 0 && value <= 3, CB_E_INVALID_ARG, "attn_impl must be 0..3");
+    CB_REQUIRE(value >= 0 && value <= 4, CB_E_INVALID_ARG, "attn_impl must be 0..4");
     c->attn_impl = (int)value;
     return CB_OK;
   }
@@ -453,7 +465,7 @@ extern "C" cb_status cb_op_attention(cb_ctx* c, const void* q, const int32_t* q_
                                      int32_t impl, void* st) {
   CB_REQUIRE(c && q && q_row && q_tok && k && v && out && n_rows >= 0 && n_keys >= 1, CB_E_INVALID_ARG,
              "cb_op_attention: bad arguments");
-  CB_REQUIRE(impl >= 0 && impl <= 3, CB_E_INVALID_ARG, "cb_op_attention: impl must be 0, 1, 2 or 3");
+  CB_REQUIRE(impl >= 0 && impl <= 4, CB_E_INVALID_ARG, "cb_op_attention: impl must be 0..4");
   return launch_attention(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, impl, (cudaStream_t)st);
 }
 

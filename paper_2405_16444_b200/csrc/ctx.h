@@ -52,6 +52,7 @@ struct cb_ctx {
   float2* attn_ml;      // [attn_part_rows] (m, l)
   int* attn_cnt;        // [T * n_q / 128 + n_kv] split arrival counters of the tcgen05 attention (zero between launches)
   int attn_cnt_n;
+  int* attn_work;       // [2] persistent attention: item claim counter, finished-CTA counter (zero between launches)
   long long attn_part_rows;
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync

@@ -173,7 +173,7 @@ def test_attention_parity(P, dtype, name):
     assert rel_err(np32(out), ref) < (1e-5 if dtype == "f32" else 1e-2)
 
 
-@pytest.mark.parametrize("impl", [2, 3])
+@pytest.mark.parametrize("impl", [2, 3, 4])
 @pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (1000, 1000, 2), (777, 50, 1), (130, 3, 8),
                                           (4100, 900, 4)])
 def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
@@ -194,8 +194,9 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     assert rel_err(np32(out), ref) < 1e-2
 
 
+@pytest.mark.parametrize("impl", [2, 4])
 @pytest.mark.parametrize("splits", [1, 2, 5, 16])
-def test_attention_tc5_split_merge(P, splits):
+def test_attention_tc5_split_merge(P, splits, impl):
     """tcgen05 attention with the key range of every row tile cut into `splits` pieces and merged
     in-kernel by the last-arriving CTA (split order, deterministic): oracle parity and bitwise
     reproducibility across launches (the arrival counters reset themselves)."""
@@ -209,11 +210,11 @@ def test_attention_tc5_split_merge(P, splits):
     ctx.set_option("attn_splits", splits)
     args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
             to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
-    out = P.api.op_attention(ctx, *args, impl=2)
+    out = P.api.op_attention(ctx, *args, impl=impl)
     ref = O.causal_attention(q[rows], np.arange(T)[rows], k, v, np.arange(T))
     assert rel_err(np32(out), ref) < 1e-2
     for _ in range(2):
-        assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
+        assert torch.equal(P.api.op_attention(ctx, *args, impl=impl), out)
 
 
 # ---- (c) the whole blend ------------------------------------------------------------------------

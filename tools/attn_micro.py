@@ -15,6 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--splits", default="0,1,2,3,4,6")
+    ap.add_argument("--impls", default="2,4")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -31,7 +32,7 @@ def main():
         qrow = torch.arange(n_sel, dtype=torch.int32, device="cuda")
         qtok = torch.from_numpy(rows).cuda()
         flops = 4.0 * s.n_q_heads * s.head_dim * float(np.sum(rows + 1))
-        for impl, splits in [(2, int(x)) for x in a.splits.split(",")] + [(3, 0)]:
+        for impl, splits in [(int(i), int(x)) for i in a.impls.split(",") for x in a.splits.split(",")]:
             ctx.set_option("attn_splits", splits)
             fn = lambda: P.api.op_attention(ctx, q, qrow, qtok, k, v, T, impl=impl)
             for _ in range(3):
