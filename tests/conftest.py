@@ -13,3 +13,15 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a); run with -m gpu")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="module")
+def P():
+    """The CUDA library's Python binding (GPU tests only; builds the in-tree .so if stale)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2405_16444_b200.build import build
+    build()
+    import paper_2405_16444_b200 as P
+    return P

@@ -18,14 +18,6 @@ pytestmark = pytest.mark.gpu
 TOL = {"f32": 1e-4, "bf16": 2e-2}
 
 
-@pytest.fixture(scope="module")
-def P():
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    from paper_2405_16444_b200.build import build
-    build()
-    import paper_2405_16444_b200 as P
-    return P
 
 
 # ---- input generator: the library's counter RNG equals the numpy spec bit for bit ---------------
