@@ -40,7 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="mistral", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="mistral", choices=sorted(CONFIGS) + ["batched"],
+                    help="batched = SURVEY config 5: 64 Mistral-shape requests of 4-8 chunks x 256-1024 "
+                         "tokens, assigned to the ranks longest-first")
+    ap.add_argument("--batched-requests", type=int, default=64)
     ap.add_argument("--ratio", type=float, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,7 +202,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    shape_name, lens, ratio = CONFIGS[args.config]
+    shape_name, lens, ratio = CONFIGS.get(args.config, CONFIGS["mistral"])  # batched: per-request Mistral
     ratio = args.ratio if args.ratio is not None else ratio
     s = W.MODELS[shape_name]
     smp = OracleSample(s, lens, ratio, args.seed)
@@ -321,11 +324,8 @@ def run_ours(args):
         dist.barrier()
     launches = per_step_launches * args.steps
     ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * N / (ms_max / 1e3)
+    from paper_2405_16444_b200.dist import job_throughput, max_over_ranks
+    value, ms_max, _ = job_throughput(N, ms, dev)  # all ranks' tokens / slowest rank's time
 
     if os.environ.get("CB_TRACE_SEL"):  # tuning: per-CTA event trace of the last matching launch of a step
         ctx.set_option("debug_trace", int(os.environ["CB_TRACE_SEL"]))
@@ -361,9 +361,7 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args)
         if world > 1:
-            tt = torch.tensor([e2e["ms"]], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e["value"] = world * N / (float(tt.item()) / 1e3)
+            e2e["value"] = world * N / (max_over_ranks(e2e["ms"], dev) / 1e3)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = OracleSample(s, lens, ratio, args.seed)
@@ -434,9 +432,103 @@ def run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args):
                     "h_out D2H; KV^new stays on the GPU" + (" (CUDA graph)" if graphed else "")}
 
 
+def run_batched(args):
+    """independent Mistral-shape requests, longest-first over the ranks, each rank
+    blending its own requests back to back (one CUDA graph per request). Weak scaling, no collective on
+    the data path; the job throughput is all ranks' context tokens over the slowest rank's time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_16444_b200.dist import assign_requests, job_throughput, world_info
+    rank, world, local = world_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2405_16444_b200.build import build
+    if rank == 0 or world == 1:
+        build()
+    if world > 1:
+        dist.barrier()
+    import paper_2405_16444_b200 as P
+    reqs = W.config_requests("batched", args.seed)[:args.batched_requests]
+    parts = assign_requests([r.n_ctx for r in reqs], world)
+    mine = [reqs[i] for i in parts[rank]]
+    s = W.MODELS["mistral-7b"]
+    dev = torch.device("cuda", local)
+    L = s.n_layers
+    Nmax = max(r.n_ctx for r in mine) if mine else 1
+    ctx = P.Context(s, "bf16", max_tokens=Nmax, max_pos=max(2 * Nmax, 4096))
+    mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
+    graphs, tokens = [], 0
+    for req in mine:
+        N = req.n_ctx
+        tok = torch.from_numpy(req.tokens(s.vocab)).to(dev)
+        pos = torch.from_numpy(req.global_positions()).to(dev)
+        cs = req.chunk_starts()
+        k_in = torch.empty(L, N, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+        v_in = torch.empty_like(k_in)
+        for c in range(len(cs) - 1):  # the request's chunk caches (standalone prefill, P:1600)
+            a, b = int(cs[c]), int(cs[c + 1])
+            kc = torch.empty(L, b - a, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+            vc = torch.empty_like(kc)
+            P.blend_forward(ctx, mw, tok[a:b].contiguous(), torch.arange(b - a, dtype=torch.int32, device=dev), [0],
+                            b - a, None, None, kc, vc, [0] * L)
+            k_in[:, a:b] = kc
+            v_in[:, a:b] = vc
+        ks = P.schedule(req.ratio, N, L)
+        kb, vb = torch.empty_like(k_in), torch.empty_like(v_in)
+        h_out = torch.empty(ks[-1], s.d_model, dtype=torch.float32, device=dev)
+
+        def step(tok=tok, pos=pos, cs=cs, k_in=k_in, v_in=v_in, kb=kb, vb=vb, ks=ks, h_out=h_out):
+            P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, kb, vb, ks, h_out=h_out)
+        step()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        graphs.append((g, step))  # the closure keeps the request's buffers alive for the replays
+        tokens += N
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for g, _ in graphs:
+            g.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            for g, _ in graphs:
+                g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    value, ms_max, tok_all = job_throughput(tokens, ms, dev)
+    if rank == 0:
+        loads = [sum(reqs[i].n_ctx for i in p) for p in parts]
+        print(json.dumps({
+            "metric": "context tok/s of independent blend requests (SURVEY config 5)", "value": value,
+            "unit": "ctx_tok/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter RNG weights/tokens; chunk caches from standalone prefill)",
+            "config": {"workload": f"batched: {len(reqs)} mistral-7b requests, 4-8 chunks x 256-1024 tokens, r=0.15",
+                       "parallelism": f"request-parallel x{world} (longest-first)", "ctx_tokens": int(tok_all),
+                       "rank_tokens": loads, "balance": max(loads) / (sum(loads) / len(loads))},
+            "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config == "batched":
+        run_batched(a)
     else:
         run_ours(a)
