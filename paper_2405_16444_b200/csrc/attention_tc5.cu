@@ -34,7 +34,8 @@ namespace {
 constexpr int HD = 128, BM = 128, BC = 128, NT = 320;
 constexpr int ATOM = 128 * 128;    // 128 rows x 128 B (64 bf16): one SWIZZLE_128B column block
 constexpr int TILE = 2 * ATOM;     // 128 rows x 128 bf16
-constexpr int SMEM = 6 * TILE + 1024 + 256 + 3072;  // Q, K[2], V[2], P + alignment + barriers + exchange
+constexpr int KST = 3;            // K ring stages (V: 2); P lives in TMEM, so SMEM = Q + 3 K + 2 V
+constexpr int SMEM = 6 * TILE + 1024 + 256 + 3072;  // + alignment + barriers + exchange
 constexpr float RESCALE_THRESHOLD = 8.0f;    // log2 units
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -70,19 +71,17 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sK = smem + TILE;          // [2] stages
-  uint8_t* sV = smem + 3 * TILE;      // [2] stages
-  uint8_t* sP = smem + 5 * TILE;
+  uint8_t* sK = smem + TILE;          // [KST] stages
+  uint8_t* sV = smem + (1 + KST) * TILE;  // [2] stages
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
-  uint64_t* k_full = bars;            // [2]  K tile landed
-  uint64_t* k_empty = bars + 2;       // [2]  S MMAs done reading the K stage
-  uint64_t* v_full = bars + 11;       // [2]  V tile landed
-  uint64_t* v_empty = bars + 13;      // [2]  PV MMAs done reading the V stage
-  uint64_t* s_full = bars + 4;        // [2]
-  uint64_t* s_empty = bars + 6;       // [2]
-  uint64_t* q_full = bars + 8;
-  uint64_t* p_full = bars + 9;
-  uint64_t* pv_done = bars + 10;
+  uint64_t* k_full = bars;            // [3]  K tile landed
+  uint64_t* k_empty = bars + 3;       // [3]  S MMAs done reading the K stage
+  uint64_t* v_full = bars + 6;        // [2]  V tile landed
+  uint64_t* v_empty = bars + 8;       // [2]  PV MMAs done reading the V stage
+  uint64_t* s_full = bars + 10;       // [2]  S_t in TMEM buffer t % 2
+  uint64_t* q_full = bars + 12;
+  uint64_t* p_full = bars + 13;       // P_t written over S_t (8 softmax warps)
+  uint64_t* pv_done = bars + 14;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,13 +109,14 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmK);
     tc::tma_prefetch(&tmV);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < KST; ++b) {
       tc::mbar_init(&k_full[b], 1);
       tc::mbar_init(&k_empty[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&v_full[b], 1);
       tc::mbar_init(&v_empty[b], 1);
       tc::mbar_init(&s_full[b], 1);
-      tc::mbar_init(&s_empty[b], 8);
     }
     tc::mbar_init(q_full, 256);
     tc::mbar_init(p_full, 8);
@@ -139,14 +139,20 @@ __global__ void __launch_bounds__(NT, 1)
         tc::tma_load_3d(dst, m, bar, 0, g, key0);
         tc::tma_load_3d(dst + ATOM, m, bar, 64, g, key0);
       };
-      for (int t = 0; t < nt; ++t) {
-        const int b = t & 1, key0 = (jb + t) * BC;
-        if (t >= 2) tc::mbar_wait(&k_empty[b], ((t >> 1) - 1) & 1);
-        DBG(4 * t);
-        load(sK + b * TILE, &tmK, &k_full[b], key0);
-        if (t >= 2) tc::mbar_wait(&v_empty[b], ((t >> 1) - 1) & 1);
-        DBG(4 * t + 1);
-        load(sV + b * TILE, &tmV, &v_full[b], key0);
+      // K and V streams advance independently (K runs up to KST tiles ahead: S_t needs K_t a full
+      // softmax earlier than PV_t needs V_t), polling their empty barriers
+      int tk = 0, tv = 0;
+      while (tk < nt || tv < nt) {
+        if (tk < nt && (tk < KST || tc::mbar_test(&k_empty[tk % KST], (tk / KST - 1) & 1))) {
+          DBG(4 * tk);
+          load(sK + (tk % KST) * TILE, &tmK, &k_full[tk % KST], (jb + tk) * BC);
+          ++tk;
+        }
+        if (tv < tk && (tv < 2 || tc::mbar_test(&v_empty[tv & 1], ((tv >> 1) - 1) & 1))) {
+          DBG(4 * tv + 1);
+          load(sV + (tv & 1) * TILE, &tmV, &v_full[tv & 1], (jb + tv) * BC);
+          ++tv;
+        }
       }
     }
   } else if (warp == 1) {
@@ -154,21 +160,22 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr uint32_t IDESC_S = tc::idesc_bf16(BM, BC);
     constexpr uint32_t IDESC_PV = tc::idesc_bf16_bmn(BM, HD);
     const uint32_t tO = tmem + 256;
+    // S_{t+2} reuses TMEM buffer t % 2, which holds P_t: it is issued after PV_t on the in-order
+    // tensor pipe, so no extra barrier is needed
     auto issue_s = [&](int t) {
-      const int b = t & 1;
-      tc::mbar_wait(&k_full[b], (t >> 1) & 1);
-      if (t >= 2) tc::mbar_wait(&s_empty[b], ((t >> 1) - 1) & 1);
+      const int b = t & 1, kb = t % KST;
+      tc::mbar_wait(&k_full[kb], (t / KST) & 1);
       if (lane == 0) DBG(400 + 4 * t);
       tc::fence_after();
       if (tc::elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint64_t a = tc::sdesc_sw128(sQ + (kk >> 2) * ATOM) + 2 * (kk & 3);
-          const uint64_t bd = tc::sdesc_sw128(sK + b * TILE + (kk >> 2) * ATOM) + 2 * (kk & 3);
+          const uint64_t bd = tc::sdesc_sw128(sK + kb * TILE + (kk >> 2) * ATOM) + 2 * (kk & 3);
           tc::mma_bf16(tmem + b * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
         }
         tc::mma_commit(&s_full[b]);
-        tc::mma_commit(&k_empty[b]);
+        tc::mma_commit(&k_empty[kb]);
       }
       __syncwarp();
     };
@@ -183,10 +190,11 @@ __global__ void __launch_bounds__(NT, 1)
       if (tc::elect_one()) {
         const int b = t & 1;
 #pragma unroll
-        for (int kk = 0; kk < BC / 16; ++kk) {  // 16 keys per step
-          const uint64_t a = tc::sdesc_sw128(sP + (kk >> 2) * ATOM) + 2 * (kk & 3);
+        for (int kk = 0; kk < BC / 16; ++kk) {  // 16 keys per step; P in TMEM (keys 0-63 at columns
+          // 0-31 of the S buffer, keys 64-127 at columns 64-95: each softmax half over its own S)
+          const uint32_t a = tmem + b * 128 + (kk < 4 ? 8 * kk : 64 + 8 * (kk - 4));
           const uint64_t bd = tc::sdesc_sw128_mn(sV + b * TILE + kk * 2048, ATOM);
-          tc::mma_bf16(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
+          tc::mma_bf16_ts(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(pv_done);
         tc::mma_commit(&v_empty[b]);
@@ -223,7 +231,6 @@ __global__ void __launch_bounds__(NT, 1)
       if (et == 0) DBG(1201);
     }
     float m_used = -INFINITY, l = 0.f;
-    const uint32_t dp = tc::smem_u32(sP);
     for (int t = 0; t < nt; ++t) {
       const int b = t & 1;
       tc::mbar_wait(&s_full[b], (t >> 1) & 1);
@@ -237,9 +244,6 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = x[i];
       }
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&s_empty[b]);
       const int key0 = (jb + t) * BC + wg * 64;
       const bool need_mask = key0 + 63 > kmin;
       // half-row max of the raw scores (scale > 0 commutes with max); 8 chains for ILP
@@ -280,34 +284,27 @@ __global__ void __launch_bounds__(NT, 1)
         rs8[i & 7] += s[i];
       }
       l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-      if (t >= 1) {  // PV_{t-1} done: the P buffer is free and O is stable
+      // rescale O only when the reference max moved; PV_{t-1} must be complete (O stable)
+      if (t >= 1 && __any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write
         tc::mbar_wait(pv_done, (t - 1) & 1);
         if (et == 0) DBG(800 + 4 * t + 2);
         tc::fence_after();
-        if (__any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write of O
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float o[32];
-            tc::tmem_ld32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
+        for (int c = 0; c < 2; ++c) {
+          float o[32];
+          tc::tmem_ld32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= corr;
-            tc::tmem_st32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
-          }
-          tc::tmem_st_wait();
+          for (int i = 0; i < 32; ++i) o[i] *= corr;
+          tc::tmem_st32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
         }
       }
+      {  // P (bf16 pairs) over this half's own S columns: keys wg*64 .. +63 -> columns b*128 + wg*64 ..
+        uint32_t pk[32];
 #pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        uint4 w;
-        w.x = pack2(s[c8 * 8 + 0], s[c8 * 8 + 1]);
-        w.y = pack2(s[c8 * 8 + 2], s[c8 * 8 + 3]);
-        w.z = pack2(s[c8 * 8 + 4], s[c8 * 8 + 5]);
-        w.w = pack2(s[c8 * 8 + 6], s[c8 * 8 + 7]);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dp + sw_off(r, wg * 8 + c8)), "r"(w.x),
-                     "r"(w.y), "r"(w.z), "r"(w.w)
-                     : "memory");
+        for (int i = 0; i < 32; ++i) pk[i] = pack2(s[2 * i], s[2 * i + 1]);
+        tc::tmem_st32u(tmem + lane_base + b * 128 + wg * 64, pk);
       }
-      tc::fence_proxy_async();
+      tc::tmem_st_wait();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full);
