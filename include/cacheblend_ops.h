@@ -58,7 +58,10 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
  *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue
  *                 kind k (0 store, 1 store_f32, 2 qkv, 3 residual, 4 swiglu)
- *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off */
+ *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
+ *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
+ *   "mlp_split"   1 = off (default); 2..4 = gate_up in K blocks on the caller's stream with the matching
+ *                 down-projection blocks on an internal stream (experiment; measured slower) */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Read-only facts about the context: "num_sms", "gemm_max_pairs" (co-resident 2-CTA clusters of the

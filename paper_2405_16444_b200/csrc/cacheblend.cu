@@ -112,7 +112,7 @@ cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb,
     if (gemm_tc_ok(c, A, lda, B, ldb, M, K, e)) return launch_gemm_tc(c, A, lda, B, ldb, M, K, e, s);
     CB_REQUIRE(impl != 2, CB_E_UNSUPPORTED, "tcgen05 GEMM does not take this shape (M=%d N=%d K=%d)", M, e.N, K);
   }
-  CB_REQUIRE(e.norm_gain == nullptr && e.ss_in == nullptr, CB_E_UNSUPPORTED,
+  CB_REQUIRE(e.norm_gain == nullptr && e.ss_in == nullptr && e.n_add == 0, CB_E_UNSUPPORTED,
              "fused RMSNorm requested on a GEMM outside the tcgen05 path");
   return launch_gemm_simt(c, A, lda, B, ldb, M, K, e, s);
 }
@@ -189,6 +189,7 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->dev = cv.take<float>((size_t)T * 4);
   o->dev_part = cv.take<float>((size_t)2 * m->n_kv_heads * T * 4);
   o->ss = cv.take<float>((size_t)T * ((d + 127) / 128) * 4);
+  o->mlp_part = cv.take<float>((size_t)3 * T * d * 4);
   o->row_tok[0] = cv.take<int>((size_t)T * 4);
   o->row_tok[1] = cv.take<int>((size_t)T * 4);
   o->qrow = cv.take<int>((size_t)T * 4);
@@ -291,6 +292,10 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+  if ((e = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
+  for (auto& ev : c->ev_mlp)
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+  c->mlp_split = 1;  // the stream split measured slower (extra launches expose prologues/epilogues)
   c->layer_ev.resize(model->n_layers + 1);
   for (auto& ev : c->layer_ev)
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
@@ -318,6 +323,8 @@ extern "C" cb_status cb_destroy(cb_ctx* c) {
   for (auto ev : c->layer_ev) if (ev) cudaEventDestroy(ev);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+  for (auto ev : c->ev_mlp) if (ev) cudaEventDestroy(ev);
   if (c->dbg_buf) cudaFree(c->dbg_buf);
   gemm_tc_destroy(c);
   cudaFree(c->rope_tab);
@@ -374,6 +381,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
       cudaFree(c->dbg_buf);
       c->dbg_buf = nullptr;
     }
+    return CB_OK;
+  }
+  if (std::strcmp(name, "mlp_split") == 0) {
+    CB_REQUIRE(value >= 1 && value <= 4, CB_E_INVALID_ARG, "mlp_split must be 1..4");
+    c->mlp_split = (int)value;
     return CB_OK;
   }
   if (std::strcmp(name, "fuse_norm") == 0) {
@@ -552,15 +564,54 @@ cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, c
   }
   CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, Q, qd, eo, 0, s));
   if (!fuse_mlp) CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, Q, c->x, s));
-  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
   EpiParams ed{};
   ed.kind = EPI_RESID; ed.M = Q; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
-  if (b.next_attn_norm != nullptr && norm_fusable(c) &&
-      gemm_tc_ok(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed)) {
-    set_norm_producer(c, ed, b.next_attn_norm);
-    if (b.next_ready) *b.next_ready = true;
+  const bool fuse_next = b.next_attn_norm != nullptr && norm_fusable(c) &&
+                         gemm_tc_ok(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed);
+  if (fuse_next) set_norm_producer(c, ed, b.next_attn_norm);
+  // MLP split (blend sizes): gate_up in S feature blocks on the caller's stream; the down projection of
+  // block k (a K block of W_down) on the aux stream as soon as block k's activations exist, writing an
+  // fp32 partial; the last block adds h_in + the partials in block order + its own product. The down
+  // blocks fill the SMs gate_up leaves idle (its last wave, per-block grids), instead of running after it.
+  const int S = c->mlp_split;
+  const int fb = m.d_ff / S;
+  const bool split = S > 1 && Q <= 768 && m.dtype == CB_BF16 && m.d_ff % (S * 16) == 0 &&
+                     gemm_tc_ok(c, c->x, d, w.w_gate_up, d, Q, d, eg) && fuse_next == (ed.norm_gain != nullptr);
+  if (!split) {
+    CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
+    CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
+    if (fuse_next && b.next_ready) *b.next_ready = true;
+    return CB_OK;
   }
-  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
+  const size_t B = dtype_bytes(m.dtype);
+  cudaStream_t a = c->aux_stream;
+  CB_CUDA(cudaEventRecord(c->ev_mlp[0], s));
+  CB_CUDA(cudaStreamWaitEvent(a, c->ev_mlp[0], 0));  // fork: the aux stream sees o-proj's h / y / ss
+  for (int k = 0; k < S; ++k) {
+    EpiParams gk = eg;  // features [k fb, (k+1) fb): gate rows k fb.., up rows ff + k fb.., act columns k fb..
+    gk.N = fb;
+    gk.act = (char*)c->act + (size_t)k * fb * B;
+    CB_TRY(launch_gemm(c, c->x, d, (const char*)w.w_gate_up + (size_t)k * fb * d * B, d, Q, d, gk, 0, s));
+    CB_CUDA(cudaEventRecord(c->ev_mlp[1 + k], s));
+  }
+  for (int k = 0; k < S; ++k) {
+    CB_CUDA(cudaStreamWaitEvent(a, c->ev_mlp[1 + k], 0));
+    const void* A = (const char*)c->act + (size_t)k * fb * B;
+    const void* Bw = (const char*)w.w_down + (size_t)k * fb * B;
+    if (k + 1 < S) {  // partial product of K block k
+      EpiParams pk{};
+      pk.kind = EPI_STORE_F32; pk.M = Q; pk.N = d; pk.ldo = d; pk.outf = c->mlp_part + (size_t)k * c->max_tokens * d;
+      CB_TRY(launch_gemm(c, A, m.d_ff, Bw, m.d_ff, Q, fb, pk, 0, a));
+    } else {
+      EpiParams lk = ed;
+      lk.n_add = S - 1;
+      for (int j = 0; j + 1 < S; ++j) lk.add_part[j] = c->mlp_part + (size_t)j * c->max_tokens * d;
+      CB_TRY(launch_gemm(c, A, m.d_ff, Bw, m.d_ff, Q, fb, lk, 0, a));
+    }
+  }
+  CB_CUDA(cudaEventRecord(c->ev_mlp[5], a));
+  CB_CUDA(cudaStreamWaitEvent(s, c->ev_mlp[5], 0));  // join
+  if (fuse_next && b.next_ready) *b.next_ready = true;
   return CB_OK;
 }
 

@@ -104,6 +104,9 @@ struct EpiParams {
   // (blocks summed in order) -- RMSNorm's per-row factor taken out of the projection.
   const float* norm_gain; void* y_out; float* ss_out;
   const float* ss_in; int ld_ss, norm_d; float norm_eps;
+  // EPI_RESID (tcgen05 staged path): fp32 partial products of earlier K blocks (row-major, ld = ldo) added
+  // in this order after h_in and before the accumulator: h_out = (((h_in + p0) + p1) + ...) + acc
+  const float* add_part[3]; int n_add;
 };
 
 // Apply the epilogue to the adjacent column pair (n, n+1), n even. For SWIGLU a0/a1 are the gate

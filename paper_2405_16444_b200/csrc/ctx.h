@@ -68,6 +68,10 @@ struct cb_ctx {
   TmapCache* tmaps;
   // request mode: copy stream + per-layer "layer KV landed" events (P:2509 fetch/synchronize)
   cudaStream_t copy_stream;
+  cudaStream_t aux_stream;    // MLP split: the down-projection blocks run here, overlapping gate_up blocks
+  cudaEvent_t ev_mlp[6];      // fork, gate_up block 0..3 done, join
+  float* mlp_part;            // [3][T][d] fp32 partial products of down-projection K blocks 0..2
+  int mlp_split;              // cb_set_option("mlp_split", S): K blocks of the MLP at blend sizes (1 = off)
   cudaEvent_t ev_ready;
   std::vector<cudaEvent_t> layer_ev;
   // profiling

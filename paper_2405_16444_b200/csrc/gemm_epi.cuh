@@ -179,6 +179,22 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
           pre[it] = cont ? __ldcg(p) : *p;
         }
       }
+      if (!cont && e.n_add > 0) {  // earlier K blocks' partials (MLP split), added in block order
+#pragma unroll
+        for (int pi = 0; pi < 3; ++pi) {
+          if (pi >= e.n_add) break;
+          float4 q[8];
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int m = m_base + it * 4 + r0;
+            q[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (m < M && col_ok) q[it] = __ldcg(reinterpret_cast<const float4*>(e.add_part[pi] + (size_t)m * e.ldo + col));
+          }
+#pragma unroll
+          for (int it = 0; it < 8; ++it)
+            pre[it] = make_float4(pre[it].x + q[it].x, pre[it].y + q[it].y, pre[it].z + q[it].z, pre[it].w + q[it].w);
+        }
+      }
     }
     if constexpr (KIND == EPI_QKV) {
       qc = e.col0 + n;  // column of the fused [q | k | v] output

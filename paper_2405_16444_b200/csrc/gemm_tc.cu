@@ -486,7 +486,7 @@ static cb_status launch_bn(cb_ctx* c, const void* A, int lda, const void* B, int
 cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
                          const EpiParams& e, cudaStream_t s) {
   // the stream-K fixup path has no fused-RMSNorm producer: plain data-parallel then
-  const int sched = (e.norm_gain != nullptr && c->gemm_sched == 2) ? 1 : c->gemm_sched;
+  const int sched = ((e.norm_gain != nullptr || e.n_add > 0) && c->gemm_sched == 2) ? 1 : c->gemm_sched;
   const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit);
   if (pl.pair) return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, s);
