@@ -33,6 +33,7 @@ cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
 void gemm_tc_force_bn(cb_ctx* c, int bn);
 void gemm_tc_force_ksplit(cb_ctx* c, int v);
+void gemm_tc_force_tail(cb_ctx* c, int v);
 void gemm_tc_force_pair(cb_ctx* c, int v);
 int gemm_tc_max_pairs(const cb_ctx* c);
 cb_status attention_tc_init();
@@ -409,6 +410,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "gemm_pair") == 0) {
     CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_pair must be 0, 1 or 2");
     gemm_tc_force_pair(c, (int)value);
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_tail") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_tail must be 0, 1 or 2");
+    gemm_tc_force_tail(c, (int)value);
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_ksplit") == 0) {

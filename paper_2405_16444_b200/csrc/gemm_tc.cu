@@ -341,15 +341,19 @@ struct TmKeyHash {
 // pair 256x256 / 256x128: ~90 % / ~65 %).
 // Pair RESID GEMMs (o-proj, down-proj: N = d_model, few tiles at blend sizes) may also split K into a
 // chain of ksplit pieces per tile, each adding onto h_out after the previous one (fixed order).
+// Pair plans may also cut each remainder tile (tiles % pairs, when it is a small last round) into
+// tail_p K pieces that fill that round; the last piece of a tile to finish merges (gemm_tc2.cu).
 struct Plan {
-  int bn, sk_ctas, grid, pair, ksplit;
+  int bn, sk_ctas, grid, pair, ksplit, tail_r = 0, tail_p = 1;
 };
+constexpr int MAX_TAIL_P = 4;  // gemm_tc2.cu merges at most 4 pieces
+constexpr double TAIL_MERGE_CYC = 6000.0;  // partial store + merge reads + TMEM rewrite
 
 constexpr int MAX_KSPLIT = 4;
 constexpr double KSPLIT_EPI_CYC = 3000.0;  // one more serialised fp32 read-modify-write epilogue
 
 Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid, int K, int force_sched, int force_bn, int force_pair,
-               int force_ksplit) {
+               int force_ksplit, int force_tail) {
   const int num_kb = (K + BK - 1) / BK;
   Plan best{256, 0, 1, 0, 1};
   double best_cost = 1e300;
@@ -378,6 +382,19 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
           const double cost =
               (double)((tiles * ks + grid - 1) / grid) * ((num_kb + ks - 1) / ks) * cyc + (ks - 1) * KSPLIT_EPI_CYC;
           if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, pair ? 2 * grid : grid, pair, ks}; }
+          if (pair && ks == 1 && force_tail != 1) {  // remainder tiles cut into K pieces
+            const long long rounds = tiles / units, rem = tiles % units;
+            if (rounds >= 1 && rem > 0) {
+              const int tp = (int)std::min<long long>(MAX_TAIL_P, units / rem);
+              if (tp > 1 && num_kb / tp >= 8) {
+                const double c2 = (double)rounds * num_kb * cyc + (double)((num_kb + tp - 1) / tp) * cyc + TAIL_MERGE_CYC;
+                if (c2 < best_cost || force_tail == 2) {
+                  best_cost = c2;
+                  best = Plan{bn, 0, 2 * units, 1, 1, (int)rem, tp};
+                }
+              }
+            }
+          }
         }
       }
       if (pair) continue;
@@ -407,12 +424,16 @@ struct TmapCache {
   int* kflags = nullptr;  // [KFLAGS] split-K chain counters of the pair kernel (zero between launches)
   int force_bn = 0;
   int max_pairs = 0;      // co-resident 2-CTA clusters of the pair kernel
+  int force_tail = 0;     // 0 auto, 1 never cut remainder tiles, 2 always when possible
+  float* tscr = nullptr;  // [max_pairs][2][128][256] fp32 tail-piece partials
+  int* tcnt = nullptr;    // [max_pairs][2] tail-piece arrival counters (zero between launches)
   int force_ksplit = 0;   // 0 auto, else force this k-split for pair RESID GEMMs (when it fits)
   int force_pair = 0;     // 0 auto, 1 CTA pairs only, 2 single CTAs only
 };
 
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
-                          int bn, int n_pairs, int ksplit, int* kflags, cudaStream_t s);
+                          int bn, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p, float* tscr,
+                          int* tcnt, cudaStream_t s);
 cb_status gemm_tc2_init(int num_sms, int* max_pairs);
 constexpr int KFLAGS = 4096;  // >= 8 per tile for every tile of a split-K launch (tiles * ksplit <= 74 pairs)
 
@@ -488,8 +509,11 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
   // the stream-K fixup path has no fused-RMSNorm producer: plain data-parallel then
   const int sched = ((e.norm_gain != nullptr || e.n_add > 0) && c->gemm_sched == 2) ? 1 : c->gemm_sched;
   const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
-                            c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit);
-  if (pl.pair) return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, s);
+                            c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit,
+                            c->tmaps->force_tail);
+  if (pl.pair)
+    return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, pl.tail_r,
+                           pl.tail_p, c->tmaps->tscr, c->tmaps->tcnt, s);
   ProfScope ps_(c, PROF_GEMM, s);
   if (pl.bn == 256) return launch_bn<256>(c, A, lda, B, ldb, M, K, e, pl, s);
   return launch_bn<128>(c, A, lda, B, ldb, M, K, e, pl, s);
@@ -498,6 +522,7 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
 void gemm_tc_force_bn(cb_ctx* c, int bn) { c->tmaps->force_bn = bn; }
 void gemm_tc_force_pair(cb_ctx* c, int v) { c->tmaps->force_pair = v; }
 void gemm_tc_force_ksplit(cb_ctx* c, int v) { c->tmaps->force_ksplit = v; }
+void gemm_tc_force_tail(cb_ctx* c, int v) { c->tmaps->force_tail = v; }
 int gemm_tc_max_pairs(const cb_ctx* c) { return c->tmaps ? c->tmaps->max_pairs : 0; }
 
 template <int BN> static cb_status set_attrs() {
@@ -528,6 +553,9 @@ cb_status gemm_tc_init(cb_ctx* c) {
   CB_CUDA(cudaMemset(c->tmaps->flags, 0, (size_t)c->num_sms * sizeof(int)));
   CB_CUDA(cudaMalloc(&c->tmaps->kflags, KFLAGS * sizeof(int)));
   CB_CUDA(cudaMemset(c->tmaps->kflags, 0, KFLAGS * sizeof(int)));
+  CB_CUDA(cudaMalloc(&c->tmaps->tscr, (size_t)c->tmaps->max_pairs * 2 * 128 * 256 * sizeof(float)));
+  CB_CUDA(cudaMalloc(&c->tmaps->tcnt, (size_t)c->tmaps->max_pairs * 2 * sizeof(int)));
+  CB_CUDA(cudaMemset(c->tmaps->tcnt, 0, (size_t)c->tmaps->max_pairs * 2 * sizeof(int)));
   return CB_OK;
 }
 
@@ -536,6 +564,8 @@ void gemm_tc_destroy(cb_ctx* c) {
     cudaFree(c->tmaps->part);
     cudaFree(c->tmaps->flags);
     cudaFree(c->tmaps->kflags);
+    cudaFree(c->tmaps->tscr);
+    cudaFree(c->tmaps->tcnt);
   }
   delete c->tmaps;
   c->tmaps = nullptr;

@@ -30,10 +30,45 @@ template <int BN> struct Cfg2 {
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
+// Work item i -> tile t and k-block range [kb0, kb1).
+//   tail_p <= 1: i = sp * tiles + t, K split into ksplit chain pieces (RESID only; 1 = whole tiles)
+//   tail_p  > 1: the first tiles - tail_r tiles whole (full rounds of pairs); each of the last tail_r
+//                tiles cut into tail_p K pieces (piece >= 0) that fill the last round, merged by the
+//                last piece to finish (fixed piece order) before the tile's epilogue.
+struct WorkItem {
+  int t, sp, kb0, kb1, piece;
+};
+__device__ __forceinline__ WorkItem work_item(int i, int tiles, int num_kb, int ksplit, int tail_r, int tail_p) {
+  WorkItem w;
+  w.piece = -1;
+  if (tail_p > 1) {
+    const int full = tiles - tail_r;
+    w.sp = 0;
+    if (i < full) {
+      w.t = i; w.kb0 = 0; w.kb1 = num_kb;
+    } else {
+      const int j = i - full;
+      w.t = full + j / tail_p;
+      w.piece = j % tail_p;
+      w.kb0 = w.piece * num_kb / tail_p;
+      w.kb1 = (w.piece + 1) * num_kb / tail_p;
+    }
+  } else {
+    w.t = i % tiles; w.sp = i / tiles;
+    w.kb0 = w.sp * num_kb / ksplit; w.kb1 = (w.sp + 1) * num_kb / ksplit;
+  }
+  return w;
+}
+
+__device__ __forceinline__ void named_bar_sync2(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 template <int KIND, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
                     int m_tiles, int n_tiles, EpiParams e, int ksplit, int* __restrict__ kflags,
+                    int tail_r, int tail_p, float* __restrict__ tscr, int* __restrict__ tcnt,
                     long long* __restrict__ dbg) {
   // debug_trace: globaltimer (ns) events of each CTA's first work item at dbg[blockIdx.x * 8 + event]
 #define DBG2(ev) do { if (dbg != nullptr && blockIdx.x < 256) dbg[blockIdx.x * 8 + (ev)] = tc::globaltimer(); } while (0)
@@ -48,6 +83,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);  // tail merge: "this CTA merges" broadcast
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -55,7 +91,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_kb = (K + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int tiles = m_tiles * n_tiles;
-  const int items = tiles * ksplit;  // work item i: tile i % tiles, k-split i / tiles
+  const int items = tail_p > 1 ? tiles - tail_r + tail_r * tail_p : tiles * ksplit;  // see work_item()
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
@@ -78,11 +114,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int i = pair; i < items; i += n_pairs) {
-        const int t = i % tiles, sp = i / tiles;
+        const WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+        const int t = w.t;
         const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
         const int b_row = SW ? (rank == 0 ? nb * OUT_N : e.ff + nb * OUT_N) : nb * BN + (int)rank * C::B_HALF;
-        const int kb1 = (sp + 1) * num_kb / ksplit;
-        for (int kb = sp * num_kb / ksplit; kb < kb1; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -101,12 +137,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int i = pair; i < items; i += n_pairs, ++it) {
-        const int sp = i / tiles;
+        const WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int kb0 = sp * num_kb / ksplit, kb1 = (sp + 1) * num_kb / ksplit;
+        const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::fence_after();
@@ -131,7 +167,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row = q * 32 + lane;
     int it = 0;
     for (int i = pair; i < items; i += n_pairs, ++it) {
-      const int t = i % tiles, sp = i / tiles;
+      const WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+      const int t = w.t, sp = w.sp;
       const int acc = it & 1;
       const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
       // split-K chain (RESID only): split sp adds onto h_out after split sp - 1 of the same 32 rows
@@ -163,6 +200,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m = m0 + row;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       float dacc = 0.f;
+      bool skip_epilogue = false;
+      if (w.piece >= 0) {
+        // tail piece: publish this K piece's fp32 partial (this CTA's 128 rows x BN); the last piece of
+        // the tile to arrive sums all pieces in piece order into its TMEM accumulator, then runs the
+        // tile's epilogue; the others are done
+        const int tr = t - (tiles - tail_r);
+        float* base = tscr + (size_t)((tr * tail_p) * 2 + rank) * 128 * BN;
+        const size_t pstride = (size_t)2 * 128 * BN;  // next piece, same rank
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + c, v);
+          // layout [BN / 4 column groups][128 rows][4]: a warp's 32 rows of one group are 512 contiguous bytes
+          float4* dst = reinterpret_cast<float4*>(base + w.piece * pstride) + (size_t)(c / 4) * 128 + row;
+#pragma unroll
+          for (int x = 0; x < 8; ++x) dst[x * 128] = make_float4(v[4 * x], v[4 * x + 1], v[4 * x + 2], v[4 * x + 3]);
+        }
+        const bool ptrace = dbg != nullptr && warp == 2 && lane == 0 && blockIdx.x < 128;
+        if (ptrace) dbg[1024 + blockIdx.x * 8 + 0] = tc::globaltimer();
+        __threadfence();
+        named_bar_sync2(1, 128);
+        if (ptrace) dbg[1024 + blockIdx.x * 8 + 1] = tc::globaltimer();
+        if (warp == 2 && lane == 0) {
+          int* cnt = tcnt + tr * 2 + rank;
+          const int last = atomicAdd(cnt, 1) == tail_p - 1;
+          if (last) *cnt = 0;  // reset for the next launch
+          *last_flag = last;
+        }
+        named_bar_sync2(1, 128);
+        skip_epilogue = *last_flag == 0;
+        named_bar_sync2(1, 128);  // everyone read the flag before it can be rewritten
+        if (ptrace) dbg[1024 + blockIdx.x * 8 + 2] = tc::globaltimer();
+        if (!skip_epilogue) {
+          __threadfence();
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            float4 u[4][8];  // every piece's 32 columns in flight before the (piece-ordered) sum
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              if (p < tail_p) {
+                const float4* src = reinterpret_cast<const float4*>(base + p * pstride) + (size_t)(c / 4) * 128 + row;
+#pragma unroll
+                for (int x = 0; x < 8; ++x) u[p][x] = __ldcg(src + x * 128);
+              }
+            }
+            float v[32];
+#pragma unroll
+            for (int x = 0; x < 32; ++x) v[x] = 0.f;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              if (p < tail_p) {
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                  v[4 * x] += u[p][x].x; v[4 * x + 1] += u[p][x].y; v[4 * x + 2] += u[p][x].z; v[4 * x + 3] += u[p][x].w;
+                }
+              }
+            }
+            tc::tmem_st32(trow + c, v);
+          }
+          tc::tmem_st_wait();
+          if (ptrace) dbg[1024 + blockIdx.x * 8 + 3] = tc::globaltimer();
+        }
+      }
+      if (!skip_epilogue) {
       if (KIND == EPI_QKV && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
         gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow, rs);
       } else if (gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {  // staged, row-contiguous
@@ -194,6 +295,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       }
+      }
       if constexpr (KIND == EPI_RESID) {
         if (ksplit > 1) {
           __threadfence();
@@ -205,6 +307,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       if (it == 0 && warp == 2 && lane == 0) DBG2(5);
+      if (w.piece >= 0 && dbg != nullptr && warp == 2 && lane == 0 && blockIdx.x < 128)
+        dbg[1024 + blockIdx.x * 8 + 4] = tc::globaltimer();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_rank0(&tempty[acc]);
@@ -225,7 +329,8 @@ cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long 
 
 template <int KIND, int BN>
 static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
-                              const EpiParams& e, int n_pairs, int ksplit, int* kflags, cudaStream_t s) {
+                              const EpiParams& e, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p,
+                              float* tscr, int* tcnt, cudaStream_t s) {
   using C = Cfg2<BN>;
   constexpr bool sw = KIND == EPI_SWIGLU;
   constexpr int out_n = sw ? BN / 2 : BN;
@@ -235,7 +340,7 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, C::B_HALF, &tb));
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
   CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
-                    m_tiles, n_tiles, e, ksplit, kflags,
+                    m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
                     (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr));
   CB_LAUNCHED(c);
   return CB_OK;
@@ -243,12 +348,17 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
 
 // Pair tiles of 256 x BN; n_pairs CTA pairs (grid = 2 * n_pairs).
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
-                          int bn, int n_pairs, int ksplit, int* kflags, cudaStream_t s) {
+                          int bn, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p, float* tscr,
+                          int* tcnt, cudaStream_t s) {
   ProfScope ps_(c, PROF_GEMM, s);
   if (e.kind != EPI_RESID) ksplit = 1;
+  if (ksplit > 1) tail_p = 1;
 #define L2_(KIND_)                                                                                      \
-  return bn == 256 ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, s)  \
-                   : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, s)
+  return bn == 256                                                                                      \
+             ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
+                                        tcnt, s)                                                             \
+             : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
+                                        tcnt, s)
   switch (e.kind) {
     case EPI_STORE: L2_(EPI_STORE);
     case EPI_STORE_F32: L2_(EPI_STORE_F32);

@@ -145,6 +145,31 @@ def test_gemm_resid_ksplit(P, M, N, K, ksplit):
         assert torch.equal(P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2), C)
 
 
+@pytest.mark.parametrize("resid", [False, True])
+@pytest.mark.parametrize("M,N,K,bn", [(500, 38 * 256, 2048, 256), (300, 75 * 128, 4096, 128), (777, 28 * 256, 3000, 256)])
+def test_gemm_tail_pieces(P, M, N, K, bn, resid):
+    """CTA-pair GEMM whose last round holds only a few tiles, with those tiles cut into K pieces merged by
+    the last piece to finish (gemm_tail = 2): fp64 reference and bitwise reproducibility."""
+    ctx = P.Context(shape("small"), "bf16", max_tokens=8)
+    ctx.set_option("gemm_pair", 1)
+    ctx.set_option("gemm_bn", bn)
+    ctx.set_option("gemm_tail", 2)
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)
+    ref = (A.double() @ B.double().T).cpu().numpy()
+    if resid:
+        C0 = torch.randn(M, N, device=DEV, generator=g)
+        run = lambda: P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2)
+        ref = ref + C0.double().cpu().numpy()
+    else:
+        run = lambda: P.api.op_gemm(ctx, A, B, out_f32=True, impl=2)
+    C = run()
+    assert rel_err(np32(C), ref) < 5e-5
+    for _ in range(2):
+        assert torch.equal(run(), C)
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("name", ["tiny", "small"])
 def test_attention_parity(P, dtype, name):
