@@ -62,6 +62,9 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *                 kind k (0 store, 1 store_f32, 2 qkv, 3 residual, 4 swiglu)
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
  *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
+ *   "mlp_fused"   0 = two separate GEMMs (default); 2..4 = the blend MLP (rows <= 768) as one persistent
+ *                 kernel: gate_up tiles + the down projection cut into that many K blocks that start as soon
+ *                 as their activations exist (experiment; parity-green, measured ~0.3 ms/step slower)
  *   "mlp_split"   1 = off (default); 2..4 = gate_up in K blocks on the caller's stream with the matching
  *                 down-projection blocks on an internal stream (experiment; measured slower) */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);

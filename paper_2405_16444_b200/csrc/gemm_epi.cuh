@@ -448,4 +448,47 @@ __device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, 
   }
 }
 
+// ---- K-piece merge (tail pieces of a pair GEMM, blocks of the fused MLP) -----------------------------
+// Piece p's fp32 partial of this CTA's 128 x BN accumulator lives at base + p * pstride in the layout
+// [BN / 4 column groups][128 rows][4] (a warp's 32 rows of a group = 512 contiguous bytes). The merge
+// sums the np <= MAXP pieces in piece order (deterministic) into the TMEM accumulator row trow. Loads of
+// the next 16-column group are in flight while the current one is summed and stored.
+template <int BN, int MAXP>
+__device__ __forceinline__ void merge_pieces_to_tmem(const float* base, size_t pstride, int np, int row, uint32_t trow) {
+  float4 cur[MAXP][4], nxt[MAXP][4];
+  auto load = [&](float4 (&dst)[MAXP][4], int c) {
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p) {
+      if (p < np) {
+        const float4* src = reinterpret_cast<const float4*>(base + p * pstride) + (size_t)(c / 4) * 128 + row;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) dst[p][x] = __ldcg(src + x * 128);
+      }
+    }
+  };
+  load(cur, 0);
+#pragma unroll
+  for (int c = 0; c < BN; c += 16) {
+    if (c + 16 < BN) load(nxt, c + 16);
+    float v[16];
+#pragma unroll
+    for (int x = 0; x < 16; ++x) v[x] = 0.f;
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p) {
+      if (p < np) {
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          v[4 * x] += cur[p][x].x; v[4 * x + 1] += cur[p][x].y; v[4 * x + 2] += cur[p][x].z; v[4 * x + 3] += cur[p][x].w;
+        }
+      }
+    }
+    tc::tmem_st16(trow + c, v);
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) cur[p][x] = nxt[p][x];
+  }
+  tc::tmem_st_wait();
+}
+
 }  // namespace gepi

@@ -234,32 +234,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (ptrace) dbg[1024 + blockIdx.x * 8 + 2] = tc::globaltimer();
         if (!skip_epilogue) {
           __threadfence();
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            float4 u[4][8];  // every piece's 32 columns in flight before the (piece-ordered) sum
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              if (p < tail_p) {
-                const float4* src = reinterpret_cast<const float4*>(base + p * pstride) + (size_t)(c / 4) * 128 + row;
-#pragma unroll
-                for (int x = 0; x < 8; ++x) u[p][x] = __ldcg(src + x * 128);
-              }
-            }
-            float v[32];
-#pragma unroll
-            for (int x = 0; x < 32; ++x) v[x] = 0.f;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              if (p < tail_p) {
-#pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                  v[4 * x] += u[p][x].x; v[4 * x + 1] += u[p][x].y; v[4 * x + 2] += u[p][x].z; v[4 * x + 3] += u[p][x].w;
-                }
-              }
-            }
-            tc::tmem_st32(trow + c, v);
-          }
-          tc::tmem_st_wait();
+          gepi::merge_pieces_to_tmem<BN, 4>(base, pstride, tail_p, row, trow);
           if (ptrace) dbg[1024 + blockIdx.x * 8 + 3] = tc::globaltimer();
         }
       }

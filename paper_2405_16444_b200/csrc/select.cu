@@ -180,9 +180,16 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
       const int shift = 24 - 8 * pass;
       if (tid < 256) hist[tid] = 0;
       __syncthreads();
-      for (int j = tid; j < n_cand; j += blockDim.x) {
-        const unsigned key = keys[j];
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+      for (int j0 = 0; j0 < n_cand; j0 += blockDim.x) {  // warp-aggregated: one atomic per distinct bin
+        const int j = j0 + tid;
+        const unsigned key = j < n_cand ? keys[j] : 0u;
+        const bool in = j < n_cand && (key & mask) == prefix;
+        const unsigned act = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int bin = (key >> shift) & 255;
+          const unsigned peers = __match_any_sync(act, bin);
+          if ((int)(tid & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+        }
       }
       __syncthreads();
       if (tid < 32) {  // warp 0: lane l owns bins [8l, 8l+8); find the digit holding the rem-th largest

@@ -170,6 +170,18 @@ def test_gemm_tail_pieces(P, M, N, K, bn, resid):
         assert torch.equal(run(), C)
 
 
+@pytest.mark.parametrize("mlp_fused", [2, 4])
+def test_blend_fused_mlp_matches_two_gemms(P, mlp_fused):
+    """The experimental fused gate_up + down kernel (mlp_fused) reproduces the two-GEMM MLP in the
+    small bf16 blend (replay mode, same selections) within bf16 tolerance."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 3, [200, 317, 150], 0, "bf16", 0.15)
+    ora = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks)
+    ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
+    ctx.set_option("mlp_fused", mlp_fused)
+    res = run_blend(P, s, "bf16", 3, req, tok, pos, cs, Kc, Vc, ks, force_sel=ora.sel, ctx=ctx)
+    _compare(res, ora, s, TOL["bf16"])
+
+
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("name", ["tiny", "small"])
 def test_attention_parity(P, dtype, name):
