@@ -220,8 +220,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": "ctx_tok/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter RNG)", "impl": "reference",
-            "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} r={ratio}", "recompute_ratio": ratio,
-                       "n_ctx": N},
+            "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} tokens, r={ratio}, 1 request per GPU",
+                       "recompute_ratio": ratio, "n_ctx": N, "parallelism": "request-parallel x1 (rank 0 only)"},
             "cpu_baseline": {"value": v, "unit": "ctx_tok/s", "cores": cores, "kind": "oracle",
                              "sample": "per step: realign all layers + layers 0-2 in full (fp64 numpy); layers 3.."
                                        f"{s.n_layers - 1} extrapolated from layer 2 by row counts; "

@@ -62,6 +62,9 @@ __global__ void __launch_bounds__(NT, 1)
                     int kt_per_split, int n_splits, float* __restrict__ opart, float2* __restrict__ ml,
                     int* __restrict__ tile_cnt, long long* __restrict__ dbg) {
   pdl_enter();
+#ifdef CB_ATTN_TRACE
+  const long long t_start = tc::globaltimer();
+#endif
 #ifdef CB_ATTN_TRACE  // tools/attn_trace.py: clock64 pipeline events of CTA 0 (build with -DCB_ATTN_TRACE)
   const bool dbg_on = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
 #define DBG(i) do { if (dbg_on && (i) < 2048) dbg[i] = clock64(); } while (0)
@@ -385,6 +388,13 @@ __global__ void __launch_bounds__(NT, 1)
   tc::fence_before();
   __syncthreads();
   DBG(1202);
+#ifdef CB_ATTN_TRACE
+  // per-CTA span (globaltimer) of every CTA with linear id < 512 at dbg[1300 + 2 id]
+  if (dbg != nullptr && threadIdx.x == 0) {
+    const int id = blockIdx.y * gridDim.x + blockIdx.x;
+    if (id < 370) { dbg[1300 + 2 * id] = t_start; dbg[1300 + 2 * id + 1] = tc::globaltimer(); }
+  }
+#endif
 #undef DBG
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
