@@ -49,7 +49,7 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
 /* Tuning knobs (for experiments; defaults are the tuned choices). Unknown names -> INVALID_ARG.
  *   "gemm_sched"  0 = auto (cost model picks data-parallel or data-parallel + stream-K tail),
  *                 1 = data-parallel only, 2 = data-parallel rounds + stream-K tail
- *   "gemm_bn"     0 = auto, 128 or 256 = force the tcgen05 GEMM tile width
+ *   "gemm_bn"     0 = auto, 128, 192 (CTA pairs only) or 256 = force the tcgen05 GEMM tile width
  *   "gemm_pair"   0 = auto, 1 = CTA-pair (cta_group::2, 256-row tiles) only, 2 = single-CTA only
  *   "gemm_ksplit" 0 = auto, 1..4 = force the k-split chain of pair residual GEMMs (when it fits one wave)
  *   "gemm_tail"   0 = auto, 1 = never, 2 = always cut the remainder tiles of a pair GEMM's last round

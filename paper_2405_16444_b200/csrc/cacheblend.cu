@@ -192,8 +192,8 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->attn = cv.take<void>((size_t)T * qd * B);
   o->act = cv.take<void>((size_t)T * m->d_ff * B);
   o->dev = cv.take<float>((size_t)T * 4);
-  o->dev_part = cv.take<float>((size_t)2 * m->n_kv_heads * T * 4);
-  o->ss = cv.take<float>((size_t)T * ((d + 127) / 128) * 4);
+  o->dev_part = cv.take<float>((size_t)2 * ((kvd + 63) / 64) * T * 4);
+  o->ss = cv.take<float>((size_t)T * ((d + 63) / 64) * 4);
   o->mlp_part = cv.take<float>((size_t)3 * T * d * 4);
   o->row_tok[0] = cv.take<int>((size_t)T * 4);
   o->row_tok[1] = cv.take<int>((size_t)T * 4);
@@ -436,7 +436,8 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_bn") == 0) {
-    CB_REQUIRE(value == 0 || value == 128 || value == 256, CB_E_INVALID_ARG, "gemm_bn must be 0, 128 or 256");
+    CB_REQUIRE(value == 0 || value == 128 || value == 192 || value == 256, CB_E_INVALID_ARG,
+               "gemm_bn must be 0, 128, 192 (CTA pairs) or 256");
     gemm_tc_force_bn(c, (int)value);
     return CB_OK;
   }
@@ -548,15 +549,15 @@ struct LayerBufs {
   bool* next_ready = nullptr;           // out: set when the down projection produced the next layer's norm
 };
 
-// RMSNorm fusion (R12): the residual GEMM writes y = bf16(h * gain) plus 128-column sums of h^2 and the
+// RMSNorm fusion (R15): the residual GEMM writes y = bf16(h * gain) plus 64-column sums of h^2 and the
 // next projection scales its accumulator rows by 1/rms. Needs the tcgen05 path on both GEMMs.
 bool norm_fusable(const cb_ctx* c) { return !c->no_fuse_norm && c->m.dtype == CB_BF16 && c->m.d_model % 512 == 0; }
 
 void set_norm_producer(const cb_ctx* c, EpiParams& e, const void* gain) {
-  e.norm_gain = (const float*)gain; e.y_out = c->x; e.ss_out = c->ss; e.ld_ss = c->m.d_model / 128;
+  e.norm_gain = (const float*)gain; e.y_out = c->x; e.ss_out = c->ss; e.ld_ss = c->m.d_model / 64;
 }
 void set_norm_consumer(const cb_ctx* c, EpiParams& e) {
-  e.ss_in = c->ss; e.ld_ss = c->m.d_model / 128; e.norm_d = c->m.d_model; e.norm_eps = c->m.rms_eps;
+  e.ss_in = c->ss; e.ld_ss = c->m.d_model / 64; e.norm_d = c->m.d_model; e.norm_eps = c->m.rms_eps;
 }
 
 // Both GEMMs of a fused RMSNorm take the tcgen05 path (otherwise the classic kernel runs).
@@ -683,8 +684,9 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   else CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, R, c->x, s));
   // 2. Delta_kv against the loaded entries: fused into the tcgen05 QKV epilogue when every
   //    k/v head lies inside one output tile, else a separate kernel
-  const bool fuse_dev = m.dtype == CB_BF16 && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e) && qd % 256 == 0 &&
-                        256 % m.head_dim == 0 && n_cand > 0 && !c->no_fuse_dev;
+  // (64-column deviation blocks: every GEMM tile edge and the q|k|v boundaries fall on a block edge)
+  const bool fuse_dev = m.dtype == CB_BF16 && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e) && qd % 64 == 0 &&
+                        kvd % 64 == 0 && n_cand > 0 && !c->no_fuse_dev;
   if (fuse_dev) {
     e.k_ref = kb; e.v_ref = vb; e.dev_part = c->dev_part; e.n_cand = n_cand; e.ld_part = c->max_tokens;
   }

@@ -90,16 +90,16 @@ struct EpiParams {
   void* q_out; void* k_out; void* v_out;
   int col0, qd, kvd, hd;
   const int* row_tok; const int* pos; const float2* rope_tab;
-  // EPI_QKV fused Delta_kv (tcgen05 path): for candidate rows m < n_cand, per kv head h
-  // dev_part[(2h + 0) * ld_part + m] = ||k_m,h - k_ref[row_tok[m], h]||^2, [(2h + 1) ...] the same for v
+  // EPI_QKV fused Delta_kv (tcgen05 path): for candidate rows m < n_cand, per 64-column block b of the
+  // k (resp. v) row: dev_part[(2b + 0) * ld_part + m] = ||k_m[b] - k_ref[row_tok[m]][b]||^2, [(2b + 1) ...] v
   const void* k_ref; const void* v_ref; float* dev_part; int n_cand, ld_part;
   // EPI_RESID
   float* h_out; const float* h_in; const int* res_row;
   // EPI_SWIGLU
   int ff; void* act;
-  // Fused RMSNorm (tcgen05 path; R12). Producer (EPI_RESID with norm_gain set): besides h_out it writes
-  // y[m][n] = bf16(h_out[m][n] * norm_gain[n]) and ss_out[m * ld_ss + n / 128] = the sum of h_out[m][n]^2
-  // over each 128-column block. Consumer (EPI_QKV / EPI_SWIGLU with ss_in set, A operand = y): every
+  // Fused RMSNorm (tcgen05 path; DESIGN R15). Producer (EPI_RESID with norm_gain set): besides h_out it writes
+  // y[m][n] = bf16(h_out[m][n] * norm_gain[n]) and ss_out[m * ld_ss + n / 64] = the sum of h_out[m][n]^2
+  // over each 64-column block (every GEMM tile edge is a block edge). Consumer (EPI_QKV / EPI_SWIGLU with ss_in set, A operand = y): every
   // accumulator of row m is scaled by rs_m = 1 / sqrt(sum_b ss_in[m * ld_ss + b] / norm_d + norm_eps)
   // (blocks summed in order) -- RMSNorm's per-row factor taken out of the projection.
   const float* norm_gain; void* y_out; float* ss_out;

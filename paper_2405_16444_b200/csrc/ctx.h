@@ -43,7 +43,7 @@ struct cb_ctx {
   void* act;        // [T][ff]
   float* dev;       // [T]
   float* dev_part;  // [2 n_kv][T] fused-deviation partials (QKV epilogue)
-  float* ss;        // [T][d / 128] fused-RMSNorm sum-of-squares blocks (residual GEMM epilogue -> next GEMM)
+  float* ss;        // [T][d / 64] fused-RMSNorm sum-of-squares blocks (residual GEMM epilogue -> next GEMM)
   int* row_tok[2];  // [T] token index of each current row (candidates, then suffix)
   int* qrow;        // [T] row (in the current compact buffers) of each kept query
   int* iota;        // [T] 0..T-1

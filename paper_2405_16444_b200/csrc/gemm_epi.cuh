@@ -33,7 +33,7 @@ __device__ __forceinline__ float sqdiff16(const float* x, const bf16* p) {
   return s;
 }
 
-// Fused RMSNorm consumer: the per-row factor 1 / sqrt(mean(h^2) + eps) from the producer's 128-column
+// Fused RMSNorm consumer: the per-row factor 1 / sqrt(mean(h^2) + eps) from the producer's 64-column
 // sum-of-squares blocks, summed in block order (1 when the fusion is off).
 __device__ __forceinline__ float row_rs(const EpiParams& e, int m, bool row_ok) {
   if (e.ss_in == nullptr || !row_ok) return 1.f;
@@ -139,7 +139,7 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
   const int my_m = m_base + lane;
   const bool my_ok = my_m < M;
   const float my_rs = (KIND == EPI_QKV || KIND == EPI_SWIGLU) ? row_rs(e, my_m, my_ok) : 1.f;
-  // fused RMSNorm producer (EPI_RESID, final split only): y = bf16(h_out * gain), 128-column sums of h_out^2
+  // fused RMSNorm producer (EPI_RESID, final split only): y = bf16(h_out * gain), 64-column sums of h_out^2
   [[maybe_unused]] const bool norm_on = KIND == EPI_RESID && e.norm_gain != nullptr && last;
   int my_a = 0, my_b = 0;  // per-row operands of the lane's own row, broadcast below
   if constexpr (KIND == EPI_RESID) {
@@ -297,7 +297,7 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
       }
     }
     if constexpr (KIND == EPI_RESID) {
-      if (norm_on && ((n + 32) % 128 == 0 || c + 32 >= OUT_N)) {  // a 128-column block ends: publish
+      if (norm_on && ((n + 32) % 64 == 0 || c + 32 >= OUT_N)) {  // a 64-column block ends: publish
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           float sq = dacc[it];  // fixed xor tree over the row's 8 lanes
@@ -305,14 +305,14 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
           sq += __shfl_xor_sync(0xffffffffu, sq, 2);
           sq += __shfl_xor_sync(0xffffffffu, sq, 4);
           const int m = m_base + it * 4 + r0;
-          if (j == 0 && m < M) e.ss_out[(size_t)m * e.ld_ss + n / 128] = sq;
+          if (j == 0 && m < M) e.ss_out[(size_t)m * e.ld_ss + n / 64] = sq;
           dacc[it] = 0.f;
         }
       }
     }
     if constexpr (KIND == EPI_QKV) {
-      if (dev_on && (qc + 32) % e.hd == 0) {  // a k or v head ends with this chunk: publish its partials
-        const int slot = !is_v ? 2 * (kv_c / e.hd) : 2 * (kv_c / e.hd) + 1;
+      if (dev_on && (qc + 32) % 64 == 0) {  // a 64-column k or v block ends with this chunk: publish it
+        const int slot = 2 * (kv_c / 64) + (is_v ? 1 : 0);
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           const int m = m_base + it * 4 + r0;
@@ -424,7 +424,7 @@ __device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool ro
 }
 
 // Whole-row QKV epilogue over OUT_N accumulator columns from output column n0 (hd % 64 == 0):
-// 64-column chunks; a k/v head's deviation partial is published when the head ends (fixed order).
+// 64-column chunks; each k/v chunk's deviation partial goes to its own slot (summed in order by top-k).
 template <int OUT_N>
 __device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, int n0, uint32_t trow, float rs) {
   int tok = 0, p = 0;
@@ -439,9 +439,9 @@ __device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, 
     if (n >= e.N) break;  // warp-uniform
     dacc += qkv64(e, m, n, row_ok, trow + c, tok, p, rs);
     const int cl = e.col0 + n;
-    if (e.dev_part != nullptr && cl >= e.qd && (cl + 64) % e.hd == 0) {
+    if (e.dev_part != nullptr && cl >= e.qd) {  // one partial per 64-column k or v block
       const int kv_col = cl - e.qd;
-      const int slot = kv_col < e.kvd ? 2 * (kv_col / e.hd) : 2 * ((kv_col - e.kvd) / e.hd) + 1;
+      const int slot = kv_col < e.kvd ? 2 * (kv_col / 64) : 2 * ((kv_col - e.kvd) / 64) + 1;
       if (row_ok && m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc;
       dacc = 0.f;
     }

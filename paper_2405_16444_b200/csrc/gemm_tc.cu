@@ -293,9 +293,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               // a k or v head ends at this chunk: publish its deviation partial (fixed in-thread order)
               dacc += d;
               const int cl = e.col0 + n;
-              if (e.dev_part != nullptr && cl >= e.qd && (cl + 16) % e.hd == 0) {
+              if (e.dev_part != nullptr && cl >= e.qd && (cl + 16) % 64 == 0) {  // 64-column k/v block ends
                 const int kv_col = cl - e.qd;
-                const int slot = kv_col < e.kvd ? 2 * (kv_col / e.hd) : 2 * ((kv_col - e.kvd) / e.hd) + 1;
+                const int slot = kv_col < e.kvd ? 2 * (kv_col / 64) : 2 * ((kv_col - e.kvd) / 64) + 1;
                 if (m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc;
                 dacc = 0.f;
               }
@@ -363,11 +363,12 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
     if (pair && force_sched == 2) continue;   // the stream-K tail exists for single CTAs only
     const int tile_m = pair ? 256 : BM;
     const int m_tiles = (M + tile_m - 1) / tile_m;
-    for (int bn : {256, 128}) {
+    for (int bn : {256, 192, 128}) {
+      if (bn == 192 && !pair) continue;  // 192-wide tiles exist for CTA pairs only
       if (force_bn && bn != force_bn) continue;
       const int out_n = sw ? bn / 2 : bn;
       const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
-      const double cyc = pair ? (bn == 256 ? 570.0 : 390.0) : (bn == 256 ? 790.0 : 450.0);
+      const double cyc = pair ? (bn == 256 ? 570.0 : bn == 192 ? 480.0 : 390.0) : (bn == 256 ? 790.0 : 450.0);
       const int units = pair ? max_pairs : num_sms;
       // (a) whole tiles only (pairs: optionally a k-split chain for RESID)
       if (force_sched != 2) {

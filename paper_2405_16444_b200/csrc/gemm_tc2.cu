@@ -27,7 +27,8 @@ template <int BN> struct Cfg2 {
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int EPI_BYTES = 4 * gepi::EPI_WARP_F4 * 16;  // epilogue staging, 4 KB per warp
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int ACC_STRIDE = BN == 192 ? 256 : BN;  // accumulator buffer stride (TMEM columns)
+  static constexpr int TMEM_COLS = 2 * ACC_STRIDE;           // power of two for tcgen05.alloc
 };
 
 // Work item i -> tile t and k-block range [kb0, kb1).
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * C::ACC_STRIDE;
         const int kb0 = w.kb0, kb1 = w.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (it == 0 && warp == 2 && lane == 0) DBG2(4);
       const int m = m0 + row;
-      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_STRIDE;
       float dacc = 0.f;
       bool skip_epilogue = false;
       if (w.piece >= 0) {
@@ -260,9 +261,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if constexpr (KIND == EPI_QKV) {
             dacc += d;
             const int cl = e.col0 + n;
-            if (e.dev_part != nullptr && cl >= e.qd && (cl + 16) % e.hd == 0) {
+            if (e.dev_part != nullptr && cl >= e.qd && (cl + 16) % 64 == 0) {  // 64-column k/v block ends
               const int kv_col = cl - e.qd;
-              const int slot = kv_col < e.kvd ? 2 * (kv_col / e.hd) : 2 * ((kv_col - e.kvd) / e.hd) + 1;
+              const int slot = kv_col < e.kvd ? 2 * (kv_col / 64) : 2 * ((kv_col - e.kvd) / 64) + 1;
               if (m < e.n_cand) e.dev_part[(size_t)slot * e.ld_part + m] = dacc;
               dacc = 0.f;
             }
@@ -332,6 +333,9 @@ cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int 
   return bn == 256                                                                                      \
              ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
                                         tcnt, s)                                                             \
+         : bn == 192                                                                                         \
+             ? launch2_kind<KIND_, 192>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
+                                        tcnt, s)                                                             \
              : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
                                         tcnt, s)
   switch (e.kind) {
@@ -377,11 +381,14 @@ template <int BN> static cb_status max_pairs2(int num_sms, int* out) {
 
 cb_status gemm_tc2_init(int num_sms, int* max_pairs) {
   CB_TRY(set_attrs2<256>());
+  CB_TRY(set_attrs2<192>());
   CB_TRY(set_attrs2<128>());
-  int a = 0, b = 0;
+  int a = 0, b = 0, c3 = 0;
   CB_TRY(max_pairs2<256>(num_sms, &a));
   CB_TRY(max_pairs2<128>(num_sms, &b));
+  CB_TRY(max_pairs2<192>(num_sms, &c3));
   *max_pairs = a < b ? a : b;
+  if (c3 < *max_pairs) *max_pairs = c3;
   CB_REQUIRE(*max_pairs >= 1, CB_E_CUDA, "no CTA pair of the tcgen05 GEMM fits on this device");
   return CB_OK;
 }

@@ -131,10 +131,11 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   __shared__ int sm_digit, sm_rem;
   const int tid = threadIdx.x;
 
-  if (dev_part != nullptr) {  // Delta_kv from the QKV epilogue's per-(head, k|v) partials, fixed head order
+  if (dev_part != nullptr) {  // Delta_kv from the QKV epilogue's per-(64-col block, k|v) partials, in order
     for (int j = tid; j < n_cand; j += blockDim.x) {
       float tot = 0.f;
-      for (int h = 0; h < n_kv; ++h) {
+#pragma unroll 8
+      for (int h = 0; h < n_kv; ++h) {  // n_kv = number of 64-column blocks of a k (or v) row here
         const float a = dev_mode != CB_DEV_V ? dev_part[(size_t)(2 * h) * ld_part + j] : 0.f;
         const float b = dev_mode != CB_DEV_K ? dev_part[(size_t)(2 * h + 1) * ld_part + j] : 0.f;
         tot += a + b;
@@ -261,7 +262,8 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
   ProfScope ps_(c, PROF_TOPK, s);
   CB_LAUNCH(c, (topk_kernel), 1, TOPK_THREADS, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
-                                            c->err_word, dev_part, c->m.n_kv_heads, ld_part, dev_mode);
+                                            c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64, ld_part,
+                                            dev_mode);
   CB_LAUNCHED(c);
   return CB_OK;
 }

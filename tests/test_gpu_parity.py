@@ -145,6 +145,26 @@ def test_gemm_resid_ksplit(P, M, N, K, ksplit):
         assert torch.equal(P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2), C)
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 1000 + 24, 1000), (461, 6144, 4096), (700, 4096, 2048)])
+def test_gemm_pair_bn192(P, M, N, K):
+    """CTA-pair tcgen05 GEMM with 256 x 192 tiles (accumulators at TMEM columns 0 / 256): fp64 reference,
+    fp32 and bf16 outputs, residual form, bitwise reproducible."""
+    ctx = P.Context(shape("small"), "bf16", max_tokens=8)
+    ctx.set_option("gemm_pair", 1)
+    ctx.set_option("gemm_bn", 192)
+    g = torch.Generator(device=DEV).manual_seed(M + N)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)
+    ref = (A.double() @ B.double().T).cpu().numpy()
+    C = P.api.op_gemm(ctx, A, B, out_f32=True, impl=2)
+    assert rel_err(np32(C), ref) < 5e-5
+    assert torch.equal(P.api.op_gemm(ctx, A, B, out_f32=True, impl=2), C)
+    assert rel_err(np32(P.api.op_gemm(ctx, A, B, out_f32=False, impl=2)), ref) < 5e-3
+    C0 = torch.randn(M, N, device=DEV, generator=g)
+    R = P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2)
+    assert rel_err(np32(R), ref + C0.double().cpu().numpy()) < 5e-5
+
+
 @pytest.mark.parametrize("resid", [False, True])
 @pytest.mark.parametrize("M,N,K,bn", [(500, 38 * 256, 2048, 256), (300, 75 * 128, 4096, 128), (777, 28 * 256, 3000, 256)])
 def test_gemm_tail_pieces(P, M, N, K, bn, resid):
