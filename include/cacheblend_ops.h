@@ -52,8 +52,10 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "gemm_bn"     0 = auto, 128, 192 (CTA pairs only) or 256 = force the tcgen05 GEMM tile width
  *   "gemm_pair"   0 = auto, 1 = CTA-pair (cta_group::2, 256-row tiles) only, 2 = single-CTA only
  *   "gemm_ksplit" 0 = auto, 1..4 = force the k-split chain of pair residual GEMMs (when it fits one wave)
- *   "gemm_tail"   0 = auto, 1 = never, 2 = always cut the remainder tiles of a pair GEMM's last round
- *                 into K pieces (merged in piece order by the last piece to finish)
+ *   "gemm_no192"  1 = exclude 256 x 192 CTA-pair tiles from GEMM plans (0 = allowed, default)
+ *   "topk_drop"   n = top-k drops the n_cand - k smallest one by one when that count is <= n (default 48)
+ *   "gemm_tail"   0 = auto (cost model), 1 = never (default; measured faster), 2 = always cut the remainder
+ *                 tiles of a pair GEMM's last round into K pieces (merged in piece order by the last piece)
  *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM per tile, 3 = mma.sync, 4 = persistent tcgen05
  *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor (impl 4: key chunks per row tile)
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel

@@ -34,6 +34,7 @@ void gemm_tc_destroy(cb_ctx* c);
 void gemm_tc_force_bn(cb_ctx* c, int bn);
 void gemm_tc_force_ksplit(cb_ctx* c, int v);
 void gemm_tc_force_tail(cb_ctx* c, int v);
+void gemm_tc_no192(cb_ctx* c, int v);
 void gemm_tc_force_pair(cb_ctx* c, int v);
 int gemm_tc_max_pairs(const cb_ctx* c);
 cb_status attention_tc_init();
@@ -309,6 +310,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = attention_tc_init();
   if (st == CB_OK) st = attention_tc5_init();
   if (st == CB_OK) st = attention_tc6_init();
+  c->topk_drop_max = 48;
   c->mlp_fused = 0;  // experimental: measured ~0.3 ms/step slower (merge + residual epilogues at the end)
   if (st == CB_OK && c->m.dtype == CB_BF16) st = gemm_mlp_init(c);
   if (st != CB_OK) {
@@ -423,6 +425,14 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "gemm_pair") == 0) {
     CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_pair must be 0, 1 or 2");
     gemm_tc_force_pair(c, (int)value);
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_no192") == 0) {
+    gemm_tc_no192(c, (int)value);
+    return CB_OK;
+  }
+  if (std::strcmp(name, "topk_drop") == 0) {
+    c->topk_drop_max = (int)value;
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_tail") == 0) {

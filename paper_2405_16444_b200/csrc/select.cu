@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
                                                             int* __restrict__ qrow, int* __restrict__ qtok,
                                                             int* __restrict__ sel_tok, int* err,
                                                             const float* __restrict__ dev_part, int n_kv, int ld_part,
-                                                            int dev_mode) {
+                                                            int dev_mode, int drop_max) {
   pdl_enter();
   extern __shared__ unsigned keys[];
   __shared__ int hist[256];
@@ -174,9 +174,45 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
     unsigned u = __float_as_uint(dev[j]);
     keys[j] = (u & 0x80000000u) ? 0u : u;  // -0.0 -> 0
   }
+  // Gradual filtering keeps almost every candidate (k_i / k_(i-1) ~ 0.99 after layer 1): when only a few
+  // are dropped, drop them one at a time (block argmin by (key, larger index first), which is exactly the
+  // complement of "k largest, ties to the lower index") instead of four radix passes.
+  constexpr unsigned DROPPED = 0xFFFFFFFFu;  // above every key (keys are bits of non-negative floats)
+  const bool drop_path = k < n_cand && n_cand - k <= drop_max;
+  if (drop_path) {
+    __syncthreads();
+    __shared__ unsigned long long sm_best[32];
+    for (int r = 0; r < n_cand - k; ++r) {
+      // order (key ascending, index descending) packed so that the minimum is the next one to drop
+      unsigned long long best = ~0ull;
+      for (int j = tid; j < n_cand; j += blockDim.x) {
+        const unsigned long long v = ((unsigned long long)keys[j] << 32) | (unsigned)(0x7FFFFFFF - j);
+        best = v < best ? v : best;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+        best = y < best ? y : best;
+      }
+      if ((tid & 31) == 0) sm_best[tid >> 5] = best;
+      __syncthreads();
+      if (tid < 32) {
+        unsigned long long b = tid < (int)(blockDim.x >> 5) ? sm_best[tid] : ~0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
+          b = y < b ? y : b;
+        }
+        if (tid == 0) keys[0x7FFFFFFF - (int)(unsigned)(b & 0xFFFFFFFFu)] = DROPPED;
+      }
+      __syncthreads();
+    }
+  }
   unsigned prefix = 0, mask = 0;
   int rem = k;
-  if (k < n_cand) {
+  if (drop_path) {
+    prefix = 0; rem = 0;  // selection below: every key that was not dropped
+  } else if (k < n_cand) {
     for (int pass = 0; pass < 4; ++pass) {
       const int shift = 24 - 8 * pass;
       if (tid < 256) hist[tid] = 0;
@@ -223,27 +259,28 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   }
   const unsigned vstar = prefix;
   const bool all = (k >= n_cand);
+  // drop path: sel = not dropped, expressed through the same compaction (key > vstar, no ties)
 
   // contiguous segment per thread so that slot order is preserved by the scans
   const int seg = (n_cand + blockDim.x - 1) / blockDim.x;
   const int j0 = min(n_cand, tid * seg), j1 = min(n_cand, j0 + seg);
   int n_eq = 0;
-  if (!all)
+  if (!all && !drop_path)
     for (int j = j0; j < j1; ++j) n_eq += (keys[j] == vstar);
   const int eq_before = block_excl_scan(n_eq, sm_warp, &sm_total);
   int n_sel = 0, eq = eq_before;
   for (int j = j0; j < j1; ++j) {
     const unsigned key = keys[j];
-    bool sel = all || key > vstar;
-    if (!all && key == vstar) { sel = eq < rem; ++eq; }
+    bool sel = drop_path ? key != DROPPED : (all || key > vstar);
+    if (!drop_path && !all && key == vstar) { sel = eq < rem; ++eq; }
     n_sel += sel;
   }
   int out = block_excl_scan(n_sel, sm_warp, &sm_total);
   eq = eq_before;
   for (int j = j0; j < j1; ++j) {
     const unsigned key = keys[j];
-    bool sel = all || key > vstar;
-    if (!all && key == vstar) { sel = eq < rem; ++eq; }
+    bool sel = drop_path ? key != DROPPED : (all || key > vstar);
+    if (!drop_path && !all && key == vstar) { sel = eq < rem; ++eq; }
     if (sel) {
       const int t = cand_tok[j];
       qrow[out] = j;
@@ -263,7 +300,7 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   ProfScope ps_(c, PROF_TOPK, s);
   CB_LAUNCH(c, (topk_kernel), 1, TOPK_THREADS, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
                                             c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64, ld_part,
-                                            dev_mode);
+                                            dev_mode, c->topk_drop_max);
   CB_LAUNCHED(c);
   return CB_OK;
 }

@@ -65,7 +65,8 @@ def test_realign_parity(P, dtype, name):
 
 # ---- (b) deviation + top-k -----------------------------------------------------------------------
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("n_cand,k", [(1000, 150), (3072, 553), (37, 0), (37, 37), (5, 1), (20000, 3333)])
+@pytest.mark.parametrize("n_cand,k", [(1000, 150), (3072, 553), (37, 0), (37, 37), (5, 1), (20000, 3333),
+                                      (553, 547), (600, 552), (600, 551), (200, 199), (1000, 999)])
 def test_deviation_topk_parity(P, dtype, n_cand, k):
     s = shape("small")
     N = n_cand + 57
