@@ -555,6 +555,7 @@ struct LayerBufs {
   const int* row_tok;  // [n_cand + n_suf]
   int* qtok;           // [k + n_suf] out
   bool x_ready = false;                 // c->x / c->ss already hold this layer's fused attention RMSNorm
+  bool x_normed = false;                // c->x already holds rmsnorm(h_in) * attn_norm (embed_norm, layer 0)
   const void* next_attn_norm = nullptr;  // next layer's attention-norm gain: fuse it into the down projection
   bool* next_ready = nullptr;           // out: set when the down projection produced the next layer's norm
 };
@@ -662,7 +663,7 @@ cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, 
   e.kind = EPI_QKV; e.M = T; e.N = qd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
   e.q_out = c->q; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
   if (b.x_ready && gemm_tc_ok(c, c->x, d, w.w_qkv, d, T, d, e)) set_norm_consumer(c, e);
-  else CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, T, c->x, s));
+  else if (!b.x_normed) CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, T, c->x, s));
   CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, T, d, e, 0, s));
   if (n_suf > 0) {
     EpiParams ek = e;
@@ -807,10 +808,14 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
                           (long long)layer_stride, s);
   };
   // (a2) layer 0 in full
-  CB_TRY(launch_embed(c, embed, tok, T, c->h[0], s));
+  // embedding gather fused with layer 0's attention RMSNorm (unless the per-kernel ablation is on)
+  const bool embed_norm = !c->no_fuse_norm;
+  if (embed_norm) CB_TRY(launch_embed_norm(c, embed, tok, (const float*)w[0].attn_norm, T, c->h[0], c->x, s));
+  else CB_TRY(launch_embed(c, embed, tok, T, c->h[0], s));
   CB_TRY(realign_layer(0));
   bool ready = false;  // the previous down projection prepared this layer's attention RMSNorm
   LayerBufs b0{c->h[0], c->h[1], c->iota, nullptr};
+  b0.x_normed = embed_norm;
   b0.next_attn_norm = L > 1 ? w[1].attn_norm : nullptr;
   b0.next_ready = &ready;
   CB_TRY(layer_full(c, w[0], b0, N, n_suffix, k_blend, v_blend, pos, s));

@@ -164,6 +164,8 @@ cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out,
                          const int* src_pos, const int* dst_pos, int n_slices, int n_tok, long long out_stride,
                          long long src_stride, cudaStream_t s);
 cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, float* h, cudaStream_t s);
+cb_status launch_embed_norm(cb_ctx* c, const void* embed, const int* tok, const float* gain, int n, float* h,
+                            void* x, cudaStream_t s);
 cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s);
 cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int* qrow, const int* qtok, int n,
                             void* kb, void* vb, cudaStream_t s);

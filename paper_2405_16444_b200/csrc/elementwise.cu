@@ -94,17 +94,27 @@ cb_status launch_realign(cb_ctx* c, void* k_out, const void* k_src, void* v_out,
 // ---------------------------------------------------------------------------------------------
 // embedding gather: h[t] = fp32(embed[tok[t]])
 // ---------------------------------------------------------------------------------------------
+template <typename T> __device__ __forceinline__ float4 ld4f(const T* p);
+template <> __device__ __forceinline__ float4 ld4f<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+template <> __device__ __forceinline__ float4 ld4f<bf16>(const bf16* p) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// One 128-thread block per row, 4 elements per thread per step (16-byte stores of h).
 template <typename T>
-__global__ void embed_kernel(const T* __restrict__ emb, const int* __restrict__ tok, float* __restrict__ h, int d) {
+__global__ void __launch_bounds__(128) embed_kernel(const T* __restrict__ emb, const int* __restrict__ tok,
+                                                    float* __restrict__ h, int d) {
   pdl_enter();
   const int t = blockIdx.x;
   const T* src = emb + (size_t)__ldg(tok + t) * d;
   float* dst = h + (size_t)t * d;
-  for (int e = threadIdx.x * Vec16<T>::N; e < d; e += blockDim.x * Vec16<T>::N) {
-    Vec16<T> v = ld16(src + e);
-#pragma unroll
-    for (int q = 0; q < Vec16<T>::N; ++q) dst[e + q] = to_f(v.v[q]);
-  }
+#pragma unroll 4
+  for (int e = threadIdx.x * 4; e < d; e += 128 * 4) *reinterpret_cast<float4*>(dst + e) = ld4f(src + e);
 }
 
 cb_status launch_embed(cb_ctx* c, const void* embed, const int* tok, int n, float* h, cudaStream_t s) {
@@ -168,6 +178,66 @@ __global__ void __launch_bounds__(RMS_THREADS) rmsnorm_kernel(const float* __res
       store4(xr + e, v[i].x * inv * gg.x, v[i].y * inv * gg.y, v[i].z * inv * gg.z, v[i].w * inv * gg.w);
     }
   }
+}
+
+// Embedding gather fused with layer 0's attention RMSNorm: h[t] = fp32(embed[tok[t]]) and
+// x[t] = rmsnorm(h[t]) * gain, with rmsnorm_kernel's exact arithmetic and reduction order (so x is
+// bitwise what embed_kernel followed by rmsnorm_kernel produce).
+template <typename T>
+__global__ void __launch_bounds__(RMS_THREADS) embed_norm_kernel(const T* __restrict__ emb, const int* __restrict__ tok,
+                                                                 const float* __restrict__ g, float* __restrict__ h,
+                                                                 T* __restrict__ x, int d, float eps) {
+  pdl_enter();
+  const int r = blockIdx.x, tid = threadIdx.x;
+  const T* src = emb + (size_t)__ldg(tok + r) * d;
+  float* hr = h + (size_t)r * d;
+  float4 v[RMS_MAXV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) {
+    const int e = (i * RMS_THREADS + tid) * 4;
+    v[i] = e < d ? ld4f(src + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) {
+    const int e = (i * RMS_THREADS + tid) * 4;
+    if (e < d) *reinterpret_cast<float4*>(hr + e) = v[i];
+  }
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  __shared__ float red[RMS_THREADS / 32];
+  ss = warp_sum(ss);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < RMS_THREADS / 32; ++w) tot += red[w];
+  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+  T* xr = x + (size_t)r * d;
+#pragma unroll
+  for (int i = 0; i < RMS_MAXV; ++i) {
+    const int e = (i * RMS_THREADS + tid) * 4;
+    if (e < d) {
+      const float4 gg = __ldg(reinterpret_cast<const float4*>(g + e));
+      store4(xr + e, v[i].x * inv * gg.x, v[i].y * inv * gg.y, v[i].z * inv * gg.z, v[i].w * inv * gg.w);
+    }
+  }
+}
+
+cb_status launch_embed_norm(cb_ctx* c, const void* embed, const int* tok, const float* gain, int n, float* h,
+                            void* x, cudaStream_t s) {
+  if (n == 0) return CB_OK;
+  CB_REQUIRE(c->m.d_model <= RMS_THREADS * RMS_MAXV * 4, CB_E_UNSUPPORTED, "embed_norm: d_model > %d",
+             RMS_THREADS * RMS_MAXV * 4);
+  ProfScope ps_(c, PROF_EMBED, s);
+  if (c->m.dtype == CB_BF16)
+    CB_LAUNCH(c, (embed_norm_kernel<bf16>), n, RMS_THREADS, 0, s, (const bf16*)embed, tok, gain, h, (bf16*)x,
+              c->m.d_model, c->m.rms_eps);
+  else
+    CB_LAUNCH(c, (embed_norm_kernel<float>), n, RMS_THREADS, 0, s, (const float*)embed, tok, gain, h, (float*)x,
+              c->m.d_model, c->m.rms_eps);
+  CB_LAUNCHED(c);
+  return CB_OK;
 }
 
 cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s) {
