@@ -53,6 +53,10 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "gemm_pair"   0 = auto, 1 = CTA-pair (cta_group::2, 256-row tiles) only, 2 = single-CTA only
  *   "gemm_ksplit" 0 = auto, 1..4 = force the k-split chain of pair residual GEMMs (when it fits one wave)
  *   "gemm_no192"  1 = exclude 256 x 192 CTA-pair tiles from GEMM plans (0 = allowed, default)
+ *   "gemm_balance" 1 = pair GEMMs use the fewest pairs that need the same number of tile rounds (default;
+ *                 the full-load mainloop is power-capped, so even rounds beat a ragged last one), 0 = all
+ *   "gemm_cap_store", "gemm_cap_store_f32", "gemm_cap_qkv", "gemm_cap_resid", "gemm_cap_swiglu"
+ *                 n > 0 = pair GEMMs of that epilogue kind use at most n CTA pairs (0 = no cap, default)
  *   "topk_drop"   n = top-k drops the n_cand - k smallest one by one when that count is <= n (default 48)
  *   "gemm_tail"   0 = auto (cost model), 1 = never (default; measured faster), 2 = always cut the remainder
  *                 tiles of a pair GEMM's last round into K pieces (merged in piece order by the last piece)

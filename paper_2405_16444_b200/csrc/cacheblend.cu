@@ -35,6 +35,8 @@ void gemm_tc_force_bn(cb_ctx* c, int bn);
 void gemm_tc_force_ksplit(cb_ctx* c, int v);
 void gemm_tc_force_tail(cb_ctx* c, int v);
 void gemm_tc_no192(cb_ctx* c, int v);
+void gemm_tc_pairs_cap(cb_ctx* c, int kind, int v);
+void gemm_tc_balance(cb_ctx* c, int v);
 void gemm_tc_force_pair(cb_ctx* c, int v);
 int gemm_tc_max_pairs(const cb_ctx* c);
 cb_status attention_tc_init();
@@ -429,6 +431,21 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   }
   if (std::strcmp(name, "gemm_no192") == 0) {
     gemm_tc_no192(c, (int)value);
+    return CB_OK;
+  }
+  {
+    static const char* kCap[5] = {"gemm_cap_store", "gemm_cap_store_f32", "gemm_cap_qkv", "gemm_cap_resid",
+                                  "gemm_cap_swiglu"};
+    static const int kKind[5] = {EPI_STORE, EPI_STORE_F32, EPI_QKV, EPI_RESID, EPI_SWIGLU};
+    for (int i = 0; i < 5; ++i)
+      if (std::strcmp(name, kCap[i]) == 0) {
+        CB_REQUIRE(value >= 0, CB_E_INVALID_ARG, "%s must be >= 0", name);
+        gemm_tc_pairs_cap(c, kKind[i], (int)value);
+        return CB_OK;
+      }
+  }
+  if (std::strcmp(name, "gemm_balance") == 0) {
+    gemm_tc_balance(c, (int)value);
     return CB_OK;
   }
   if (std::strcmp(name, "topk_drop") == 0) {

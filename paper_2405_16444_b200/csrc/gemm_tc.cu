@@ -353,7 +353,8 @@ constexpr int MAX_KSPLIT = 4;
 constexpr double KSPLIT_EPI_CYC = 3000.0;  // one more serialised fp32 read-modify-write epilogue
 
 Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid, int K, int force_sched, int force_bn, int force_pair,
-               int force_ksplit, int force_tail, bool no192) {
+               int force_ksplit, int force_tail, bool no192, int pairs_cap, bool balance) {
+  if (pairs_cap > 0 && pairs_cap < max_pairs) max_pairs = pairs_cap;
   const int num_kb = (K + BK - 1) / BK;
   Plan best{256, 0, 1, 0, 1};
   double best_cost = 1e300;
@@ -379,7 +380,14 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
           if (!fits(ks)) continue;
           // forced: that split when it fits, else no split
           if (pair && resid && force_ksplit && ks != (fits(force_ksplit) ? force_ksplit : 1)) continue;
-          const int grid = (int)std::min<long long>(units, tiles * ks);
+          int grid = (int)std::min<long long>(units, tiles * ks);
+          // balanced rounds: the fewest pairs that still need the same number of rounds (the pair
+          // mainloop is power-capped at full load, so a ragged last round costs more than spreading
+          // the tiles evenly over fewer pairs; tools/gemm_cap.py)
+          if (pair && balance) {
+            const long long rounds = (tiles * ks + grid - 1) / grid;
+            grid = (int)((tiles * ks + rounds - 1) / rounds);
+          }
           const double cost =
               (double)((tiles * ks + grid - 1) / grid) * ((num_kb + ks - 1) / ks) * cyc + (ks - 1) * KSPLIT_EPI_CYC;
           if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, pair ? 2 * grid : grid, pair, ks}; }
@@ -427,6 +435,8 @@ struct TmapCache {
   int max_pairs = 0;      // co-resident 2-CTA clusters of the pair kernel
   int force_tail = 1;     // 0 auto, 1 never cut remainder tiles (default: measured 0.2 ms/step slower), 2 always
   bool no192 = false;     // exclude 256 x 192 pair tiles from the plan
+  int pairs_cap[5] = {0, 0, 0, 0, 0};  // per epilogue kind: use at most this many CTA pairs (0: all)
+  bool balance = true;    // spread pair tiles evenly over the rounds they need (plan_gemm)
   float* tscr = nullptr;  // [max_pairs][2][128][256] fp32 tail-piece partials
   int* tcnt = nullptr;    // [max_pairs][2] tail-piece arrival counters (zero between launches)
   int force_ksplit = 0;   // 0 auto, else force this k-split for pair RESID GEMMs (when it fits)
@@ -512,7 +522,8 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
   const int sched = ((e.norm_gain != nullptr || e.n_add > 0) && c->gemm_sched == 2) ? 1 : c->gemm_sched;
   const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit,
-                            c->tmaps->force_tail, c->tmaps->no192);
+                            c->tmaps->force_tail, c->tmaps->no192, c->tmaps->pairs_cap[e.kind],
+                            c->tmaps->balance);
   if (pl.pair)
     return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, pl.tail_r,
                            pl.tail_p, c->tmaps->tscr, c->tmaps->tcnt, s);
@@ -526,6 +537,8 @@ void gemm_tc_force_pair(cb_ctx* c, int v) { c->tmaps->force_pair = v; }
 void gemm_tc_force_ksplit(cb_ctx* c, int v) { c->tmaps->force_ksplit = v; }
 void gemm_tc_force_tail(cb_ctx* c, int v) { c->tmaps->force_tail = v; }
 void gemm_tc_no192(cb_ctx* c, int v) { c->tmaps->no192 = v != 0; }
+void gemm_tc_pairs_cap(cb_ctx* c, int kind, int v) { c->tmaps->pairs_cap[kind] = v; }
+void gemm_tc_balance(cb_ctx* c, int v) { c->tmaps->balance = v != 0; }
 int gemm_tc_max_pairs(const cb_ctx* c) { return c->tmaps ? c->tmaps->max_pairs : 0; }
 
 template <int BN> static cb_status set_attrs() {

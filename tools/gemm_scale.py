@@ -1,4 +1,4 @@
-"""Per-tile mainloop time of the CTA-pair GEMM vs the number of concurrently busy pairs (L2-feed check).
+"""Per-tile mainloop time of the CTA-pair GEMM vs the number of concurrently busy pairs (full-load scaling check).
 python tools/gemm_scale.py [M] [K]   (STORE epilogue, pair 256x256 tiles; needs a B200)"""
 import os
 import sys
