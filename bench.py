@@ -29,6 +29,7 @@ from synth import workload as W  # noqa: E402
 CONFIGS = {  # name -> (model shape, chunk lens, ratio)
     "mistral": ("mistral-7b", [512] * 6, 0.15),
     "yi": ("yi-34b", [1024] * 8, 0.15),
+    "llama": ("llama-70b", [1024] * 10, 0.15),
     "small": ("small", [200, 317, 150], 0.15),
 }
 METRIC = "blend latency ms & context tok/s at 15% recompute (Mistral-7B shape)"
@@ -44,6 +45,9 @@ def parse():
                     help="batched = SURVEY config 5: 64 Mistral-shape requests of 4-8 chunks x 256-1024 "
                          "tokens, assigned to the ranks longest-first")
     ap.add_argument("--batched-requests", type=int, default=64)
+    ap.add_argument("--parallel", default="request", choices=["request", "heads"],
+                    help="N>1: request-parallel (weak scaling, default) or head-parallel tensor parallelism over "
+                         "the N GPUs (strong scaling, NCCL all-gather / all-reduces inside the blend)")
     ap.add_argument("--ratio", type=float, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -255,29 +259,38 @@ def run_ours(args):
     shape_name, lens, ratio = CONFIGS[args.config]
     ratio = args.ratio if args.ratio is not None else ratio
     s = W.MODELS[shape_name]
-    seed = args.seed + rank  # weak scaling: every rank blends its own request
+    heads = args.parallel == "heads"
+    # request-parallel (weak scaling): every rank blends its own request; head-parallel (strong scaling):
+    # all ranks blend the same request, each with its heads / d_ff features
+    seed = args.seed if heads else args.seed + rank
     req = W.Request(list(lens), 0, seed, ratio)
-    N, L, kvd = req.n_ctx, s.n_layers, s.kvd
+    N, L = req.n_ctx, s.n_layers
     dev = torch.device("cuda", local)
-    ctx = P.Context(s, "bf16", max_tokens=max(N, max(lens)), max_pos=max(2 * N, 4096))
+    from paper_2405_16444_b200 import dist as D
+    sh = D.head_shard_shape(s, world) if heads else s  # the model this rank's context holds
+    ctx = P.Context(sh, "bf16", max_tokens=max(N, max(lens)), max_pos=max(2 * N, 4096))
+    if heads and world > 1:
+        uid = D.broadcast_bytes(P.nccl_unique_id() if rank == 0 else b"", src=0)
+        ctx.set_comm(uid, rank, world)
     if args.no_pdl:
         ctx.set_option("pdl", 0)
     for kv in filter(None, os.environ.get("CB_OPTS", "").split(",")):  # tuning: CB_OPTS=name=value,...
         k_, v_ = kv.split("=")
         ctx.set_option(k_, int(v_))
-    mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
+    mw = (P.ModelWeights.synth_shard(s, args.seed, "bf16", dev, rank, world) if heads and world > 1
+          else P.ModelWeights.synth(s, args.seed, "bf16", dev))
     tok_h = req.tokens(s.vocab)
     tok = torch.from_numpy(tok_h).to(dev)
     pos = torch.from_numpy(req.global_positions()).to(dev)
     # chunk caches: standalone prefill of each chunk at local positions 0..L_c-1, produced by
     # this library (cb_blend_forward with the whole chunk as uncached suffix = full prefill)
-    k_in = torch.empty(L, N, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+    k_in = torch.empty(L, N, sh.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
     v_in = torch.empty_like(k_in)
     cs = req.chunk_starts()
     for c in range(len(lens)):
         a, b = int(cs[c]), int(cs[c + 1])
         n = b - a
-        kc = torch.empty(L, n, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+        kc = torch.empty(L, n, sh.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
         vc = torch.empty_like(kc)
         P.blend_forward(ctx, mw, tok[a:b].contiguous(), torch.arange(n, dtype=torch.int32, device=dev), [0], n,
                         None, None, kc, vc, [0] * L)
@@ -325,7 +338,11 @@ def run_ours(args):
     launches = per_step_launches * args.steps
     ms = e0.elapsed_time(e1) / args.steps
     from paper_2405_16444_b200.dist import job_throughput, max_over_ranks
-    value, ms_max, _ = job_throughput(N, ms, dev)  # all ranks' tokens / slowest rank's time
+    if heads:  # one request over all ranks: its tokens / the slowest rank's time
+        ms_max = max_over_ranks(ms, dev)
+        value = N / (ms_max / 1e3)
+    else:
+        value, ms_max, _ = job_throughput(N, ms, dev)  # all ranks' tokens / slowest rank's time
 
     if os.environ.get("CB_TRACE_SEL"):  # tuning: per-CTA event trace of the last matching launch of a step
         ctx.set_option("debug_trace", int(os.environ["CB_TRACE_SEL"]))
@@ -339,7 +356,7 @@ def run_ours(args):
 
     # per-kernel profile pass (same steps, per-launch CUDA events on the launching stream)
     prof = P.api.profile_steps(ctx, step_eager, max(3, min(args.steps, 10)))
-    work = algorithmic_work(s, N, 0, ks)
+    work = algorithmic_work(sh, N, 0, ks)  # this rank's share (its heads / features) under head parallelism
     hbm, tf_burst, tf_sus, peak_src = measured_peaks()
     gemm_ms = prof.get("gemm", 0.0)
     roof = None
@@ -361,7 +378,7 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args)
         if world > 1:
-            e2e["value"] = world * N / (max_over_ranks(e2e["ms"], dev) / 1e3)
+            e2e["value"] = (1 if heads else world) * N / (max_over_ranks(e2e["ms"], dev) / 1e3)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = OracleSample(s, lens, ratio, args.seed)
@@ -372,13 +389,17 @@ def run_ours(args):
                          f"layers 3..{L - 1} extrapolated from layer 2 by row counts"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "ctx_tok/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong" if heads else "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter RNG weights/tokens; "
                 "chunk caches from standalone prefill of each chunk)",
-                "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} tokens, r={ratio}, 1 request per GPU",
+                "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} tokens, r={ratio}, " +
+                                       (f"1 request split by heads over {world} GPU(s)" if heads else "1 request per GPU"),
                            "recompute_ratio": ratio, "n_ctx": N, "k_sched_first_last": [ks[1], ks[-1]],
-                           "parallelism": f"request-parallel x{world}",
-                           "l2": "inputs larger than L2 (14.5 GB of weights streamed per step)"},
+                           "parallelism": f"head-parallel tp{world} (NCCL all-gather of Delta_kv partials, "
+                                          "all-reduce after o_proj and down_proj)" if heads else
+                                          f"request-parallel x{world}",
+                           "l2": f"inputs larger than L2 ({work['weight_bytes'] / 1e9:.1f} GB of weights streamed "
+                                 "per step per GPU)"},
                 "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
                 "cpu_baseline": cpu, "e2e": e2e,
                 "kernel_ms": {k: round(v, 4) for k, v in prof.items()},

@@ -178,6 +178,39 @@ CB_API cb_status cb_blend_request(cb_ctx* ctx, const cb_layer_w* w, const void* 
                                   void* v_blend, const int32_t* k_sched, int32_t* sel_out_host, float* h_out_host,
                                   void* stream);
 
+/* ---- head-parallel blend (SURVEY §8(e) partitioning 1) ------------------------------ */
+/* Tensor parallelism by attention heads within a layer (BASELINE north_star: "partitioned ... by attention
+ * heads within a layer, with an NCCL all-reduce over NVLink after the output projection and none inside
+ * attention"). Rank r of world w creates its context with the SHARD model: n_q_heads / w, n_kv_heads / w,
+ * d_ff / w (d_model, head_dim, vocab unchanged), and passes shard weights in the same cb_layer_w layouts:
+ *   w_qkv rows = q heads [r n_q/w, (r+1) n_q/w), then k heads and v heads [r n_kv/w, (r+1) n_kv/w)
+ *   w_o = columns [r qd/w, (r+1) qd/w) of the full w_o;  w_gate_up = gate rows then up rows of features
+ *   [r ff/w, (r+1) ff/w);  w_down = the same feature columns of the full w_down;  norms and embed replicated.
+ * k_in/v_in/k_blend/v_blend hold the rank's kv heads only ([L][T][n_kv/w][hd]). Every rank calls
+ * cb_blend_forward / cb_blend_layer with identical tokens, positions, chunks and k_sched; per layer the
+ * library all-gathers the Delta_kv partials (identical top-k on every rank), all-reduces the o_proj
+ * output and the down_proj output (fp32 sums; rank 0 adds the residual). RMSNorm runs replicated after
+ * the all-reduce. Outputs: S_i and h_out identical on every rank; k_blend/v_blend the rank's heads.
+ * cb_kv_deviation_topk stays rank-local. */
+typedef struct cb_group cb_group; /* opaque loopback group (one process, one device) */
+
+/* NCCL unique id (128 host bytes) for cb_set_comm; call on one rank and broadcast it. libnccl.so.2 is
+ * resolved at run time (the already-loaded copy, else the loader path, else $CB_NCCL_LIB):
+ * CB_E_UNSUPPORTED if absent. */
+CB_API cb_status cb_nccl_unique_id(void* uid_out);
+/* Make ctx rank `rank` of an NCCL communicator of `world` ranks (one process per GPU, collective over the
+ * ranks: every rank must call it). Collectives run on the blend's stream (graph-capturable).
+ * Errors: world outside [1, 8], rank outside [0, world), ctx already joined -> INVALID_ARG; NCCL -> E_NCCL. */
+CB_API cb_status cb_set_comm(cb_ctx* ctx, const void* uid, int32_t rank, int32_t world);
+/* Loopback group for testing the head-parallel path in ONE process on one device: world contexts, each
+ * joined with cb_set_comm_local and driven by its own host thread and stream, run the same per-rank
+ * kernels; exchanges are stream-event ordering plus a fixed-order reduce kernel. Eager launches only
+ * (not graph-capturable). A member that stops calling turns the others' calls into CB_E_NCCL after 120 s.
+ * Destroy the group after its contexts. */
+CB_API cb_status cb_group_create(int32_t world, cb_group** out);
+CB_API cb_status cb_group_destroy(cb_group* group);
+CB_API cb_status cb_set_comm_local(cb_ctx* ctx, cb_group* group, int32_t rank);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,6 +5,7 @@ library's sm_100a kernels. Nothing here computes any part of the method."""
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 from typing import Dict, List, Optional, Sequence
 
 import numpy as np
@@ -70,10 +71,49 @@ class Context:
     def set_option(self, name: str, value: int):
         check(lib().cb_set_option(self.handle, name.encode(), int(value)))
 
+    def set_comm(self, uid: bytes, rank: int, world: int):
+        """Join an NCCL communicator for the head-parallel blend (cb_set_comm). The context must have been
+        created with dist.head_shard_shape(shape, world)."""
+        assert len(uid) == 128
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        with torch.cuda.device(self.device):
+            check(lib().cb_set_comm(self.handle, buf, int(rank), int(world)))
+        self.tp = (int(rank), int(world))
+
+    def set_comm_local(self, group: "Group", rank: int):
+        """Join a one-process loopback group (cb_set_comm_local; tests of the head-parallel path on one GPU)."""
+        with torch.cuda.device(self.device):
+            check(lib().cb_set_comm_local(self.handle, group.handle, int(rank)))
+        self.tp = (int(rank), group.world)
+        self._group = group  # the group must outlive the context
+
     def info(self, name: str) -> int:
         v = ctypes.c_int64(0)
         check(lib().cb_get_info(self.handle, name.encode(), ctypes.byref(v)))
         return v.value
+
+
+class Group:
+    """cb_group: loopback head-parallel group of `world` contexts in this process (cb_group_create)."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        check(lib().cb_group_create(int(world), ctypes.byref(h)))
+        self.handle, self.world = h, int(world)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().cb_group_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().cb_nccl_unique_id(buf))
+    return buf.raw
 
 
 class ModelWeights:
@@ -103,10 +143,12 @@ class ModelWeights:
         return ModelWeights(shape, dtype, torch.empty(shape.vocab, d, dtype=td, device=device), layers)
 
     @staticmethod
-    def synth(shape, seed: int, dtype: str, device) -> "ModelWeights":
-        """Fill with the synth.workload recipe through the library's counter RNG (cb_gen_fill)."""
+    def synth(shape, seed: int, dtype: str, device, layer_ids: Optional[Sequence[int]] = None) -> "ModelWeights":
+        """Fill with the synth.workload recipe through the library's counter RNG (cb_gen_fill). layer_ids:
+        which model layers the shape's layers hold (default 0..n_layers-1)."""
         from synth import workload as W
         mw = ModelWeights.empty(shape, dtype, device)
+        ids = list(range(shape.n_layers)) if layer_ids is None else list(layer_ids)
         s = _stream(None)
 
         def fill(t: torch.Tensor, rec, row0: int = 0, is_f32: bool = False):
@@ -116,7 +158,7 @@ class ModelWeights:
 
         fill(mw.embed, W.embed_recipe(shape))
         qd, kvd, ff = shape.n_q_heads * shape.head_dim, shape.n_kv_heads * shape.head_dim, shape.d_ff
-        for i, w in enumerate(mw.layers):
+        for i, w in zip(ids, mw.layers):
             r = W.layer_recipes(shape, i)
             fill(w["attn_norm"], r["attn_norm"], is_f32=True)
             fill(w["mlp_norm"], r["mlp_norm"], is_f32=True)
@@ -128,6 +170,21 @@ class ModelWeights:
             fill(w["w_gate_up"], r["wu"], ff)
             fill(w["w_down"], r["wd"])
         return mw
+
+    @staticmethod
+    def synth_shard(shape, seed: int, dtype: str, device, rank: int, world: int) -> "ModelWeights":
+        """Rank's head-parallel shard of the synth recipe: each layer is generated in full (cb_gen_fill, one
+        layer at a time) and sliced with dist.shard_layer. Returns weights of dist.head_shard_shape."""
+        from . import dist as D
+        one = dataclasses.replace(shape, n_layers=1)
+        layers, embed = [], None
+        for i in range(shape.n_layers):
+            full = ModelWeights.synth(one, seed, dtype, device, layer_ids=[i])
+            if embed is None:
+                embed = full.embed
+            layers.append(D.shard_layer(full.layers[0], shape, rank, world))
+            del full
+        return ModelWeights(D.head_shard_shape(shape, world), dtype, embed, layers)
 
     @staticmethod
     def from_host(shape, dtype: str, embed: np.ndarray, layers: List[Dict[str, np.ndarray]], device) -> "ModelWeights":
@@ -220,7 +277,7 @@ def blend_request(ctx: Context, weights: ModelWeights, tok_host: torch.Tensor, p
 
 def profile_steps(ctx: Context, step, n: int) -> Dict[str, float]:
     """Runs `step` n times with per-launch CUDA events; returns device ms per step for each kernel class."""
-    N_CLS = 9
+    N_CLS = 10
     check(lib().cb_profile_begin(ctx.handle))
     for _ in range(n):
         step()
@@ -267,6 +324,6 @@ def op_embed(ctx: Context, embed: torch.Tensor, tok: torch.Tensor, stream=None):
     return h
 
 
-__all__ = ["Context", "ModelWeights", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
+__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
            "blend_layer", "blend_forward", "gen_fill", "gen_ints", "op_gemm", "op_attention", "op_rmsnorm",
            "op_embed"]

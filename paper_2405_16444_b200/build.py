@@ -66,7 +66,8 @@ def build(force: bool = False, ptxas_v: bool = False, quiet: bool = True) -> str
             print(log, file=sys.stderr)
     if _mtime(LIB) < max(_mtime(o) for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-lcuda_stub_absent"]
-        cmd = cmd[:-1]  # the driver API is resolved at run time (cudaGetDriverEntryPoint); no -lcuda
+        cmd = cmd[:-1] + ["-ldl"]  # the driver API is resolved at run time (cudaGetDriverEntryPoint); no -lcuda;
+        # NCCL is dlopen'ed by cb_set_comm (comm.cu)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

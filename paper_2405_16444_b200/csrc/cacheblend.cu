@@ -82,7 +82,7 @@ ProfScope::~ProfScope() {
 }
 
 static const char* kProfNames[PROF_N] = {"realign", "embed", "rmsnorm", "gemm", "deviation", "topk", "scatter",
-                                         "attention", "misc"};
+                                         "attention", "misc", "comm"};
 
 extern "C" const char* cb_profile_class_name(int32_t cls) {
   return (cls >= 0 && cls < PROF_N) ? kProfNames[cls] : "";
@@ -246,6 +246,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   c->m = *model;
   c->max_tokens = max_tokens;
   c->pdl = 1;
+  c->tp_world = 1;
   cudaError_t e = cudaGetDevice(&c->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   int cc_major = 0, cc_minor = 0;
@@ -339,6 +340,7 @@ extern "C" cb_status cb_destroy(cb_ctx* c) {
   if (c->mlp_cnt) cudaFree(c->mlp_cnt);
   for (auto ev : c->ev_mlp) if (ev) cudaEventDestroy(ev);
   if (c->dbg_buf) cudaFree(c->dbg_buf);
+  comm_destroy(c);
   gemm_tc_destroy(c);
   cudaFree(c->rope_tab);
   cudaFree(c->err_word);
@@ -579,7 +581,20 @@ struct LayerBufs {
 
 // RMSNorm fusion (R15): the residual GEMM writes y = bf16(h * gain) plus 64-column sums of h^2 and the
 // next projection scales its accumulator rows by 1/rms. Needs the tcgen05 path on both GEMMs.
-bool norm_fusable(const cb_ctx* c) { return !c->no_fuse_norm && c->m.dtype == CB_BF16 && c->m.d_model % 512 == 0; }
+// Head-parallel ranks hold partial sums of h until the all-reduce, so RMSNorm runs after it (replicated).
+bool norm_fusable(const cb_ctx* c) {
+  return !c->no_fuse_norm && c->m.dtype == CB_BF16 && c->m.d_model % 512 == 0 && c->tp_world <= 1;
+}
+
+// Head-parallel residual GEMM (o_proj / down_proj with a row shard of the contraction): rank 0 adds the
+// residual, the other ranks store their partial product; comm_allreduce_f32 then sums the ranks.
+void tp_partial_resid(const cb_ctx* c, EpiParams& e) {
+  if (c->tp_world <= 1 || c->tp_rank == 0) return;
+  e.kind = EPI_STORE_F32;
+  e.outf = e.h_out;
+  e.h_in = nullptr;
+  e.res_row = nullptr;
+}
 
 void set_norm_producer(const cb_ctx* c, EpiParams& e, const void* gain) {
   e.norm_gain = (const float*)gain; e.y_out = c->x; e.ss_out = c->ss; e.ld_ss = c->m.d_model / 64;
@@ -610,13 +625,21 @@ cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, c
     set_norm_producer(c, eo, w.mlp_norm);
     set_norm_consumer(c, eg);
   }
+  tp_partial_resid(c, eo);
   CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, Q, qd, eo, 0, s));
+  CB_TRY(comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s));  // (ii) all-reduce after o_proj
   if (!fuse_mlp) CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, Q, c->x, s));
   EpiParams ed{};
   ed.kind = EPI_RESID; ed.M = Q; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
   const bool fuse_next = b.next_attn_norm != nullptr && norm_fusable(c) &&
                          gemm_tc_ok(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed);
   if (fuse_next) set_norm_producer(c, ed, b.next_attn_norm);
+  if (c->tp_world > 1) {  // (iii) Megatron MLP: column-sharded gate/up, row-sharded down, one all-reduce
+    tp_partial_resid(c, ed);
+    CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
+    CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
+    return comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s);
+  }
   // MLP split (blend sizes): gate_up in S feature blocks on the caller's stream; the down projection of
   // block k (a K block of W_down) on the aux stream as soon as block k's activations exist, writing an
   // fp32 partial; the last block adds h_in + the partials in block order + its own product. The down
@@ -715,15 +738,24 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   // (64-column deviation blocks: every GEMM tile edge and the q|k|v boundaries fall on a block edge)
   const bool fuse_dev = m.dtype == CB_BF16 && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e) && qd % 64 == 0 &&
                         kvd % 64 == 0 && n_cand > 0 && !c->no_fuse_dev;
+  // head-parallel: this rank's (64-column block, k|v) partials land in its segment of the gathered buffer;
+  // the global block order (rank-major = kv-head-major) is the single-GPU order, so all ranks sum alike
+  const size_t nb_local = (size_t)(kvd + 63) / 64;
+  float* dev_part = c->tp_world > 1 ? c->dev_gath : c->dev_part;
   if (fuse_dev) {
-    e.k_ref = kb; e.v_ref = vb; e.dev_part = c->dev_part; e.n_cand = n_cand; e.ld_part = c->max_tokens;
+    e.k_ref = kb; e.v_ref = vb; e.n_cand = n_cand; e.ld_part = c->max_tokens;
+    e.dev_part = dev_part + (c->tp_world > 1 ? 2 * nb_local * c->tp_rank * c->max_tokens : 0);
   }
   CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, R, d, e, 0, s));
+  if (fuse_dev) CB_TRY(comm_allgather_f32(c, dev_part, 2 * nb_local * c->max_tokens, s));  // (i)
   // 3. HKVD = top-k of Delta_kv (Insight 1)
   float* dev = dev_out ? dev_out : c->dev;
-  if (!fuse_dev) CB_TRY(launch_deviation(c, c->kf, c->vf, kb, vb, b.row_tok, n_cand, dev_mode, dev, s));
+  if (!fuse_dev) {
+    CB_TRY(launch_deviation(c, c->kf, c->vf, kb, vb, b.row_tok, n_cand, dev_mode, dev, s));
+    CB_TRY(comm_allreduce_f32(c, dev, (size_t)n_cand, s));  // (i) unfused: sum the ranks' head sums
+  }
   CB_TRY(launch_topk(c, dev, b.row_tok, n_cand, k, n_suf, N, force_sel, c->qrow, b.qtok, sel_tok, s,
-                     fuse_dev ? c->dev_part : nullptr, c->max_tokens, dev_mode));
+                     fuse_dev ? dev_part : nullptr, c->max_tokens, dev_mode));
   if (Q == 0) return CB_OK;
   // 4. only the KV of the HKVD tokens (and the suffix) is updated (R3)
   CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));

@@ -10,12 +10,17 @@
 #include <vector>
 
 struct TmapCache;  // tcgen05 GEMM tensor-map cache (gemm_tc.cu)
+struct cb_group;   // loopback tensor-parallel group (comm.cu)
 
 // Kernel classes for the per-launch profile (bench roofline: CUDA events on the launching stream).
 enum ProfClass : int {
   PROF_REALIGN = 0, PROF_EMBED, PROF_RMSNORM, PROF_GEMM, PROF_DEVIATION, PROF_TOPK, PROF_SCATTER, PROF_ATTN,
-  PROF_MISC, PROF_N
+  PROF_MISC, PROF_COMM, PROF_N
 };
+
+// Head-parallel (tensor-parallel) communicator kinds (comm.cu).
+enum CommKind : int { CB_COMM_NONE = 0, CB_COMM_NCCL = 1, CB_COMM_LOOPBACK = 2 };
+constexpr int kMaxTp = 8;
 
 struct ProfRec {
   int cls;
@@ -78,6 +83,15 @@ struct cb_ctx {
   int* mlp_cnt;               // fused MLP: block / merge counters (zero between launches)
   cudaEvent_t ev_ready;
   std::vector<cudaEvent_t> layer_ev;
+  // head-parallel blend (comm.cu): this context holds rank tp_rank's shard of the model (heads, d_ff / world)
+  int tp_rank;
+  int tp_world;               // <= 1: no tensor parallelism
+  int comm_kind;              // CommKind
+  void* nccl_comm;            // ncclComm_t
+  cb_group* group;            // loopback group (one process, one device)
+  float* dev_gath;            // [2 nb_local world][max_tokens] gathered Delta_kv partials
+  float* tp_scratch;          // loopback all-reduce scratch
+  size_t tp_scratch_n;
   // profiling
   bool prof_on;
   std::vector<ProfRec> prof;
@@ -184,5 +198,10 @@ cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb,
                       int impl, cudaStream_t s);
 cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                            const void* v, int n_keys, void* out, int impl, cudaStream_t s);
+// Head-parallel collectives on `s` (no-ops when tp_world <= 1). All-reduce: in-place fp32 sum. All-gather:
+// in place, this rank's n_per_rank floats already at buf + tp_rank * n_per_rank.
+cb_status comm_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s);
+cb_status comm_allgather_f32(cb_ctx* c, float* buf, size_t n_per_rank, cudaStream_t s);
+void comm_destroy(cb_ctx* c);
 cb_status launch_gen_fill(void* out, int dtype, long long count, unsigned long long seed, unsigned long long stream_id,
                           long long start, float scale, float offset, cudaStream_t s);

@@ -299,7 +299,7 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
   ProfScope ps_(c, PROF_TOPK, s);
   CB_LAUNCH(c, (topk_kernel), 1, TOPK_THREADS, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
-                                            c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64, ld_part,
+                                            c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64 * std::max(1, c->tp_world), ld_part,
                                             dev_mode, c->topk_drop_max);
   CB_LAUNCHED(c);
   return CB_OK;

@@ -59,3 +59,64 @@ def job_throughput(tokens_this_rank: int, ms_this_rank: float, device=None):
     ms = max_over_ranks(ms_this_rank, device)
     tok = sum_over_ranks(tokens_this_rank, device)
     return tok / (ms / 1e3), ms, tok
+
+
+# ---- head-parallel (tensor-parallel) sharding (SURVEY.md §8(e) partitioning 1; include/cacheblend.h) ----
+# Rank r of w owns q heads [r n_q/w, (r+1) n_q/w) and kv heads [r n_kv/w, (r+1) n_kv/w): with GQA group
+# g = n_q/n_kv, q head h reads kv head h // g, so a rank's q heads only read its own kv heads and
+# attention needs no communication. The MLP is split by d_ff features (Megatron column/row split).
+def head_shard_shape(shape, world: int):
+    """The model a rank's cb_ctx is created with: heads and d_ff divided by world."""
+    if world < 1 or shape.n_kv_heads % world or shape.n_q_heads % world or shape.d_ff % world:
+        raise ValueError(f"{shape.name}: n_q {shape.n_q_heads}, n_kv {shape.n_kv_heads}, d_ff {shape.d_ff} "
+                         f"not divisible by world {world}")
+    import dataclasses
+    return dataclasses.replace(shape, n_q_heads=shape.n_q_heads // world, n_kv_heads=shape.n_kv_heads // world,
+                               d_ff=shape.d_ff // world)
+
+
+def head_shard_ranges(shape, rank: int, world: int):
+    """Row / column ranges of rank's shard in the full cb_layer_w layouts."""
+    head_shard_shape(shape, world)
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside [0, {world})")
+    hd, qd, kvd, ff = shape.head_dim, shape.n_q_heads * shape.head_dim, shape.n_kv_heads * shape.head_dim, shape.d_ff
+    ql, kvl, fl = qd // world, kvd // world, ff // world
+    return {"q_rows": (rank * ql, (rank + 1) * ql),
+            "k_rows": (qd + rank * kvl, qd + (rank + 1) * kvl),
+            "v_rows": (qd + kvd + rank * kvl, qd + kvd + (rank + 1) * kvl),
+            "o_cols": (rank * ql, (rank + 1) * ql),
+            "gate_rows": (rank * fl, (rank + 1) * fl),
+            "up_rows": (ff + rank * fl, ff + (rank + 1) * fl),
+            "down_cols": (rank * fl, (rank + 1) * fl),
+            "kv_heads": (rank * shape.n_kv_heads // world, (rank + 1) * shape.n_kv_heads // world)}
+
+
+def shard_layer(w, shape, rank: int, world: int):
+    """Rank's shard of one layer's weights (dict in the cb_layer_w layout: attn_norm, w_qkv, w_o, mlp_norm,
+    w_gate_up, w_down), as new contiguous tensors on the same device."""
+    r = head_shard_ranges(shape, rank, world)
+    rows = lambda t, a: t[a[0]:a[1]]
+    cols = lambda t, a: t[:, a[0]:a[1]]
+    return {"attn_norm": w["attn_norm"].clone(), "mlp_norm": w["mlp_norm"].clone(),
+            "w_qkv": torch.cat([rows(w["w_qkv"], r["q_rows"]), rows(w["w_qkv"], r["k_rows"]),
+                                rows(w["w_qkv"], r["v_rows"])], 0).contiguous(),
+            "w_o": cols(w["w_o"], r["o_cols"]).contiguous(),
+            "w_gate_up": torch.cat([rows(w["w_gate_up"], r["gate_rows"]), rows(w["w_gate_up"], r["up_rows"])],
+                                   0).contiguous(),
+            "w_down": cols(w["w_down"], r["down_cols"]).contiguous()}
+
+
+def shard_kv(kv, shape, rank: int, world: int):
+    """Rank's kv heads of a KV tensor [..., n_kv, head_dim]."""
+    a, b = head_shard_ranges(shape, rank, world)["kv_heads"]
+    return kv[..., a:b, :].contiguous()
+
+
+def broadcast_bytes(payload: bytes, src: int = 0) -> bytes:
+    """Broadcast a small host byte string (the NCCL unique id) over the default process group."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return payload
+    obj = [payload if dist.get_rank() == src else None]
+    dist.broadcast_object_list(obj, src=src)
+    return obj[0]
