@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NT, 1)
   const long long t_start = tc::globaltimer();
 #endif
 #ifdef CB_ATTN_TRACE  // tools/attn_trace.py: clock64 pipeline events of CTA 0 (build with -DCB_ATTN_TRACE)
-  const bool dbg_on = dbg != nullptr && blockIdx.x == 0 && blockIdx.y == 0;
+  const bool dbg_on = dbg != nullptr && blockIdx.x == 0;
 #define DBG(i) do { if (dbg_on && (i) < 2048) dbg[i] = clock64(); } while (0)
 #else
 #define DBG(i) do { } while (0)
@@ -88,10 +88,13 @@ __global__ void __launch_bounds__(NT, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.y, G = n_q / n_kv, R = n_rows * G;
-  const int tiles = gridDim.x / n_splits;
-  const int tile = tiles - 1 - (int)blockIdx.x / n_splits;  // heaviest (latest rows) first
-  const int split = (int)blockIdx.x % n_splits;
+  // 1-D grid, kv head fastest: the heaviest row tiles (latest tokens) of EVERY head launch first, then
+  // their later key ranges, then lighter tiles (a global longest-first order across heads)
+  const int g = (int)blockIdx.x % n_kv, G = n_q / n_kv, R = n_rows * G;
+  const int tiles = gridDim.x / (n_splits * n_kv);
+  const int rest = (int)blockIdx.x / n_kv;
+  const int tile = tiles - 1 - rest / n_splits;
+  const int split = rest % n_splits;
   const int rho0 = tile * BM;
   const int qd = n_q * HD;
 
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(NT, 1)
 #ifdef CB_ATTN_TRACE
   // per-CTA span (globaltimer) of every CTA with linear id < 512 at dbg[1300 + 2 id]
   if (dbg != nullptr && threadIdx.x == 0) {
-    const int id = blockIdx.y * gridDim.x + blockIdx.x;
+    const int id = blockIdx.x;
     if (id < 370) { dbg[1300 + 2 * id] = t_start; dbg[1300 + 2 * id + 1] = tc::globaltimer(); }
   }
 #endif
@@ -461,7 +464,7 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   CUtensorMap tk, tv;
   CB_TRY(kv_tmap(c, k, n_keys, &tk));
   CB_TRY(kv_tmap(c, v, n_keys, &tv));
-  dim3 grid(tiles * n_splits, n_kv);
+  dim3 grid(tiles * n_splits * n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
   CB_LAUNCH(c, (attn_tc5_kernel), grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
                                          c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,

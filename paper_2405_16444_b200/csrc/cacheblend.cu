@@ -35,6 +35,7 @@ void gemm_tc_force_bn(cb_ctx* c, int bn);
 void gemm_tc_force_ksplit(cb_ctx* c, int v);
 void gemm_tc_force_tail(cb_ctx* c, int v);
 void gemm_tc_no192(cb_ctx* c, int v);
+void gemm_tc_no224(cb_ctx* c, int v);
 void gemm_tc_pairs_cap(cb_ctx* c, int kind, int v);
 void gemm_tc_balance(cb_ctx* c, int v);
 void gemm_tc_force_pair(cb_ctx* c, int v);
@@ -431,6 +432,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     gemm_tc_force_pair(c, (int)value);
     return CB_OK;
   }
+  if (std::strcmp(name, "gemm_no224") == 0) {
+    gemm_tc_no224(c, (int)value);
+    return CB_OK;
+  }
   if (std::strcmp(name, "gemm_no192") == 0) {
     gemm_tc_no192(c, (int)value);
     return CB_OK;
@@ -465,8 +470,8 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_bn") == 0) {
-    CB_REQUIRE(value == 0 || value == 128 || value == 192 || value == 256, CB_E_INVALID_ARG,
-               "gemm_bn must be 0, 128, 192 (CTA pairs) or 256");
+    CB_REQUIRE(value == 0 || value == 128 || value == 192 || value == 224 || value == 256, CB_E_INVALID_ARG,
+               "gemm_bn must be 0, 128, 192 (CTA pairs), 224 (SwiGLU pairs) or 256");
     gemm_tc_force_bn(c, (int)value);
     return CB_OK;
   }

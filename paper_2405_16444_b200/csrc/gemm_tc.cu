@@ -353,7 +353,7 @@ constexpr int MAX_KSPLIT = 4;
 constexpr double KSPLIT_EPI_CYC = 3000.0;  // one more serialised fp32 read-modify-write epilogue
 
 Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid, int K, int force_sched, int force_bn, int force_pair,
-               int force_ksplit, int force_tail, bool no192, int pairs_cap, bool balance) {
+               int force_ksplit, int force_tail, bool no192, int pairs_cap, bool balance, bool no224) {
   if (pairs_cap > 0 && pairs_cap < max_pairs) max_pairs = pairs_cap;
   const int num_kb = (K + BK - 1) / BK;
   Plan best{256, 0, 1, 0, 1};
@@ -364,12 +364,17 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
     if (pair && force_sched == 2) continue;   // the stream-K tail exists for single CTAs only
     const int tile_m = pair ? 256 : BM;
     const int m_tiles = (M + tile_m - 1) / tile_m;
-    for (int bn : {256, 192, 128}) {
+    for (int bn : {256, 224, 192, 128}) {
       if (bn == 192 && (!pair || no192)) continue;  // 192-wide tiles exist for CTA pairs only
+      // 224 = 112 gate + 112 up columns (SwiGLU pairs only): d_ff = 14336 is 128 x 112 features, so at
+      // blend sizes (2 row tiles) 256 tiles fill 4 rounds of 64 pairs instead of 224 tiles needing a 4th
+      // round of 2 at 256 wide
+      if (bn == 224 && (!pair || !sw || no224)) continue;
       if (force_bn && bn != force_bn) continue;
       const int out_n = sw ? bn / 2 : bn;
       const long long tiles = (long long)m_tiles * ((N_out + out_n - 1) / out_n);
-      const double cyc = pair ? (bn == 256 ? 570.0 : bn == 192 ? 480.0 : 390.0) : (bn == 256 ? 790.0 : 450.0);
+      const double cyc = pair ? (bn == 256 ? 570.0 : bn == 224 ? 525.0 : bn == 192 ? 480.0 : 390.0)
+                              : (bn == 256 ? 790.0 : 450.0);
       const int units = pair ? max_pairs : num_sms;
       // (a) whole tiles only (pairs: optionally a k-split chain for RESID)
       if (force_sched != 2) {
@@ -435,6 +440,7 @@ struct TmapCache {
   int max_pairs = 0;      // co-resident 2-CTA clusters of the pair kernel
   int force_tail = 1;     // 0 auto, 1 never cut remainder tiles (default: measured 0.2 ms/step slower), 2 always
   bool no192 = false;     // exclude 256 x 192 pair tiles from the plan
+  bool no224 = false;     // exclude 256 x 224 SwiGLU pair tiles from the plan
   int pairs_cap[5] = {0, 0, 0, 0, 0};  // per epilogue kind: use at most this many CTA pairs (0: all)
   bool balance = true;    // spread pair tiles evenly over the rounds they need (plan_gemm)
   float* tscr = nullptr;  // [max_pairs][2][128][256] fp32 tail-piece partials
@@ -523,7 +529,7 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
   const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit,
                             c->tmaps->force_tail, c->tmaps->no192, c->tmaps->pairs_cap[e.kind],
-                            c->tmaps->balance);
+                            c->tmaps->balance, c->tmaps->no224);
   if (pl.pair)
     return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, pl.tail_r,
                            pl.tail_p, c->tmaps->tscr, c->tmaps->tcnt, s);
@@ -537,6 +543,7 @@ void gemm_tc_force_pair(cb_ctx* c, int v) { c->tmaps->force_pair = v; }
 void gemm_tc_force_ksplit(cb_ctx* c, int v) { c->tmaps->force_ksplit = v; }
 void gemm_tc_force_tail(cb_ctx* c, int v) { c->tmaps->force_tail = v; }
 void gemm_tc_no192(cb_ctx* c, int v) { c->tmaps->no192 = v != 0; }
+void gemm_tc_no224(cb_ctx* c, int v) { c->tmaps->no224 = v != 0; }
 void gemm_tc_pairs_cap(cb_ctx* c, int kind, int v) { c->tmaps->pairs_cap[kind] = v; }
 void gemm_tc_balance(cb_ctx* c, int v) { c->tmaps->balance = v != 0; }
 int gemm_tc_max_pairs(const cb_ctx* c) { return c->tmaps ? c->tmaps->max_pairs : 0; }

@@ -27,7 +27,7 @@ template <int BN> struct Cfg2 {
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int EPI_BYTES = 4 * gepi::EPI_WARP_F4 * 16;  // epilogue staging, 4 KB per warp
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
-  static constexpr int ACC_STRIDE = BN == 192 ? 256 : BN;  // accumulator buffer stride (TMEM columns)
+  static constexpr int ACC_STRIDE = (BN == 192 || BN == 224) ? 256 : BN;  // accumulator buffer stride (TMEM columns)
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE;           // power of two for tcgen05.alloc
 };
 
@@ -329,6 +329,11 @@ cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int 
   ProfScope ps_(c, PROF_GEMM, s);
   if (e.kind != EPI_RESID) ksplit = 1;
   if (ksplit > 1) tail_p = 1;
+  if (bn == 224) {  // SwiGLU only: 112 gate + 112 up columns (14336 = 128 x 112 features, Mistral d_ff)
+    CB_REQUIRE(e.kind == EPI_SWIGLU, CB_E_INVALID_ARG, "224-wide pair tiles are for the SwiGLU GEMM only");
+    return launch2_kind<EPI_SWIGLU, 224>(c, A, lda, B, ldb, M, K, e, n_pairs, 1, kflags, tail_r, tail_p, tscr, tcnt,
+                                         s);
+  }
 #define L2_(KIND_)                                                                                      \
   return bn == 256                                                                                      \
              ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
@@ -362,7 +367,7 @@ template <int BN> static cb_status set_attrs2() {
 }
 
 // How many 2-CTA clusters of the kernel can be co-resident (GPC boundaries can leave fewer than SMs / 2).
-template <int BN> static cb_status max_pairs2(int num_sms, int* out) {
+template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms, int* out) {
   using C = Cfg2<BN>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms);
@@ -374,7 +379,7 @@ template <int BN> static cb_status max_pairs2(int num_sms, int* out) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  CB_CUDA(cudaOccupancyMaxActiveClusters(&n, gemm_tc2_kernel<EPI_RESID, BN>, &cfg));
+  CB_CUDA(cudaOccupancyMaxActiveClusters(&n, gemm_tc2_kernel<KIND, BN>, &cfg));
   *out = n;
   return CB_OK;
 }
@@ -383,12 +388,16 @@ cb_status gemm_tc2_init(int num_sms, int* max_pairs) {
   CB_TRY(set_attrs2<256>());
   CB_TRY(set_attrs2<192>());
   CB_TRY(set_attrs2<128>());
-  int a = 0, b = 0, c3 = 0;
+  CB_CUDA(cudaFuncSetAttribute(gemm_tc2_kernel<EPI_SWIGLU, 224>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Cfg2<224>::SMEM));
+  int a = 0, b = 0, c3 = 0, c4 = 0;
   CB_TRY(max_pairs2<256>(num_sms, &a));
   CB_TRY(max_pairs2<128>(num_sms, &b));
   CB_TRY(max_pairs2<192>(num_sms, &c3));
+  CB_TRY((max_pairs2<224, EPI_SWIGLU>(num_sms, &c4)));
   *max_pairs = a < b ? a : b;
   if (c3 < *max_pairs) *max_pairs = c3;
+  if (c4 < *max_pairs) *max_pairs = c4;
   CB_REQUIRE(*max_pairs >= 1, CB_E_CUDA, "no CTA pair of the tcgen05 GEMM fits on this device");
   return CB_OK;
 }

@@ -191,6 +191,22 @@ def test_gemm_tail_pieces(P, M, N, K, bn, resid):
         assert torch.equal(run(), C)
 
 
+@pytest.mark.parametrize("lens", [[200, 317, 150], [40, 30]])
+def test_blend_swiglu_224_tiles(P, lens):
+    """gate_up on 256 x 224 CTA-pair tiles (112 gate + 112 up features; d_ff = 2816 leaves a ragged last
+    tile of 16 features) in the small bf16 blend, replay mode: oracle tolerance, and close to the default
+    tiling (same math, different tiles)."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 5, lens, 0, "bf16", 0.15)
+    ora = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks)
+    ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
+    ctx.set_option("gemm_pair", 1)
+    ctx.set_option("gemm_bn", 224)
+    res = run_blend(P, s, "bf16", 5, req, tok, pos, cs, Kc, Vc, ks, force_sel=ora.sel, ctx=ctx)
+    _compare(res, ora, s, TOL["bf16"])
+    ref = run_blend(P, s, "bf16", 5, req, tok, pos, cs, Kc, Vc, ks, force_sel=ora.sel)
+    assert rel_err(res["h"], ref["h"]) < 5e-3
+
+
 @pytest.mark.parametrize("mlp_fused", [2, 4])
 def test_blend_fused_mlp_matches_two_gemms(P, mlp_fused):
     """The experimental fused gate_up + down kernel (mlp_fused) reproduces the two-GEMM MLP in the
