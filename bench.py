@@ -413,6 +413,30 @@ def run_ours(args):
                      "note": "same library kernels and inputs, one CUDA graph each; full prefill = every token "
                              "recomputed (no cache), full KV reuse = r=0 (realign + full layer 0 only). The paper "
                              "quotes 2.2-3.3x TTFT vs full prefill on its GPUs (P:731), context only"}
+    # the loading controller for this request with the chunk KV in pinned
+    # host memory: T_load from the measured host->HBM copy rate of one layer, Prefill from the full-prefill
+    # baseline above (per layer), r = max(r_eq, 15 %)
+    controller = None
+    if baselines is not None:
+        kv_tok = 2 * sh.n_kv_heads * s.head_dim * 2  # K and V of one token, one layer, bf16 (this rank's heads)
+        host = torch.empty(N * kv_tok // 2, dtype=torch.bfloat16).pin_memory()
+        devb = torch.empty_like(host, device=dev)
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(2):
+            devb.copy_(host, non_blocking=True)
+        a_.record(stream)
+        for _ in range(5):
+            devb.copy_(host, non_blocking=True)
+        b_.record(stream)
+        torch.cuda.synchronize()
+        bpm = 5 * host.numel() * 2 / a_.elapsed_time(b_)  # bytes per ms
+        pre_layer = baselines["full_prefill_ms"] / L
+        r_ctl, load_ms = P.api.controller_ratio(pre_layer, kv_tok, N, bpm, 0.15)
+        controller = {"h2d_GBps": bpm / 1e6, "load_ms_per_layer": load_ms, "prefill_ms_per_layer": pre_layer,
+                      "r": r_ctl, "r_eq": load_ms / pre_layer,
+                      "note": "cb_controller_ratio: T_recompute(r) = r x Prefill per layer equals T_load per layer "
+                              "(pinned host -> HBM), then max(r, 15%) (P:2693-2700)"}
+        del host, devb
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         smp = OracleSample(s, lens, ratio, args.seed)
@@ -435,7 +459,7 @@ def run_ours(args):
                            "l2": f"inputs larger than L2 ({work['weight_bytes'] / 1e9:.1f} GB of weights streamed "
                                  "per step per GPU)"},
                 "gpu_launches": int(launches), "clocks": clk.summary(), "roofline": roof,
-                "cpu_baseline": cpu, "e2e": e2e, "baselines": baselines,
+                "cpu_baseline": cpu, "e2e": e2e, "baselines": baselines, "controller": controller,
                 "kernel_ms": {k: round(v, 4) for k, v in prof.items()},
                 "work": {k: float(v) for k, v in work.items()}}
         print(json.dumps(line), flush=True)

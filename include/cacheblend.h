@@ -94,6 +94,19 @@ CB_API cb_status cb_check_device_errors(cb_ctx* ctx);
  * k_sched_out: host int32[n_layers]. ratio outside [0,1] -> INVALID_ARG. */
 CB_API cb_status cb_schedule(double ratio, int32_t n_ctx, int32_t n_layers, int32_t* k_sched_out);
 
+/* Loading controller (§6 "Loading Controller"), host only. Per layer:
+ *   T_load = kv_bytes_per_token * n_tokens / bytes_per_ms          (footnote P:2696)
+ *   T_recompute(r) = r * prefill_ms, prefill_ms profiled offline   (footnote P:2695)
+ * cb_controller_ratio: r_out = min(1, max(r_eq, r_min)) with T_recompute(r_eq) = T_load (
+ * the paper's r* = 15 %); load_ms_out (optional) = T_load. Errors: non-positive prefill/throughput,
+ * r_min outside [0, 1] -> INVALID_ARG.
+ * cb_controller_pick_device: the cheapest of n_dev storage devices (host arrays load_ms[d] = T_load on
+ * device d, cost[d]) with T_recompute(r_fixed) >= T_load; ties -> lower index; -1 if none. */
+CB_API cb_status cb_controller_ratio(double prefill_ms, double kv_bytes_per_token, int64_t n_tokens,
+                                     double bytes_per_ms, double r_min, double* r_out, double* load_ms_out);
+CB_API cb_status cb_controller_pick_device(double prefill_ms, const double* load_ms, const double* cost,
+                                           int32_t n_dev, double r_fixed, int32_t* pick_out);
+
 /* ---- (a) positional recovery --------------------------------------------------------------- */
 /* Footnote P:208-211, Appendix: K_out[s][t] = R(dst_pos[t] - src_pos[t]) K_src[s][t]
  * for every slice s (a layer) and token t, per kv head; V is untouched. src_pos = chunk-local

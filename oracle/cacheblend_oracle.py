@@ -381,3 +381,36 @@ def full_prefill_macs(model: Model, tok, pos) -> int:
     mc = MacCounter()
     full_prefill(model, tok, pos, mc)
     return mc.macs
+
+
+# ---------------------------------------------------------------------------------------
+# Loading controller (§6 "Loading Controller", P:2693-2705 and its two footnotes)
+# ---------------------------------------------------------------------------------------
+def t_recompute(ratio: float, prefill_ms: float) -> float:
+    """Recompute delay estimator: T_recompute(r%, LLM, L) = r% x Prefill(LLM, L) (footnote),
+    Prefill profiled offline. Per layer (P:2655-2659 compare one layer's recompute with one layer's load)."""
+    return float(ratio) * float(prefill_ms)
+
+
+def t_load(kv_bytes_per_token: float, n_tokens: int, bytes_per_ms: float) -> float:
+    """Loading delay estimator: T_load = PerTokenKVSize(LLM) x L / Throughput(storage_device) (footnote,
+    P:2696), for one layer's KV."""
+    return float(kv_bytes_per_token) * int(n_tokens) / float(bytes_per_ms)
+
+
+def controller_ratio(prefill_ms: float, load_ms: float, r_min: float = 0.15) -> float:
+    """Pick r% with T_recompute(r%) = T_load, then take max(r%, r*%) with r* = 15 %; a
+    ratio is at most 100 %."""
+    r_eq = float(load_ms) / float(prefill_ms)
+    return min(1.0, max(r_eq, float(r_min)))
+
+
+def controller_pick_device(prefill_ms: float, load_ms: Sequence[float], cost: Sequence[float],
+                           r_fixed: float = 0.15) -> int:
+    """The cheapest storage device whose loading delay is hidden by the fixed-ratio recompute,
+    T_recompute(r_fixed) >= T_load; ties -> the earlier device; -1 if none qualifies."""
+    best = -1
+    for d in range(len(load_ms)):
+        if t_recompute(r_fixed, prefill_ms) >= load_ms[d] and (best < 0 or cost[d] < cost[best]):
+            best = d
+    return best

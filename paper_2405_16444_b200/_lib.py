@@ -57,6 +57,9 @@ _SIGS = {
     "cb_profile_end": (c_i32, [c_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "cb_profile_class_name": (ctypes.c_char_p, [c_i32]),
     "cb_nccl_unique_id": (c_i32, [c_vp]),
+    "cb_controller_ratio": (c_i32, [c_f64, c_f64, c_i64, c_f64, c_f64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64)]),
+    "cb_controller_pick_device": (c_i32, [c_f64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64), c_i32, c_f64,
+                                          ctypes.POINTER(c_i32)]),
     "cb_set_comm": (c_i32, [c_vp, c_vp, c_i32, c_i32]),
     "cb_group_create": (c_i32, [c_i32, ctypes.POINTER(c_vp)]),
     "cb_group_destroy": (c_i32, [c_vp]),

@@ -216,6 +216,25 @@ def schedule(ratio: float, n_ctx: int, n_layers: int) -> List[int]:
     return list(out)
 
 
+def controller_ratio(prefill_ms: float, kv_bytes_per_token: float, n_tokens: int, bytes_per_ms: float,
+                     r_min: float = 0.15):
+    """Loading controller (cb_controller_ratio): (recompute ratio, T_load in ms) for one layer."""
+    r, ld = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    check(lib().cb_controller_ratio(float(prefill_ms), float(kv_bytes_per_token), int(n_tokens), float(bytes_per_ms),
+                                    float(r_min), ctypes.byref(r), ctypes.byref(ld)))
+    return r.value, ld.value
+
+
+def controller_pick_device(prefill_ms: float, load_ms: Sequence[float], cost: Sequence[float],
+                           r_fixed: float = 0.15) -> int:
+    """cb_controller_pick_device: index of the cheapest storage device whose load is hidden, or -1."""
+    n = len(load_ms)
+    lm, co = (ctypes.c_double * max(n, 1))(*load_ms), (ctypes.c_double * max(n, 1))(*cost)
+    out = ctypes.c_int32(0)
+    check(lib().cb_controller_pick_device(float(prefill_ms), lm, co, n, float(r_fixed), ctypes.byref(out)))
+    return out.value
+
+
 def rope_realign(ctx: Context, k_out: torch.Tensor, k_src: torch.Tensor, src_pos: torch.Tensor,
                  dst_pos: torch.Tensor, n_slices: int, n_tok: int, slice_stride: int, stream=None):
     check(lib().cb_rope_realign(ctx.handle, _p(k_out), _p(k_src), _p(src_pos), _p(dst_pos), n_slices, n_tok,
@@ -324,6 +343,6 @@ def op_embed(ctx: Context, embed: torch.Tensor, tok: torch.Tensor, stream=None):
     return h
 
 
-__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
+__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "controller_ratio", "controller_pick_device", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
            "blend_layer", "blend_forward", "gen_fill", "gen_ints", "op_gemm", "op_attention", "op_rmsnorm",
            "op_embed"]

@@ -479,6 +479,33 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   return CB_E_INVALID_ARG;
 }
 
+// ---- loading controller (host; §6 "Loading Controller") ---------------------------------
+extern "C" cb_status cb_controller_ratio(double prefill_ms, double kv_bytes_per_token, int64_t n_tokens,
+                                         double bytes_per_ms, double r_min, double* r_out, double* load_ms_out) {
+  CB_REQUIRE(r_out != nullptr, CB_E_INVALID_ARG, "r_out is NULL");
+  CB_REQUIRE(prefill_ms > 0.0 && bytes_per_ms > 0.0 && kv_bytes_per_token >= 0.0 && n_tokens >= 0, CB_E_INVALID_ARG,
+             "controller: need prefill_ms > 0, bytes_per_ms > 0, kv_bytes_per_token >= 0, n_tokens >= 0");
+  CB_REQUIRE(r_min >= 0.0 && r_min <= 1.0, CB_E_INVALID_ARG, "r_min %g outside [0, 1]", r_min);
+  const double load_ms = kv_bytes_per_token * (double)n_tokens / bytes_per_ms;  // T_load (footnote P:2696)
+  const double r_eq = load_ms / prefill_ms;  // T_recompute(r_eq) = r_eq * Prefill = T_load
+  *r_out = std::min(1.0, std::max(r_eq, r_min));  // max(r%, r*%)
+  if (load_ms_out) *load_ms_out = load_ms;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_controller_pick_device(double prefill_ms, const double* load_ms, const double* cost,
+                                               int32_t n_dev, double r_fixed, int32_t* pick_out) {
+  CB_REQUIRE(pick_out != nullptr && n_dev >= 0 && (n_dev == 0 || (load_ms && cost)), CB_E_INVALID_ARG,
+             "controller: bad device arrays");
+  CB_REQUIRE(prefill_ms > 0.0 && r_fixed >= 0.0 && r_fixed <= 1.0, CB_E_INVALID_ARG, "controller: bad ratio / prefill");
+  const double t_rec = r_fixed * prefill_ms;
+  int best = -1;
+  for (int d = 0; d < n_dev; ++d)  // cheapest device with T_recompute >= T_load; ties -> earlier
+    if (t_rec >= load_ms[d] && (best < 0 || cost[d] < cost[best])) best = d;
+  *pick_out = best;
+  return CB_OK;
+}
+
 // ---- schedule (host) ----------------------------------------------------------------------------
 extern "C" cb_status cb_schedule(double ratio, int32_t n_ctx, int32_t n_layers, int32_t* k) {
   CB_REQUIRE(k != nullptr && n_layers >= 1 && n_ctx >= 0, CB_E_INVALID_ARG, "bad arguments to cb_schedule");
