@@ -364,7 +364,7 @@ def run_ours(args):
     if gemm_ms > 0:
         achieved = work["gemm_flops"] / (gemm_ms / 1e3) / 1e12
         traffic, tnote = None, None
-        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01b_traffic.json")
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_traffic.json")
         if os.path.exists(tpath):  # committed ncu measurement of the largest GEMM launch (bytes per launch)
             tj = json.load(open(tpath))
             traffic = tj["dram_bytes"]
