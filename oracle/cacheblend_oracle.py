@@ -414,3 +414,17 @@ def controller_pick_device(prefill_ms: float, load_ms: Sequence[float], cost: Se
         if t_recompute(r_fixed, prefill_ms) >= load_ms[d] and (best < 0 or cost[d] < cost[best]):
             best = d
     return best
+
+
+# ---------------------------------------------------------------------------------------
+# Hand-off to a paged decode cache ("the fused KV cache is input into the LLM inference
+# engine"; vLLM pages KV in fixed-size blocks)
+# ---------------------------------------------------------------------------------------
+def kv_to_paged(kv: np.ndarray, block_table: Sequence[int], block_size: int, n_pages: int) -> np.ndarray:
+    """kv [L][T][n_kv][hd] -> pages [L][n_pages][block_size][n_kv][hd]: token t at page
+    block_table[t // block_size], slot t % block_size. Unwritten slots are NaN."""
+    L, T = kv.shape[:2]
+    out = np.full((L, n_pages, block_size) + kv.shape[2:], np.nan, dtype=kv.dtype)
+    for t in range(T):
+        out[:, block_table[t // block_size], t % block_size] = kv[:, t]
+    return out

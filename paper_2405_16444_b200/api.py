@@ -216,6 +216,78 @@ def schedule(ratio: float, n_ctx: int, n_layers: int) -> List[int]:
     return list(out)
 
 
+def kv_to_paged(ctx: Context, k_blend: torch.Tensor, v_blend: torch.Tensor, block_table: torch.Tensor,
+                block_size: int, k_pages: torch.Tensor, v_pages: torch.Tensor, n_tok: Optional[int] = None,
+                stream=None):
+    """cb_kv_to_paged: k_blend/v_blend [L][T][n_kv][hd] -> k_pages/v_pages [L][n_pages][block_size][n_kv][hd]."""
+    L, T = k_blend.shape[0], k_blend.shape[1]
+    n = T if n_tok is None else int(n_tok)
+    check(lib().cb_kv_to_paged(ctx.handle, _p(k_blend), _p(v_blend), L, n, k_blend[0].numel(), _p(block_table),
+                               int(block_size), _p(k_pages), _p(v_pages), k_pages[0].numel(), _stream(stream)))
+
+
+def chunk_hash(tokens) -> int:
+    """cb_chunk_hash of a chunk's token ids (host)."""
+    a = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
+    return int(lib().cb_chunk_hash(a.ctypes.data, a.size))
+
+
+class Store:
+    """cb_store: chunk hash -> chunk KV (host RAM, LRU eviction)."""
+
+    def __init__(self, capacity_bytes: int, pinned: bool = True):
+        h = ctypes.c_void_p()
+        check(lib().cb_store_create(int(capacity_bytes), int(pinned), ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().cb_store_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def put(self, key: int, k: torch.Tensor, v: torch.Tensor):
+        """k, v: [L][n_tok][n_kv][hd] (host or device, contiguous)."""
+        assert k.is_contiguous() and v.is_contiguous() and k.shape == v.shape
+        check(lib().cb_store_put(self.handle, int(key), k.data_ptr(), v.data_ptr(), k.numel() * k.element_size(),
+                                 int(k.shape[1])))
+
+    def lookup(self, key: int, touch: bool = True) -> int:
+        n = ctypes.c_int32(0)
+        check(lib().cb_store_lookup(self.handle, int(key), int(touch), ctypes.byref(n), None, None))
+        return n.value
+
+    def stats(self) -> Dict[str, int]:
+        o = (ctypes.c_int64 * 6)()
+        check(lib().cb_store_stats(self.handle, o))
+        return dict(zip(("used", "capacity", "entries", "hits", "misses", "evictions"), list(o)))
+
+    def keys(self) -> List[int]:
+        n = ctypes.c_int32(0)
+        check(lib().cb_store_keys(self.handle, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint64 * max(n.value, 1))()
+        check(lib().cb_store_keys(self.handle, buf, n.value, ctypes.byref(n)))
+        return list(buf[:n.value])
+
+
+def blend_request_store(ctx: Context, store: Store, chunk_keys: Sequence[int], weights: ModelWeights,
+                        tok_host: torch.Tensor, pos_host: torch.Tensor, chunk_start: Sequence[int], n_suffix: int,
+                        k_blend: torch.Tensor, v_blend: torch.Tensor, k_sched: Sequence[int],
+                        h_out_host: torch.Tensor, sel_out_host: Optional[torch.Tensor] = None, stream=None):
+    """cb_blend_request_store: chunk KV fetched from the store layer by layer."""
+    N = int(chunk_start[-1])
+    keys = (ctypes.c_uint64 * max(len(chunk_keys), 1))(*[int(x) for x in chunk_keys])
+    check(lib().cb_blend_request_store(ctx.handle, store.handle, keys, weights.cw, _p(weights.embed), _p(tok_host),
+                                       _p(pos_host), N, n_suffix, _i32(chunk_start), len(chunk_start) - 1,
+                                       _p(k_blend), _p(v_blend), _i32(k_sched), _p(sel_out_host), _p(h_out_host),
+                                       _stream(stream)))
+
+
 def controller_ratio(prefill_ms: float, kv_bytes_per_token: float, n_tokens: int, bytes_per_ms: float,
                      r_min: float = 0.15):
     """Loading controller (cb_controller_ratio): (recompute ratio, T_load in ms) for one layer."""
@@ -343,6 +415,7 @@ def op_embed(ctx: Context, embed: torch.Tensor, tok: torch.Tensor, stream=None):
     return h
 
 
-__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "controller_ratio", "controller_pick_device", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
+__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "controller_ratio", "controller_pick_device", "kv_to_paged", "Store", "chunk_hash",
+           "blend_request_store", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
            "blend_layer", "blend_forward", "gen_fill", "gen_ints", "op_gemm", "op_attention", "op_rmsnorm",
            "op_embed"]

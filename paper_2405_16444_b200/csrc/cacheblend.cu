@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <vector>
 
 #include "ctx.h"
@@ -953,14 +954,13 @@ extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void
                       h_out, s, false);
 }
 
-extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
-                                      const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
-                                      int32_t n_chunks, const void* k_in_host, const void* v_in_host, void* k_blend,
-                                      void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,
-                                      float* h_out_host, void* st) {
-  CB_TRY(check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in_host, v_in_host,
-                       k_blend, v_blend, k_sched, h_out_host));
-  cudaStream_t s = (cudaStream_t)st, cs = c->copy_stream;
+// The request path (fetch_kv -> synchronize -> prefill_layer) with the layer fetch supplied
+// by the caller: fetch(i, k_dst, v_dst, cs) enqueues layer i's chunk KV (rows [0, N)) on the copy stream.
+cb_status blend_request_impl(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                             const int32_t* pos_host, int N, int n_suffix, const int32_t* chunk_start, int n_chunks,
+                             void* k_blend, void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,
+                             float* h_out_host, cudaStream_t s, const FetchLayer& fetch) {
+  cudaStream_t cs = c->copy_stream;
   const cb_model& m = c->m;
   const int L = m.n_layers, T = N + n_suffix, kvd = m.n_kv_heads * m.head_dim;
   const size_t B = dtype_bytes(m.dtype);
@@ -973,10 +973,7 @@ extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void
   // fetch_kv(layer i) for every layer, in layer order on the copy stream
   for (int i = 0; i < L && N > 0; ++i) {
     const size_t row = (size_t)kvd * B;
-    CB_CUDA(cudaMemcpy2DAsync((char*)k_blend + (size_t)i * T * row, row * T, (const char*)k_in_host + (size_t)i * N * row,
-                              row * N, row * N, 1, cudaMemcpyHostToDevice, cs));
-    CB_CUDA(cudaMemcpy2DAsync((char*)v_blend + (size_t)i * T * row, row * T, (const char*)v_in_host + (size_t)i * N * row,
-                              row * N, row * N, 1, cudaMemcpyHostToDevice, cs));
+    CB_TRY(fetch(i, (char*)k_blend + (size_t)i * T * row, (char*)v_blend + (size_t)i * T * row, cs));
     CB_CUDA(cudaEventRecord(c->layer_ev[i], cs));
   }
   CB_CUDA(cudaStreamWaitEvent(s, c->layer_ev[L], 0));
@@ -988,4 +985,33 @@ extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void
     CB_CUDA(cudaMemcpyAsync(sel_out_host, c->row_tok[(L - 2) & 1], (size_t)(final_rows - n_suffix) * 4,
                             cudaMemcpyDeviceToHost, s));
   return CB_OK;
+}
+
+cb_status check_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                        const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                        int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend, void* v_blend,
+                        const int32_t* k_sched, const void* h_out) {
+  return check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in, v_in, k_blend,
+                       v_blend, k_sched, h_out);
+}
+
+extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                                      const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                                      int32_t n_chunks, const void* k_in_host, const void* v_in_host, void* k_blend,
+                                      void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,
+                                      float* h_out_host, void* st) {
+  CB_TRY(check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in_host, v_in_host,
+                       k_blend, v_blend, k_sched, h_out_host));
+  const int T = N + n_suffix;
+  const size_t row = (size_t)c->m.n_kv_heads * c->m.head_dim * dtype_bytes(c->m.dtype);
+  // request KV in one host buffer per tensor, [L][N][n_kv][hd]
+  FetchLayer fetch = [&](int i, char* kd, char* vd, cudaStream_t cs) -> cb_status {
+    CB_CUDA(cudaMemcpy2DAsync(kd, row * T, (const char*)k_in_host + (size_t)i * N * row, row * N, row * N, 1,
+                              cudaMemcpyHostToDevice, cs));
+    CB_CUDA(cudaMemcpy2DAsync(vd, row * T, (const char*)v_in_host + (size_t)i * N * row, row * N, row * N, 1,
+                              cudaMemcpyHostToDevice, cs));
+    return CB_OK;
+  };
+  return blend_request_impl(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_blend, v_blend,
+                            k_sched, sel_out_host, h_out_host, (cudaStream_t)st, fetch);
 }

@@ -198,6 +198,17 @@ cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb,
                       int impl, cudaStream_t s);
 cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                            const void* v, int n_keys, void* out, int impl, cudaStream_t s);
+// Request path with a caller-supplied per-layer fetch (cb_blend_request, cb_blend_request_store).
+#include <functional>
+using FetchLayer = std::function<cb_status(int layer, char* k_dst, char* v_dst, cudaStream_t copy_stream)>;
+cb_status blend_request_impl(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                             const int32_t* pos_host, int N, int n_suffix, const int32_t* chunk_start, int n_chunks,
+                             void* k_blend, void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,
+                             float* h_out_host, cudaStream_t s, const FetchLayer& fetch);
+cb_status check_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
+                        const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
+                        int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend, void* v_blend,
+                        const int32_t* k_sched, const void* h_out);
 // Head-parallel collectives on `s` (no-ops when tp_world <= 1). All-reduce: in-place fp32 sum. All-gather:
 // in place, this rank's n_per_rank floats already at buf + tp_rank * n_per_rank.
 cb_status comm_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s);

@@ -331,3 +331,61 @@ cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* row, cud
   CB_LAUNCHED(c);
   return CB_OK;
 }
+
+// ---------------------------------------------------------------------------------------------
+// KV^new -> paged decode cache ("the fused KV cache is input into the LLM inference
+// engine", which pages its KV in fixed-size blocks, P:2496 / P:2722): token t of layer l goes to
+// page block_table[t / block_size], slot t % block_size of that layer's pool. A thread moves one 16-B
+// vector; consecutive threads cover a token row, then the next token, so reads are contiguous and
+// writes are contiguous within a page.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void kv_to_paged_kernel(const T* __restrict__ k, const T* __restrict__ v, long long src_layer_stride,
+                                   int n_layers, int n_tok, int row, const int* __restrict__ block_table,
+                                   int block_size, T* __restrict__ kp, T* __restrict__ vp, long long dst_layer_stride) {
+  pdl_enter();
+  constexpr int V = Vec16<T>::N;
+  const int vec_per_row = row / V;
+  const long long per_layer = (long long)n_tok * vec_per_row;
+  const long long total = per_layer * n_layers;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(i / per_layer);
+    const long long r = i - (long long)l * per_layer;
+    const int t = (int)(r / vec_per_row), e = (int)(r - (long long)t * vec_per_row) * V;
+    const long long src = l * src_layer_stride + (long long)t * row + e;
+    const long long dst = l * dst_layer_stride +
+                          ((long long)__ldg(block_table + t / block_size) * block_size + t % block_size) * row + e;
+    st16(kp + dst, ld16(k + src));
+    st16(vp + dst, ld16(v + src));
+  }
+}
+
+extern "C" cb_status cb_kv_to_paged(cb_ctx* c, const void* k_blend, const void* v_blend, int32_t n_layers,
+                                    int32_t n_tok, int64_t src_layer_stride, const int32_t* block_table,
+                                    int32_t block_size, void* k_pages, void* v_pages, int64_t dst_layer_stride,
+                                    void* st) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  CB_REQUIRE(n_layers >= 0 && n_tok >= 0 && block_size >= 1, CB_E_INVALID_ARG, "bad sizes");
+  if (n_layers == 0 || n_tok == 0) return CB_OK;
+  CB_REQUIRE(k_blend && v_blend && block_table && k_pages && v_pages, CB_E_INVALID_ARG, "NULL pointer");
+  const int row = c->m.n_kv_heads * c->m.head_dim;
+  CB_REQUIRE(src_layer_stride >= (int64_t)n_tok * row, CB_E_SHAPE, "src_layer_stride < n_tok * n_kv * head_dim");
+  CB_REQUIRE(dst_layer_stride >= (int64_t)((n_tok + block_size - 1) / block_size) * block_size * row, CB_E_SHAPE,
+             "dst_layer_stride smaller than the pages of n_tok tokens");
+  const uintptr_t al = (uintptr_t)k_blend | (uintptr_t)v_blend | (uintptr_t)k_pages | (uintptr_t)v_pages;
+  CB_REQUIRE(al % 16 == 0, CB_E_INVALID_ARG, "KV buffers must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)st;
+  ProfScope ps_(c, PROF_SCATTER, s);
+  const long long vecs = (long long)n_layers * n_tok * (row * (long long)dtype_bytes(c->m.dtype) / 16);
+  const int blocks = (int)std::min<long long>(8LL * c->num_sms, (vecs + 255) / 256);
+  if (c->m.dtype == CB_BF16)
+    CB_LAUNCH(c, (kv_to_paged_kernel<bf16>), blocks, 256, 0, s, (const bf16*)k_blend, (const bf16*)v_blend,
+              (long long)src_layer_stride, n_layers, n_tok, row, block_table, block_size, (bf16*)k_pages,
+              (bf16*)v_pages, (long long)dst_layer_stride);
+  else
+    CB_LAUNCH(c, (kv_to_paged_kernel<float>), blocks, 256, 0, s, (const float*)k_blend, (const float*)v_blend,
+              (long long)src_layer_stride, n_layers, n_tok, row, block_table, block_size, (float*)k_pages,
+              (float*)v_pages, (long long)dst_layer_stride);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}

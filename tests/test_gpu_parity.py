@@ -434,3 +434,62 @@ def test_blend_request_equals_forward(P, name, dtype, n_suf):
     np.testing.assert_array_equal(np32(vb), a["V"])
     np.testing.assert_array_equal(hh.numpy(), a["h"])
     np.testing.assert_array_equal(sel.numpy()[:ks[-1]], a["sel"][-1])
+
+
+# ---- hand-off to a paged decode cache ----------------------------------------------------
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("T,bs", [(1, 16), (667, 16), (3072, 16), (300, 7)])
+def test_kv_to_paged_bitexact(P, dtype, T, bs):
+    s = shape("small")
+    ctx = P.Context(s, dtype, max_tokens=8)
+    td = P.api.TORCH_DTYPES[dtype]
+    g = torch.Generator(device=DEV).manual_seed(T + bs)
+    L = 3
+    k = torch.randn(L, T, s.n_kv_heads, s.head_dim, device=DEV, generator=g).to(td)
+    v = torch.randn(L, T, s.n_kv_heads, s.head_dim, device=DEV, generator=g).to(td)
+    nb = -(-T // bs)
+    table = np.random.default_rng(T).permutation(nb + 5)[:nb].astype(np.int32)
+    kp = torch.full((L, nb + 5, bs, s.n_kv_heads, s.head_dim), float("nan"), dtype=td, device=DEV)
+    vp = torch.full_like(kp, float("nan"))
+    P.api.kv_to_paged(ctx, k, v, to_dev(table, torch.int32), bs, kp, vp)
+    torch.cuda.synchronize()
+    for src, dst in ((k, kp), (v, vp)):
+        want = O.kv_to_paged(np32(src), table, bs, nb + 5)
+        np.testing.assert_array_equal(np32(dst), want)  # bit-exact copy (NaN where nothing is written)
+
+
+# ---- the request path through the chunk KV store -----------------------------------------
+@pytest.mark.parametrize("name,dtype,n_suf", [("tiny", "f32", 0), ("small", "bf16", 6)])
+def test_blend_request_store_equals_forward(P, name, dtype, n_suf):
+    """Chunk caches put into the store under their token hashes, fetched layer by layer by
+    cb_blend_request_store: exactly cb_blend_forward's result; a missing chunk is CB_E_MISS before any
+    launch; the fetched chunks become the most recently used."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case(name, 6, [40, 57, 31], n_suf, dtype, 0.2)
+    a = run_blend(P, s, dtype, 6, req, tok, pos, cs, Kc, Vc, ks)
+    td = P.api.TORCH_DTYPES[dtype]
+    store = P.api.Store(1 << 30, pinned=True)
+    keys = []
+    for c in range(len(cs) - 1):
+        sl = slice(int(cs[c]), int(cs[c + 1]))
+        key = P.api.chunk_hash(tok[sl])
+        keys.append(key)
+        store.put(key, torch.from_numpy(np.ascontiguousarray(Kc[:, sl])).to(td).contiguous(),
+                  torch.from_numpy(np.ascontiguousarray(Vc[:, sl])).to(td).contiguous())
+    store.put(12345, torch.zeros(1, 4, 1, 1), torch.zeros(1, 4, 1, 1))  # most recent before the request
+    T = req.n_total
+    kb = torch.empty(s.n_layers, T, s.n_kv_heads, s.head_dim, dtype=td, device=DEV)
+    vb = torch.empty_like(kb)
+    hh = torch.empty(ks[-1] + n_suf, s.d_model, dtype=torch.float32).pin_memory()
+    toks = torch.from_numpy(tok.astype(np.int32)).pin_memory()
+    poss = torch.from_numpy(pos.astype(np.int32)).pin_memory()
+    with pytest.raises(P.CacheBlendError, match="not in the KV store"):
+        P.api.blend_request_store(a["ctx"], store, keys[:-1] + [999], a["mw"], toks, poss, list(cs), n_suf, kb, vb,
+                                  ks, hh)
+    P.api.blend_request_store(a["ctx"], store, keys, a["mw"], toks, poss, list(cs), n_suf, kb, vb, ks, hh)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(np32(kb), a["K"])
+    np.testing.assert_array_equal(np32(vb), a["V"])
+    np.testing.assert_array_equal(hh.numpy(), a["h"])
+    assert store.keys()[:len(keys)] == list(reversed(keys))  # fetched chunks refreshed, last chunk first
+    st = store.stats()
+    assert st["misses"] == 1 and st["hits"] >= len(keys)
