@@ -37,6 +37,7 @@ constexpr int TILE = 2 * ATOM;     // 128 rows x 128 bf16
 constexpr int KST = 3;            // K ring stages (V: 2); P lives in TMEM, so SMEM = Q + 3 K + 2 V
 constexpr int SMEM = 6 * TILE + 1024 + 256 + 3072;  // + alignment + barriers + exchange
 constexpr float RESCALE_THRESHOLD = 8.0f;    // log2 units
+constexpr uint32_t QCOL = 384;               // TMEM columns of Q (QTM): 64 x 32-bit = 128 bf16 per row
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -45,6 +46,17 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ~2 ulp; ex2(-inf) 
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// 2^x on the FMA / integer pipes instead of MUFU (the softmax is MUFU-bound: 16 ex2/clk/SM): round
+// x to an integer j with the 1.5 * 2^23 trick, 2^(x - j) on [-0.5, 0.5] by a degree-3 minimax polynomial
+// (relative error 7.5e-5, below the bf16 rounding of P), 2^j added into the exponent bits. x is clamped
+// at -126, so masked scores give ~1e-38 instead of 0 (negligible against any visible key's weight).
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float t = fmaxf(x, -126.f);
+  const float r = t + 12582912.f;
+  const float f = t - (r - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517132f, f, 0.24261054f), f, 0.69326099f), f, 0.99992811f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
 }
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -55,6 +67,10 @@ __device__ __forceinline__ uint32_t sw_off(int r, int ch) {
   return (uint32_t)((ch >> 3) * ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
 }
 
+// POLY: share of the softmax exponentials computed by ex2_poly (0: none, 1: 1 in 4, 2: 1 in 2).
+// QTM: Q lives in TMEM (columns 384..447, written by the softmax threads with tcgen05.st) and S = Q K^T
+// reads it as the A operand from tensor memory, so the QK^T MMAs read only K from shared memory.
+template <int POLY, bool QTM>
 __global__ void __launch_bounds__(NT, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
@@ -176,9 +192,13 @@ __global__ void __launch_bounds__(NT, 1)
       if (tc::elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint64_t a = tc::sdesc_sw128(sQ + (kk >> 2) * ATOM) + 2 * (kk & 3);
           const uint64_t bd = tc::sdesc_sw128(sK + kb * TILE + (kk >> 2) * ATOM) + 2 * (kk & 3);
-          tc::mma_bf16(tmem + b * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
+          if constexpr (QTM) {
+            tc::mma_bf16_ts(tmem + b * 128, tmem + QCOL + 8 * kk, bd, IDESC_S, kk > 0 ? 1u : 0u);
+          } else {
+            const uint64_t a = tc::sdesc_sw128(sQ + (kk >> 2) * ATOM) + 2 * (kk & 3);
+            tc::mma_bf16(tmem + b * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
+          }
         }
         tc::mma_commit(&s_full[b]);
         tc::mma_commit(&k_empty[kb]);
@@ -220,7 +240,19 @@ __global__ void __launch_bounds__(NT, 1)
     const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
     float* xmax = reinterpret_cast<float*>(bars + 16);  // [2 parity][2 wg][128 rows], then l [2][128]
     float* xl = xmax + 512;
-    {  // stage this row's half of Q (one SWIZZLE_128B column block)
+    if constexpr (QTM) {  // this row's half of Q (64 bf16) -> TMEM columns QCOL + wg * 32 .. + 31
+      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD + wg * 64);
+      uint32_t pk[32];
+#pragma unroll
+      for (int c8 = 0; c8 < 8; ++c8) {
+        const uint4 u = valid ? __ldg(src + c8) : make_uint4(0u, 0u, 0u, 0u);
+        pk[4 * c8] = u.x; pk[4 * c8 + 1] = u.y; pk[4 * c8 + 2] = u.z; pk[4 * c8 + 3] = u.w;
+      }
+      tc::tmem_st32u(tmem + lane_base + QCOL + wg * 32, pk);
+      tc::tmem_st_wait();
+      tc::fence_before();
+      tc::mbar_arrive(q_full);
+    } else {  // stage this row's half of Q (one SWIZZLE_128B column block)
       const bf16* src = q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD;
       const uint32_t dq = tc::smem_u32(sQ);
 #pragma unroll
@@ -286,7 +318,10 @@ __global__ void __launch_bounds__(NT, 1)
       for (int i = 0; i < 8; ++i) rs8[i] = 0.f;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        s[i] = ex2(fmaf(s[i], scale_log2, nref));  // -inf -> 0
+        const float xa = fmaf(s[i], scale_log2, nref);
+        if constexpr (POLY == 1) s[i] = (i & 3) == 3 ? ex2_poly(xa) : ex2(xa);  // -inf -> 0 (MUFU)
+        else if constexpr (POLY == 2) s[i] = (i & 1) ? ex2_poly(xa) : ex2(xa);
+        else s[i] = ex2(xa);
         rs8[i & 7] += s[i];
       }
       l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
@@ -466,7 +501,10 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   CB_TRY(kv_tmap(c, v, n_keys, &tv));
   dim3 grid(tiles * n_splits * n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
-  CB_LAUNCH(c, (attn_tc5_kernel), grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
+  auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, false>
+            : c->attn_poly == 1 ? attn_tc5_kernel<1, false>
+            : c->attn_qtm ? attn_tc5_kernel<0, true> : attn_tc5_kernel<0, false>;
+  CB_LAUNCH(c, kern, grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
                                          c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
                                          c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
@@ -482,6 +520,9 @@ cb_status attention_tc5_init() {
     g_encode5 = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (g_kvmaps == nullptr) g_kvmaps = new std::unordered_map<KvKey, CUtensorMap, KvKeyHash>();
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   return CB_OK;
 }

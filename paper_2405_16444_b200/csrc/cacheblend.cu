@@ -316,6 +316,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = attention_tc5_init();
   if (st == CB_OK) st = attention_tc6_init();
   c->topk_drop_max = 48;
+  c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
   c->mlp_fused = 0;  // experimental: measured ~0.3 ms/step slower (merge + residual epilogues at the end)
   if (st == CB_OK && c->m.dtype == CB_BF16) st = gemm_mlp_init(c);
   if (st != CB_OK) {
@@ -416,6 +417,15 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   }
   if (std::strcmp(name, "fuse_deviation") == 0) {
     c->no_fuse_dev = value == 0;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "attn_qtm") == 0) {
+    c->attn_qtm = value != 0;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "attn_poly") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "attn_poly must be 0, 1 or 2");
+    c->attn_poly = (int)value;
     return CB_OK;
   }
   if (std::strcmp(name, "attn_splits") == 0) {

@@ -62,6 +62,8 @@ struct cb_ctx {
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
+  int attn_qtm;     // cb_set_option("attn_qtm"): Q in TMEM as the QK^T A operand (tcgen05 attention)
+  int attn_poly;    // cb_set_option("attn_poly"): share of softmax exp2 on the FMA pipe (0, 1 = 1/4, 2 = 1/2)
   int no_fuse_norm;  // cb_set_option("fuse_norm", 0): separate RMSNorm kernels between the projections
   int no_fuse_dev;  // cb_set_option("fuse_deviation", 0) disables the QKV-epilogue deviation
   int dbg_sel;         // debug_trace value: 1 = attention + every CTA-pair GEMM, 100 + k = pair GEMMs of kind k only

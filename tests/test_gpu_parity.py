@@ -260,6 +260,29 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     assert rel_err(np32(out), ref) < 1e-2
 
 
+@pytest.mark.parametrize("opt", [("attn_poly", 1), ("attn_poly", 2), ("attn_qtm", 1)])
+@pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (4100, 900, 4)])
+def test_attention_tc5_variants(P, T, n_sel, n_kv, opt):
+    """tcgen05 attention variants against the oracle and close to the default kernel: attn_poly (a share of
+    the softmax exponentials on the FMA pipe, degree-3 polynomial with relative error 7.5e-5) and attn_qtm
+    (Q in TMEM as the A operand of QK^T: bitwise the same products, so the same result)."""
+    s = shape("small", n_kv_heads=n_kv)
+    g = lambda st, n, H: rng.values(13, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
+    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
+    rows = np.sort(np.random.default_rng(T + 1).choice(T, n_sel, replace=False)).astype(np.int32)
+    qrow = np.arange(n_sel, dtype=np.int32)
+    ctx = P.Context(s, "bf16", max_tokens=T)
+    args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
+            to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
+    base = P.api.op_attention(ctx, *args, impl=2)
+    ctx.set_option(*opt)
+    out = P.api.op_attention(ctx, *args, impl=2)
+    pos = np.arange(T)
+    ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
+    assert rel_err(np32(out), ref) < 1e-2
+    assert rel_err(np32(out), np32(base)) < 4e-3
+
+
 @pytest.mark.parametrize("impl", [2, 4])
 @pytest.mark.parametrize("splits", [1, 2, 5, 16])
 def test_attention_tc5_split_merge(P, splits, impl):
