@@ -70,7 +70,8 @@ __device__ __forceinline__ uint32_t sw_off(int r, int ch) {
 // POLY: share of the softmax exponentials computed by ex2_poly (0: none, 1: 1 in 4, 2: 1 in 2).
 // QTM: Q lives in TMEM (columns 384..447, written by the softmax threads with tcgen05.st) and S = Q K^T
 // reads it as the A operand from tensor memory, so the QK^T MMAs read only K from shared memory.
-template <int POLY, bool QTM>
+// PK: packed fp32x2 FFMA2 / FADD2 for the exponent argument and the row sum (bitwise the same results).
+template <int POLY, bool QTM, bool PK>
 __global__ void __launch_bounds__(NT, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
@@ -313,18 +314,42 @@ __global__ void __launch_bounds__(NT, 1)
       }
       const float nref = m_used == -INFINITY ? 0.f : -m_used;
       l *= corr;
-      float rs8[8];
+      // packed fp32x2 FFMA2 / FADD2 (sm_100) halve the FMA-pipe issue slots of the scale and the row sum;
+      // accumulator j of rs2 holds elements 8m + 2j (.x) and 8m + 2j + 1 (.y), the same partition and
+      // order as eight scalar accumulators indexed by element % 8
+      const float2 sc2 = make_float2(scale_log2, scale_log2), nr2 = make_float2(nref, nref);
+      float2 rs2[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) rs8[i] = 0.f;
+      for (int i = 0; i < 4; ++i) rs2[i] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float xa = fmaf(s[i], scale_log2, nref);
-        if constexpr (POLY == 1) s[i] = (i & 3) == 3 ? ex2_poly(xa) : ex2(xa);  // -inf -> 0 (MUFU)
-        else if constexpr (POLY == 2) s[i] = (i & 1) ? ex2_poly(xa) : ex2(xa);
-        else s[i] = ex2(xa);
-        rs8[i & 7] += s[i];
+      for (int i = 0; i < 32; ++i) {
+        float2 xa;
+        if constexpr (PK) {
+          xa = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nr2);
+        } else {
+          xa.x = fmaf(s[2 * i], scale_log2, nref);
+          xa.y = fmaf(s[2 * i + 1], scale_log2, nref);
+        }
+        if constexpr (POLY == 1) {
+          xa.x = ex2(xa.x);
+          xa.y = (i & 1) ? ex2_poly(xa.y) : ex2(xa.y);  // -inf -> 0 (MUFU)
+        } else if constexpr (POLY == 2) {
+          xa.x = ex2(xa.x);
+          xa.y = ex2_poly(xa.y);
+        } else {
+          xa.x = ex2(xa.x);
+          xa.y = ex2(xa.y);
+        }
+        s[2 * i] = xa.x;
+        s[2 * i + 1] = xa.y;
+        if constexpr (PK) {
+          rs2[i & 3] = __fadd2_rn(rs2[i & 3], xa);
+        } else {
+          rs2[i & 3].x += xa.x;
+          rs2[i & 3].y += xa.y;
+        }
       }
-      l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      l += ((rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y)) + ((rs2[2].x + rs2[2].y) + (rs2[3].x + rs2[3].y));
       // rescale O only when the reference max moved; PV_{t-1} must be complete (O stable)
       if (t >= 1 && __any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write
         tc::mbar_wait(pv_done, (t - 1) & 1);
@@ -501,9 +526,10 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   CB_TRY(kv_tmap(c, v, n_keys, &tv));
   dim3 grid(tiles * n_splits * n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
-  auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, false>
-            : c->attn_poly == 1 ? attn_tc5_kernel<1, false>
-            : c->attn_qtm ? attn_tc5_kernel<0, true> : attn_tc5_kernel<0, false>;
+  auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, true, true>
+            : c->attn_poly == 1 ? attn_tc5_kernel<1, true, true>
+            : !c->attn_qtm ? attn_tc5_kernel<0, false, true>
+            : c->attn_nopk ? attn_tc5_kernel<0, true, false> : attn_tc5_kernel<0, true, true>;
   CB_LAUNCH(c, kern, grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
                                          c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
                                          c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr);
@@ -520,9 +546,10 @@ cb_status attention_tc5_init() {
     g_encode5 = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (g_kvmaps == nullptr) g_kvmaps = new std::unordered_map<KvKey, CUtensorMap, KvKeyHash>();
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   return CB_OK;
 }

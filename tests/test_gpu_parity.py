@@ -260,7 +260,7 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     assert rel_err(np32(out), ref) < 1e-2
 
 
-@pytest.mark.parametrize("opt", [("attn_poly", 1), ("attn_poly", 2), ("attn_qtm", 1)])
+@pytest.mark.parametrize("opt", [("attn_poly", 1), ("attn_poly", 2), ("attn_qtm", 0), ("attn_packed", 0)])
 @pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (4100, 900, 4)])
 def test_attention_tc5_variants(P, T, n_sel, n_kv, opt):
     """tcgen05 attention variants against the oracle and close to the default kernel: attn_poly (a share of
