@@ -31,11 +31,14 @@
 #include "tc_common.cuh"
 
 namespace {
-constexpr int HD = 128, BM = 128, BC = 128, NT = 320;
+constexpr int HD = 128, BM = 128, BC = 128;
+// NWG softmax warpgroups: thread = (query row, KW = 128 / NWG keys of the tile, the same KW O columns)
+template <int NWG> constexpr int nt_of() { return 64 + 128 * NWG; }
+template <int NWG> constexpr int smem_of() { return 6 * (2 * 128 * 128) + 1024 + 256 + (3 * NWG + 1) * 128 * 4 + 64; }
 constexpr int ATOM = 128 * 128;    // 128 rows x 128 B (64 bf16): one SWIZZLE_128B column block
 constexpr int TILE = 2 * ATOM;     // 128 rows x 128 bf16
 constexpr int KST = 3;            // K ring stages (V: 2); P lives in TMEM, so SMEM = Q + 3 K + 2 V
-constexpr int SMEM = 6 * TILE + 1024 + 256 + 3072;  // + alignment + barriers + exchange
+constexpr int SMEM = smem_of<4>();  // + alignment + barriers + exchange (xmax [2][NWG][128], l [NWG][128], flag)
 constexpr float RESCALE_THRESHOLD = 8.0f;    // log2 units
 constexpr uint32_t QCOL = 384;               // TMEM columns of Q (QTM): 64 x 32-bit = 128 bf16 per row
 
@@ -62,6 +65,19 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// N consecutive 32-bit TMEM columns of this thread's lane (N = 16 or 32; no wait)
+template <int N>
+__device__ __forceinline__ void tmem_st_words(uint32_t taddr, const uint32_t (&w)[N]) {
+  if constexpr (N == 32) {
+    tc::tmem_st32u(taddr, w);
+  } else {
+    static_assert(N == 16, "16 or 32 columns");
+    float f[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(w[i]);
+    tc::tmem_st16(taddr, f);
+  }
+}
 // byte offset of 16-B chunk `ch` (0..15) of row `r` in a [2 atoms][128 rows][128 B] swizzled tile
 __device__ __forceinline__ uint32_t sw_off(int r, int ch) {
   return (uint32_t)((ch >> 3) * ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
@@ -71,8 +87,10 @@ __device__ __forceinline__ uint32_t sw_off(int r, int ch) {
 // QTM: Q lives in TMEM (columns 384..447, written by the softmax threads with tcgen05.st) and S = Q K^T
 // reads it as the A operand from tensor memory, so the QK^T MMAs read only K from shared memory.
 // PK: packed fp32x2 FFMA2 / FADD2 for the exponent argument and the row sum (bitwise the same results).
-template <int POLY, bool QTM, bool PK>
-__global__ void __launch_bounds__(NT, 1)
+// NWG: softmax warpgroups (2: 64 keys per thread; 4: 32 keys per thread, twice the warps per SMSP to
+// hide the softmax's dependency latencies).
+template <int POLY, bool QTM, bool PK, int NWG>
+__global__ void __launch_bounds__(nt_of<NWG>(), 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
                     int n_rows, int n_keys, bf16* __restrict__ out, int n_q, int n_kv, float scale_log2,
@@ -141,8 +159,8 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_init(&v_empty[b], 1);
       tc::mbar_init(&s_full[b], 1);
     }
-    tc::mbar_init(q_full, 256);
-    tc::mbar_init(p_full, 8);
+    tc::mbar_init(q_full, 128 * NWG);
+    tc::mbar_init(p_full, 4 * NWG);
     tc::mbar_init(pv_done, 1);
     tc::fence_barrier_init();
   }
@@ -219,7 +237,8 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int kk = 0; kk < BC / 16; ++kk) {  // 16 keys per step; P in TMEM (keys 0-63 at columns
           // 0-31 of the S buffer, keys 64-127 at columns 64-95: each softmax half over its own S)
-          const uint32_t a = tmem + b * 128 + (kk < 4 ? 8 * kk : 64 + 8 * (kk - 4));
+          constexpr int KWc = BC / NWG;  // keys per softmax group: P of group q at columns q * KWc ..
+          const uint32_t a = tmem + b * 128 + (kk * 16 / KWc) * KWc + ((kk * 16) % KWc) / 2;
           const uint64_t bd = tc::sdesc_sw128_mn(sV + b * TILE + kk * 2048, ATOM);
           tc::mma_bf16_ts(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
         }
@@ -233,23 +252,24 @@ __global__ void __launch_bounds__(NT, 1)
     // (thread = (row, half)); the halves agree on the row max through shared memory every tile =====
     const int wg = (warp - 2) >> 2;              // 0: keys / O columns 0..63, 1: 64..127
     const int r = (warp & 3) * 32 + lane;
-    const int et = threadIdx.x - 64;             // 0..255 among softmax threads
+    constexpr int KW = BC / NWG, OW = HD / NWG, NSM = 128 * NWG;
+    const int et = threadIdx.x - 64;             // 0..NSM-1 among softmax threads
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int rho = rho0 + r;
     const bool valid = rho < R;
     const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
     const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
-    float* xmax = reinterpret_cast<float*>(bars + 16);  // [2 parity][2 wg][128 rows], then l [2][128]
-    float* xl = xmax + 512;
-    if constexpr (QTM) {  // this row's half of Q (64 bf16) -> TMEM columns QCOL + wg * 32 .. + 31
-      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD + wg * 64);
-      uint32_t pk[32];
+    float* xmax = reinterpret_cast<float*>(bars + 16);  // [2 parity][NWG][128 rows], then l [NWG][128]
+    float* xl = xmax + 2 * NWG * 128;
+    if constexpr (QTM) {  // this row's KW elements of Q -> TMEM columns QCOL + wg * KW / 2 ..
+      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD + wg * KW);
+      uint32_t pk[KW / 2];
 #pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
+      for (int c8 = 0; c8 < KW / 8; ++c8) {
         const uint4 u = valid ? __ldg(src + c8) : make_uint4(0u, 0u, 0u, 0u);
         pk[4 * c8] = u.x; pk[4 * c8 + 1] = u.y; pk[4 * c8 + 2] = u.z; pk[4 * c8 + 3] = u.w;
       }
-      tc::tmem_st32u(tmem + lane_base + QCOL + wg * 32, pk);
+      tmem_st_words<KW / 2>(tmem + lane_base + QCOL + wg * (KW / 2), pk);
       tc::tmem_st_wait();
       tc::fence_before();
       tc::mbar_arrive(q_full);
@@ -257,8 +277,8 @@ __global__ void __launch_bounds__(NT, 1)
       const bf16* src = q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD;
       const uint32_t dq = tc::smem_u32(sQ);
 #pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        const int ch = wg * 8 + c8;
+      for (int c8 = 0; c8 < KW / 8; ++c8) {
+        const int ch = wg * (KW / 8) + c8;
         const int sz = valid ? 16 : 0;
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dq + sw_off(r, ch)), "l"(src + ch * 8),
                      "r"(sz)
@@ -275,35 +295,38 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_wait(&s_full[b], (t >> 1) & 1);
       if (et == 0) DBG(800 + 4 * t);
       tc::fence_after();
-      float s[64];
+      float s[KW];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < KW / 32; ++c) {
         float x[32];
-        tc::tmem_ld32(tmem + lane_base + b * 128 + wg * 64 + c * 32, x);
+        tc::tmem_ld32(tmem + lane_base + b * 128 + wg * KW + c * 32, x);
 #pragma unroll
         for (int i = 0; i < 32; ++i) s[c * 32 + i] = x[i];
       }
-      const int key0 = (jb + t) * BC + wg * 64;
-      const bool need_mask = key0 + 63 > kmin;
+      const int key0 = (jb + t) * BC + wg * KW;
+      const bool need_mask = key0 + KW - 1 > kmin;
       // half-row max of the raw scores (scale > 0 commutes with max); 8 chains for ILP
       float mx8[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
       if (need_mask) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < KW; ++i) {
           if (key0 + i > tok) s[i] = -INFINITY;
           mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < 64; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+        for (int i = 0; i < KW; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
       }
       const float hmx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      xmax[(b * 2 + wg) * 128 + r] = hmx;
-      named_bar_sync(1, 256);
-      const float mx = fmaxf(hmx, xmax[(b * 2 + (wg ^ 1)) * 128 + r]) * scale_log2;
+      xmax[(b * NWG + wg) * 128 + r] = hmx;
+      named_bar_sync(1, NSM);
+      float mxall = hmx;
+#pragma unroll
+      for (int j = 0; j < NWG; ++j) mxall = fmaxf(mxall, xmax[(b * NWG + j) * 128 + r]);  // exact, any order
+      const float mx = mxall * scale_log2;
       if (et == 0) DBG(800 + 4 * t + 1);
       // lazy rescale (identical decision in both halves): move the reference max only when it grew
       // by more than 2^8
@@ -322,7 +345,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int i = 0; i < 4; ++i) rs2[i] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < KW / 2; ++i) {
         float2 xa;
         if constexpr (PK) {
           xa = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nr2);
@@ -356,19 +379,19 @@ __global__ void __launch_bounds__(NT, 1)
         if (et == 0) DBG(800 + 4 * t + 2);
         tc::fence_after();
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < OW / 32; ++c) {
           float o[32];
-          tc::tmem_ld32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
+          tc::tmem_ld32(tmem + lane_base + 256 + wg * OW + c * 32, o);
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] *= corr;
-          tc::tmem_st32(tmem + lane_base + 256 + wg * 64 + c * 32, o);
+          tc::tmem_st32(tmem + lane_base + 256 + wg * OW + c * 32, o);
         }
       }
-      {  // P (bf16 pairs) over this half's own S columns: keys wg*64 .. +63 -> columns b*128 + wg*64 ..
-        uint32_t pk[32];
+      {  // P (bf16 pairs) over this group's own S columns: keys wg*KW .. -> columns b*128 + wg*KW ..
+        uint32_t pk[KW / 2];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = pack2(s[2 * i], s[2 * i + 1]);
-        tc::tmem_st32u(tmem + lane_base + b * 128 + wg * 64, pk);
+        for (int i = 0; i < KW / 2; ++i) pk[i] = pack2(s[2 * i], s[2 * i + 1]);
+        tmem_st_words<KW / 2>(tmem + lane_base + b * 128 + wg * KW, pk);
       }
       tc::tmem_st_wait();
       tc::fence_before();
@@ -376,38 +399,42 @@ __global__ void __launch_bounds__(NT, 1)
       if (lane == 0) tc::mbar_arrive(p_full);
       if (et == 0) DBG(800 + 4 * t + 3);
     }
-    // total row sum = both halves (same reference max)
+    // total row sum = all groups (same reference max), in group order
     xl[wg * 128 + r] = l;
-    named_bar_sync(1, 256);
-    l += xl[(wg ^ 1) * 128 + r];
+    named_bar_sync(1, NSM);
+    if constexpr (NWG == 2) {
+      l = xl[r] + xl[128 + r];
+    } else {
+      l = (xl[r] + xl[128 + r]) + (xl[256 + r] + xl[384 + r]);
+    }
     tc::mbar_wait(pv_done, (nt - 1) & 1);
     tc::fence_after();
-    float o[64];
+    float o[OW];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < OW / 32; ++c) {
       float x[32];
-      tc::tmem_ld32(tmem + lane_base + 256 + wg * 64 + c * 32, x);
+      tc::tmem_ld32(tmem + lane_base + 256 + wg * OW + c * 32, x);
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[c * 32 + i] = x[i];
     }
     bool write_out = !partial;
     if (partial) {
       if (valid) {
-        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD + wg * 64);
+        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD + wg * OW);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        for (int i = 0; i < OW / 4; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
         if (wg == 0) ml[part_row0 + rho] = make_float2(m_used, l);
       }
       __threadfence();  // partials visible device-wide before the arrival is counted
-      named_bar_sync(1, 256);
-      int* flag = reinterpret_cast<int*>(xl + 256);
+      named_bar_sync(1, NSM);
+      int* flag = reinterpret_cast<int*>(xl + NWG * 128);
       if (et == 0) {
         const int old = atomicAdd(tile_cnt + (size_t)tile * n_kv + g, 1);
         const int last = old == n_active - 1;
         if (last) tile_cnt[(size_t)tile * n_kv + g] = 0;  // reset for the next launch
         *flag = last;
       }
-      named_bar_sync(1, 256);
+      named_bar_sync(1, NSM);
       write_out = *flag != 0;
       if (write_out) {  // last arrival: merge every range's partial in split order
         __threadfence();
@@ -416,16 +443,16 @@ __global__ void __launch_bounds__(NT, 1)
           if (valid) mstar = fmaxf(mstar, __ldcg(&ml[((size_t)sp * n_kv + g) * R + rho].x));
         float lt = 0.f;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) o[i] = 0.f;
+        for (int i = 0; i < OW; ++i) o[i] = 0.f;
         for (int sp = 0; sp < n_active && valid; ++sp) {
           const size_t prow = ((size_t)sp * n_kv + g) * R + rho;
           const float2 ms = __ldcg(&ml[prow]);
           if (ms.x == -INFINITY) continue;
           const float f = ex2(ms.x - mstar);
           lt += ms.y * f;
-          const float4* src = reinterpret_cast<const float4*>(opart + prow * HD + wg * 64);
+          const float4* src = reinterpret_cast<const float4*>(opart + prow * HD + wg * OW);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < OW / 4; ++i) {
             const float4 x = __ldcg(src + i);
             o[4 * i] += x.x * f; o[4 * i + 1] += x.y * f; o[4 * i + 2] += x.z * f; o[4 * i + 3] += x.w * f;
           }
@@ -435,9 +462,9 @@ __global__ void __launch_bounds__(NT, 1)
     }
     if (valid && write_out) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD + wg * 64);
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD + wg * OW);
 #pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
+      for (int c8 = 0; c8 < OW / 8; ++c8) {
         uint4 w;
         w.x = pack2(o[c8 * 8 + 0] * inv, o[c8 * 8 + 1] * inv);
         w.y = pack2(o[c8 * 8 + 2] * inv, o[c8 * 8 + 3] * inv);
@@ -526,11 +553,13 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   CB_TRY(kv_tmap(c, v, n_keys, &tv));
   dim3 grid(tiles * n_splits * n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
-  auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, true, true>
-            : c->attn_poly == 1 ? attn_tc5_kernel<1, true, true>
-            : !c->attn_qtm ? attn_tc5_kernel<0, false, true>
-            : c->attn_nopk ? attn_tc5_kernel<0, true, false> : attn_tc5_kernel<0, true, true>;
-  CB_LAUNCH(c, kern, grid, NT, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
+  auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, true, true, 2>
+            : c->attn_poly == 1 ? attn_tc5_kernel<1, true, true, 2>
+            : !c->attn_qtm ? attn_tc5_kernel<0, false, true, 2>
+            : c->attn_nopk ? attn_tc5_kernel<0, true, false, 2>
+            : c->attn_wg4 ? attn_tc5_kernel<0, true, true, 4> : attn_tc5_kernel<0, true, true, 2>;
+  const int nthreads = c->attn_wg4 && !c->attn_poly && c->attn_qtm && !c->attn_nopk ? nt_of<4>() : nt_of<2>();
+  CB_LAUNCH(c, kern, grid, nthreads, SMEM, s, tk, tv, (const bf16*)q, q_row, q_tok, n_rows, n_keys, (bf16*)out,
                                          c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
                                          c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
@@ -546,10 +575,11 @@ cb_status attention_tc5_init() {
     g_encode5 = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (g_kvmaps == nullptr) g_kvmaps = new std::unordered_map<KvKey, CUtensorMap, KvKeyHash>();
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   return CB_OK;
 }

@@ -423,6 +423,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     c->attn_nopk = value == 0;
     return CB_OK;
   }
+  if (std::strcmp(name, "attn_wg4") == 0) {
+    c->attn_wg4 = value != 0;
+    return CB_OK;
+  }
   if (std::strcmp(name, "attn_qtm") == 0) {
     c->attn_qtm = value != 0;
     return CB_OK;

@@ -63,6 +63,7 @@ struct cb_ctx {
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
   int attn_nopk;    // cb_set_option("attn_packed", 0): scalar FFMA/FADD in the softmax (A/B of FFMA2/FADD2)
+  int attn_wg4;     // cb_set_option("attn_wg4"): four softmax warpgroups (32 keys per thread) instead of two
   int attn_qtm;     // cb_set_option("attn_qtm"): Q in TMEM as the QK^T A operand (tcgen05 attention)
   int attn_poly;    // cb_set_option("attn_poly"): share of softmax exp2 on the FMA pipe (0, 1 = 1/4, 2 = 1/2)
   int no_fuse_norm;  // cb_set_option("fuse_norm", 0): separate RMSNorm kernels between the projections

@@ -260,7 +260,8 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     assert rel_err(np32(out), ref) < 1e-2
 
 
-@pytest.mark.parametrize("opt", [("attn_poly", 1), ("attn_poly", 2), ("attn_qtm", 0), ("attn_packed", 0)])
+@pytest.mark.parametrize("opt", [("attn_poly", 1), ("attn_poly", 2), ("attn_qtm", 0), ("attn_packed", 0), ("attn_wg4", 1),
+                                 ("attn_wg4", 0)])
 @pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (4100, 900, 4)])
 def test_attention_tc5_variants(P, T, n_sel, n_kv, opt):
     """tcgen05 attention variants against the oracle and close to the default kernel: attn_poly (a share of
@@ -281,6 +282,28 @@ def test_attention_tc5_variants(P, T, n_sel, n_kv, opt):
     ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
     assert rel_err(np32(out), ref) < 1e-2
     assert rel_err(np32(out), np32(base)) < 4e-3
+
+
+@pytest.mark.parametrize("wg4", [0, 1])
+@pytest.mark.parametrize("splits", [2, 5])
+def test_attention_tc5_softmax_groups_split(P, splits, wg4):
+    """Two or four softmax warpgroups, with forced split-KV and the in-kernel merge: oracle tolerance and
+    bitwise reproducible across launches."""
+    s = shape("small", n_kv_heads=2)
+    T, n_sel = 3072, 460
+    g = lambda st, n, H: rng.values(14, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
+    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
+    rows = np.sort(np.random.default_rng(5).choice(T, n_sel, replace=False)).astype(np.int32)
+    ctx = P.Context(s, "bf16", max_tokens=T)
+    ctx.set_option("attn_wg4", wg4)
+    ctx.set_option("attn_splits", splits)
+    args = (to_dev(q[rows], torch.bfloat16), to_dev(np.arange(n_sel, dtype=np.int32), torch.int32),
+            to_dev(rows, torch.int32), to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
+    out = P.api.op_attention(ctx, *args, impl=2)
+    pos = np.arange(T)
+    assert rel_err(np32(out), O.causal_attention(q[rows], pos[rows], k, v, pos)) < 1e-2
+    for _ in range(2):
+        assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
 
 
 @pytest.mark.parametrize("impl", [2, 4])
