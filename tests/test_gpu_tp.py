@@ -222,3 +222,47 @@ def test_tp_argument_errors(P):
     ctx2 = P.Context(s, "f32", max_tokens=64)
     with pytest.raises(P.CacheBlendError):  # rank taken
         ctx2.set_comm_local(g, 0)
+
+
+def test_tp_request_path_equals_forward(P):
+    """The host-buffer request path (cb_blend_request: layer-pipelined copies on each rank's copy stream)
+    under the loopback head-parallel group gives every rank exactly its cb_blend_forward result."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _case("small", 7, [96, 130, 64], 0, "bf16", 0.15)
+    world = 2
+    ref = run_blend_tp(P, s, "bf16", 7, req, tok, pos, cs, Kc, Vc, ks, world)
+    ranks = ref["ranks"]
+    td = P.api.TORCH_DTYPES["bf16"]
+    L, T = s.n_layers, req.n_total
+    toks = torch.from_numpy(tok.astype(np.int32)).pin_memory()
+    poss = torch.from_numpy(pos.astype(np.int32)).pin_memory()
+    outs, errors = [], [None] * world
+    for r, x in enumerate(ranks):
+        kh = D.shard_kv(torch.from_numpy(np.ascontiguousarray(Kc)).to(td), s, r, world).pin_memory()
+        vh = D.shard_kv(torch.from_numpy(np.ascontiguousarray(Vc)).to(td), s, r, world).pin_memory()
+        kb, vb = torch.empty_like(x["kb"]), torch.empty_like(x["vb"])
+        hh = torch.empty(ks[-1], s.d_model, dtype=torch.float32).pin_memory()
+        outs.append((kh, vh, kb, vb, hh))
+    torch.cuda.synchronize()
+
+    def work(r):
+        kh, vh, kb, vb, hh = outs[r]
+        try:
+            P.api.blend_request(ranks[r]["ctx"], ranks[r]["mw"], toks, poss, list(cs), 0, kh, vh, kb, vb, ks, hh,
+                                stream=ranks[r]["stream"])
+            ranks[r]["stream"].synchronize()
+        except Exception as e:
+            errors[r] = e
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert all(not t.is_alive() for t in th)
+    for e in errors:
+        if e is not None:
+            raise e
+    for r, x in enumerate(ranks):
+        _, _, kb, vb, hh = outs[r]
+        assert torch.equal(kb, x["kb"]) and torch.equal(vb, x["vb"])
+        np.testing.assert_array_equal(hh.numpy(), np32(x["h"][:ks[-1]]))
