@@ -745,8 +745,10 @@ cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, c
 
 // Layer 0, the full layer (R2): every row is a query; context rows keep the realigned cache
 // (P:1750), suffix rows write fresh K,V.
+// before_kv (request mode): runs after the projections, before anything reads this layer's cached K/V
+// (the fetch of layer 0's chunk KV then overlaps the embedding and the Q projection).
 cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, int n_suf, void* kb, void* vb,
-                     const int* pos, cudaStream_t s) {
+                     const int* pos, cudaStream_t s, const std::function<cb_status()>& before_kv = nullptr) {
   const cb_model& m = c->m;
   const int T = N + n_suf, d = m.d_model, qd = m.n_q_heads * m.head_dim, kvd = m.n_kv_heads * m.head_dim;
   const size_t B = dtype_bytes(m.dtype);
@@ -766,6 +768,7 @@ cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, 
     CB_TRY(launch_gemm(c, (const char*)c->x + (size_t)N * d * B, d, (const char*)w.w_qkv + (size_t)qd * d * B, d,
                        n_suf, d, ek, 0, s));
   }
+  if (before_kv) CB_TRY(before_kv());
   CB_TRY(launch_attention(c, c->q, c->iota, b.row_tok, T, kb, vb, T, c->attn, 0, s));
   return mlp_block(c, w, b, T, nullptr, s);
 }
@@ -912,13 +915,12 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
   const bool embed_norm = !c->no_fuse_norm;
   if (embed_norm) CB_TRY(launch_embed_norm(c, embed, tok, (const float*)w[0].attn_norm, T, c->h[0], c->x, s));
   else CB_TRY(launch_embed(c, embed, tok, T, c->h[0], s));
-  CB_TRY(realign_layer(0));
   bool ready = false;  // the previous down projection prepared this layer's attention RMSNorm
   LayerBufs b0{c->h[0], c->h[1], c->iota, nullptr};
   b0.x_normed = embed_norm;
   b0.next_attn_norm = L > 1 ? w[1].attn_norm : nullptr;
   b0.next_ready = &ready;
-  CB_TRY(layer_full(c, w[0], b0, N, n_suffix, k_blend, v_blend, pos, s));
+  CB_TRY(layer_full(c, w[0], b0, N, n_suffix, k_blend, v_blend, pos, s, [&]() { return realign_layer(0); }));
   if (sel_out) CB_TRY(launch_sel_out(c, c->iota, N, N, sel_out, s));
   // (a3-a8) layers 1..L-1 with gradual filtering: C_1 = all context tokens, C_{i+1} = S_i
   int cur = 1, n_cand = N, rt = 0;
