@@ -70,6 +70,22 @@ def rope_rotate(x: np.ndarray, m: np.ndarray, base: float) -> np.ndarray:
     return out
 
 
+def rope_rotate_half(x: np.ndarray, m: np.ndarray, base: float) -> np.ndarray:
+    """The half-split RoPE convention of common checkpoints (SURVEY §8(c) R9 "the half-split variant";
+    N3 real-checkpoint loading): the pair (x[i], x[i + d/2]) is rotated by m theta_i, i.e.
+    y = x cos + rotate_half(x) sin with rotate_half([a, b]) = [-b, a] over the two halves. Test
+    reference for the loader-side conversion to the paper's interleaved pairing (R9)."""
+    x = np.asarray(x, dtype=F64)
+    d = x.shape[-1]
+    th = rope_thetas(d, base)
+    m = np.asarray(m, dtype=F64)
+    m = m.reshape(m.shape + (1,) * (x.ndim - 1 - m.ndim))
+    ang = m[..., None] * th
+    c, s = np.cos(ang), np.sin(ang)
+    a, b = x[..., : d // 2], x[..., d // 2:]
+    return np.concatenate([c * a - s * b, s * a + c * b], axis=-1)
+
+
 def realign(k_cached: np.ndarray, src_pos: np.ndarray, dst_pos: np.ndarray, base: float) -> np.ndarray:
     """Positional recovery (footnote P:208-211): K_hat[t] = R(dst_t - src_t) K_cached[t].
 

@@ -120,3 +120,44 @@ def broadcast_bytes(payload: bytes, src: int = 0) -> bytes:
     obj = [payload if dist.get_rank() == src else None]
     dist.broadcast_object_list(obj, src=src)
     return obj[0]
+
+
+# ---- half-split RoPE checkpoints ----------------------------------------------
+# The library rotates interleaved pairs (2i, 2i+1) as the paper's appendix does. Checkpoints and
+# engines that rotate half-split pairs (i, i + hd/2) are converted at load time, not in the kernels: with
+# perm[2i] = i, perm[2i+1] = i + hd/2, interleaved RoPE of z[perm] equals (half-split RoPE of z)[perm], so
+# permuting the q and k rows of W_qkv inside each head, and the head dims of a cached K, makes every kernel
+# compute the permuted half-split result. Attention scores (q . k), the KV deviation (an L2 norm) and V are
+# unchanged by the common permutation; the blended K is handed back with the inverse permutation.
+def rope_interleave_perm(head_dim: int):
+    import numpy as np
+    h = head_dim // 2
+    p = np.empty(head_dim, dtype=np.int64)
+    p[0::2] = np.arange(h)
+    p[1::2] = np.arange(h) + h
+    return p
+
+
+def interleave_rope_weights(w_qkv, shape):
+    """W_qkv [(n_q + 2 n_kv) hd][d] of a half-split checkpoint -> the library's interleaved layout (q and k
+    head rows permuted, v rows untouched). Works for numpy arrays and torch tensors."""
+    hd = shape.head_dim
+    p = rope_interleave_perm(hd)
+    n_rot = shape.n_q_heads + shape.n_kv_heads  # q heads then k heads carry RoPE
+    idx = [h * hd + p for h in range(n_rot)]
+    import numpy as np
+    rows = np.concatenate(idx + [np.arange(n_rot * hd, w_qkv.shape[0])])
+    if isinstance(w_qkv, torch.Tensor):
+        return w_qkv[torch.from_numpy(rows).to(w_qkv.device)].contiguous()
+    return np.ascontiguousarray(w_qkv[rows])
+
+
+def interleave_rope_cache(k, inverse: bool = False):
+    """Cached K [..., head_dim] of a half-split engine -> interleaved order (inverse=True: back)."""
+    import numpy as np
+    p = rope_interleave_perm(k.shape[-1])
+    if inverse:
+        p = np.argsort(p)
+    if isinstance(k, torch.Tensor):
+        return k[..., torch.from_numpy(p).to(k.device)].contiguous()
+    return np.ascontiguousarray(k[..., p])

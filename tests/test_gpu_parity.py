@@ -539,3 +539,27 @@ def test_blend_request_store_equals_forward(P, name, dtype, n_suf):
     assert store.keys()[:len(keys)] == list(reversed(keys))  # fetched chunks refreshed, last chunk first
     st = store.stats()
     assert st["misses"] == 1 and st["hits"] >= len(keys)
+
+
+# ---- half-split RoPE checkpoints through the loader conversion -------------------
+def test_blend_half_split_rope_checkpoint(P, monkeypatch):
+    """A model and chunk caches in the half-split RoPE convention (the oracle rotates (i, i + hd/2) pairs
+    everywhere), converted at load time by dist.interleave_rope_weights / interleave_rope_cache, blended by
+    the unchanged kernels: the de-permuted K, V and h match the half-split oracle (fp32, replay)."""
+    from paper_2405_16444_b200 import dist as D
+    monkeypatch.setattr(O, "rope_rotate", O.rope_rotate_half)
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("tiny", 9, [40, 24, 32], 3, "f32", 0.25, n_layers=3)
+    ora = O.blend_forward(m, tok, pos, cs, req.n_suffix, Kc, Vc, ks)
+    layers = []
+    for i in range(s.n_layers):
+        w = W.layer_weights(s, i, 9, "f32")
+        qkv = D.interleave_rope_weights(np.concatenate([w["wq"], w["wk"], w["wv"]], 0), s)
+        w = dict(w, wq=qkv[:s.qd], wk=qkv[s.qd:s.qd + s.kvd], wv=qkv[s.qd + s.kvd:])
+        layers.append(w)
+    mw = P.ModelWeights.from_host(s, "f32", W.embed_weights(s, 9, "f32"), layers, DEV)
+    res = run_blend(P, s, "f32", 9, req, tok, pos, cs, D.interleave_rope_cache(Kc), Vc, ks, force_sel=ora.sel, mw=mw)
+    K = D.interleave_rope_cache(res["K"], inverse=True)
+    for i in range(s.n_layers):
+        assert rel_err(K[i], ora.K[i]) < TOL["f32"], f"K layer {i}"
+        assert rel_err(res["V"][i], ora.V[i]) < TOL["f32"], f"V layer {i}"
+    assert rel_err(res["h"], ora.h_final) < TOL["f32"]

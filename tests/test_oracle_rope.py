@@ -78,3 +78,45 @@ def test_realign_preserves_within_chunk_scores():
     k_re = O.realign(O.rope_rotate(k, p0, 10000.0), p0, p0 + D, 10000.0)
     s1 = O.rope_rotate(q, p0 + D, 10000.0) @ k_re.T
     np.testing.assert_allclose(s1, s0, atol=1e-9)
+
+
+# ---- half-split RoPE (R9 variant; N3 loader conversion) ------------------------------------------------------
+def test_rope_half_hand_values_and_invariants():
+    # hd = 4, position 1: the pair (x0, x2) turns by theta_0 = 1 rad, (x1, x3) by theta_1 = base^(-1/2)
+    y = O.rope_rotate_half(np.array([1.0, 0.0, 0.0, 0.0]), np.array(1.0), 10000.0)
+    np.testing.assert_allclose(y, [np.cos(1.0), 0.0, np.sin(1.0), 0.0], atol=1e-15)
+    y = O.rope_rotate_half(np.array([0.0, 1.0, 0.0, 0.0]), np.array(2.0), 10000.0)
+    np.testing.assert_allclose(y, [0.0, np.cos(0.02), 0.0, np.sin(0.02)], atol=1e-15)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((50, 8))
+    # hd = 2: one pair, both conventions are the same rotation
+    np.testing.assert_allclose(O.rope_rotate_half(x[:, :2], np.arange(50), 1e4), O.rope_rotate(x[:, :2], np.arange(50), 1e4))
+    # norm preserved; q.k depends only on the position difference
+    yq = O.rope_rotate_half(x, np.arange(50), 1e4)
+    np.testing.assert_allclose(np.linalg.norm(yq, axis=1), np.linalg.norm(x, axis=1), rtol=1e-13)
+    q, k = rng.standard_normal(8), rng.standard_normal(8)
+    d1 = O.rope_rotate_half(q, np.array(17.0), 1e4) @ O.rope_rotate_half(k, np.array(5.0), 1e4)
+    d2 = O.rope_rotate_half(q, np.array(112.0), 1e4) @ O.rope_rotate_half(k, np.array(100.0), 1e4)
+    assert abs(d1 - d2) < 1e-12
+
+
+def test_half_split_conversion_identity():
+    """Loader conversion (paper_2405_16444_b200.dist): interleaved RoPE of the permuted projection equals the
+    permuted half-split RoPE, and the inverse cache permutation restores the half-split order."""
+    from paper_2405_16444_b200 import dist as D
+    from synth import workload as W
+    rng = np.random.default_rng(4)
+    s = W.MODELS["tiny"]
+    w = rng.standard_normal((s.qd + 2 * s.kvd, s.d_model))
+    x = rng.standard_normal((9, s.d_model))
+    pos = np.arange(9) + 30
+    wp = D.interleave_rope_weights(w, s)
+    z, zp = x @ w.T, x @ wp.T
+    np.testing.assert_array_equal(zp[:, s.qd + s.kvd:], z[:, s.qd + s.kvd:])        # v rows untouched
+    for h in range(s.n_q_heads + s.n_kv_heads):
+        sl = slice(h * s.head_dim, (h + 1) * s.head_dim)
+        half = O.rope_rotate_half(z[:, sl], pos, s.rope_theta)
+        inter = O.rope_rotate(zp[:, sl], pos, s.rope_theta)
+        np.testing.assert_allclose(D.interleave_rope_cache(inter, inverse=True), half, atol=1e-12)
+    k = rng.standard_normal((3, 5, s.head_dim))
+    np.testing.assert_array_equal(D.interleave_rope_cache(D.interleave_rope_cache(k), inverse=True), k)
