@@ -272,6 +272,18 @@ CB_API cb_status cb_set_comm(cb_ctx* ctx, const void* uid, int32_t rank, int32_t
 CB_API cb_status cb_group_create(int32_t world, cb_group** out);
 CB_API cb_status cb_group_destroy(cb_group* group);
 CB_API cb_status cb_set_comm_local(cb_ctx* ctx, cb_group* group, int32_t rank);
+/* NVLink peer-memory collectives in place of the NCCL / loopback-event calls (after cb_set_comm or
+ * cb_set_comm_local, before the first blend): the rank's residual stream, gathered Delta_kv partials and
+ * barrier flags move into one exchange block with the same layout on every rank; each collective is one
+ * small kernel that raises/waits flags in every peer's block (system-scope release/acquire), sums its slice of
+ * the buffer over all ranks in rank order (the same bits as the event path) and writes the sum into every
+ * rank's block, then waits until every rank has finished. Graph-capturable (device-side sequence numbers).
+ * One process per GPU: exchange cb_tp_ipc_handle (64 host bytes per rank, e.g. all-gathered with
+ * torch.distributed) and call cb_tp_ipc_open with the world's handles in rank order. Loopback group: the
+ * members' blocks are used directly (every member must enable it). */
+CB_API cb_status cb_tp_p2p_enable(cb_ctx* ctx);
+CB_API cb_status cb_tp_ipc_handle(cb_ctx* ctx, void* handle_out_64B);
+CB_API cb_status cb_tp_ipc_open(cb_ctx* ctx, const void* handles_world_x_64B);
 
 #ifdef __cplusplus
 }

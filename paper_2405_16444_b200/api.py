@@ -87,6 +87,23 @@ class Context:
         self.tp = (int(rank), group.world)
         self._group = group  # the group must outlive the context
 
+    def enable_tp_p2p(self):
+        """NVLink peer-memory collectives (cb_tp_p2p_enable) after set_comm / set_comm_local."""
+        with torch.cuda.device(self.device):
+            check(lib().cb_tp_p2p_enable(self.handle))
+
+    def tp_ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        check(lib().cb_tp_ipc_handle(self.handle, buf))
+        return buf.raw
+
+    def tp_ipc_open(self, handles: Sequence[bytes]):
+        """handles: every rank's tp_ipc_handle() in rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        with torch.cuda.device(self.device):
+            check(lib().cb_tp_ipc_open(self.handle, buf))
+
     def info(self, name: str) -> int:
         v = ctypes.c_int64(0)
         check(lib().cb_get_info(self.handle, name.encode(), ctypes.byref(v)))

@@ -180,9 +180,13 @@ cb_status tp_alloc(cb_ctx* c) {
 }
 }  // namespace
 
+cb_status p2p_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s);
+cb_status p2p_allgather_f32(cb_ctx* c, float* buf, size_t n_per_rank, cudaStream_t s);
+
 cb_status comm_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s) {
   if (c->comm_kind == CB_COMM_NONE || n == 0) return CB_OK;
   ProfScope ps_(c, PROF_COMM, s);
+  if (c->xblock) return p2p_allreduce_f32(c, buf, n, s);
   if (c->comm_kind == CB_COMM_LOOPBACK) return loop_allreduce(c, buf, n, s);
   const NcclApi* a = nccl_api();
   CB_NCCL(a, a->allReduce(buf, buf, n, ncclFloat32, ncclSum, (ncclComm_t)c->nccl_comm, s));
@@ -192,6 +196,7 @@ cb_status comm_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s) {
 cb_status comm_allgather_f32(cb_ctx* c, float* buf, size_t n_per_rank, cudaStream_t s) {
   if (c->comm_kind == CB_COMM_NONE || n_per_rank == 0) return CB_OK;
   ProfScope ps_(c, PROF_COMM, s);
+  if (c->xblock) return p2p_allgather_f32(c, buf, n_per_rank, s);
   if (c->comm_kind == CB_COMM_LOOPBACK) return loop_allgather(c, buf, n_per_rank, s);
   const NcclApi* a = nccl_api();
   // in place: this rank's segment already sits at buf + rank * n_per_rank
@@ -208,6 +213,16 @@ void comm_destroy(cb_ctx* c) {
   if (c->comm_kind == CB_COMM_LOOPBACK && c->group) {
     std::lock_guard<std::mutex> lk(c->group->mu);
     c->group->member[c->tp_rank] = nullptr;
+  }
+  for (int j = 0; j < kMaxTp; ++j) {
+    if (c->p2p_ipc[j] && c->p2p_peer[j]) cudaIpcCloseMemHandle(c->p2p_peer[j]);
+    c->p2p_ipc[j] = false;
+    c->p2p_peer[j] = nullptr;
+  }
+  if (c->xblock) {
+    if (c->dev_gath == (float*)(c->xblock + c->x_gath_off)) c->dev_gath = nullptr;
+    cudaFree(c->xblock);
+    c->xblock = nullptr;
   }
   if (c->dev_gath) cudaFree(c->dev_gath);
   if (c->tp_scratch) cudaFree(c->tp_scratch);
@@ -304,4 +319,179 @@ extern "C" cb_status cb_set_comm_local(cb_ctx* c, cb_group* g, int32_t rank) {
   if (e != cudaSuccess) cb_set_error("cb_set_comm_local: %s", cudaGetErrorString(e));
   if (st != CB_OK) comm_destroy(c);
   return st;
+}
+
+// ---- NVLink peer-memory collectives ------------------------------------------------------------------------
+// The B200-native replacement of the NCCL calls above: every rank maps every peer's exchange
+// block (NVLink P2P over NVSwitch), and one small kernel per collective does
+//   entry barrier  -- each rank's buffer is final (stream order + PDL wait), so it raises flag[0][rank] = seq
+//                     in every peer's block (st.release.sys) and waits for all peers' flags (ld.acquire.sys);
+//   data movement  -- all-reduce: rank r owns the r-th slice of the buffer: it sums the slice over all ranks'
+//                     buffers in rank order (deterministic, the same bits as the loopback event path) and
+//                     writes the sum into every rank's buffer; all-gather: rank r pushes its segment to all;
+//   exit barrier   -- the last CTA of each rank raises flag[1][rank] = seq everywhere and waits for all, so
+//                     the kernel completes only when every rank's writes are done (nobody overwrites a buffer
+//                     a peer is still reading). seq is a device-side counter, so a CUDA graph can replay it.
+// The grid is small (64 CTAs): on one GPU (loopback test) the spinning CTAs co-reside with the other ranks'
+// GEMM CTAs instead of starving them.
+namespace {
+constexpr int P2P_CTAS = 64, P2P_THREADS = 256;
+
+__device__ __forceinline__ void st_release_sys(int* p, int v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct PeerTable { char* base[kMaxTp]; };
+
+// flags (ints at flags_off of every block): [0, kMaxTp) entry, [kMaxTp, 2 kMaxTp) exit, [2 kMaxTp] seq,
+// [2 kMaxTp + 1] finished-CTA counter
+__global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable pt, int rank, int world,
+                                                                     size_t off, long long n, int mode,
+                                                                     size_t flags_off) {
+  pdl_enter();
+  int* myf = reinterpret_cast<int*>(pt.base[rank] + flags_off);
+  __shared__ int seq_s;
+  if (threadIdx.x == 0) seq_s = *reinterpret_cast<volatile int*>(myf + 2 * kMaxTp) + 1;
+  __syncthreads();
+  const int seq = seq_s;
+  if (blockIdx.x == 0 && threadIdx.x < world) {
+    __threadfence_system();
+    st_release_sys(reinterpret_cast<int*>(pt.base[threadIdx.x] + flags_off) + rank, seq);
+  }
+  if (threadIdx.x < world)
+    while (ld_acquire_sys(myf + threadIdx.x) < seq) __nanosleep(64);
+  __syncthreads();
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (mode == 0) {  // all-reduce: this rank's slice, summed in rank order, written to every rank
+    const long long chunk = ((n + world - 1) / world + 3) / 4 * 4;
+    const long long lo = (long long)rank * chunk, hi = lo + chunk < n ? lo + chunk : n;
+    const long long lo4 = lo / 4, hi4 = hi / 4;  // lo is a multiple of 4; off is 16-B aligned
+    for (long long i = lo4 + t0; i < hi4; i += stride) {
+      float4 a = __ldcg(reinterpret_cast<const float4*>(pt.base[0] + off) + i);
+      for (int j = 1; j < world; ++j) {
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(pt.base[j] + off) + i);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      for (int j = 0; j < world; ++j) __stcg(reinterpret_cast<float4*>(pt.base[j] + off) + i, a);
+    }
+    for (long long i = hi4 * 4 + t0; i < hi; i += stride) {
+      float a = __ldcg(reinterpret_cast<const float*>(pt.base[0] + off) + i);
+      for (int j = 1; j < world; ++j) a += __ldcg(reinterpret_cast<const float*>(pt.base[j] + off) + i);
+      for (int j = 0; j < world; ++j) __stcg(reinterpret_cast<float*>(pt.base[j] + off) + i, a);
+    }
+  } else {  // all-gather: push this rank's segment of n floats to every peer
+    const float4* src = reinterpret_cast<const float4*>(pt.base[rank] + off) + (size_t)rank * (n / 4);
+    for (long long i = t0; i < n / 4; i += stride) {
+      const float4 v = __ldcg(src + i);
+      for (int j = 0; j < world; ++j)
+        if (j != rank) __stcg(reinterpret_cast<float4*>(pt.base[j] + off) + (size_t)rank * (n / 4) + i, v);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const int done = atomicAdd(myf + 2 * kMaxTp + 1, 1);
+    if (done == (int)gridDim.x - 1) {  // every CTA of this rank has written: exit barrier
+      myf[2 * kMaxTp + 1] = 0;
+      __threadfence_system();
+      for (int j = 0; j < world; ++j)
+        st_release_sys(reinterpret_cast<int*>(pt.base[j] + flags_off) + kMaxTp + rank, seq);
+      for (int j = 0; j < world; ++j)
+        while (ld_acquire_sys(myf + kMaxTp + j) < seq) __nanosleep(64);
+      *reinterpret_cast<volatile int*>(myf + 2 * kMaxTp) = seq;
+    }
+  }
+}
+
+cb_status p2p_peers(cb_ctx* c, PeerTable* pt) {
+  for (int j = 0; j < c->tp_world; ++j) {
+    char* b = c->p2p_peer[j];
+    if (b == nullptr && c->comm_kind == CB_COMM_LOOPBACK && c->group->member[j] != nullptr)
+      b = c->p2p_peer[j] = c->group->member[j]->xblock;  // one device: the member's own pointer
+    CB_REQUIRE(b != nullptr, CB_E_INVALID_ARG, "peer-memory collectives: rank %d's exchange block is not mapped", j);
+    pt->base[j] = b;
+  }
+  return CB_OK;
+}
+
+cb_status p2p_launch(cb_ctx* c, size_t off, long long n, int mode, cudaStream_t s) {
+  PeerTable pt{};
+  CB_TRY(p2p_peers(c, &pt));
+  CB_LAUNCH(c, p2p_collective_kernel, P2P_CTAS, P2P_THREADS, 0, s, pt, c->tp_rank, c->tp_world, off, n, mode,
+            c->x_flags_off);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+bool in_block(const cb_ctx* c, const void* p) {
+  return c->xblock && (const char*)p >= c->xblock && (const char*)p < c->xblock + c->x_total;
+}
+}  // namespace
+
+cb_status p2p_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s) {
+  if (in_block(c, buf)) return p2p_launch(c, (size_t)((char*)buf - c->xblock), (long long)n, 0, s);
+  // a buffer outside the exchange block (a caller's dev_out row): through the staging row
+  CB_REQUIRE(n * sizeof(float) <= c->x_flags_off - c->x_stage_off, CB_E_SHAPE, "p2p all-reduce staging too small");
+  CB_CUDA(cudaMemcpyAsync(c->xblock + c->x_stage_off, buf, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  CB_TRY(p2p_launch(c, c->x_stage_off, (long long)n, 0, s));
+  CB_CUDA(cudaMemcpyAsync(buf, c->xblock + c->x_stage_off, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  return CB_OK;
+}
+
+cb_status p2p_allgather_f32(cb_ctx* c, float* buf, size_t n_per_rank, cudaStream_t s) {
+  CB_REQUIRE(in_block(c, buf) && n_per_rank % 4 == 0, CB_E_INVALID_ARG, "p2p all-gather outside the exchange block");
+  return p2p_launch(c, (size_t)((char*)buf - c->xblock), (long long)n_per_rank, 1, s);
+}
+
+extern "C" cb_status cb_tp_p2p_enable(cb_ctx* c) {
+  CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
+  CB_REQUIRE(c->comm_kind != CB_COMM_NONE && c->tp_world >= 1, CB_E_INVALID_ARG,
+             "join a communicator (cb_set_comm / cb_set_comm_local) first");
+  if (c->xblock) return CB_OK;
+  const size_t T = (size_t)c->max_tokens, d = (size_t)c->m.d_model;
+  const size_t nb = (size_t)(c->m.n_kv_heads * c->m.head_dim + 63) / 64;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  c->x_h_bytes = al(T * d * sizeof(float));
+  c->x_gath_off = 2 * c->x_h_bytes;
+  c->x_stage_off = c->x_gath_off + al(2 * nb * c->tp_world * T * sizeof(float));
+  c->x_flags_off = c->x_stage_off + al(T * sizeof(float));
+  c->x_total = c->x_flags_off + 256;
+  void* p = nullptr;
+  CB_CUDA(cudaMalloc(&p, c->x_total));
+  CB_CUDA(cudaMemset(p, 0, c->x_total));
+  c->xblock = (char*)p;
+  c->h[0] = (float*)c->xblock;  // the residual stream (o_proj / down_proj outputs) lives in the block
+  c->h[1] = (float*)(c->xblock + c->x_h_bytes);
+  if (c->dev_gath) cudaFree(c->dev_gath);
+  c->dev_gath = (float*)(c->xblock + c->x_gath_off);
+  c->p2p_peer[c->tp_rank] = c->xblock;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_tp_ipc_handle(cb_ctx* c, void* handle_out) {
+  CB_REQUIRE(c && handle_out && c->xblock, CB_E_INVALID_ARG, "cb_tp_ipc_handle: enable peer-memory collectives first");
+  cudaIpcMemHandle_t h;
+  CB_CUDA(cudaIpcGetMemHandle(&h, c->xblock));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return CB_OK;
+}
+
+extern "C" cb_status cb_tp_ipc_open(cb_ctx* c, const void* handles) {
+  CB_REQUIRE(c && handles && c->xblock, CB_E_INVALID_ARG, "cb_tp_ipc_open: enable peer-memory collectives first");
+  for (int j = 0; j < c->tp_world; ++j) {
+    if (j == c->tp_rank || c->p2p_peer[j]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, (const char*)handles + (size_t)j * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    CB_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->p2p_peer[j] = (char*)p;
+    c->p2p_ipc[j] = true;
+  }
+  return CB_OK;
 }

@@ -96,6 +96,13 @@ struct cb_ctx {
   float* dev_gath;            // [2 nb_local world][max_tokens] gathered Delta_kv partials
   float* tp_scratch;          // loopback all-reduce scratch
   size_t tp_scratch_n;
+  // NVLink peer-memory collectives (comm.cu, cb_tp_p2p_enable): h[0], h[1], dev_gath, a staging row and the
+  // flags live in one exchange block per rank with the same layout on every rank; peers' blocks are mapped
+  // through CUDA IPC (one process per GPU) or taken from the loopback group's members
+  char* xblock;
+  size_t x_h_bytes, x_gath_off, x_stage_off, x_flags_off, x_total;
+  char* p2p_peer[kMaxTp];     // every rank's exchange block as seen from this device (own included)
+  bool p2p_ipc[kMaxTp];       // opened with cudaIpcOpenMemHandle (closed in comm_destroy)
   // profiling
   bool prof_on;
   std::vector<ProfRec> prof;

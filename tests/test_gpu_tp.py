@@ -25,7 +25,7 @@ pytestmark = pytest.mark.gpu
 TOL = {"f32": 1e-4, "bf16": 2e-2}
 
 
-def run_blend_tp(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, world, force_sel=None):
+def run_blend_tp(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, world, force_sel=None, p2p=False):
     """cb_blend_forward on `world` loopback ranks; returns per-rank outputs plus K/V reassembled over heads."""
     td = P.api.TORCH_DTYPES[dtype]
     L, N, n_suf = s.n_layers, req.n_ctx, req.n_suffix
@@ -37,6 +37,8 @@ def run_blend_tp(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, world, force_
     for r in range(world):
         ctx = P.Context(ss, dtype, max_tokens=T, max_pos=max(int(np.max(pos)) + 1, 2 * T))
         ctx.set_comm_local(group, r)
+        if p2p:
+            ctx.enable_tp_p2p()
         mw = P.ModelWeights(ss, dtype, full.embed, [D.shard_layer(w, s, r, world) for w in full.layers])
         k_in = D.shard_kv(to_dev(Kc, td), s, r, world)
         v_in = D.shard_kv(to_dev(Vc, td), s, r, world)
@@ -171,12 +173,15 @@ def test_tp_small_bf16_free_run_consistent(P):
     _compare(res, ora, s, TOL["bf16"])
 
 
-def _nccl_world1(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, comm: bool, graph: bool):
+def _nccl_world1(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, comm: bool, graph: bool, p2p: bool = False):
     td = P.api.TORCH_DTYPES[dtype]
     L, N = s.n_layers, req.n_ctx
     ctx = P.Context(s, dtype, max_tokens=N, max_pos=2 * N)
     if comm:
         ctx.set_comm(P.nccl_unique_id(), 0, 1)
+    if p2p:
+        ctx.enable_tp_p2p()
+        ctx.tp_ipc_open([ctx.tp_ipc_handle()])
     mw = P.ModelWeights.synth(s, seed, dtype, DEV)
     k_in, v_in = to_dev(Kc, td), to_dev(Vc, td)
     kb, vb = torch.empty_like(k_in), torch.empty_like(v_in)
@@ -266,3 +271,31 @@ def test_tp_request_path_equals_forward(P):
         _, _, kb, vb, hh = outs[r]
         assert torch.equal(kb, x["kb"]) and torch.equal(vb, x["vb"])
         np.testing.assert_array_equal(hh.numpy(), np32(x["h"][:ks[-1]]))
+
+
+@pytest.mark.parametrize("name,dtype,world,n_suf", [("tiny", "f32", 2, 0), ("tiny", "f32", 4, 5), ("small", "bf16", 2, 0)])
+def test_tp_p2p_equals_event_path(P, name, dtype, world, n_suf):
+    """NVLink peer-memory collectives (cb_tp_p2p_enable; here the loopback members' blocks on one device):
+    bitwise the results of the event-ordered loopback path (same rank-order sums), so they inherit its
+    oracle parity."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _case(name, 11, [64, 40, 57] if name == "small" else [32, 32, 32], n_suf,
+                                                dtype, 0.2, **({"n_layers": 3} if name == "tiny" else {}))
+    a = run_blend_tp(P, s, dtype, 11, req, tok, pos, cs, Kc, Vc, ks, world)
+    b = run_blend_tp(P, s, dtype, 11, req, tok, pos, cs, Kc, Vc, ks, world, p2p=True)
+    np.testing.assert_array_equal(a["K"], b["K"])
+    np.testing.assert_array_equal(a["V"], b["V"])
+    np.testing.assert_array_equal(a["h"], b["h"])
+    np.testing.assert_array_equal(a["dev"], b["dev"])
+    for x, y in zip(a["sel"], b["sel"]):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_p2p_world1_ipc_graph(P):
+    """Peer-memory collectives with a one-rank communicator through the IPC API, eager and replayed from a
+    CUDA graph (device-side sequence numbers): bitwise equal to no communicator."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _case("small", 3, [128, 200], 0, "bf16", 0.15)
+    ref = _nccl_world1(P, s, "bf16", 3, req, tok, pos, cs, Kc, Vc, ks, comm=False, graph=False)
+    for graph in (False, True):
+        got = _nccl_world1(P, s, "bf16", 3, req, tok, pos, cs, Kc, Vc, ks, comm=True, graph=graph, p2p=True)
+        for a, b in zip(got, ref):
+            assert torch.equal(a, b)
