@@ -45,6 +45,8 @@ def parse():
                     help="batched = SURVEY config 5: 64 Mistral-shape requests of 4-8 chunks x 256-1024 "
                          "tokens, assigned to the ranks longest-first")
     ap.add_argument("--batched-requests", type=int, default=64)
+    ap.add_argument("--tp-comm", default="nccl", choices=["nccl", "p2p"],
+                    help="--parallel heads: NCCL collectives or the library's NVLink peer-memory kernels")
     ap.add_argument("--parallel", default="request", choices=["request", "heads"],
                     help="N>1: request-parallel (weak scaling, default) or head-parallel tensor parallelism over "
                          "the N GPUs (strong scaling, NCCL all-gather / all-reduces inside the blend)")
@@ -273,6 +275,11 @@ def run_ours(args):
     if heads and world > 1:
         uid = D.broadcast_bytes(P.nccl_unique_id() if rank == 0 else b"", src=0)
         ctx.set_comm(uid, rank, world)
+        if args.tp_comm == "p2p":  # NVLink peer-memory collectives instead of NCCL calls
+            ctx.enable_tp_p2p()
+            hs = [None] * world
+            dist.all_gather_object(hs, ctx.tp_ipc_handle())
+            ctx.tp_ipc_open(hs)
     if args.no_pdl:
         ctx.set_option("pdl", 0)
     for kv in filter(None, os.environ.get("CB_OPTS", "").split(",")):  # tuning: CB_OPTS=name=value,...
@@ -453,7 +460,7 @@ def run_ours(args):
                 "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} tokens, r={ratio}, " +
                                        (f"1 request split by heads over {world} GPU(s)" if heads else "1 request per GPU"),
                            "recompute_ratio": ratio, "n_ctx": N, "k_sched_first_last": [ks[1], ks[-1]],
-                           "parallelism": f"head-parallel tp{world} (NCCL all-gather of Delta_kv partials, "
+                           "parallelism": f"head-parallel tp{world} ({args.tp_comm} all-gather of Delta_kv partials, "
                                           "all-reduce after o_proj and down_proj)" if heads else
                                           f"request-parallel x{world}",
                            "l2": f"inputs larger than L2 ({work['weight_bytes'] / 1e9:.1f} GB of weights streamed "

@@ -280,7 +280,9 @@ CB_API cb_status cb_set_comm_local(cb_ctx* ctx, cb_group* group, int32_t rank);
  * rank's block, then waits until every rank has finished. Graph-capturable (device-side sequence numbers).
  * One process per GPU: exchange cb_tp_ipc_handle (64 host bytes per rank, e.g. all-gathered with
  * torch.distributed) and call cb_tp_ipc_open with the world's handles in rank order. Loopback group: the
- * members' blocks are used directly (every member must enable it). */
+ * members' blocks are used directly (every member must enable it; run the process with
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 4 * world so no rank's stream shares a hardware queue with a spinning
+ * collective of another rank). */
 CB_API cb_status cb_tp_p2p_enable(cb_ctx* ctx);
 CB_API cb_status cb_tp_ipc_handle(cb_ctx* ctx, void* handle_out_64B);
 CB_API cb_status cb_tp_ipc_open(cb_ctx* ctx, const void* handles_world_x_64B);

@@ -75,6 +75,7 @@ _SIGS = {
     "cb_group_destroy": (c_i32, [c_vp]),
     "cb_set_comm_local": (c_i32, [c_vp, c_vp, c_i32]),
     "cb_tp_p2p_enable": (c_i32, [c_vp]),
+    "cb_debug_p2p_flags": (c_i32, [c_vp, c_i32p]),
     "cb_tp_ipc_handle": (c_i32, [c_vp, c_vp]),
     "cb_tp_ipc_open": (c_i32, [c_vp, c_vp]),
 }

@@ -359,6 +359,7 @@ extern "C" cb_status cb_check_device_errors(cb_ctx* c) {
   CB_CUDA(cudaMemset(c->err_word, 0, sizeof(int)));
   if (h & CB_DEVERR_FORCE_SEL) { cb_set_error("device: a force_sel token is not a candidate of its layer"); return CB_E_DEVICE; }
   if (h & CB_DEVERR_POS_RANGE) { cb_set_error("device: |dst_pos - src_pos| >= max_pos in realign"); return CB_E_DEVICE; }
+  if (h & CB_DEVERR_COMM) { cb_set_error("device: a peer-memory collective timed out waiting for a rank"); return CB_E_DEVICE; }
   return CB_OK;
 }
 

@@ -332,8 +332,8 @@ extern "C" cb_status cb_set_comm_local(cb_ctx* c, cb_group* g, int32_t rank) {
 //   exit barrier   -- the last CTA of each rank raises flag[1][rank] = seq everywhere and waits for all, so
 //                     the kernel completes only when every rank's writes are done (nobody overwrites a buffer
 //                     a peer is still reading). seq is a device-side counter, so a CUDA graph can replay it.
-// The grid is small (64 CTAs): on one GPU (loopback test) the spinning CTAs co-reside with the other ranks'
-// GEMM CTAs instead of starving them.
+// The grid is small (64 CTAs; 4 in the one-device loopback test, where every rank's spinning CTAs share the
+// SMs with the other ranks' kernels).
 namespace {
 constexpr int P2P_CTAS = 64, P2P_THREADS = 256;
 
@@ -348,12 +348,32 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
 
 struct PeerTable { char* base[kMaxTp]; };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *f >= seq, or give up after 10 s (a peer that never arrives must not hang the GPU): the
+// device error word then carries CB_DEVERR_COMM (cb_check_device_errors) and the data are invalid.
+__device__ __forceinline__ void wait_flag(const int* f, int seq, int* err) {
+  const unsigned long long t0 = gtimer();
+  while (ld_acquire_sys(f) < seq) {
+    __nanosleep(64);
+    if (gtimer() - t0 > 10000000000ull) {
+      atomicOr(err, CB_DEVERR_COMM);
+      return;
+    }
+  }
+}
+
 // flags (ints at flags_off of every block): [0, kMaxTp) entry, [kMaxTp, 2 kMaxTp) exit, [2 kMaxTp] seq,
 // [2 kMaxTp + 1] finished-CTA counter
 __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable pt, int rank, int world,
                                                                      size_t off, long long n, int mode,
-                                                                     size_t flags_off) {
-  pdl_enter();
+                                                                     size_t flags_off, int* err) {
+  // wait for this rank's producer, but do NOT let the dependent kernel launch early: on one device
+  // (loopback) its waiting CTAs could fill the SMs the other ranks need to reach their barrier
+  pdl_wait();
   int* myf = reinterpret_cast<int*>(pt.base[rank] + flags_off);
   __shared__ int seq_s;
   if (threadIdx.x == 0) seq_s = *reinterpret_cast<volatile int*>(myf + 2 * kMaxTp) + 1;
@@ -363,8 +383,7 @@ __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable p
     __threadfence_system();
     st_release_sys(reinterpret_cast<int*>(pt.base[threadIdx.x] + flags_off) + rank, seq);
   }
-  if (threadIdx.x < world)
-    while (ld_acquire_sys(myf + threadIdx.x) < seq) __nanosleep(64);
+  if (threadIdx.x < world) wait_flag(myf + threadIdx.x, seq, err);
   __syncthreads();
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -402,8 +421,7 @@ __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable p
       __threadfence_system();
       for (int j = 0; j < world; ++j)
         st_release_sys(reinterpret_cast<int*>(pt.base[j] + flags_off) + kMaxTp + rank, seq);
-      for (int j = 0; j < world; ++j)
-        while (ld_acquire_sys(myf + kMaxTp + j) < seq) __nanosleep(64);
+      for (int j = 0; j < world; ++j) wait_flag(myf + kMaxTp + j, seq, err);
       *reinterpret_cast<volatile int*>(myf + 2 * kMaxTp) = seq;
     }
   }
@@ -423,8 +441,11 @@ cb_status p2p_peers(cb_ctx* c, PeerTable* pt) {
 cb_status p2p_launch(cb_ctx* c, size_t off, long long n, int mode, cudaStream_t s) {
   PeerTable pt{};
   CB_TRY(p2p_peers(c, &pt));
-  CB_LAUNCH(c, p2p_collective_kernel, P2P_CTAS, P2P_THREADS, 0, s, pt, c->tp_rank, c->tp_world, off, n, mode,
-            c->x_flags_off);
+  // one device (loopback): 4 CTAs per rank, so the spinning CTAs of all ranks occupy at most 32 SMs and the
+  // other ranks' kernels (which may need a whole SM) always find free SMs
+  const int ctas = c->comm_kind == CB_COMM_LOOPBACK ? 4 : P2P_CTAS;
+  CB_LAUNCH(c, p2p_collective_kernel, ctas, P2P_THREADS, 0, s, pt, c->tp_rank, c->tp_world, off, n, mode,
+            c->x_flags_off, c->err_word);
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -445,6 +466,7 @@ cb_status p2p_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s) {
 }
 
 cb_status p2p_allgather_f32(cb_ctx* c, float* buf, size_t n_per_rank, cudaStream_t s) {
+  if (c->tp_world == 1) return CB_OK;  // nothing to gather
   CB_REQUIRE(in_block(c, buf) && n_per_rank % 4 == 0, CB_E_INVALID_ARG, "p2p all-gather outside the exchange block");
   return p2p_launch(c, (size_t)((char*)buf - c->xblock), (long long)n_per_rank, 1, s);
 }
@@ -471,6 +493,9 @@ extern "C" cb_status cb_tp_p2p_enable(cb_ctx* c) {
   if (c->dev_gath) cudaFree(c->dev_gath);
   c->dev_gath = (float*)(c->xblock + c->x_gath_off);
   c->p2p_peer[c->tp_rank] = c->xblock;
+  // one device (loopback): no programmatic early launch at all, so the only resident waiters are the
+  // collective kernels' own 64 spinning CTAs and the other ranks' kernels always find SMs
+  if (c->comm_kind == CB_COMM_LOOPBACK) c->pdl = 0;
   return CB_OK;
 }
 
@@ -493,5 +518,19 @@ extern "C" cb_status cb_tp_ipc_open(cb_ctx* c, const void* handles) {
     c->p2p_peer[j] = (char*)p;
     c->p2p_ipc[j] = true;
   }
+  return CB_OK;
+}
+
+// Diagnostics: copy this rank's flag words (entry[kMaxTp], exit[kMaxTp], seq, finished-CTA counter) to the
+// host through a private non-blocking stream (does not wait for work queued on other streams).
+extern "C" cb_status cb_debug_p2p_flags(cb_ctx* c, int32_t* out) {
+  CB_REQUIRE(c && out && c->xblock, CB_E_INVALID_ARG, "cb_debug_p2p_flags: no exchange block");
+  cudaStream_t st;
+  CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  cudaError_t e = cudaMemcpyAsync(out, c->xblock + c->x_flags_off, (2 * kMaxTp + 2) * sizeof(int),
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  CB_CUDA(e);
   return CB_OK;
 }

@@ -70,7 +70,7 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 // Device-side error word bits (cb_check_device_errors).
-enum : int { CB_DEVERR_FORCE_SEL = 1, CB_DEVERR_POS_RANGE = 2 };
+enum : int { CB_DEVERR_FORCE_SEL = 1, CB_DEVERR_POS_RANGE = 2, CB_DEVERR_COMM = 4 };
 
 // ---- epilogues shared by the SIMT and tcgen05 GEMMs -----------------------------------------
 // acc[m][n] = sum_k A[m][k] B[n][k];   kinds:

@@ -1,6 +1,11 @@
 import os
 import sys
 
+# The loopback head-parallel tests run several ranks' streams in one process; with the default 8 hardware
+# work queues, streams share queues and a spinning peer-memory collective of one rank could sit in front of
+# another rank's kernels (false serialisation). Read when the CUDA context is created, i.e. before any test.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -1,0 +1,75 @@
+"""Loopback diagnostics of the peer-memory collectives: two tiny fp32 head-parallel ranks on one GPU, forward
+in two threads, flag words of both ranks printed while / after it runs.  python tools/p2p_diag.py [p2p 0|1]"""
+import ctypes
+import os
+import sys
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+import threading
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    p2p = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    import paper_2405_16444_b200 as P
+    from paper_2405_16444_b200 import dist as D
+    from synth import workload as W
+    import dataclasses
+    s = dataclasses.replace(W.MODELS["tiny"], n_layers=3)
+    world, N = int(sys.argv[2]) if len(sys.argv) > 2 else 2, 96
+    ss = D.head_shard_shape(s, world)
+    g = P.Group(world)
+    full = P.ModelWeights.synth(s, 1, "f32", "cuda")
+    req = W.Request([32, 32, 32], 0, 1, 0.2)
+    tok = torch.from_numpy(req.tokens(s.vocab)).cuda()
+    pos = torch.from_numpy(req.global_positions()).cuda()
+    ks = P.schedule(0.2, N, s.n_layers)
+    ranks = []
+    for r in range(world):
+        ctx = P.Context(ss, "f32", max_tokens=N)
+        ctx.set_comm_local(g, r)
+        if p2p:
+            ctx.enable_tp_p2p()
+        mw = P.ModelWeights(ss, "f32", full.embed, [D.shard_layer(w, s, r, world) for w in full.layers])
+        k = torch.randn(s.n_layers, N, ss.n_kv_heads, s.head_dim, device="cuda")
+        ranks.append(dict(ctx=ctx, mw=mw, k=k, v=torch.randn_like(k), kb=torch.empty_like(k), vb=torch.empty_like(k),
+                          h=torch.empty(ks[-1], s.d_model, device="cuda"), st=torch.cuda.Stream()))
+    torch.cuda.synchronize()
+    t0 = time.time()
+    done = [None] * world
+
+    def work(r):
+        x = ranks[r]
+        P.blend_forward(x["ctx"], x["mw"], tok, pos, list(req.chunk_starts()), 0, x["k"], x["v"], x["kb"], x["vb"], ks,
+                        h_out=x["h"], stream=x["st"])
+        done[r] = ("enqueued", time.time() - t0)
+        x["st"].synchronize()
+        done[r] = ("finished", time.time() - t0)
+
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for it in range(8):
+        time.sleep(2)
+        line = [f"t={time.time() - t0:.0f}s"]
+        for r, x in enumerate(ranks):
+            if p2p:
+                f = (ctypes.c_int32 * 18)()
+                P.api.check(P.api.lib().cb_debug_p2p_flags(x["ctx"].handle, f))
+                line.append(f"r{r} {done[r]} entry {list(f[:world])} exit {list(f[8:8 + world])} seq {f[16]} cnt {f[17]}")
+            else:
+                line.append(f"r{r} {done[r]}")
+        print(" | ".join(line), flush=True)
+        if all(d and d[0] == "finished" for d in done):
+            break
+    print("launches", [x["ctx"].launch_count() for x in ranks], flush=True)
+    os._exit(0)
+
+
+if __name__ == "__main__":
+    main()
