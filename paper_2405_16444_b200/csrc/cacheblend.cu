@@ -420,6 +420,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     c->no_fuse_dev = value == 0;
     return CB_OK;
   }
+  if (std::strcmp(name, "tp_fuse") == 0) {
+    CB_REQUIRE(c->xblock == nullptr, CB_E_INVALID_ARG, "set tp_fuse before cb_tp_p2p_enable");
+    c->tp_nofuse = value == 0;
+    return CB_OK;
+  }
   if (std::strcmp(name, "attn_packed") == 0) {
     c->attn_nopk = value == 0;
     return CB_OK;
@@ -678,8 +683,11 @@ cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, c
     set_norm_consumer(c, eg);
   }
   tp_partial_resid(c, eo);
+  const bool push = tp_push_on(c);  // peer-memory mode: the epilogue pushes each row to its owner (fused RS)
+  if (push) CB_TRY(tp_push_params(c, eo, Q));
   CB_TRY(launch_gemm(c, c->attn, qd, w.w_o, qd, Q, qd, eo, 0, s));
-  CB_TRY(comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s));  // (ii) all-reduce after o_proj
+  if (push) CB_TRY(comm_allreduce_pushed(c, b.h_out, Q, s));               // (ii) after o_proj
+  else CB_TRY(comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s));
   if (!fuse_mlp) CB_TRY(launch_rmsnorm(c, b.h_out, (const float*)w.mlp_norm, Q, c->x, s));
   EpiParams ed{};
   ed.kind = EPI_RESID; ed.M = Q; ed.N = d; ed.ldo = d; ed.h_in = b.h_out; ed.h_out = b.h_out; ed.res_row = nullptr;
@@ -688,9 +696,10 @@ cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, c
   if (fuse_next) set_norm_producer(c, ed, b.next_attn_norm);
   if (c->tp_world > 1) {  // (iii) Megatron MLP: column-sharded gate/up, row-sharded down, one all-reduce
     tp_partial_resid(c, ed);
+    if (push) CB_TRY(tp_push_params(c, ed, Q));
     CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
     CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
-    return comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s);
+    return push ? comm_allreduce_pushed(c, b.h_out, Q, s) : comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s);
   }
   // MLP split (blend sizes): gate_up in S feature blocks on the caller's stream; the down projection of
   // block k (a K block of W_down) on the aux stream as soon as block k's activations exist, writing an

@@ -368,9 +368,13 @@ __device__ __forceinline__ void wait_flag(const int* f, int seq, int* err) {
 
 // flags (ints at flags_off of every block): [0, kMaxTp) entry, [kMaxTp, 2 kMaxTp) exit, [2 kMaxTp] seq,
 // [2 kMaxTp + 1] finished-CTA counter
+// mode 0: all-reduce of n floats at off; 1: all-gather (segments of n floats); 2: fused reduce-scatter
+// epilogue: rows were pushed by the GEMMs into this rank's receive planes (recv_off, plane floats apart);
+// this rank's chunk of the n floats is summed over the planes and written at off in every rank's block.
 __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable pt, int rank, int world,
                                                                      size_t off, long long n, int mode,
-                                                                     size_t flags_off, int* err) {
+                                                                     size_t flags_off, int* err, size_t recv_off,
+                                                                     long long plane, long long chunk2) {
   // wait for this rank's producer, but do NOT let the dependent kernel launch early: on one device
   // (loopback) its waiting CTAs could fill the SMs the other ranks need to reach their barrier
   pdl_wait();
@@ -403,6 +407,17 @@ __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable p
       float a = __ldcg(reinterpret_cast<const float*>(pt.base[0] + off) + i);
       for (int j = 1; j < world; ++j) a += __ldcg(reinterpret_cast<const float*>(pt.base[j] + off) + i);
       for (int j = 0; j < world; ++j) __stcg(reinterpret_cast<float*>(pt.base[j] + off) + i, a);
+    }
+  } else if (mode == 2) {  // the rows this rank owns: sum the pushed planes in rank order, write everywhere
+    const long long lo = (long long)rank * chunk2, hi = lo + chunk2 < n ? lo + chunk2 : n;
+    const float* own = reinterpret_cast<const float*>(pt.base[rank] + recv_off);
+    for (long long i = lo / 4 + t0; i < hi / 4; i += stride) {
+      float4 a = __ldcg(reinterpret_cast<const float4*>(own) + i);
+      for (int j = 1; j < world; ++j) {
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(own + (size_t)j * plane) + i);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+      }
+      for (int j = 0; j < world; ++j) __stcg(reinterpret_cast<float4*>(pt.base[j] + off) + i, a);
     }
   } else {  // all-gather: push this rank's segment of n floats to every peer
     const float4* src = reinterpret_cast<const float4*>(pt.base[rank] + off) + (size_t)rank * (n / 4);
@@ -438,14 +453,14 @@ cb_status p2p_peers(cb_ctx* c, PeerTable* pt) {
   return CB_OK;
 }
 
-cb_status p2p_launch(cb_ctx* c, size_t off, long long n, int mode, cudaStream_t s) {
+cb_status p2p_launch(cb_ctx* c, size_t off, long long n, int mode, cudaStream_t s, long long chunk2 = 0) {
   PeerTable pt{};
   CB_TRY(p2p_peers(c, &pt));
   // one device (loopback): 4 CTAs per rank, so the spinning CTAs of all ranks occupy at most 32 SMs and the
   // other ranks' kernels (which may need a whole SM) always find free SMs
   const int ctas = c->comm_kind == CB_COMM_LOOPBACK ? 4 : P2P_CTAS;
   CB_LAUNCH(c, p2p_collective_kernel, ctas, P2P_THREADS, 0, s, pt, c->tp_rank, c->tp_world, off, n, mode,
-            c->x_flags_off, c->err_word);
+            c->x_flags_off, c->err_word, c->x_recv_off, (long long)c->max_tokens * c->m.d_model, chunk2);
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -483,7 +498,9 @@ extern "C" cb_status cb_tp_p2p_enable(cb_ctx* c) {
   c->x_gath_off = 2 * c->x_h_bytes;
   c->x_stage_off = c->x_gath_off + al(2 * nb * c->tp_world * T * sizeof(float));
   c->x_flags_off = c->x_stage_off + al(T * sizeof(float));
-  c->x_total = c->x_flags_off + 256;
+  // receive planes of the fused reduce-scatter: one [T][d] fp32 plane per rank (skipped with tp_fuse = 0)
+  c->x_recv_off = c->tp_world > 1 && !c->tp_nofuse ? c->x_flags_off + 256 : 0;
+  c->x_total = c->x_flags_off + 256 + (c->x_recv_off ? (size_t)c->tp_world * c->x_h_bytes : 0);
   void* p = nullptr;
   CB_CUDA(cudaMalloc(&p, c->x_total));
   CB_CUDA(cudaMemset(p, 0, c->x_total));
@@ -533,4 +550,24 @@ extern "C" cb_status cb_debug_p2p_flags(cb_ctx* c, int32_t* out) {
   cudaStreamDestroy(st);
   CB_CUDA(e);
   return CB_OK;
+}
+
+bool tp_push_on(const cb_ctx* c) { return c->xblock != nullptr && c->x_recv_off != 0 && c->tp_world > 1; }
+
+cb_status tp_push_params(cb_ctx* c, EpiParams& e, int rows) {
+  PeerTable pt{};
+  CB_TRY(p2p_peers(c, &pt));
+  for (int j = 0; j < kMaxTp; ++j) e.push_base[j] = j < c->tp_world ? pt.base[j] : nullptr;
+  e.push_rows = (rows + c->tp_world - 1) / c->tp_world;
+  e.push_off = (long long)(c->x_recv_off + (size_t)c->tp_rank * c->x_h_bytes);
+  CB_REQUIRE(e.ldo == c->m.d_model, CB_E_INVALID_ARG, "pushed rows must be d_model wide");
+  return CB_OK;
+}
+
+cb_status comm_allreduce_pushed(cb_ctx* c, float* h_out, int rows, cudaStream_t s) {
+  CB_REQUIRE(in_block(c, h_out), CB_E_INVALID_ARG, "pushed all-reduce: h_out outside the exchange block");
+  ProfScope ps_(c, PROF_COMM, s);
+  const long long d = c->m.d_model;
+  const long long chunk = (long long)((rows + c->tp_world - 1) / c->tp_world) * d;  // the rows each rank owns
+  return p2p_launch(c, (size_t)((char*)h_out - c->xblock), (long long)rows * d, 2, s, chunk);
 }

@@ -107,7 +107,18 @@ struct EpiParams {
   // EPI_RESID (tcgen05 staged path): fp32 partial products of earlier K blocks (row-major, ld = ldo) added
   // in this order after h_in and before the accumulator: h_out = (((h_in + p0) + p1) + ...) + acc
   const float* add_part[3]; int n_add;
+  // Head-parallel fused reduce-scatter (comm.cu): when push_base[0] is set, the fp32 output row m of
+  // EPI_STORE_F32 / EPI_RESID goes to push_base[m / push_rows] + push_off (this rank's receive plane in the
+  // block of the rank that owns row m, over NVLink) instead of outf / h_out.
+  char* push_base[8]; long long push_off; int push_rows;
 };
+
+// Output row m of an fp32 epilogue (outf / h_out), or its owner's receive plane when pushing.
+__device__ __forceinline__ float* out_row_f32(const EpiParams& e, float* local, int m) {
+  if (e.push_base[0] != nullptr)
+    return reinterpret_cast<float*>(e.push_base[m / e.push_rows] + e.push_off) + (size_t)m * e.ldo;
+  return local + (size_t)m * e.ldo;
+}
 
 // Apply the epilogue to the adjacent column pair (n, n+1), n even. For SWIGLU a0/a1 are the gate
 // accumulators and u0/u1 the up accumulators of output columns n, n+1.
@@ -122,7 +133,7 @@ __device__ __forceinline__ void epi_pair(const EpiParams& e, int m, int n, float
       if (has1) o[1] = from_f<T>(a1);
     } break;
     case EPI_STORE_F32: {
-      float* o = e.outf + (size_t)m * e.ldo + n;
+      float* o = out_row_f32(e, e.outf, m) + n;
       o[0] = a0;
       if (has1) o[1] = a1;
     } break;
@@ -147,7 +158,7 @@ __device__ __forceinline__ void epi_pair(const EpiParams& e, int m, int n, float
     case EPI_RESID: {
       const int src = e.res_row ? e.res_row[m] : m;
       const float* hi = e.h_in + (size_t)src * e.ldo + n;
-      float* ho = e.h_out + (size_t)m * e.ldo + n;
+      float* ho = out_row_f32(e, e.h_out, m) + n;
       const float h0 = hi[0];
       const float h1 = has1 ? hi[1] : 0.f;
       ho[0] = h0 + a0;

@@ -100,7 +100,8 @@ struct cb_ctx {
   // flags live in one exchange block per rank with the same layout on every rank; peers' blocks are mapped
   // through CUDA IPC (one process per GPU) or taken from the loopback group's members
   char* xblock;
-  size_t x_h_bytes, x_gath_off, x_stage_off, x_flags_off, x_total;
+  size_t x_h_bytes, x_gath_off, x_stage_off, x_flags_off, x_recv_off, x_total;
+  int tp_nofuse;              // cb_set_option("tp_fuse", 0): o_proj / down_proj write locally, then a plain all-reduce
   char* p2p_peer[kMaxTp];     // every rank's exchange block as seen from this device (own included)
   bool p2p_ipc[kMaxTp];       // opened with cudaIpcOpenMemHandle (closed in comm_destroy)
   // profiling
@@ -225,5 +226,11 @@ cb_status check_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const
 cb_status comm_allreduce_f32(cb_ctx* c, float* buf, size_t n, cudaStream_t s);
 cb_status comm_allgather_f32(cb_ctx* c, float* buf, size_t n_per_rank, cudaStream_t s);
 void comm_destroy(cb_ctx* c);
+// Fused reduce-scatter of the head-parallel residual GEMMs (peer-memory mode): tp_push_on() says whether the
+// o_proj / down_proj epilogues push their rows to the owners' receive planes (tp_push_params fills EpiParams);
+// comm_allreduce_pushed then sums each rank's owned rows over the planes and writes them to every rank's h_out.
+bool tp_push_on(const cb_ctx* c);
+cb_status tp_push_params(cb_ctx* c, EpiParams& e, int rows);
+cb_status comm_allreduce_pushed(cb_ctx* c, float* h_out, int rows, cudaStream_t s);
 cb_status launch_gen_fill(void* out, int dtype, long long count, unsigned long long seed, unsigned long long stream_id,
                           long long start, float scale, float offset, cudaStream_t s);

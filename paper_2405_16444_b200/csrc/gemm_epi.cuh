@@ -55,7 +55,7 @@ __device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const f
   if constexpr (KIND == EPI_STORE) {
     st_bf16x16(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + n, v);
   } else if constexpr (KIND == EPI_STORE_F32) {
-    float4* p = reinterpret_cast<float4*>(e.outf + (size_t)m * e.ldo + n);
+    float4* p = reinterpret_cast<float4*>(out_row_f32(e, e.outf, m) + n);
 #pragma unroll
     for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
   } else if constexpr (KIND == EPI_QKV) {
@@ -87,7 +87,7 @@ __device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const f
   } else if constexpr (KIND == EPI_RESID) {
     const int src = e.res_row ? __ldg(e.res_row + m) : m;
     const float4* hi = reinterpret_cast<const float4*>(e.h_in + (size_t)src * e.ldo + n);
-    float4* ho = reinterpret_cast<float4*>(e.h_out + (size_t)m * e.ldo + n);
+    float4* ho = reinterpret_cast<float4*>(out_row_f32(e, e.h_out, m) + n);
     float4 hv[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) hv[i] = hi[i];
@@ -260,12 +260,12 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
       if constexpr (KIND == EPI_STORE) {
         if (ok) *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + col) = pack4_bf16(a);
       } else if constexpr (KIND == EPI_STORE_F32) {
-        if (ok) *reinterpret_cast<float4*>(e.outf + (size_t)m * e.ldo + col) = a;
+        if (ok) *reinterpret_cast<float4*>(out_row_f32(e, e.outf, m) + col) = a;
       } else if constexpr (KIND == EPI_SWIGLU) {
         if (ok) *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.act) + (size_t)m * e.ff + col) = pack4_bf16(a);
       } else if constexpr (KIND == EPI_RESID) {
         const float4 o = make_float4(pre[it].x + a.x, pre[it].y + a.y, pre[it].z + a.z, pre[it].w + a.w);
-        if (ok) *reinterpret_cast<float4*>(e.h_out + (size_t)m * e.ldo + col) = o;
+        if (ok) *reinterpret_cast<float4*>(out_row_f32(e, e.h_out, m) + col) = o;
         if (norm_on && ok) {  // lane-local sum of squares; reduced over the row's 8 lanes at the block end
           *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.y_out) + (size_t)m * e.ldo + col) =
               pack4_bf16(make_float4(o.x * gain.x, o.y * gain.y, o.z * gain.z, o.w * gain.w));

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ A,
       epi_pair<T>(e, m, n, acc[i][j], acc[i][j + 1], accu[i][j], accu[i][j + 1]);
     }
   }
+  if (e.push_base[0] != nullptr) __threadfence_system();  // pushed rows reach the peers before the signal
 }
 }  // namespace
 

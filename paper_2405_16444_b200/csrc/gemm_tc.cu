@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
   }
+  if (e.push_base[0] != nullptr) __threadfence_system();  // pushed rows reach the peers before the signal
   __syncthreads();
   if (warp == 2) tc::tmem_dealloc(tmem_base, C::TMEM_COLS);
 }

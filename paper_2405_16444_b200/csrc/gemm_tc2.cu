@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) tc::mbar_arrive_rank0(&tempty[acc]);
     }
   }
+  if (e.push_base[0] != nullptr) __threadfence_system();  // pushed rows reach the peers before the signal
   if (threadIdx.x == 0) DBG2(6);
   tc::fence_before();
   tc::cluster_sync();  // no multicast commit or remote arrive may target an exited CTA

@@ -38,6 +38,8 @@ def run_blend_tp(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, world, force_
         ctx = P.Context(ss, dtype, max_tokens=T, max_pos=max(int(np.max(pos)) + 1, 2 * T))
         ctx.set_comm_local(group, r)
         if p2p:
+            if p2p == "plain":
+                ctx.set_option("tp_fuse", 0)
             ctx.enable_tp_p2p()
         mw = P.ModelWeights(ss, dtype, full.embed, [D.shard_layer(w, s, r, world) for w in full.layers])
         k_in = D.shard_kv(to_dev(Kc, td), s, r, world)
@@ -273,15 +275,17 @@ def test_tp_request_path_equals_forward(P):
         np.testing.assert_array_equal(hh.numpy(), np32(x["h"][:ks[-1]]))
 
 
+@pytest.mark.parametrize("mode", ["fused", "plain"])
 @pytest.mark.parametrize("name,dtype,world,n_suf", [("tiny", "f32", 2, 0), ("tiny", "f32", 4, 5), ("small", "bf16", 2, 0)])
-def test_tp_p2p_equals_event_path(P, name, dtype, world, n_suf):
+def test_tp_p2p_equals_event_path(P, name, dtype, world, n_suf, mode):
     """NVLink peer-memory collectives (cb_tp_p2p_enable; here the loopback members' blocks on one device):
-    bitwise the results of the event-ordered loopback path (same rank-order sums), so they inherit its
-    oracle parity."""
+    fused (the o_proj / down_proj epilogues push each row into its owner's receive plane, the owner sums the
+    planes and writes everywhere) and plain (local writes, then the one-kernel all-reduce). Both are bitwise
+    the results of the event-ordered loopback path (same rank-order sums), so they inherit its parity."""
     s, m, req, tok, pos, cs, Kc, Vc, ks = _case(name, 11, [64, 40, 57] if name == "small" else [32, 32, 32], n_suf,
                                                 dtype, 0.2, **({"n_layers": 3} if name == "tiny" else {}))
     a = run_blend_tp(P, s, dtype, 11, req, tok, pos, cs, Kc, Vc, ks, world)
-    b = run_blend_tp(P, s, dtype, 11, req, tok, pos, cs, Kc, Vc, ks, world, p2p=True)
+    b = run_blend_tp(P, s, dtype, 11, req, tok, pos, cs, Kc, Vc, ks, world, p2p=mode)
     np.testing.assert_array_equal(a["K"], b["K"])
     np.testing.assert_array_equal(a["V"], b["V"])
     np.testing.assert_array_equal(a["h"], b["h"])
