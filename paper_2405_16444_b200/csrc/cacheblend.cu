@@ -303,6 +303,8 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
   if ((e = cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
+  for (auto& ev : c->ev_realign)
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
   for (auto& ev : c->ev_mlp)
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
@@ -337,6 +339,7 @@ extern "C" cb_status cb_destroy(cb_ctx* c) {
   for (auto ev : c->ev_pool) cudaEventDestroy(ev);
   for (auto ev : c->layer_ev) if (ev) cudaEventDestroy(ev);
   if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+  for (auto ev : c->ev_realign) if (ev) cudaEventDestroy(ev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
   if (c->mlp_scr) cudaFree(c->mlp_scr);
@@ -418,6 +421,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   }
   if (std::strcmp(name, "fuse_deviation") == 0) {
     c->no_fuse_dev = value == 0;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "realign_overlap") == 0) {
+    c->realign_overlap = value != 0;
     return CB_OK;
   }
   if (std::strcmp(name, "tp_fuse") == 0) {
@@ -908,7 +915,8 @@ cb_status check_forward(cb_ctx* c, const cb_layer_w* w, const void* embed, const
 // layer i (fetch_kv / synchronize / prefill_layer); otherwise the realign already ran.
 cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const int* tok, const int* pos, int N,
                        int n_suffix, void* k_blend, void* v_blend, const int* k_sched, const int* force_sel,
-                       int* sel_out, float* dev_out, float* h_out, cudaStream_t s, bool realign_per_layer) {
+                       int* sel_out, float* dev_out, float* h_out, cudaStream_t s, bool realign_per_layer,
+                       cudaEvent_t realign_done = nullptr) {
   const cb_model& m = c->m;
   const int L = m.n_layers, T = N + n_suffix, kvd = m.n_kv_heads * m.head_dim;
   const size_t B = dtype_bytes(m.dtype);
@@ -938,6 +946,7 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
   for (int i = 1; i < L; ++i) {
     const int k = k_sched[i];
     CB_TRY(realign_layer(i));
+    if (i == 1 && realign_done) CB_CUDA(cudaStreamWaitEvent(s, realign_done, 0));  // layers 1.. realigned
     LayerBufs b{c->h[cur], c->h[cur ^ 1], rows, c->row_tok[rt]};
     b.x_ready = ready;
     ready = false;
@@ -975,13 +984,29 @@ extern "C" cb_status cb_blend_forward(cb_ctx* c, const cb_layer_w* w, const void
   const cb_model& m = c->m;
   const int T = N + n_suffix, kvd = m.n_kv_heads * m.head_dim;
   // (a1) positional recovery of every layer's cached K in one launch (+ carry V over when out of place)
+  cudaEvent_t realign_done = nullptr;
   if (N > 0) {
     CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, s));
-    CB_TRY(launch_realign(c, k_blend, k_in, v_inplace ? nullptr : v_blend, v_in, c->src_pos, pos, m.n_layers, N,
-                          (long long)T * kvd, (long long)N * kvd, s));
+    const long long os = (long long)T * kvd, is = (long long)N * kvd;
+    if (c->realign_overlap && m.n_layers > 1) {
+      // layer 0 here; layers 1..L-1 (HBM-bound) on the aux stream under layer 0's compute-bound GEMMs,
+      // joined before layer 1 reads its cache
+      CB_TRY(launch_realign(c, k_blend, k_in, v_inplace ? nullptr : v_blend, v_in, c->src_pos, pos, 1, N, os, is, s));
+      const size_t B = dtype_bytes(m.dtype);
+      CB_CUDA(cudaEventRecord(c->ev_realign[0], s));
+      CB_CUDA(cudaStreamWaitEvent(c->aux_stream, c->ev_realign[0], 0));
+      CB_TRY(launch_realign(c, (char*)k_blend + os * B, (const char*)k_in + is * B,
+                            v_inplace ? nullptr : (char*)v_blend + os * B, (const char*)v_in + is * B, c->src_pos,
+                            pos, m.n_layers - 1, N, os, is, c->aux_stream));
+      CB_CUDA(cudaEventRecord(c->ev_realign[1], c->aux_stream));
+      realign_done = c->ev_realign[1];
+    } else {
+      CB_TRY(launch_realign(c, k_blend, k_in, v_inplace ? nullptr : v_blend, v_in, c->src_pos, pos, m.n_layers, N,
+                            os, is, s));
+    }
   }
   return blend_layers(c, w, embed, tok, pos, N, n_suffix, k_blend, v_blend, k_sched, force_sel, sel_out, dev_out,
-                      h_out, s, false);
+                      h_out, s, false, realign_done);
 }
 
 // The request path (fetch_kv -> synchronize -> prefill_layer) with the layer fetch supplied

@@ -86,6 +86,8 @@ struct cb_ctx {
   float* mlp_scr;             // fused MLP: fp32 partials of the down projection's K blocks
   int* mlp_cnt;               // fused MLP: block / merge counters (zero between launches)
   cudaEvent_t ev_ready;
+  cudaEvent_t ev_realign[2];  // realign of layers 1..L-1 on the aux stream: fork, done
+  int realign_overlap;        // cb_set_option("realign_overlap"): that realign runs under layer 0
   std::vector<cudaEvent_t> layer_ev;
   // head-parallel blend (comm.cu): this context holds rank tp_rank's shard of the model (heads, d_ff / world)
   int tp_rank;

@@ -563,3 +563,17 @@ def test_blend_half_split_rope_checkpoint(P, monkeypatch):
         assert rel_err(K[i], ora.K[i]) < TOL["f32"], f"K layer {i}"
         assert rel_err(res["V"][i], ora.V[i]) < TOL["f32"], f"V layer {i}"
     assert rel_err(res["h"], ora.h_final) < TOL["f32"]
+
+
+@pytest.mark.parametrize("name,dtype,in_place", [("tiny", "f32", False), ("small", "bf16", False), ("small", "bf16", True)])
+def test_blend_realign_overlap_bitwise(P, name, dtype, in_place):
+    """realign_overlap (layers 1..L-1 realigned on the aux stream under layer 0, joined before layer 1): the
+    same kernels on the same data, so bitwise the serial order."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case(name, 12, [96, 70, 33], 0, dtype, 0.2)
+    outs = []
+    for ov in (0, 1):
+        ctx = P.Context(s, dtype, max_tokens=req.n_total, max_pos=4096)
+        ctx.set_option("realign_overlap", ov)
+        outs.append(run_blend(P, s, dtype, 12, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx, in_place=in_place))
+    for key in ("K", "V", "h"):
+        np.testing.assert_array_equal(outs[0][key], outs[1][key])
