@@ -45,9 +45,9 @@ def parse():
                     help="batched = SURVEY config 5: 64 Mistral-shape requests of 4-8 chunks x 256-1024 "
                          "tokens, assigned to the ranks longest-first")
     ap.add_argument("--batched-requests", type=int, default=64)
-    ap.add_argument("--tp-comm", default="p2p", choices=["nccl", "p2p"],
-                    help="--parallel heads: the library's NVLink peer-memory collectives (default; o_proj / "
-                         "down_proj epilogues push rows to their owners) or NCCL calls")
+    ap.add_argument("--tp-comm", default="nccl", choices=["nccl", "p2p"],
+                    help="--parallel heads: NCCL calls (default) or the library's NVLink peer-memory collectives "
+                         "(o_proj / down_proj epilogues push rows to their owners; experimental, DESIGN.md §7)")
     ap.add_argument("--parallel", default="request", choices=["request", "heads"],
                     help="N>1: request-parallel (weak scaling, default) or head-parallel tensor parallelism over "
                          "the N GPUs (strong scaling, NCCL all-gather / all-reduces inside the blend)")

@@ -25,6 +25,7 @@
 // (deterministic) and writes the output -- no separate merge launch.
 #include <cudaTypedefs.h>
 
+#include <mutex>
 #include <unordered_map>
 
 #include "ctx.h"
@@ -491,18 +492,23 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode5 = nullptr;
 
+// Tensor maps of K/V buffers, cached across calls and contexts: the key holds every field the map encodes
+// (an address reused by another context with other kv heads must not hit a stale map), and the cache is
+// shared by all host threads (head-parallel loopback ranks), hence the mutex.
 struct KvKey {
   const void* p;
-  int n_keys;
-  bool operator==(const KvKey& o) const { return p == o.p && n_keys == o.n_keys; }
+  int n_keys, n_kv;
+  bool operator==(const KvKey& o) const { return p == o.p && n_keys == o.n_keys && n_kv == o.n_kv; }
 };
+std::mutex g_kvmaps_mu;
 struct KvKeyHash {
-  size_t operator()(const KvKey& k) const { return std::hash<const void*>()(k.p) ^ ((size_t)k.n_keys * 0x9e3779b9); }
+  size_t operator()(const KvKey& k) const { return std::hash<const void*>()(k.p) ^ ((size_t)k.n_keys * 0x9e3779b9) ^ ((size_t)k.n_kv << 40); }
 };
 std::unordered_map<KvKey, CUtensorMap, KvKeyHash>* g_kvmaps = nullptr;
 
 cb_status kv_tmap(const cb_ctx* c, const void* p, int n_keys, CUtensorMap* out) {
-  KvKey key{p, n_keys};
+  KvKey key{p, n_keys, c->m.n_kv_heads};
+  std::lock_guard<std::mutex> lk(g_kvmaps_mu);
   auto it = g_kvmaps->find(key);
   if (it != g_kvmaps->end()) { *out = it->second; return CB_OK; }
   const int n_kv = c->m.n_kv_heads;

@@ -20,23 +20,26 @@ def main():
     from paper_2405_16444_b200 import dist as D
     from synth import workload as W
     import dataclasses
-    s = dataclasses.replace(W.MODELS["tiny"], n_layers=3)
-    world, N = int(sys.argv[2]) if len(sys.argv) > 2 else 2, 96
+    name = sys.argv[3] if len(sys.argv) > 3 else "tiny"
+    dt = "f32" if name == "tiny" else "bf16"
+    s = dataclasses.replace(W.MODELS[name], n_layers=3) if name == "tiny" else W.MODELS[name]
+    world = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    req = W.Request([32, 32, 32] if name == "tiny" else [512] * 6, 0, 1, 0.2)
+    N = req.n_ctx
     ss = D.head_shard_shape(s, world)
     g = P.Group(world)
-    full = P.ModelWeights.synth(s, 1, "f32", "cuda")
-    req = W.Request([32, 32, 32], 0, 1, 0.2)
+    full = P.ModelWeights.synth(s, 1, dt, "cuda")
     tok = torch.from_numpy(req.tokens(s.vocab)).cuda()
     pos = torch.from_numpy(req.global_positions()).cuda()
     ks = P.schedule(0.2, N, s.n_layers)
     ranks = []
     for r in range(world):
-        ctx = P.Context(ss, "f32", max_tokens=N)
+        ctx = P.Context(ss, dt, max_tokens=N, max_pos=2 * N)
         ctx.set_comm_local(g, r)
         if p2p:
             ctx.enable_tp_p2p()
-        mw = P.ModelWeights(ss, "f32", full.embed, [D.shard_layer(w, s, r, world) for w in full.layers])
-        k = torch.randn(s.n_layers, N, ss.n_kv_heads, s.head_dim, device="cuda")
+        mw = P.ModelWeights(ss, dt, full.embed, [D.shard_layer(w, s, r, world) for w in full.layers])
+        k = torch.randn(s.n_layers, N, ss.n_kv_heads, s.head_dim, device="cuda").to(P.api.TORCH_DTYPES[dt])
         ranks.append(dict(ctx=ctx, mw=mw, k=k, v=torch.randn_like(k), kb=torch.empty_like(k), vb=torch.empty_like(k),
                           h=torch.empty(ks[-1], s.d_model, device="cuda"), st=torch.cuda.Stream()))
     torch.cuda.synchronize()
@@ -54,13 +57,15 @@ def main():
     th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
     for t in th:
         t.start()
-    for it in range(8):
+    for it in range(12):
         time.sleep(2)
         line = [f"t={time.time() - t0:.0f}s"]
         for r, x in enumerate(ranks):
             if p2p:
-                f = (ctypes.c_int32 * 18)()
-                P.api.check(P.api.lib().cb_debug_p2p_flags(x["ctx"].handle, f))
+                fb = torch.zeros(18, dtype=torch.int32).pin_memory()
+                P.api.check(P.api.lib().cb_debug_p2p_flags(x["ctx"].handle,
+                                                           ctypes.cast(fb.data_ptr(), ctypes.POINTER(ctypes.c_int32))))
+                f = fb.tolist()
                 line.append(f"r{r} {done[r]} entry {list(f[:world])} exit {list(f[8:8 + world])} seq {f[16]} cnt {f[17]}")
             else:
                 line.append(f"r{r} {done[r]}")
