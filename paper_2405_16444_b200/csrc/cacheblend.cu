@@ -487,6 +487,12 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     gemm_tc_balance(c, (int)value);
     return CB_OK;
   }
+  if (std::strcmp(name, "topk_threads") == 0) {
+    CB_REQUIRE(value == 0 || value == 256 || value == 512 || value == 1024, CB_E_INVALID_ARG,
+               "topk_threads must be 0, 256, 512 or 1024");
+    c->topk_threads = (int)value;
+    return CB_OK;
+  }
   if (std::strcmp(name, "topk_drop") == 0) {
     c->topk_drop_max = (int)value;
     return CB_OK;

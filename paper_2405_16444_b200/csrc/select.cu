@@ -100,7 +100,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sm_warp, int* total) 
   if (lane == 31) sm_warp[w] = x;
   __syncthreads();
   if (w == 0) {
-    int t = sm_warp[lane];
+    int t = lane < (int)(blockDim.x >> 5) ? sm_warp[lane] : 0;  // blocks of fewer than 32 warps
     int u = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -298,7 +298,10 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   if (k_keep + n_suffix == 0 && (dev_part == nullptr || n_cand == 0)) return CB_OK;
   const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);
   ProfScope ps_(c, PROF_TOPK, s);
-  CB_LAUNCH(c, (topk_kernel), 1, TOPK_THREADS, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
+  // threads: 1024, or fewer when the candidates are few (cheaper block barriers), cb_set_option("topk_threads")
+  int nt = TOPK_THREADS;
+  if (c->topk_threads > 0) nt = c->topk_threads;
+  CB_LAUNCH(c, (topk_kernel), 1, nt, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
                                             c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64 * std::max(1, c->tp_world), ld_part,
                                             dev_mode, c->topk_drop_max);
   CB_LAUNCHED(c);

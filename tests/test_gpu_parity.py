@@ -577,3 +577,30 @@ def test_blend_realign_overlap_bitwise(P, name, dtype, in_place):
         outs.append(run_blend(P, s, dtype, 12, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx, in_place=in_place))
     for key in ("K", "V", "h"):
         np.testing.assert_array_equal(outs[0][key], outs[1][key])
+
+
+@pytest.mark.parametrize("threads", [256, 512])
+def test_topk_block_size_bitwise(P, threads):
+    """The top-k kernel at 256 / 512 threads (topk_threads) selects exactly what the 1024-thread block does:
+    radix path at layer 1, drop-smallest path later, plus the ABI call on tie-heavy deviations."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 13, [300, 211, 157], 4, "bf16", 0.15)
+    outs = []
+    for t in (0, threads):
+        ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
+        ctx.set_option("topk_threads", t)
+        outs.append(run_blend(P, s, "bf16", 13, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx))
+    for a, b in zip(outs[0]["sel"], outs[1]["sel"]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(outs[0]["h"], outs[1]["h"])
+    ctx = P.Context(s, "bf16", max_tokens=5000)
+    g = torch.Generator(device=DEV).manual_seed(threads)
+    n = 4000
+    kn = torch.randint(0, 3, (n, s.n_kv_heads, s.head_dim), device=DEV, generator=g).to(torch.bfloat16)
+    vn = torch.zeros_like(kn)
+    ref = torch.zeros(n, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=DEV)
+    cand = torch.arange(n, dtype=torch.int32, device=DEV)
+    res = []
+    for t in (0, threads):
+        ctx.set_option("topk_threads", t)
+        res.append(P.api.kv_deviation_topk(ctx, kn, vn, ref, ref, cand, 1234))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][2], res[1][2])
