@@ -8,6 +8,7 @@ oracle of the UNSHARDED model on identical inputs, with the tolerances of test_g
 and every rank must agree bitwise on S_i, Delta_kv and h (the top-k is the same on every rank).
 The NCCL backend itself is exercised at world 1 (a real communicator; the all-reduce/all-gather calls
 run in the forward and inside a CUDA graph), bitwise equal to the context without a communicator."""
+import os
 import threading
 
 import numpy as np
@@ -275,6 +276,9 @@ def test_tp_request_path_equals_forward(P):
         np.testing.assert_array_equal(hh.numpy(), np32(x["h"][:ks[-1]]))
 
 
+@pytest.mark.skipif(os.environ.get("CB_TEST_P2P") != "1",
+                    reason="experimental peer-memory collectives: multi-rank loopback runs can desync "
+                           "(DESIGN.md §7 open issue); set CB_TEST_P2P=1 to run")
 @pytest.mark.parametrize("mode", ["fused", "plain"])
 @pytest.mark.parametrize("name,dtype,world,n_suf", [("tiny", "f32", 2, 0), ("tiny", "f32", 4, 5), ("small", "bf16", 2, 0)])
 def test_tp_p2p_equals_event_path(P, name, dtype, world, n_suf, mode):

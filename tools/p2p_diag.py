@@ -37,6 +37,8 @@ def main():
         ctx = P.Context(ss, dt, max_tokens=N, max_pos=2 * N)
         ctx.set_comm_local(g, r)
         if p2p:
+            if p2p == 2:
+                ctx.set_option("tp_fuse", 0)
             ctx.enable_tp_p2p()
         mw = P.ModelWeights(ss, dt, full.embed, [D.shard_layer(w, s, r, world) for w in full.layers])
         k = torch.randn(s.n_layers, N, ss.n_kv_heads, s.head_dim, device="cuda").to(P.api.TORCH_DTYPES[dt])
