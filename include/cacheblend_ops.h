@@ -92,9 +92,10 @@ CB_API cb_status cb_profile_begin(cb_ctx* ctx);
 CB_API cb_status cb_profile_end(cb_ctx* ctx, double* ms_out, int64_t* counts_out, int32_t n_classes);
 CB_API const char* cb_profile_class_name(int32_t cls);
 
-/* Peer-memory collectives diagnostics: out = this rank's flag words {entry[8], exit[8], seq, finished CTAs},
- * read through a private non-blocking stream. */
-CB_API cb_status cb_debug_p2p_flags(cb_ctx* ctx, int32_t* out18);
+/* Peer-memory collectives diagnostics: out[0..51] = this rank's flag words {entry[8], exit[8], seq, finished
+ * CTAs, 2 spare, ring of the last 8 collectives (seq, rank, block tag, mode)}, out[52] = this block's tag;
+ * read through a private non-blocking stream (out: 53 host ints, pinned for an asynchronous read). */
+CB_API cb_status cb_debug_p2p_flags(cb_ctx* ctx, int32_t* out53);
 
 #ifdef __cplusplus
 }

@@ -383,6 +383,10 @@ __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable p
   if (threadIdx.x == 0) seq_s = *reinterpret_cast<volatile int*>(myf + 2 * kMaxTp) + 1;
   __syncthreads();
   const int seq = seq_s;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // diagnostics ring (ints 20..51): seq, rank, own-block tag, mode
+    int* r = myf + 20 + (seq & 7) * 4;
+    r[0] = seq; r[1] = rank; r[2] = (int)(reinterpret_cast<uintptr_t>(myf) >> 8); r[3] = mode;
+  }
   if (blockIdx.x == 0 && threadIdx.x < world) {
     __threadfence_system();
     st_release_sys(reinterpret_cast<int*>(pt.base[threadIdx.x] + flags_off) + rank, seq);
@@ -544,8 +548,8 @@ extern "C" cb_status cb_debug_p2p_flags(cb_ctx* c, int32_t* out) {
   CB_REQUIRE(c && out && c->xblock, CB_E_INVALID_ARG, "cb_debug_p2p_flags: no exchange block");
   cudaStream_t st;
   CB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  cudaError_t e = cudaMemcpyAsync(out, c->xblock + c->x_flags_off, (2 * kMaxTp + 2) * sizeof(int),
-                                  cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaMemcpyAsync(out, c->xblock + c->x_flags_off, 52 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  out[52] = (int)(reinterpret_cast<uintptr_t>(c->xblock + c->x_flags_off) >> 8);  // this block's tag
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   CB_CUDA(e);

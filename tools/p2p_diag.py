@@ -64,11 +64,14 @@ def main():
         line = [f"t={time.time() - t0:.0f}s"]
         for r, x in enumerate(ranks):
             if p2p:
-                fb = torch.zeros(18, dtype=torch.int32).pin_memory()
+                fb = torch.zeros(53, dtype=torch.int32).pin_memory()
                 P.api.check(P.api.lib().cb_debug_p2p_flags(x["ctx"].handle,
                                                            ctypes.cast(fb.data_ptr(), ctypes.POINTER(ctypes.c_int32))))
                 f = fb.tolist()
-                line.append(f"r{r} {done[r]} entry {list(f[:world])} exit {list(f[8:8 + world])} seq {f[16]} cnt {f[17]}")
+                ring = [tuple(f[20 + 4 * i:24 + 4 * i]) for i in range(8)]
+                ring = [(q, rk, "own" if tag == f[52] else hex(tag & 0xffff), md) for q, rk, tag, md in ring if q]
+                line.append(f"r{r} {done[r]} entry {list(f[:world])} exit {list(f[8:8 + world])} seq {f[16]} "
+                            f"cnt {f[17]} ring {sorted(ring)}")
             else:
                 line.append(f"r{r} {done[r]}")
         print(" | ".join(line), flush=True)
