@@ -385,7 +385,9 @@ __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable p
   const int seq = seq_s;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // diagnostics ring (ints 20..51): seq, rank, own-block tag, mode
     int* r = myf + 20 + (seq & 7) * 4;
-    r[0] = seq; r[1] = rank; r[2] = (int)(reinterpret_cast<uintptr_t>(myf) >> 8); r[3] = mode;
+    r[0] = seq; r[1] = rank * 16 + mode;
+    r[2] = (int)(reinterpret_cast<uintptr_t>(pt.base[0] + flags_off) >> 8);
+    r[3] = (int)(reinterpret_cast<uintptr_t>(pt.base[world > 1 ? 1 : 0] + flags_off) >> 8);
   }
   if (blockIdx.x == 0 && threadIdx.x < world) {
     __threadfence_system();

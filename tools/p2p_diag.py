@@ -62,6 +62,7 @@ def main():
     for it in range(12):
         time.sleep(2)
         line = [f"t={time.time() - t0:.0f}s"]
+        tags = []
         for r, x in enumerate(ranks):
             if p2p:
                 fb = torch.zeros(53, dtype=torch.int32).pin_memory()
@@ -69,12 +70,13 @@ def main():
                                                            ctypes.cast(fb.data_ptr(), ctypes.POINTER(ctypes.c_int32))))
                 f = fb.tolist()
                 ring = [tuple(f[20 + 4 * i:24 + 4 * i]) for i in range(8)]
-                ring = [(q, rk, "own" if tag == f[52] else hex(tag & 0xffff), md) for q, rk, tag, md in ring if q]
+                tags.append(f[52])
+                ring = [(q, rkm // 16, rkm % 16, hex(b0 & 0xffffff), hex(b1 & 0xffffff)) for q, rkm, b0, b1 in ring if q]
                 line.append(f"r{r} {done[r]} entry {list(f[:world])} exit {list(f[8:8 + world])} seq {f[16]} "
                             f"cnt {f[17]} ring {sorted(ring)}")
             else:
                 line.append(f"r{r} {done[r]}")
-        print(" | ".join(line), flush=True)
+        print(" | ".join(line), [hex(t & 0xffffff) for t in tags], flush=True)
         if all(d and d[0] == "finished" for d in done):
             break
     print("launches", [x["ctx"].launch_count() for x in ranks], flush=True)
