@@ -35,6 +35,9 @@ def main():
     ranks = []
     for r in range(world):
         ctx = P.Context(ss, dt, max_tokens=N, max_pos=2 * N)
+        for kv in filter(None, os.environ.get("CB_OPTS", "").split(",")):  # e.g. CB_OPTS=gemm_pair=2
+            k_, v_ = kv.split("=")
+            ctx.set_option(k_, int(v_))
         ctx.set_comm_local(g, r)
         if p2p:
             if p2p == 2:
