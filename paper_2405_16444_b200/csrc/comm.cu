@@ -342,7 +342,11 @@ __device__ __forceinline__ void st_release_sys(int* p, int v) {
 }
 __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   int v;
+#ifdef CB_P2P_ACQ_GPU
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#else
   asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#endif
   return v;
 }
 
@@ -393,8 +397,11 @@ __global__ void __launch_bounds__(P2P_THREADS) p2p_collective_kernel(PeerTable p
     __threadfence_system();
     st_release_sys(reinterpret_cast<int*>(pt.base[threadIdx.x] + flags_off) + rank, seq);
   }
+  const unsigned long long t_wait = gtimer();
   if (threadIdx.x < world) wait_flag(myf + threadIdx.x, seq, err);
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0)  // diagnostics: entry-wait time (us) and the peers' flags seen
+    myf[20 + (seq & 7) * 4 + 1] = (rank * 16 + mode) + 256 * (int)min(1000000ull, (gtimer() - t_wait) / 1000ull);
   const long long stride = (long long)gridDim.x * blockDim.x;
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (mode == 0) {  // all-reduce: this rank's slice, summed in rank order, written to every rank
@@ -462,6 +469,7 @@ cb_status p2p_peers(cb_ctx* c, PeerTable* pt) {
 cb_status p2p_launch(cb_ctx* c, size_t off, long long n, int mode, cudaStream_t s, long long chunk2 = 0) {
   PeerTable pt{};
   CB_TRY(p2p_peers(c, &pt));
+
   // one device (loopback): 4 CTAs per rank, so the spinning CTAs of all ranks occupy at most 32 SMs and the
   // other ranks' kernels (which may need a whole SM) always find free SMs
   const int ctas = c->comm_kind == CB_COMM_LOOPBACK ? (getenv("CB_P2P_LOOP_CTAS") ? atoi(getenv("CB_P2P_LOOP_CTAS")) : 4) : P2P_CTAS;

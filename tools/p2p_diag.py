@@ -74,7 +74,7 @@ def main():
                 f = fb.tolist()
                 ring = [tuple(f[20 + 4 * i:24 + 4 * i]) for i in range(8)]
                 tags.append(f[52])
-                ring = [(q, rkm // 16, rkm % 16, hex(b0 & 0xffffff), hex(b1 & 0xffffff)) for q, rkm, b0, b1 in ring if q]
+                ring = [(q, (rkm % 256) // 16, rkm % 16, f"wait {rkm // 256} us") for q, rkm, b0, b1 in ring if q]
                 line.append(f"r{r} {done[r]} entry {list(f[:world])} exit {list(f[8:8 + world])} seq {f[16]} "
                             f"cnt {f[17]} ring {sorted(ring)}")
             else:
