@@ -62,6 +62,11 @@ def main():
     th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(world)]
     for t in th:
         t.start()
+    if os.environ.get("CB_DIAG_NOPOLL"):  # no flag reads while it runs: only the per-rank finish times
+        for t in th:
+            t.join(timeout=60)
+        print("nopoll", done, flush=True)
+        os._exit(0)
     for it in range(12):
         time.sleep(2)
         line = [f"t={time.time() - t0:.0f}s"]
