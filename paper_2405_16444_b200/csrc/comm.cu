@@ -344,6 +344,9 @@ __device__ __forceinline__ int ld_acquire_sys(const int* p) {
   int v;
 #ifdef CB_P2P_ACQ_GPU
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#elif defined(CB_P2P_POLL_ATOMIC)
+  v = atomicAdd(const_cast<int*>(p), 0);  // always served by L2
+  __threadfence_system();
 #else
   asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
 #endif
