@@ -197,12 +197,14 @@ CB_API cb_status cb_blend_request(cb_ctx* ctx, const cb_layer_w* w, const void* 
  * blocks (vLLM). Copies KV^new into per-layer page pools:
  *   k_pages[l * dst_layer_stride + (block_table[t / block_size] * block_size + t % block_size) * row + e]
  *     = k_blend[l * src_layer_stride + t * row + e]      (same for V), row = n_kv * head_dim,
- * for l < n_layers, t < n_tok. block_table: device int32[ceil(n_tok / block_size)] page ids (distinct,
- * inside the pool, not checked). Bit-exact copy in the model dtype; slots of a last partial page past
- * n_tok are untouched. Errors: strides too small -> SHAPE; unaligned buffers / NULL -> INVALID_ARG. */
+ * for l < n_layers, t < n_tok. block_table: device int32[ceil(n_tok / block_size)] page ids of a pool of
+ * n_pages pages per layer (dst_layer_stride >= n_pages * block_size * row); an id outside [0, n_pages) is
+ * not written and raises CB_E_DEVICE at cb_check_device_errors. Bit-exact copy in the model dtype; slots of
+ * a last partial page past n_tok are untouched. Errors: strides too small -> SHAPE; unaligned buffers /
+ * NULL -> INVALID_ARG. */
 CB_API cb_status cb_kv_to_paged(cb_ctx* ctx, const void* k_blend, const void* v_blend, int32_t n_layers, int32_t n_tok,
                                 int64_t src_layer_stride, const int32_t* block_table, int32_t block_size,
-                                void* k_pages, void* v_pages, int64_t dst_layer_stride, void* stream);
+                                void* k_pages, void* v_pages, int32_t n_pages, int64_t dst_layer_stride, void* stream);
 
 /* ---- chunk KV store (§6 "KV cache store") ---------------------------- */
 /* Maps a chunk's hash to its precomputed KV cache, on one storage level (host RAM), evicting the
@@ -211,30 +213,36 @@ CB_API cb_status cb_kv_to_paged(cb_ctx* ctx, const void* k_blend, const void* v_
  * page-locked entries, needed by cb_blend_request_store (asynchronous per-layer DMA); 0: malloc (host
  * bookkeeping only). Thread-safe. Host-side bookkeeping: no method arithmetic. */
 typedef struct cb_store cb_store;
-/* 64-bit hash of a chunk's token ids (FNV-1a over the int32 bytes + splitmix64 finaliser). Host only. */
-CB_API uint64_t cb_chunk_hash(const int32_t* tokens, int32_t n_tok);
+/* A chunk's store key: 32-byte SHA-256 digest of (u32 little-endian byte length of model_id || model_id ||
+ * the chunk's token ids as little-endian int32). model_id identifies the model whose KV the entry holds
+ * (e.g. a digest of its configuration and weights), so one store can serve several models without one
+ * model's KV answering another's lookup ("each chunk is hashed"). Host only; NULL out /
+ * negative lengths -> INVALID_ARG. */
+typedef struct { uint8_t bytes[32]; } cb_chunk_key;
+CB_API cb_status cb_chunk_digest(const void* model_id, int32_t model_id_len, const int32_t* tokens, int32_t n_tok,
+                                 cb_chunk_key* out);
 CB_API cb_status cb_store_create(size_t capacity_bytes, int32_t pinned, cb_store** out);
 CB_API cb_status cb_store_destroy(cb_store* store);
 /* Insert (or replace) key -> (k, v), `bytes` each, copied synchronously from host or device memory. Evicts
  * LRU entries until 2 * bytes fit (waiting for in-flight fetches from them). An entry larger than the
  * capacity -> SHAPE. The new entry is the most recently used. */
-CB_API cb_status cb_store_put(cb_store* store, uint64_t key, const void* k, const void* v, int64_t bytes,
+CB_API cb_status cb_store_put(cb_store* store, const cb_chunk_key* key, const void* k, const void* v, int64_t bytes,
                               int32_t n_tok);
 /* fetch_kv's lookup: n_tok_out = the entry's token count or -1 when absent; k_out / v_out
  * (optional) = its host pointers (valid until evicted). touch != 0 counts a hit / miss and refreshes the
  * entry's recency. */
-CB_API cb_status cb_store_lookup(cb_store* store, uint64_t key, int32_t touch, int32_t* n_tok_out, const void** k_out,
-                                 const void** v_out);
+CB_API cb_status cb_store_lookup(cb_store* store, const cb_chunk_key* key, int32_t touch, int32_t* n_tok_out,
+                                 const void** k_out, const void** v_out);
 /* out6 = {used bytes, capacity, entries, hits, misses, evictions}. */
 CB_API cb_status cb_store_stats(cb_store* store, int64_t* out6);
 /* The first n keys in recency order (most recent first); n_out = number of entries. */
-CB_API cb_status cb_store_keys(cb_store* store, uint64_t* keys, int32_t n, int32_t* n_out);
-/* cb_blend_request with chunk c's KV fetched from the store under chunk_keys[c] (host uint64[n_chunks]):
+CB_API cb_status cb_store_keys(cb_store* store, cb_chunk_key* keys, int32_t n, int32_t* n_out);
+/* cb_blend_request with chunk c's KV fetched from the store under chunk_keys[c] (host cb_chunk_key[n_chunks]):
  * layer i's KV of every chunk is copied on the copy stream while layer i-1 computes. Every key
  * must be present with n_tok = chunk length and L * n_tok * n_kv * hd elements, else CB_E_MISS / CB_E_SHAPE
  * before any launch; the chunks' recency is refreshed. Needs a pinned store; not graph-capturable. Other
  * arguments as cb_blend_request. */
-CB_API cb_status cb_blend_request_store(cb_ctx* ctx, cb_store* store, const uint64_t* chunk_keys, const cb_layer_w* w,
+CB_API cb_status cb_blend_request_store(cb_ctx* ctx, cb_store* store, const cb_chunk_key* chunk_keys, const cb_layer_w* w,
                                         const void* embed, const int32_t* tok_host, const int32_t* pos_host,
                                         int32_t N, int32_t n_suffix, const int32_t* chunk_start, int32_t n_chunks,
                                         void* k_blend, void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,

@@ -14,7 +14,7 @@ extern "C" {
 
 /* ---- synthetic input generation (NOT method arithmetic) -----------------------------------
  * Device implementation of the counter-RNG spec in synth/counter_rng.py (the spec, not the code,
- * is shared with the oracle; tests/test_gen_parity.py pins the two bit-for-bit):
+ * is shared with the oracle; tests/test_gpu_parity.py::test_gen_fill_bitexact pins the two bit-for-bit):
  *   raw(i) = mix64(mix64(mix64(seed) ^ stream_id) + i), u = fp32(raw >> 40) * 2^-23 - 1,
  *   out[i - start] = fp32(offset + fp32(u * scale)) [-> bf16 RNE when dtype == CB_BF16]
  * for i in [start, start + count).  cb_gen_ints: out[i - start] = raw(i) % modulus. */

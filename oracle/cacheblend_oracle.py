@@ -27,6 +27,8 @@ one check that does not restate its formula:
   schedule          golden S:263-265 + closed form R4/R5
   blend_forward     r=1 -> full prefill; r=0 -> realigned cache; single chunk -> prefix
                     reuse; nesting, untouched entries bitwise, MAC ratio.
+  blend_replay_rows equals blend_forward(force_sel) on the rows it returns (to fp64 rounding: the
+                    same functions on row subsets), tests/test_oracle_blend.py.
   Intermediate-r selected sets/values: the oracle IS the definition ("parity unpinned"
   beyond the invariants above; SURVEY §8(c) last row).
 """
@@ -122,28 +124,38 @@ def silu(x: np.ndarray) -> np.ndarray:
 
 
 def causal_attention(q: np.ndarray, q_pos: np.ndarray, k: np.ndarray, v: np.ndarray,
-                     k_pos: np.ndarray, mc: Optional[MacCounter] = None) -> np.ndarray:
+                     k_pos: np.ndarray, mc: Optional[MacCounter] = None, threads: int = 1) -> np.ndarray:
     """Forward attention of query rows over ALL given keys, masked by original position.
 
     q [R][n_q][hd] (rotated), k/v [T][n_kv][hd] (k rotated), mask: key visible iff
     k_pos <= q_pos (causal by original position; the selected tokens attend to "all
     other tokens", P:156). GQA: q head h reads kv head h // (n_q / n_kv).
-    Returns [R][n_q*hd]."""
+    Returns [R][n_q*hd]. `threads` > 1 evaluates the (independent) heads on a thread pool;
+    every head's arithmetic is the same either way."""
     R, n_q, hd = q.shape
     n_kv = k.shape[1]
     grp = n_q // n_kv
     visible = np.asarray(k_pos)[None, :] <= np.asarray(q_pos)[:, None]      # [R][T]
     out = np.zeros((R, n_q, hd), dtype=F64)
-    for h in range(n_q):
+
+    def head(h):
         g = h // grp
         s = (q[:, h, :] @ k[:, g, :].T) / math.sqrt(hd)                     # [R][T]
-        if mc is not None:
-            mc.macs += 2 * R * int(visible.sum(axis=1).mean() if R else 0) * hd
-        s = np.where(visible, s, -np.inf)
-        s = s - s.max(axis=1, keepdims=True)
-        p = np.exp(s)
-        p = p / p.sum(axis=1, keepdims=True)
-        out[:, h, :] = p @ v[:, g, :]
+        s[~visible] = -np.inf
+        s -= s.max(axis=1, keepdims=True)
+        np.exp(s, out=s)                                                    # p (unnormalised)
+        s /= s.sum(axis=1, keepdims=True)
+        out[:, h, :] = s @ v[:, g, :]
+
+    if mc is not None:
+        mc.macs += n_q * 2 * R * int(visible.sum(axis=1).mean() if R else 0) * hd
+    if threads > 1 and n_q > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(threads, n_q)) as ex:
+            list(ex.map(head, range(n_q)))
+    else:
+        for h in range(n_q):
+            head(h)
     return out.reshape(R, n_q * hd)
 
 
@@ -391,6 +403,71 @@ def blend_forward(model: Model, tok: np.ndarray, pos: np.ndarray, chunk_starts: 
         if keep_layers:
             h_layers.append(h.copy())
     return BlendResult(K, V, sel, devs, cands, h, h_layers, mc.macs if mc else 0)
+
+
+def blend_replay_rows(tok: np.ndarray, pos: np.ndarray, chunk_starts: Sequence[int], Kc: np.ndarray,
+                      Vc: np.ndarray, force_sel: Sequence[np.ndarray], layer_model, embed_rows: np.ndarray,
+                      dev_rows_1: Sequence[int] = (), h_rows_last: Optional[Sequence[int]] = None,
+                      threads: int = 1, h0: Optional[np.ndarray] = None):
+    """The blend of `blend_forward` in replay mode (forced S_i, R14), n_suf = 0, evaluated only on the rows
+    the comparison needs -- for full-width models whose full oracle run would take hours.
+
+    Every row of every layer is computed exactly as in `blend_layer` / `blend_forward` (same functions,
+    same order); rows whose results cannot reach a compared output are skipped:
+    - layer 0 runs its queries only for S_1 plus `dev_rows_1` (layer-0 K/V of context rows are the realigned
+      cache, P:1750, so no other row is needed);
+    - layer i >= 1 runs Q, K, V for its candidates C_i = S_{i-1} (C_1 restricted to the rows above), takes
+      Delta_kv of all of them, writes S_i's fresh K, V (P:156, R3) and runs attention + W_o + MLP for S_i;
+    - on the last layer attention + MLP run only for `h_rows_last` (a subset of S_{L-1}; all when None).
+    layer_model(i) returns a `Model` whose layers[i] holds layer i's weights (fp64); embed_rows[t] is the
+    embedding row of token t (embed[tok[t]]). h0: layer 0's output for every context row, when the caller
+    already has it (layer 0 does not depend on the selections; it is then not recomputed). Returns dict(K,
+    V [L][N][n_kv][hd] (KV^new), dev {i: (rows, Delta_kv)}, h_rows (token ids), h (their final hidden
+    rows))."""
+    tok = np.asarray(tok)
+    pos = np.asarray(pos).astype(np.int64)
+    N = int(chunk_starts[-1])
+    L = len(Kc)
+    loc = np.zeros(N, dtype=np.int64)
+    for c in range(len(chunk_starts) - 1):
+        loc[chunk_starts[c]:chunk_starts[c + 1]] = np.arange(chunk_starts[c + 1] - chunk_starts[c])
+    m0 = layer_model(0)
+    n_kv, hd, theta = m0.n_kv_heads, m0.head_dim, m0.rope_theta
+    K = np.zeros((L, N, n_kv, hd), dtype=F64)
+    V = np.zeros_like(K)
+    for i in range(L):  # 1. realign (P:208-211)
+        K[i] = realign(Kc[i], loc, pos[:N], theta)
+        V[i] = np.asarray(Vc[i], F64)
+    sel = [np.arange(N)] + [np.sort(np.asarray(s, np.int64)) for s in force_sel[1:L]]
+    rows = np.arange(N) if L == 1 else np.union1d(sel[1], np.asarray(dev_rows_1, np.int64))
+    if L == 1 and h_rows_last is not None:
+        rows = np.sort(np.asarray(h_rows_last, np.int64))
+    # 2. layer 0 on `rows`: queries over the realigned cache, W_o, MLP (P:272, R2)
+    if h0 is not None:
+        h = np.asarray(h0, F64)[rows]
+    else:
+        h = np.asarray(embed_rows, F64)[rows]
+        q, _, _ = qkv(m0, 0, h, pos[rows])
+        a = causal_attention(q, pos[rows], K[0], V[0], pos[:N], threads=threads)
+        h = attn_out_mlp(m0, 0, h, a)
+    del m0
+    dev = {}
+    # 3. layers 1..L-1 in replay (P:150-161, P:2507)
+    for i in range(1, L):
+        mi = layer_model(i)
+        q, k, v = qkv(mi, i, h, pos[rows])
+        dev[i] = (rows.copy(), kv_deviation(k, v, K[i][rows], V[i][rows]))
+        slot = np.searchsorted(rows, sel[i])
+        if len(sel[i]) and not np.array_equal(rows[np.minimum(slot, len(rows) - 1)], sel[i]):
+            raise ValueError("force_sel is not a subset of the candidates")
+        K[i][sel[i]] = k[slot]
+        V[i][sel[i]] = v[slot]
+        qsel = sel[i] if (i < L - 1 or h_rows_last is None) else np.sort(np.asarray(h_rows_last, np.int64))
+        qs = np.searchsorted(rows, qsel)
+        a = causal_attention(q[qs], pos[qsel], K[i], V[i], pos[:N], threads=threads)
+        h = attn_out_mlp(mi, i, h[qs], a)
+        rows = qsel
+    return dict(K=K, V=V, dev=dev, h_rows=rows, h=h)
 
 
 def full_prefill_macs(model: Model, tok, pos) -> int:

@@ -57,16 +57,16 @@ _SIGS = {
     "cb_profile_end": (c_i32, [c_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64), c_i32]),
     "cb_profile_class_name": (ctypes.c_char_p, [c_i32]),
     "cb_nccl_unique_id": (c_i32, [c_vp]),
-    "cb_chunk_hash": (c_u64, [c_vp, c_i32]),
+    "cb_chunk_digest": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_vp]),
     "cb_store_create": (c_i32, [ctypes.c_size_t, c_i32, ctypes.POINTER(c_vp)]),
     "cb_store_destroy": (c_i32, [c_vp]),
-    "cb_store_put": (c_i32, [c_vp, c_u64, c_vp, c_vp, c_i64, c_i32]),
-    "cb_store_lookup": (c_i32, [c_vp, c_u64, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
+    "cb_store_put": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32]),
+    "cb_store_lookup": (c_i32, [c_vp, c_vp, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     "cb_store_stats": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
-    "cb_store_keys": (c_i32, [c_vp, ctypes.POINTER(c_u64), c_i32, ctypes.POINTER(c_i32)]),
-    "cb_blend_request_store": (c_i32, [c_vp, c_vp, ctypes.POINTER(c_u64), ctypes.POINTER(CbLayerW), c_vp, c_vp, c_vp,
+    "cb_store_keys": (c_i32, [c_vp, c_vp, c_i32, ctypes.POINTER(c_i32)]),
+    "cb_blend_request_store": (c_i32, [c_vp, c_vp, c_vp, ctypes.POINTER(CbLayerW), c_vp, c_vp, c_vp,
                                        c_i32, c_i32, c_i32p, c_i32, c_vp, c_vp, c_i32p, c_vp, c_vp, c_vp]),
-    "cb_kv_to_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp, c_i32, c_vp, c_vp, c_i64, c_vp]),
+    "cb_kv_to_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_vp]),
     "cb_controller_ratio": (c_i32, [c_f64, c_f64, c_i64, c_f64, c_f64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64)]),
     "cb_controller_pick_device": (c_i32, [c_f64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64), c_i32, c_f64,
                                           ctypes.POINTER(c_i32)]),

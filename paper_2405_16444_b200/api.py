@@ -240,13 +240,33 @@ def kv_to_paged(ctx: Context, k_blend: torch.Tensor, v_blend: torch.Tensor, bloc
     L, T = k_blend.shape[0], k_blend.shape[1]
     n = T if n_tok is None else int(n_tok)
     check(lib().cb_kv_to_paged(ctx.handle, _p(k_blend), _p(v_blend), L, n, k_blend[0].numel(), _p(block_table),
-                               int(block_size), _p(k_pages), _p(v_pages), k_pages[0].numel(), _stream(stream)))
+                               int(block_size), _p(k_pages), _p(v_pages), int(k_pages.shape[1]), k_pages[0].numel(),
+                               _stream(stream)))
 
 
-def chunk_hash(tokens) -> int:
-    """cb_chunk_hash of a chunk's token ids (host)."""
+def chunk_digest(model_id: bytes, tokens) -> bytes:
+    """cb_chunk_digest: the chunk's 32-byte store key, SHA-256 of (len(model_id) as u32 LE || model_id ||
+    token ids as LE int32) (host)."""
     a = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
-    return int(lib().cb_chunk_hash(a.ctypes.data, a.size))
+    mid = bytes(model_id)
+    out = ctypes.create_string_buffer(32)
+    check(lib().cb_chunk_digest(mid, len(mid), a.ctypes.data if a.size else None, a.size, out))
+    return out.raw
+
+
+def model_identity(shape, dtype: str, weights_id: str) -> bytes:
+    """A model id for chunk_digest: the model configuration plus the caller's weights identifier (e.g. the
+    checkpoint's hash, or the synthetic recipe and seed)."""
+    f = (shape.n_layers, shape.d_model, shape.n_q_heads, shape.n_kv_heads, shape.head_dim, shape.d_ff, shape.vocab,
+         float(shape.rope_theta), float(shape.rms_eps), dtype, weights_id)
+    return repr(f).encode()
+
+
+def _key(key: bytes):
+    b = bytes(key)
+    if len(b) != 32:
+        raise ValueError("a store key is a 32-byte chunk_digest")
+    return ctypes.create_string_buffer(b, 32)
 
 
 class Store:
@@ -268,15 +288,15 @@ class Store:
         except Exception:
             pass
 
-    def put(self, key: int, k: torch.Tensor, v: torch.Tensor):
-        """k, v: [L][n_tok][n_kv][hd] (host or device, contiguous)."""
+    def put(self, key: bytes, k: torch.Tensor, v: torch.Tensor):
+        """key: chunk_digest(...) (32 bytes); k, v: [L][n_tok][n_kv][hd] (host or device, contiguous)."""
         assert k.is_contiguous() and v.is_contiguous() and k.shape == v.shape
-        check(lib().cb_store_put(self.handle, int(key), k.data_ptr(), v.data_ptr(), k.numel() * k.element_size(),
+        check(lib().cb_store_put(self.handle, _key(key), k.data_ptr(), v.data_ptr(), k.numel() * k.element_size(),
                                  int(k.shape[1])))
 
-    def lookup(self, key: int, touch: bool = True) -> int:
+    def lookup(self, key: bytes, touch: bool = True) -> int:
         n = ctypes.c_int32(0)
-        check(lib().cb_store_lookup(self.handle, int(key), int(touch), ctypes.byref(n), None, None))
+        check(lib().cb_store_lookup(self.handle, _key(key), int(touch), ctypes.byref(n), None, None))
         return n.value
 
     def stats(self) -> Dict[str, int]:
@@ -284,21 +304,22 @@ class Store:
         check(lib().cb_store_stats(self.handle, o))
         return dict(zip(("used", "capacity", "entries", "hits", "misses", "evictions"), list(o)))
 
-    def keys(self) -> List[int]:
+    def keys(self) -> List[bytes]:
         n = ctypes.c_int32(0)
         check(lib().cb_store_keys(self.handle, None, 0, ctypes.byref(n)))
-        buf = (ctypes.c_uint64 * max(n.value, 1))()
+        buf = ctypes.create_string_buffer(32 * max(n.value, 1))
         check(lib().cb_store_keys(self.handle, buf, n.value, ctypes.byref(n)))
-        return list(buf[:n.value])
+        return [buf.raw[32 * i:32 * (i + 1)] for i in range(n.value)]
 
 
-def blend_request_store(ctx: Context, store: Store, chunk_keys: Sequence[int], weights: ModelWeights,
+def blend_request_store(ctx: Context, store: Store, chunk_keys: Sequence[bytes], weights: ModelWeights,
                         tok_host: torch.Tensor, pos_host: torch.Tensor, chunk_start: Sequence[int], n_suffix: int,
                         k_blend: torch.Tensor, v_blend: torch.Tensor, k_sched: Sequence[int],
                         h_out_host: torch.Tensor, sel_out_host: Optional[torch.Tensor] = None, stream=None):
     """cb_blend_request_store: chunk KV fetched from the store layer by layer."""
     N = int(chunk_start[-1])
-    keys = (ctypes.c_uint64 * max(len(chunk_keys), 1))(*[int(x) for x in chunk_keys])
+    blob = b"".join(_key(k).raw for k in chunk_keys)
+    keys = ctypes.create_string_buffer(blob, max(len(blob), 32))
     check(lib().cb_blend_request_store(ctx.handle, store.handle, keys, weights.cw, _p(weights.embed), _p(tok_host),
                                        _p(pos_host), N, n_suffix, _i32(chunk_start), len(chunk_start) - 1,
                                        _p(k_blend), _p(v_blend), _i32(k_sched), _p(sel_out_host), _p(h_out_host),
@@ -432,7 +453,7 @@ def op_embed(ctx: Context, embed: torch.Tensor, tok: torch.Tensor, stream=None):
     return h
 
 
-__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "controller_ratio", "controller_pick_device", "kv_to_paged", "Store", "chunk_hash",
+__all__ = ["Context", "Group", "nccl_unique_id", "ModelWeights", "controller_ratio", "controller_pick_device", "kv_to_paged", "Store", "chunk_digest", "model_identity",
            "blend_request_store", "CacheBlendError", "schedule", "rope_realign", "kv_deviation_topk",
            "blend_layer", "blend_forward", "gen_fill", "gen_ints", "op_gemm", "op_attention", "op_rmsnorm",
            "op_embed"]

@@ -361,7 +361,15 @@ extern "C" cb_status cb_check_device_errors(cb_ctx* c) {
   CB_CUDA(cudaMemcpy(&h, c->err_word, sizeof(int), cudaMemcpyDeviceToHost));
   CB_CUDA(cudaMemset(c->err_word, 0, sizeof(int)));
   if (h & CB_DEVERR_FORCE_SEL) { cb_set_error("device: a force_sel token is not a candidate of its layer"); return CB_E_DEVICE; }
-  if (h & CB_DEVERR_POS_RANGE) { cb_set_error("device: |dst_pos - src_pos| >= max_pos in realign"); return CB_E_DEVICE; }
+  if (h & CB_DEVERR_POS_RANGE) {
+    cb_set_error("device: a position is outside [0, max_pos) (pos, or |dst_pos - src_pos| in realign)");
+    return CB_E_DEVICE;
+  }
+  if (h & CB_DEVERR_POS_ORDER) {
+    cb_set_error("device: global positions are not strictly increasing (the attention mask orders keys by token index)");
+    return CB_E_DEVICE;
+  }
+  if (h & CB_DEVERR_PAGE) { cb_set_error("device: a block_table page id is outside [0, n_pages) (nothing written there)"); return CB_E_DEVICE; }
   if (h & CB_DEVERR_COMM) { cb_set_error("device: a peer-memory collective timed out waiting for a rank"); return CB_E_DEVICE; }
   return CB_OK;
 }
@@ -777,7 +785,7 @@ cb_status layer_full(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int N, 
   const size_t B = dtype_bytes(m.dtype);
   EpiParams e{};
   e.kind = EPI_QKV; e.M = T; e.N = qd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
-  e.q_out = c->q; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  e.q_out = c->q; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab; e.max_pos = c->m.max_pos;
   if (b.x_ready && gemm_tc_ok(c, c->x, d, w.w_qkv, d, T, d, e)) set_norm_consumer(c, e);
   else if (!b.x_normed) CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, T, c->x, s));
   CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, T, d, e, 0, s));
@@ -807,7 +815,7 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   // 1. mask the input to the candidate rows and transform them into Q, K, V
   EpiParams e{};
   e.kind = EPI_QKV; e.M = R; e.N = qd + 2 * kvd; e.col0 = 0; e.qd = qd; e.kvd = kvd; e.hd = m.head_dim;
-  e.q_out = c->q; e.k_out = c->kf; e.v_out = c->vf; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab;
+  e.q_out = c->q; e.k_out = c->kf; e.v_out = c->vf; e.row_tok = b.row_tok; e.pos = pos; e.rope_tab = c->rope_tab; e.max_pos = c->m.max_pos;
   if (b.x_ready && gemm_tc_ok(c, c->x, d, w.w_qkv, d, R, d, e)) set_norm_consumer(c, e);
   else CB_TRY(launch_rmsnorm(c, b.h_in, (const float*)w.attn_norm, R, c->x, s));
   // 2. Delta_kv against the loaded entries: fused into the tcgen05 QKV epilogue when every
@@ -865,6 +873,7 @@ extern "C" cb_status cb_blend_layer(cb_ctx* c, int32_t layer, const cb_layer_w* 
   CB_REQUIRE(k_keep == 0 || sel_tok, CB_E_INVALID_ARG, "sel_tok is NULL");
   cudaStream_t s = (cudaStream_t)st;
   const int rows = n_cand + n_suffix;
+  CB_TRY(launch_pos_check(c, pos, N + n_suffix, s));
   if (rows > 0) {
     ProfScope ps_(c, PROF_MISC, s);
     CB_LAUNCH(c, (make_rows_kernel), std::min(256, (rows + 255) / 256), 256, 0, s, cand_tok, n_cand, n_suffix, N, c->row_tok[0]);
@@ -934,6 +943,7 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
     return launch_realign(c, kb, kb, nullptr, nullptr, c->src_pos, pos, 1, N, (long long)layer_stride,
                           (long long)layer_stride, s);
   };
+  CB_TRY(launch_pos_check(c, pos, T, s));  // positions in range and strictly increasing (device error word)
   // (a2) layer 0 in full
   // embedding gather fused with layer 0's attention RMSNorm (unless the per-kernel ablation is on)
   const bool embed_norm = !c->no_fuse_norm;
@@ -1048,12 +1058,24 @@ cb_status blend_request_impl(cb_ctx* c, const cb_layer_w* w, const void* embed, 
   return CB_OK;
 }
 
+// Host-memory positions (request paths): in [0, max_pos) and strictly increasing, checked before any launch.
+cb_status check_host_pos(const cb_ctx* c, const int32_t* pos, int T) {
+  for (int t = 0; t < T; ++t) {
+    CB_REQUIRE(pos[t] >= 0 && pos[t] < c->m.max_pos, CB_E_INVALID_ARG, "pos[%d] = %d outside [0, max_pos = %d)", t,
+               pos[t], c->m.max_pos);
+    CB_REQUIRE(t == 0 || pos[t] > pos[t - 1], CB_E_INVALID_ARG, "pos not strictly increasing at %d (%d after %d)", t,
+               pos[t], pos[t - 1]);
+  }
+  return CB_OK;
+}
+
 cb_status check_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
                         const int32_t* pos_host, int32_t N, int32_t n_suffix, const int32_t* chunk_start,
                         int32_t n_chunks, const void* k_in, const void* v_in, void* k_blend, void* v_blend,
                         const int32_t* k_sched, const void* h_out) {
-  return check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in, v_in, k_blend,
-                       v_blend, k_sched, h_out);
+  CB_TRY(check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in, v_in, k_blend,
+                       v_blend, k_sched, h_out));
+  return check_host_pos(c, pos_host, N + n_suffix);
 }
 
 extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void* embed, const int32_t* tok_host,
@@ -1061,7 +1083,7 @@ extern "C" cb_status cb_blend_request(cb_ctx* c, const cb_layer_w* w, const void
                                       int32_t n_chunks, const void* k_in_host, const void* v_in_host, void* k_blend,
                                       void* v_blend, const int32_t* k_sched, int32_t* sel_out_host,
                                       float* h_out_host, void* st) {
-  CB_TRY(check_forward(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in_host, v_in_host,
+  CB_TRY(check_request(c, w, embed, tok_host, pos_host, N, n_suffix, chunk_start, n_chunks, k_in_host, v_in_host,
                        k_blend, v_blend, k_sched, h_out_host));
   const int T = N + n_suffix;
   const size_t row = (size_t)c->m.n_kv_heads * c->m.head_dim * dtype_bytes(c->m.dtype);

@@ -477,7 +477,7 @@ cb_status p2p_launch(cb_ctx* c, size_t off, long long n, int mode, cudaStream_t 
   // other ranks' kernels (which may need a whole SM) always find free SMs
   const int ctas = c->comm_kind == CB_COMM_LOOPBACK ? (getenv("CB_P2P_LOOP_CTAS") ? atoi(getenv("CB_P2P_LOOP_CTAS")) : 4) : P2P_CTAS;
   CB_LAUNCH(c, p2p_collective_kernel, ctas, P2P_THREADS, 0, s, pt, c->tp_rank, c->tp_world, off, n, mode,
-            c->x_flags_off, c->err_word, c->x_recv_off, (long long)c->max_tokens * c->m.d_model, chunk2);
+            c->x_flags_off, c->err_word, c->x_recv_off, (long long)(c->x_h_bytes / sizeof(float)), chunk2);
   CB_LAUNCHED(c);
   return CB_OK;
 }

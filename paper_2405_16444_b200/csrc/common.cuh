@@ -70,7 +70,8 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 // Device-side error word bits (cb_check_device_errors).
-enum : int { CB_DEVERR_FORCE_SEL = 1, CB_DEVERR_POS_RANGE = 2, CB_DEVERR_COMM = 4 };
+enum : int { CB_DEVERR_FORCE_SEL = 1, CB_DEVERR_POS_RANGE = 2, CB_DEVERR_COMM = 4, CB_DEVERR_POS_ORDER = 8,
+             CB_DEVERR_PAGE = 16 };
 
 // ---- epilogues shared by the SIMT and tcgen05 GEMMs -----------------------------------------
 // acc[m][n] = sum_k A[m][k] B[n][k];   kinds:
@@ -89,7 +90,7 @@ struct EpiParams {
   // EPI_QKV
   void* q_out; void* k_out; void* v_out;
   int col0, qd, kvd, hd;
-  const int* row_tok; const int* pos; const float2* rope_tab;
+  const int* row_tok; const int* pos; const float2* rope_tab; int max_pos;  // pos clamped to [0, max_pos)
   // EPI_QKV fused Delta_kv (tcgen05 path): for candidate rows m < n_cand, per 64-column block b of the
   // k (resp. v) row: dev_part[(2b + 0) * ld_part + m] = ||k_m[b] - k_ref[row_tok[m]][b]||^2, [(2b + 1) ...] v
   const void* k_ref; const void* v_ref; float* dev_part; int n_cand, ld_part;
@@ -112,6 +113,12 @@ struct EpiParams {
   // block of the rank that owns row m, over NVLink) instead of outf / h_out.
   char* push_base[8]; long long push_off; int push_rows;
 };
+// Global position of token `tok` for the RoPE table, clamped so that a position outside [0, max_pos) cannot
+// read past the table (pos_check_kernel reports it through the device error word, CB_DEVERR_POS_RANGE).
+__device__ __forceinline__ int epi_pos(const EpiParams& e, int tok) {
+  return min(max(__ldg(e.pos + tok), 0), e.max_pos - 1);
+}
+
 
 // Output row m of an fp32 epilogue (outf / h_out), or its owner's receive plane when pushing.
 __device__ __forceinline__ float* out_row_f32(const EpiParams& e, float* local, int m) {
@@ -141,7 +148,7 @@ __device__ __forceinline__ void epi_pair(const EpiParams& e, int m, int n, float
       const int c = e.col0 + n;  // logical column in [q | k | v]
       if (c < e.qd + e.kvd) {    // q or k: rotate the pair (2i, 2i+1) of the head
         const int dim = (c < e.qd ? c : c - e.qd) % e.hd;
-        const int p = e.pos[e.row_tok[m]];
+        const int p = epi_pos(e, e.row_tok[m]);
         const float2 cs = e.rope_tab[(size_t)p * (e.hd >> 1) + (dim >> 1)];
         const float r0 = cs.x * a0 - cs.y * a1;
         const float r1 = cs.y * a0 + cs.x * a1;

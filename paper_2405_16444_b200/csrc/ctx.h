@@ -199,6 +199,8 @@ cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_row
 cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int* qrow, const int* qtok, int n,
                             void* kb, void* vb, cudaStream_t s);
 cb_status launch_local_pos(cb_ctx* c, const int* chunk_start_host, int n_chunks, int* src_pos, cudaStream_t s);
+// device positions: 0 <= pos[t] < max_pos (else CB_DEVERR_POS_RANGE) and strictly increasing (else CB_DEVERR_POS_ORDER)
+cb_status launch_pos_check(cb_ctx* c, const int* pos, int T, cudaStream_t s);
 cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* sel_row, cudaStream_t s);
 cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, const void* k_ref, const void* v_ref,
                            const int* cand_tok, int n_cand, int dev_mode, float* dev, cudaStream_t s);

@@ -304,6 +304,28 @@ __global__ void local_pos_kernel(ChunkTable ct, int base_chunk, int* __restrict_
   (void)base_chunk;
 }
 
+// The attention mask compares token indices (key row <= query row), which equals the paper's position mask
+// (causal by original position) only when positions increase with the token index; the RoPE table
+// holds positions [0, max_pos). A violation is reported through the device error word.
+__global__ void pos_check_kernel(const int* __restrict__ pos, int T, int max_pos, int* err) {
+  pdl_enter();
+  int bad = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T; t += gridDim.x * blockDim.x) {
+    const int p = pos[t];
+    if (p < 0 || p >= max_pos) bad |= CB_DEVERR_POS_RANGE;
+    if (t > 0 && p <= pos[t - 1]) bad |= CB_DEVERR_POS_ORDER;
+  }
+  if (bad) atomicOr(err, bad);
+}
+
+cb_status launch_pos_check(cb_ctx* c, const int* pos, int T, cudaStream_t s) {
+  if (T <= 0) return CB_OK;
+  ProfScope ps_(c, PROF_MISC, s);
+  CB_LAUNCH(c, (pos_check_kernel), std::min(64, (T + 255) / 256), 256, 0, s, pos, T, c->m.max_pos, c->err_word);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
 cb_status launch_local_pos(cb_ctx* c, const int* cs, int n_chunks, int* src_pos, cudaStream_t s) {
   for (int b = 0; b < n_chunks; b += 128) {
     ChunkTable ct;
@@ -342,7 +364,8 @@ cb_status launch_sel_out(cb_ctx* c, const int* qtok, int k, int N, int* row, cud
 template <typename T>
 __global__ void kv_to_paged_kernel(const T* __restrict__ k, const T* __restrict__ v, long long src_layer_stride,
                                    int n_layers, int n_tok, int row, const int* __restrict__ block_table,
-                                   int block_size, T* __restrict__ kp, T* __restrict__ vp, long long dst_layer_stride) {
+                                   int block_size, T* __restrict__ kp, T* __restrict__ vp, int n_pages,
+                                   long long dst_layer_stride, int* err) {
   pdl_enter();
   constexpr int V = Vec16<T>::N;
   const int vec_per_row = row / V;
@@ -353,8 +376,12 @@ __global__ void kv_to_paged_kernel(const T* __restrict__ k, const T* __restrict_
     const long long r = i - (long long)l * per_layer;
     const int t = (int)(r / vec_per_row), e = (int)(r - (long long)t * vec_per_row) * V;
     const long long src = l * src_layer_stride + (long long)t * row + e;
-    const long long dst = l * dst_layer_stride +
-                          ((long long)__ldg(block_table + t / block_size) * block_size + t % block_size) * row + e;
+    const int page = __ldg(block_table + t / block_size);
+    if (page < 0 || page >= n_pages) {  // outside the pool: report, never write
+      atomicOr(err, CB_DEVERR_PAGE);
+      continue;
+    }
+    const long long dst = l * dst_layer_stride + ((long long)page * block_size + t % block_size) * row + e;
     st16(kp + dst, ld16(k + src));
     st16(vp + dst, ld16(v + src));
   }
@@ -362,16 +389,17 @@ __global__ void kv_to_paged_kernel(const T* __restrict__ k, const T* __restrict_
 
 extern "C" cb_status cb_kv_to_paged(cb_ctx* c, const void* k_blend, const void* v_blend, int32_t n_layers,
                                     int32_t n_tok, int64_t src_layer_stride, const int32_t* block_table,
-                                    int32_t block_size, void* k_pages, void* v_pages, int64_t dst_layer_stride,
-                                    void* st) {
+                                    int32_t block_size, void* k_pages, void* v_pages, int32_t n_pages,
+                                    int64_t dst_layer_stride, void* st) {
   CB_REQUIRE(c != nullptr, CB_E_INVALID_ARG, "ctx is NULL");
   CB_REQUIRE(n_layers >= 0 && n_tok >= 0 && block_size >= 1, CB_E_INVALID_ARG, "bad sizes");
   if (n_layers == 0 || n_tok == 0) return CB_OK;
   CB_REQUIRE(k_blend && v_blend && block_table && k_pages && v_pages, CB_E_INVALID_ARG, "NULL pointer");
   const int row = c->m.n_kv_heads * c->m.head_dim;
   CB_REQUIRE(src_layer_stride >= (int64_t)n_tok * row, CB_E_SHAPE, "src_layer_stride < n_tok * n_kv * head_dim");
-  CB_REQUIRE(dst_layer_stride >= (int64_t)((n_tok + block_size - 1) / block_size) * block_size * row, CB_E_SHAPE,
-             "dst_layer_stride smaller than the pages of n_tok tokens");
+  CB_REQUIRE(n_pages >= 1, CB_E_INVALID_ARG, "n_pages must be >= 1");
+  CB_REQUIRE(dst_layer_stride >= (int64_t)n_pages * block_size * row, CB_E_SHAPE,
+             "dst_layer_stride smaller than n_pages pages of block_size tokens");
   const uintptr_t al = (uintptr_t)k_blend | (uintptr_t)v_blend | (uintptr_t)k_pages | (uintptr_t)v_pages;
   CB_REQUIRE(al % 16 == 0, CB_E_INVALID_ARG, "KV buffers must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)st;
@@ -381,11 +409,11 @@ extern "C" cb_status cb_kv_to_paged(cb_ctx* c, const void* k_blend, const void* 
   if (c->m.dtype == CB_BF16)
     CB_LAUNCH(c, (kv_to_paged_kernel<bf16>), blocks, 256, 0, s, (const bf16*)k_blend, (const bf16*)v_blend,
               (long long)src_layer_stride, n_layers, n_tok, row, block_table, block_size, (bf16*)k_pages,
-              (bf16*)v_pages, (long long)dst_layer_stride);
+              (bf16*)v_pages, n_pages, (long long)dst_layer_stride, c->err_word);
   else
     CB_LAUNCH(c, (kv_to_paged_kernel<float>), blocks, 256, 0, s, (const float*)k_blend, (const float*)v_blend,
               (long long)src_layer_stride, n_layers, n_tok, row, block_table, block_size, (float*)k_pages,
-              (float*)v_pages, (long long)dst_layer_stride);
+              (float*)v_pages, n_pages, (long long)dst_layer_stride, c->err_word);
   CB_LAUNCHED(c);
   return CB_OK;
 }

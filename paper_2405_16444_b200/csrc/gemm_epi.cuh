@@ -62,7 +62,7 @@ __device__ __forceinline__ float epi16(const EpiParams& e, int m, int n, const f
     const int c = e.col0 + n;
     if (c < e.qd + e.kvd) {  // q or k head: rotate pairs (2i, 2i+1) at the row's global position
       const int dim = (c < e.qd ? c : c - e.qd) % e.hd;
-      const int p = __ldg(e.pos + __ldg(e.row_tok + m));
+      const int p = epi_pos(e, __ldg(e.row_tok + m));
       const float4* cs = reinterpret_cast<const float4*>(e.rope_tab + (size_t)p * (e.hd >> 1) + (dim >> 1));
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -146,7 +146,7 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
     if (my_ok) my_a = cont ? my_m : (e.res_row ? __ldg(e.res_row + my_m) : my_m);
   }
   if constexpr (KIND == EPI_QKV) {
-    if (my_ok) { my_a = __ldg(e.row_tok + my_m); my_b = __ldg(e.pos + my_a); }
+    if (my_ok) { my_a = __ldg(e.row_tok + my_m); my_b = epi_pos(e, my_a); }
   }
   int ra[8], rb[8];
 #pragma unroll
@@ -339,7 +339,7 @@ __device__ __forceinline__ void qkv_prefetch(const EpiParams& e, int m, bool row
   const int c0 = e.col0 + n0;
   const int c1 = min(e.col0 + e.N, c0 + out_n);  // exclusive
   if (c0 < e.qd + e.kvd) {  // rope row (cos, sin of all pairs) at the row's position
-    const int p = __ldg(e.pos + tok);
+    const int p = epi_pos(e, tok);
     prefetch_l2(e.rope_tab + (size_t)p * (e.hd >> 1), (uint32_t)(e.hd >> 1) * 8u);
   }
   if (e.dev_part != nullptr && m < e.n_cand && c1 > e.qd) {
@@ -430,7 +430,7 @@ __device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, 
   int tok = 0, p = 0;
   if (row_ok) {
     tok = __ldg(e.row_tok + m);
-    p = __ldg(e.pos + tok);
+    p = epi_pos(e, tok);
   }
   float dacc = 0.f;
 #pragma unroll 1

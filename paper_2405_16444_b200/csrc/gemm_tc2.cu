@@ -328,7 +328,9 @@ cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int 
                           int bn, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p, float* tscr,
                           int* tcnt, cudaStream_t s) {
   ProfScope ps_(c, PROF_GEMM, s);
-  if (e.kind != EPI_RESID) ksplit = 1;
+  // k-split chains continue from the running sum in local h_out; a peer-memory push (fused reduce-scatter)
+  // sends each piece's rows to their owner instead, so pushed GEMMs always run whole tiles
+  if (e.kind != EPI_RESID || e.push_base[0] != nullptr) ksplit = 1;
   if (ksplit > 1) tail_p = 1;
   if (bn == 224) {  // SwiGLU only: 112 gate + 112 up columns (14336 = 128 x 112 features, Mistral d_ff)
     CB_REQUIRE(e.kind == EPI_SWIGLU, CB_E_INVALID_ARG, "224-wide pair tiles are for the SwiGLU GEMM only");

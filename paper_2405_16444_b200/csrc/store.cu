@@ -11,13 +11,16 @@
 #include <cstring>
 #include <list>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 
 #include "ctx.h"
 
 namespace {
+std::string key_str(const cb_chunk_key* k) { return std::string(reinterpret_cast<const char*>(k->bytes), 32); }
+
 struct Entry {
-  uint64_t key;
+  std::string key;  // the chunk's 32-byte digest (model identity || token ids)
   void* k;
   void* v;
   int64_t bytes;  // of K (and of V)
@@ -33,7 +36,7 @@ struct cb_store {
   bool pinned;
   std::mutex mu;
   std::list<Entry> lru;  // front = most recently used
-  std::unordered_map<uint64_t, std::list<Entry>::iterator> index;
+  std::unordered_map<std::string, std::list<Entry>::iterator> index;  // full digest -> entry
   long long hits = 0, misses = 0, evictions = 0;
 };
 
@@ -58,20 +61,81 @@ void* host_alloc(cb_store* st, size_t n) {
 }
 }  // namespace
 
-// 64-bit FNV-1a over the chunk's token ids (little-endian int32 bytes), then a splitmix64 finaliser.
-extern "C" uint64_t cb_chunk_hash(const int32_t* tokens, int32_t n_tok) {
-  uint64_t h = 1469598103934665603ull;
-  for (int32_t i = 0; i < n_tok && tokens; ++i) {
-    const uint32_t t = (uint32_t)tokens[i];
-    for (int b = 0; b < 4; ++b) {
-      h ^= (t >> (8 * b)) & 0xFFu;
-      h *= 1099511628211ull;
+// ---- SHA-256 (FIPS 180-4), host only ----------------------------------------------------------------
+namespace {
+struct Sha256 {
+  uint32_t h[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au, 0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+  uint8_t buf[64];
+  size_t n = 0;        // bytes in buf
+  uint64_t total = 0;  // message bytes so far
+  static uint32_t rotr(uint32_t x, int r) { return (x >> r) | (x << (32 - r)); }
+  void block(const uint8_t* p) {
+    static const uint32_t K[64] = {
+        0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,
+        0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,
+        0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+        0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,
+        0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
+        0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+        0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+        0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
+    uint32_t w[64];
+    for (int i = 0; i < 16; ++i)
+      w[i] = (uint32_t)p[4 * i] << 24 | (uint32_t)p[4 * i + 1] << 16 | (uint32_t)p[4 * i + 2] << 8 | p[4 * i + 3];
+    for (int i = 16; i < 64; ++i) {
+      const uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
+      const uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
+      w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    for (int i = 0; i < 64; ++i) {
+      const uint32_t t1 = hh + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + K[i] + w[i];
+      const uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+      hh = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+  }
+  void update(const void* data, size_t len) {
+    const uint8_t* p = static_cast<const uint8_t*>(data);
+    total += len;
+    while (len > 0) {
+      const size_t take = std::min(len, 64 - n);
+      memcpy(buf + n, p, take);
+      n += take; p += take; len -= take;
+      if (n == 64) { block(buf); n = 0; }
     }
   }
-  h ^= (uint64_t)(uint32_t)n_tok * 0x9E3779B97F4A7C15ull;
-  h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
-  h = (h ^ (h >> 27)) * 0x94D049BB133111EBull;
-  return h ^ (h >> 31);
+  void final(uint8_t out[32]) {
+    const uint64_t bits = total * 8;
+    const uint8_t one = 0x80, zero = 0;
+    update(&one, 1);
+    while (n != 56) update(&zero, 1);
+    uint8_t len[8];
+    for (int i = 0; i < 8; ++i) len[i] = (uint8_t)(bits >> (56 - 8 * i));
+    update(len, 8);
+    for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 4; ++j) out[4 * i + j] = (uint8_t)(h[i] >> (24 - 8 * j));
+  }
+};
+}  // namespace
+
+// The chunk's key: SHA-256 over (u32 LE length of model_id || model_id || the token ids as LE int32), so KV
+// of one model never answers a lookup for another and keys are collision resistant.
+extern "C" cb_status cb_chunk_digest(const void* model_id, int32_t model_id_len, const int32_t* tokens, int32_t n_tok,
+                                     cb_chunk_key* out) {
+  CB_REQUIRE(out && model_id_len >= 0 && n_tok >= 0 && (model_id_len == 0 || model_id) && (n_tok == 0 || tokens),
+             CB_E_INVALID_ARG, "cb_chunk_digest: bad arguments");
+  Sha256 sh;
+  uint8_t le[4];
+  for (int b = 0; b < 4; ++b) le[b] = (uint8_t)((uint32_t)model_id_len >> (8 * b));
+  sh.update(le, 4);
+  if (model_id_len) sh.update(model_id, (size_t)model_id_len);
+  for (int32_t i = 0; i < n_tok; ++i) {
+    for (int b = 0; b < 4; ++b) le[b] = (uint8_t)((uint32_t)tokens[i] >> (8 * b));
+    sh.update(le, 4);
+  }
+  sh.final(out->bytes);
+  return CB_OK;
 }
 
 extern "C" cb_status cb_store_create(size_t capacity_bytes, int32_t pinned, cb_store** out) {
@@ -90,9 +154,10 @@ extern "C" cb_status cb_store_destroy(cb_store* s) {
   return CB_OK;
 }
 
-extern "C" cb_status cb_store_put(cb_store* s, uint64_t key, const void* k, const void* v, int64_t bytes,
+extern "C" cb_status cb_store_put(cb_store* s, const cb_chunk_key* key_d, const void* k, const void* v, int64_t bytes,
                                   int32_t n_tok) {
-  CB_REQUIRE(s && k && v && bytes > 0 && n_tok > 0, CB_E_INVALID_ARG, "cb_store_put: bad arguments");
+  CB_REQUIRE(s && key_d && k && v && bytes > 0 && n_tok > 0, CB_E_INVALID_ARG, "cb_store_put: bad arguments");
+  const std::string key = key_str(key_d);
   CB_REQUIRE(2 * (size_t)bytes <= s->capacity, CB_E_SHAPE, "entry of %lld bytes exceeds the store capacity %zu",
              (long long)(2 * bytes), s->capacity);
   std::lock_guard<std::mutex> lk(s->mu);
@@ -138,11 +203,11 @@ extern "C" cb_status cb_store_put(cb_store* s, uint64_t key, const void* k, cons
 
 // fetch_kv's lookup ("returns -1 if the KV cache is not in the system"): n_tok_out = the entry's
 // tokens, or -1 on a miss. touch != 0 counts a hit / miss and moves a hit to the front of the LRU order.
-extern "C" cb_status cb_store_lookup(cb_store* s, uint64_t key, int32_t touch, int32_t* n_tok_out,
+extern "C" cb_status cb_store_lookup(cb_store* s, const cb_chunk_key* key, int32_t touch, int32_t* n_tok_out,
                                      const void** k_out, const void** v_out) {
-  CB_REQUIRE(s && n_tok_out, CB_E_INVALID_ARG, "cb_store_lookup: bad arguments");
+  CB_REQUIRE(s && key && n_tok_out, CB_E_INVALID_ARG, "cb_store_lookup: bad arguments");
   std::lock_guard<std::mutex> lk(s->mu);
-  auto it = s->index.find(key);
+  auto it = s->index.find(key_str(key));
   if (it == s->index.end()) {
     if (touch) ++s->misses;
     *n_tok_out = -1;
@@ -173,20 +238,20 @@ extern "C" cb_status cb_store_stats(cb_store* s, int64_t* out6) {
 }
 
 // Keys of the store in LRU order (most recent first), up to n.
-extern "C" cb_status cb_store_keys(cb_store* s, uint64_t* keys, int32_t n, int32_t* n_out) {
+extern "C" cb_status cb_store_keys(cb_store* s, cb_chunk_key* keys, int32_t n, int32_t* n_out) {
   CB_REQUIRE(s && n_out && (n == 0 || keys), CB_E_INVALID_ARG, "cb_store_keys: bad arguments");
   std::lock_guard<std::mutex> lk(s->mu);
   int i = 0;
   for (auto& e : s->lru) {
     if (i >= n) break;
-    keys[i++] = e.key;
+    memcpy(keys[i++].bytes, e.key.data(), 32);
   }
   *n_out = (int32_t)s->lru.size();
   return CB_OK;
 }
 
 // The blend request fetching each chunk's KV from the store (layer by layer, on the copy stream).
-extern "C" cb_status cb_blend_request_store(cb_ctx* c, cb_store* store, const uint64_t* chunk_keys,
+extern "C" cb_status cb_blend_request_store(cb_ctx* c, cb_store* store, const cb_chunk_key* chunk_keys,
                                             const cb_layer_w* w, const void* embed, const int32_t* tok_host,
                                             const int32_t* pos_host, int32_t N, int32_t n_suffix,
                                             const int32_t* chunk_start, int32_t n_chunks, void* k_blend,
@@ -207,10 +272,11 @@ extern "C" cb_status cb_blend_request_store(cb_ctx* c, cb_store* store, const ui
   {
     for (size_t ci = 0; ci < ent.size(); ++ci) {
       const int n_c = chunk_start[ci + 1] - chunk_start[ci];
-      auto it = store->index.find(chunk_keys[ci]);
+      auto it = store->index.find(key_str(&chunk_keys[ci]));
       if (it == store->index.end()) {
         ++store->misses;
-        cb_set_error("chunk %zu (key %016llx) is not in the KV store", ci, (unsigned long long)chunk_keys[ci]);
+        const uint8_t* kb = chunk_keys[ci].bytes;
+        cb_set_error("chunk %zu (key %02x%02x%02x%02x...) is not in the KV store", ci, kb[0], kb[1], kb[2], kb[3]);
         return CB_E_MISS;
       }
       CB_REQUIRE(it->second->n_tok == n_c && it->second->bytes == (int64_t)((size_t)L * n_c * row), CB_E_SHAPE,

@@ -5,7 +5,7 @@ no attention, no selection). Both the oracle (`oracle/`) and the CUDA path draw
 their inputs from this module: the oracle through the numpy generator
 (`synth.counter_rng`), the CUDA path either by uploading these arrays or by
 running the library's own implementation of the same counter RNG spec
-(`cb_gen_fill`), which `tests/test_gen_parity.py` pins bit-for-bit.
+(`cb_gen_fill`), which `tests/test_gpu_parity.py::test_gen_fill_bitexact` pins bit-for-bit.
 
 Model shapes come from the public model configs (PAPER.md names the models at
 P:1819 but not their shapes). Random-init recipe
@@ -180,6 +180,31 @@ def random_cache(m: ModelShape, layer: int, n_tok: int, seed: int, dtype: str, k
     """Random-cache mode: cached K (already rotated at local positions) / V rows of one layer."""
     return rng.values(seed, cache_stream(layer, kind), n_tok * m.kvd, 1.0, 0.0, dtype).reshape(
         n_tok, m.n_kv_heads, m.head_dim)
+
+
+STREAM_PERM = 0x5E1
+
+
+def random_order(seed: int, stream: int, n: int) -> np.ndarray:
+    """A seeded permutation of 0..n-1 (argsort of counter-RNG keys, ties by index)."""
+    keys = rng.raw(seed, stream, 0, n)
+    return np.argsort(keys, kind="stable").astype(np.int64)
+
+
+def nested_selection(seed: int, n_ctx: int, k_sched: Sequence[int]) -> List[np.ndarray]:
+    """Seeded replay selections S_1 >= S_2 >= ... for forced-selection runs (k_sched[i] = |S_i|, i >= 1):
+    S_i = the first k_i tokens of one seeded permutation, sorted; nested because k_i is non-increasing.
+    Entry 0 is all context tokens. An input recipe only (no deviation, no top-k)."""
+    order = random_order(seed, STREAM_PERM, n_ctx)
+    out = [np.arange(n_ctx, dtype=np.int64)]
+    for k in list(k_sched)[1:]:
+        out.append(np.sort(order[:int(k)]))
+    return out
+
+
+def sample_rows(seed: int, stream: int, n: int, k: int) -> np.ndarray:
+    """k distinct seeded rows of 0..n-1, sorted."""
+    return np.sort(random_order(seed, stream, n)[:min(k, n)])
 
 
 # BASELINE.json configs, as concrete requests (SURVEY.md §8(d) table).

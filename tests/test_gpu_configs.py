@@ -1,0 +1,172 @@
+"""GPU parity at every BASELINE.json configuration, at the configurations' full model width (tests/fullsize.py
+states the inputs, the truncated-depth design and the per-row tolerances):
+
+- configs 1-3 (Mistral-7B 6x512 15 %, Yi-34B 8x1024 at 5/15/30/50 %, Llama-70B 10x1024 15 %): cb_blend_forward
+  in replay mode against the fp64 oracle's row-restricted replay (fresh K/V rows per kv head, untouched rows
+  at the bf16 realign bound / bitwise, every evaluated Delta_kv per candidate, sampled final h rows per row),
+  then free-running: S_1 against the oracle's own top-k_1 over all N tokens, flips only inside the measured
+  Delta_kv error band; later layers sorted / nested / exactly the top-k of the reported Delta_kv;
+- full depth (Mistral 32 layers, Yi 60 layers, the launch configuration bench.py times): S_1, S_2 and their
+  Delta_kv bitwise equal to the oracle-checked truncated run, every layer's selection well formed;
+- config 5 (batched): four variable-length requests (4 x 256, 8 x 1024 and two ragged ones from the config's
+  own list) blended one after another through ONE context sized for the largest, as bench.py --config batched;
+- attention at the configurations' head shapes (GQA 7 = Yi 56/8 and its TP8 shard 7/1, Llama 64/8 and 8/1,
+  Mistral 32/8) against the oracle per (row, head);
+- N = 0 (all rows suffix: the chunk precompute path bench.py uses) against the oracle's full prefill.
+- sensitivity: a 1 % error injected into one kv head of one layer's weights on the GPU only must fail the
+  replay comparison."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import cacheblend_oracle as O
+from synth import counter_rng as rng
+from synth import workload as W
+from tests import fullsize as F
+from tests.helpers import oracle_model, shape, topk_tokens
+
+pytestmark = pytest.mark.gpu
+
+
+def _replay_and_free(P, c, ctx=None, stats=None):
+    ora = F.oracle(c)
+    mw, k_in, v_in, tok, pos = F.gpu_inputs(P, c)
+    ctx = ctx or P.Context(c.s, "bf16", max_tokens=c.N, max_pos=2 * c.N)
+    stats = {} if stats is None else stats
+    rep = F.run_gpu(P, ctx, mw, k_in, v_in, tok, pos, c, c.ks, force=True)
+    bad = []
+    for i in range(1, F.L_T):
+        if not np.array_equal(rep["sel"][i], c.S[i]):
+            bad.append(f"layer {i}: replay did not keep the forced selection")
+    bad += F.check_kv(rep["kb"], rep["vb"], c.Kc, c.Vc, ora, c.S, F.L_T, stats)
+    bad += F.check_dev(rep["dev"], ora, c.S, F.L_T, stats)
+    bad += F.check_h(rep["h"], ora, c.S[-1], stats)
+    free = F.run_gpu(P, ctx, mw, k_in, v_in, tok, pos, c, c.ks, force=False)
+    bad += F.check_free_selection(free["sel"], free["dev"], ora, c.ks, c.N, stats)
+    if not np.array_equal(free["dev"][1], rep["dev"][1]):
+        bad.append("layer 1: Delta_kv differs between the replay and the free run (it precedes the selection)")
+    return bad, stats, dict(mw=mw, k_in=k_in, v_in=v_in, tok=tok, pos=pos, ctx=ctx, rep=rep, free=free, ora=ora)
+
+
+@pytest.mark.parametrize("name", list(F.CONFIGS))
+def test_config_parity(P, name):
+    c = F.case_for(name)
+    bad, stats, _ = _replay_and_free(P, c)
+    print(name, {k: (round(v, 5) if isinstance(v, float) else v) for k, v in stats.items()})
+    assert not bad, "\n".join(bad)
+
+
+def test_batched_requests_parity(P):
+    reqs = F.batched_requests()
+    cases = [F.make_case(f"batched{j}", "mistral-7b", r.chunk_lens, r.ratio, req_seed=r.seed)
+             for j, r in enumerate(reqs)]
+    nmax = max(c.N for c in cases)
+    ctx = P.Context(cases[0].s, "bf16", max_tokens=nmax, max_pos=2 * nmax)
+    bad = []
+    for c in cases:
+        b, stats, _ = _replay_and_free(P, c, ctx=ctx)
+        print(c.name, c.req.chunk_lens, {k: (round(v, 5) if isinstance(v, float) else v) for k, v in stats.items()})
+        bad += [f"{c.name}: {x}" for x in b]
+    assert not bad, "\n".join(bad)
+
+
+def test_injected_error_is_caught(P):
+    """A 1 % error in ONE kv head of ONE layer (W_k rows of kv head 5 at layer 2 scaled by 1.01, GPU side
+    only) must fail the per-(row, head) comparison, and the unperturbed run must pass it."""
+    c = F.case_for("mistral15")
+    ora = F.oracle(c)
+    mw, k_in, v_in, tok, pos = F.gpu_inputs(P, c)
+    ctx = P.Context(c.s, "bf16", max_tokens=c.N, max_pos=2 * c.N)
+    base = F.run_gpu(P, ctx, mw, k_in, v_in, tok, pos, c, c.ks, force=True)
+    assert not F.check_kv(base["kb"], base["vb"], c.Kc, c.Vc, ora, c.S, F.L_T, {})
+    s = c.s
+    r0 = s.qd + 5 * s.head_dim
+    with torch.no_grad():
+        w = mw.layers[2]["w_qkv"]
+        w[r0:r0 + s.head_dim] = (w[r0:r0 + s.head_dim].float() * 1.01).to(w.dtype)
+    bad = F.check_kv(F.run_gpu(P, ctx, mw, k_in, v_in, tok, pos, c, c.ks, force=True)["kb"], base["vb"], c.Kc,
+                     c.Vc, ora, c.S, F.L_T, {})
+    assert any("layer 2: fresh K" in b and "head 5" in b for b in bad), bad
+    assert not any("layer 1" in b for b in bad), bad
+
+
+@pytest.mark.parametrize("name", ["mistral15", "yi15"])
+def test_full_depth_matches_checked_truncation(P, name):
+    """The full-depth blend (bench.py's launch configuration) computes layers 0-2 exactly as the truncated
+    model the oracle checked: S_1, S_2 and Delta_kv of layers 1-2 are bitwise equal; every later layer's
+    selection is sorted, sized k_i, nested and the top-k of its reported Delta_kv; V rows never selected
+    keep the cache bytes."""
+    c = F.case_for(name)
+    mw, k_in, v_in, tok, pos = F.gpu_inputs(P, c)
+    ctx = P.Context(c.s, "bf16", max_tokens=c.N, max_pos=2 * c.N)
+    trunc = F.run_gpu(P, ctx, mw, k_in, v_in, tok, pos, c, c.ks, force=False)
+    del mw, k_in, v_in, ctx
+    torch.cuda.empty_cache()
+    mwf, kf, vf, tok, pos = F.gpu_inputs(P, c, shape=c.full)
+    ctxf = P.Context(c.full, "bf16", max_tokens=c.N, max_pos=2 * c.N)
+    full = F.run_gpu(P, ctxf, mwf, kf, vf, tok, pos, c, c.ks_full, force=False)
+    for i in (1, 2):
+        np.testing.assert_array_equal(full["sel"][i], trunc["sel"][i])
+        np.testing.assert_array_equal(full["dev"][i], trunc["dev"][i])
+    prev = np.arange(c.N)
+    L = c.full.n_layers
+    for i in range(1, L):
+        si = full["sel"][i]
+        assert len(si) == c.ks_full[i] and np.all(np.diff(si) > 0) and np.isin(si, prev).all(), i
+        d = full["dev"][i][:len(prev)].astype(np.float64)
+        assert np.all(np.isfinite(d)) and np.all(d >= 0), i
+        np.testing.assert_array_equal(topk_tokens(d, prev, c.ks_full[i]), si, err_msg=f"layer {i}")
+        prev = si
+    for i in (L // 2, L - 1):
+        keep = np.setdiff1d(np.arange(c.N), full["sel"][i])
+        assert torch.equal(full["vb"][i][keep], vf[i][keep]), i
+    assert np.all(np.isfinite(full["h"]))
+    del mwf, kf, vf, ctxf, full
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n_q,n_kv,T,n_sel", [(56, 8, 8192, 1475), (7, 1, 8192, 4916), (64, 8, 10240, 1844),
+                                              (8, 1, 10240, 1844), (32, 8, 3072, 553), (28, 4, 2048, 1000)])
+def test_attention_config_heads(P, n_q, n_kv, T, n_sel):
+    """tcgen05 attention at the configurations' head shapes (GQA 7: Yi 56/8, its TP8 shard 7/1 and TP2 28/4;
+    Llama 64/8 and 8/1; Mistral 32/8), gathered query rows, against the oracle per (row, head)."""
+    s = shape("small", n_q_heads=n_q, n_kv_heads=n_kv)
+    g = lambda st, n, H: rng.values(21, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
+    q, k, v = g(1, n_sel, n_q), g(2, T, n_kv), g(3, T, n_kv)
+    rows = W.sample_rows(22, 0x31, T, n_sel).astype(np.int32)
+    ctx = P.Context(s, "bf16", max_tokens=T)
+    out = P.api.op_attention(ctx, F.to_dev(q, torch.bfloat16), F.to_dev(np.arange(n_sel, dtype=np.int32), torch.int32),
+                             F.to_dev(rows, torch.int32), F.to_dev(k, torch.bfloat16), F.to_dev(v, torch.bfloat16),
+                             T, impl=2)
+    pos = np.arange(T)
+    ref = O.causal_attention(q, pos[rows], k, v, pos, threads=F.THREADS).reshape(n_sel, n_q, s.head_dim)
+    e = F.row_head_errors(out.float().cpu().numpy().reshape(n_sel, n_q, s.head_dim), ref)
+    assert e.max() < F.KV_TOL, (e.max(), np.unravel_index(e.argmax(), e.shape))
+
+
+@pytest.mark.parametrize("name,dtype,lens,layers,tol", [("tiny", "f32", (96,), 2, 1e-4), ("small", "bf16", (333,), 3, 2e-2),
+                                                        ("tiny", "f32", (17,), 3, 1e-4)])
+def test_all_suffix_is_full_prefill(P, name, dtype, lens, layers, tol):
+    """N = 0, every row a suffix row (how bench.py and the full-size tests precompute chunk caches):
+    K/V of every layer and the final h equal the oracle's full prefill (the textbook forward)."""
+    s = shape(name, n_layers=layers)
+    m = oracle_model(s, 5, dtype)
+    T = int(sum(lens))
+    req = W.Request([T], 0, 5, 0.15)
+    tok, loc = req.tokens(s.vocab), np.arange(T)
+    Kf, Vf, hf = O.full_prefill(m, tok, loc)
+    td = P.api.TORCH_DTYPES[dtype]
+    ctx = P.Context(s, dtype, max_tokens=T)
+    mw = P.ModelWeights.synth(s, 5, dtype, F.DEV)
+    kb = torch.empty(layers, T, s.n_kv_heads, s.head_dim, dtype=td, device=F.DEV)
+    vb = torch.empty_like(kb)
+    h = P.blend_forward(ctx, mw, F.to_dev(tok, torch.int32), F.to_dev(loc, torch.int32), [0], T, None, None, kb, vb,
+                        [0] * layers)
+    torch.cuda.synchronize()
+    ctx.check_device_errors()
+    for i in range(layers):
+        ek = F.row_head_errors(kb[i].float().cpu().numpy(), Kf[i])
+        ev = F.row_head_errors(vb[i].float().cpu().numpy(), Vf[i])
+        assert ek.max() < tol and ev.max() < tol, (i, ek.max(), ev.max())
+    eh = np.linalg.norm(h.cpu().numpy() - hf, axis=1) / np.linalg.norm(hf, axis=1)
+    assert eh.max() < tol, eh.max()

@@ -11,7 +11,7 @@ from oracle import cacheblend_oracle as O
 from synth import counter_rng as rng
 from synth import workload as W
 from tests.gpu_helpers import DEV, near_tie_ok, np32, run_blend, to_dev
-from tests.helpers import oracle_model, rel_err, request_inputs, round_to, shape
+from tests.helpers import band_check, oracle_model, rel_err, request_inputs, round_to, shape, topk_tokens
 
 pytestmark = pytest.mark.gpu
 
@@ -414,10 +414,10 @@ def test_blend_small_bf16_replay(P, n_suf):
     for i in range(1, s.n_layers):
         d = res["dev"][i][:len(ora.cand[i])]
         assert rel_err(d, ora.dev[i]) < TOL["bf16"], f"dev layer {i}"
-        # the forced (oracle) set is also (nearly) the GPU's own top-k of its own deviations
-        gsel = O.select_hkvd(d, ora.cand[i], ks[i])
-        jac = len(set(gsel) & set(ora.sel[i])) / max(1, len(set(gsel) | set(ora.sel[i])))
-        assert jac > 0.8, f"layer {i} Jaccard {jac}"
+        # the GPU's own top-k of its own deviations differs from the forced (oracle) set only inside the
+        # measured Delta_kv error band around the k-th value (R14)
+        ok, flips, band = band_check(topk_tokens(d, ora.cand[i], ks[i]), d, ora.dev[i], ora.cand[i], ks[i])
+        assert ok, f"layer {i}: {flips} flips outside the band {band}"
 
 
 def test_blend_layer_api_steps_match_oracle(P):
@@ -502,6 +502,16 @@ def test_kv_to_paged_bitexact(P, dtype, T, bs):
     for src, dst in ((k, kp), (v, vp)):
         want = O.kv_to_paged(np32(src), table, bs, nb + 5)
         np.testing.assert_array_equal(np32(dst), want)  # bit-exact copy (NaN where nothing is written)
+    ctx.check_device_errors()
+    # a page id outside the pool is reported and not written
+    bad = table.copy()
+    bad[-1] = nb + 5
+    kp2, vp2 = kp.clone(), vp.clone()
+    P.api.kv_to_paged(ctx, k, v, to_dev(bad, torch.int32), bs, kp2, vp2)
+    torch.cuda.synchronize()
+    with pytest.raises(P.CacheBlendError, match="page id"):
+        ctx.check_device_errors()
+    assert torch.equal(kp2[:, :nb + 5].isnan(), kp.isnan())  # nothing written outside the table's pages
 
 
 # ---- the request path through the chunk KV store -----------------------------------------
@@ -514,14 +524,16 @@ def test_blend_request_store_equals_forward(P, name, dtype, n_suf):
     a = run_blend(P, s, dtype, 6, req, tok, pos, cs, Kc, Vc, ks)
     td = P.api.TORCH_DTYPES[dtype]
     store = P.api.Store(1 << 30, pinned=True)
+    mid = P.api.model_identity(s, dtype, "synth seed 6")
     keys = []
     for c in range(len(cs) - 1):
         sl = slice(int(cs[c]), int(cs[c + 1]))
-        key = P.api.chunk_hash(tok[sl])
+        key = P.api.chunk_digest(mid, tok[sl])
         keys.append(key)
         store.put(key, torch.from_numpy(np.ascontiguousarray(Kc[:, sl])).to(td).contiguous(),
                   torch.from_numpy(np.ascontiguousarray(Vc[:, sl])).to(td).contiguous())
-    store.put(12345, torch.zeros(1, 4, 1, 1), torch.zeros(1, 4, 1, 1))  # most recent before the request
+    store.put(P.api.chunk_digest(b"other", [1, 2]), torch.zeros(1, 4, 1, 1), torch.zeros(1, 4, 1, 1))  # most recent
+    other_model = P.api.chunk_digest(P.api.model_identity(s, dtype, "another checkpoint"), tok[int(cs[-2]):int(cs[-1])])
     T = req.n_total
     kb = torch.empty(s.n_layers, T, s.n_kv_heads, s.head_dim, dtype=td, device=DEV)
     vb = torch.empty_like(kb)
@@ -529,8 +541,8 @@ def test_blend_request_store_equals_forward(P, name, dtype, n_suf):
     toks = torch.from_numpy(tok.astype(np.int32)).pin_memory()
     poss = torch.from_numpy(pos.astype(np.int32)).pin_memory()
     with pytest.raises(P.CacheBlendError, match="not in the KV store"):
-        P.api.blend_request_store(a["ctx"], store, keys[:-1] + [999], a["mw"], toks, poss, list(cs), n_suf, kb, vb,
-                                  ks, hh)
+        P.api.blend_request_store(a["ctx"], store, keys[:-1] + [other_model], a["mw"], toks, poss, list(cs), n_suf,
+                                  kb, vb, ks, hh)
     P.api.blend_request_store(a["ctx"], store, keys, a["mw"], toks, poss, list(cs), n_suf, kb, vb, ks, hh)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(np32(kb), a["K"])
@@ -604,3 +616,30 @@ def test_topk_block_size_bitwise(P, threads):
         ctx.set_option("topk_threads", t)
         res.append(P.api.kv_deviation_topk(ctx, kn, vn, ref, ref, cand, 1234))
     assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("bad", ["range", "order"])
+def test_bad_positions_are_reported(P, bad):
+    """Positions outside [0, max_pos) or not strictly increasing (the attention mask compares token indices,
+    which is the paper's position mask only for increasing positions) raise CB_E_DEVICE after a device
+    forward (the RoPE index is clamped, so no out-of-bounds read), and CB_E_INVALID_ARG before any launch on
+    the host-buffer request path."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("tiny", 1, [32, 32], 0, "f32", 0.2, n_layers=3)
+    pos = pos.copy()
+    if bad == "range":
+        pos[40] = 5000
+    else:
+        pos[40] = pos[39]
+    ctx = P.Context(s, "f32", max_tokens=req.n_total, max_pos=1024)
+    with pytest.raises(P.CacheBlendError, match="position"):
+        run_blend(P, s, "f32", 1, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx)
+    ctx.check_device_errors()  # the error word was cleared by the report
+    mw = P.ModelWeights.synth(s, 1, "f32", DEV)
+    T = req.n_total
+    kb = torch.empty(s.n_layers, T, s.n_kv_heads, s.head_dim, device=DEV)
+    vb = torch.empty_like(kb)
+    hh = torch.empty(ks[-1], s.d_model).pin_memory()
+    with pytest.raises(P.CacheBlendError, match="pos"):
+        P.api.blend_request(ctx, mw, torch.from_numpy(tok.astype(np.int32)), torch.from_numpy(pos.astype(np.int32)),
+                            list(cs), 0, torch.from_numpy(Kc.astype(np.float32)), torch.from_numpy(Vc.astype(np.float32)),
+                            kb, vb, ks, hh)

@@ -19,7 +19,7 @@ from oracle import cacheblend_oracle as O
 from paper_2405_16444_b200 import dist as D
 from synth import workload as W
 from tests.gpu_helpers import DEV, near_tie_ok, np32, to_dev
-from tests.helpers import oracle_model, rel_err, request_inputs, shape
+from tests.helpers import band_check, oracle_model, rel_err, request_inputs, shape, topk_tokens
 
 pytestmark = pytest.mark.gpu
 
@@ -155,25 +155,27 @@ def test_tp_small_bf16_replay(P, n_suf):
     for i in range(1, s.n_layers):
         d = res["dev"][i][:len(ora.cand[i])]
         assert rel_err(d, ora.dev[i]) < TOL["bf16"], f"dev layer {i}"
-        gsel = O.select_hkvd(d, ora.cand[i], ks[i])
-        jac = len(set(gsel) & set(ora.sel[i])) / max(1, len(set(gsel) | set(ora.sel[i])))
-        assert jac > 0.8, f"layer {i} Jaccard {jac}"
+        ok, flips, band = band_check(topk_tokens(d, ora.cand[i], ks[i]), d, ora.dev[i], ora.cand[i], ks[i])
+        assert ok, f"layer {i}: {flips} flips outside the band {band}"
 
 
 def test_tp_small_bf16_free_run_consistent(P):
     """Free-running bf16 over 2 ranks: ranks agree bitwise (checked in run_blend_tp), selections are nested
-    top-k sets of the reported deviations, and values stay within tolerance of the oracle replayed on the
-    GPU's selections."""
+    top-k sets of the reported deviations, layer 1's Delta_kv (identical candidates on both sides) is within
+    bf16 tolerance of the oracle's and its S_1 differs from the oracle's only inside the error band."""
     s, m, req, tok, pos, cs, Kc, Vc, ks = _case("small", 4, [256, 256, 128], 0, "bf16", 0.15)
     res = run_blend_tp(P, s, "bf16", 4, req, tok, pos, cs, Kc, Vc, ks, 2)
     cand = np.arange(req.n_ctx)
     for i in range(1, s.n_layers):
         d = res["dev"][i][:len(cand)]
-        np.testing.assert_array_equal(res["sel"][i], O.select_hkvd(d.astype(np.float64), cand, ks[i]))
+        np.testing.assert_array_equal(res["sel"][i], topk_tokens(d, cand, ks[i]))
         assert set(res["sel"][i]) <= set(cand)
         cand = res["sel"][i]
-    ora = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks, force_sel=res["sel"])
-    _compare(res, ora, s, TOL["bf16"])
+    ora = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks)
+    d1 = res["dev"][1][:req.n_ctx]
+    assert rel_err(d1, ora.dev[1]) < TOL["bf16"]
+    ok, flips, band = band_check(res["sel"][1], d1, ora.dev[1], ora.cand[1], ks[1])
+    assert ok, f"layer 1: {flips} flips outside the band {band}"
 
 
 def _nccl_world1(P, s, dtype, seed, req, tok, pos, cs, Kc, Vc, ks, comm: bool, graph: bool, p2p: bool = False):

@@ -124,3 +124,48 @@ def test_mac_proportionality(r):
     res = O.blend_forward(m, tok, pos, cs, 0, Kc, Kc, O.schedule(r, 120, 32), count_macs=True)
     ratio = res.macs / O.full_prefill_macs(m, tok, pos)
     assert r - 0.05 <= ratio <= r + 0.10, ratio
+
+
+@pytest.mark.parametrize("name,lens,layers,ratio,threads", [("tiny", (32, 32, 32), 3, 0.15, 1),
+                                                           ("tiny", (20, 45, 31), 4, 0.5, 4),
+                                                           ("small", (100, 77, 60), 3, 0.3, 8)])
+def test_replay_rows_equals_forced_blend(name, lens, layers, ratio, threads):
+    """blend_replay_rows (the row-restricted replay used at full model width) equals blend_forward with the
+    same forced selections on every row it returns: KV^new of every layer, Delta_kv of every evaluated
+    candidate, and the final h rows (a subset of S_{L-1} on the last layer)."""
+    s = shape(name, n_layers=layers)
+    m = oracle_model(s, 3, "f32")
+    req = W.Request(list(lens), 0, 3, ratio)
+    tok, pos, cs, Kc, Vc = request_inputs(s, req, m, "f32")
+    N = req.n_ctx
+    ks = O.schedule(ratio, N, layers)
+    S = W.nested_selection(3, N, ks)
+    d1 = W.sample_rows(3, 0x77, N, 11)
+    full = O.blend_forward(m, tok, pos, cs, 0, Kc, Vc, ks, force_sel=S)
+    last = S[-1][::3]
+    rr = O.blend_replay_rows(tok, pos, cs, Kc, Vc, S, lambda i: m, m.embed[tok], dev_rows_1=d1,
+                             h_rows_last=last, threads=threads)
+    np.testing.assert_allclose(rr["K"], full.K, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(rr["V"], full.V, rtol=0, atol=1e-12)
+    for i in range(1, layers):
+        untouched = np.setdiff1d(np.arange(N), S[i])
+        np.testing.assert_array_equal(rr["V"][i][untouched], Vc[i][untouched])
+        rows, dv = rr["dev"][i]
+        pos_in = np.searchsorted(full.cand[i], rows)
+        np.testing.assert_allclose(dv, full.dev[i][pos_in], rtol=1e-12, atol=1e-12)
+        assert set(full.sel[i]) == set(S[i].tolist())
+    assert set(d1.tolist()) <= set(rr["dev"][1][0].tolist())
+    h0 = O.blend_replay_rows(tok, pos, cs, Kc[:1], Vc[:1], S[:1], lambda i: m, m.embed[tok])["h"]
+    r2 = O.blend_replay_rows(tok, pos, cs, Kc, Vc, S, lambda i: m, None, dev_rows_1=d1, h_rows_last=last, h0=h0)
+    np.testing.assert_allclose(r2["h"], rr["h"], rtol=1e-11, atol=1e-11)
+    np.testing.assert_array_equal(rr["h_rows"], last)
+    np.testing.assert_allclose(rr["h"], full.h_final[np.searchsorted(S[-1], last)], rtol=1e-11, atol=1e-11)
+
+
+def test_nested_selection_recipe():
+    """The forced-selection recipe nests and has the scheduled sizes (an input generator, no method)."""
+    ks = O.schedule(0.3, 500, 6)
+    S = W.nested_selection(1, 500, ks)
+    assert len(S) == 6 and np.array_equal(S[0], np.arange(500))
+    for i in range(1, 6):
+        assert len(S[i]) == ks[i] and np.all(np.diff(S[i]) > 0) and set(S[i]) <= set(S[i - 1])

@@ -18,15 +18,49 @@ def api():
     return api
 
 
-def test_chunk_hash(api):
+def _sha_ref(model_id: bytes, tokens) -> bytes:
+    import hashlib
+    import struct
+    a = np.asarray(tokens, dtype="<i4")
+    return hashlib.sha256(struct.pack("<I", len(model_id)) + model_id + a.tobytes()).digest()
+
+
+def test_chunk_digest_is_sha256(api):
+    """The store key is SHA-256 (FIPS 180-4, here hashlib as the reference) of (u32 LE len(model_id) ||
+    model_id || LE int32 token ids), across the 55/56/64-byte padding boundaries and long inputs."""
+    rng = np.random.default_rng(0)
+    for n in [0, 1, 11, 12, 13, 14, 15, 16, 100, 512, 1024]:
+        for mid in [b"", b"m", b"mistral-7b|bf16|seed1", bytes(range(200))]:
+            tok = rng.integers(-(2 ** 31), 2 ** 31 - 1, n, dtype=np.int64).astype(np.int32)
+            assert api.chunk_digest(mid, tok) == _sha_ref(mid, tok), (n, mid)
+
+
+def test_chunk_digest_binds_model(api):
     a = np.arange(100, dtype=np.int32)
-    assert api.chunk_hash(a) == api.chunk_hash(a.copy())          # deterministic
+    m1 = api.model_identity(_Shape(), "bf16", "seed1")
+    m2 = api.model_identity(_Shape(d_model=64), "bf16", "seed1")
+    assert api.chunk_digest(m1, a) == api.chunk_digest(m1, a.copy())   # deterministic
+    assert api.chunk_digest(m1, a) != api.chunk_digest(m2, a)          # another model, same tokens
     b = a.copy(); b[57] += 1
-    assert api.chunk_hash(a) != api.chunk_hash(b)                  # one token differs
-    assert api.chunk_hash(a[:99]) != api.chunk_hash(a)             # prefix differs
-    assert api.chunk_hash(a[::-1].copy()) != api.chunk_hash(a)     # order matters
-    hs = {api.chunk_hash(np.random.default_rng(i).integers(0, 32000, 512)) for i in range(2000)}
-    assert len(hs) == 2000
+    assert api.chunk_digest(m1, a) != api.chunk_digest(m1, b)          # one token differs
+    assert api.chunk_digest(m1, a[:99]) != api.chunk_digest(m1, a)     # prefix differs
+    st = api.Store(1 << 20, pinned=False)
+    st.put(api.chunk_digest(m1, a), torch.ones(1, 4, 1, 1), torch.ones(1, 4, 1, 1))
+    assert st.lookup(api.chunk_digest(m1, a)) == 4
+    assert st.lookup(api.chunk_digest(m2, a)) == -1                    # model 2 never sees model 1's KV
+    with pytest.raises(ValueError):
+        st.lookup(b"short")
+
+
+class _Shape:
+    def __init__(self, **kw):
+        self.n_layers, self.d_model, self.n_q_heads, self.n_kv_heads, self.head_dim = 2, 32, 4, 2, 8
+        self.d_ff, self.vocab, self.rope_theta, self.rms_eps = 64, 100, 10000.0, 1e-5
+        self.__dict__.update(kw)
+
+
+def _k(i: int) -> bytes:
+    return int(i).to_bytes(4, "little") * 8
 
 
 def test_lru_matches_model(api):
@@ -40,14 +74,14 @@ def test_lru_matches_model(api):
         if rng.random() < 0.5:
             nbytes = int(rng.integers(1, 1200)) * 4
             k = torch.full((1, nbytes // 4), float(step)); v = -k
-            st.put(key, k.view(1, nbytes // 4, 1, 1), v.view(1, nbytes // 4, 1, 1))
+            st.put(_k(key), k.view(1, nbytes // 4, 1, 1), v.view(1, nbytes // 4, 1, 1))
             model.pop(key, None)
             while model and sum(model.values()) + 2 * nbytes > cap:
                 model.popitem(last=False)
                 evictions += 1
             model[key] = 2 * nbytes
         else:
-            n = st.lookup(key)
+            n = st.lookup(_k(key))
             if key in model:
                 hits += 1
                 model.move_to_end(key)
@@ -55,7 +89,7 @@ def test_lru_matches_model(api):
             else:
                 misses += 1
                 assert n == -1
-        assert st.keys() == list(reversed(model.keys()))
+        assert st.keys() == [_k(x) for x in reversed(model.keys())]
     s = st.stats()
     assert s["used"] == sum(model.values()) <= cap
     assert (s["hits"], s["misses"], s["evictions"], s["entries"]) == (hits, misses, evictions, len(model))
@@ -64,5 +98,5 @@ def test_lru_matches_model(api):
 def test_put_errors(api):
     st = api.Store(100, pinned=False)
     with pytest.raises(api.CacheBlendError):
-        st.put(1, torch.zeros(1, 20, 1, 1), torch.zeros(1, 20, 1, 1))  # 160 B > 100 B
-    assert st.lookup(1, touch=False) == -1
+        st.put(_k(1), torch.zeros(1, 20, 1, 1), torch.zeros(1, 20, 1, 1))  # 160 B > 100 B
+    assert st.lookup(_k(1), touch=False) == -1
