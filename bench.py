@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--ratio", type=float, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="time one whole fp64 oracle blend (layer-streamed "
+                    "weights) and the sampled estimate, then exit (validates the cpu_baseline extrapolation)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baselines", action="store_true", help="skip the full-prefill / full-reuse timings")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of one CUDA graph per step")
@@ -64,26 +66,59 @@ def parse():
 # ---------------------------------------------------------------------------------------------------
 # algorithmic work; the avoided dense work is not counted
 # ---------------------------------------------------------------------------------------------------
-def algorithmic_work(s, N, n_suf, ks):
+def algorithmic_work(s, N, n_suf, ks, sel=None):
+    """SURVEY §8(d) algorithmic FLOPs and bytes of one blend, per kernel class.
+
+    sel: the step's selected token ids per layer (sel[0] unused, layer 0 is full). Attention is then
+    counted exactly, 4 qd (g_j + 1) FLOP per query j with global position g_j = j (positions 0..T-1);
+    without it, with the mean causal span of the kept queries estimated as (T + 1) / 2."""
     d, qd, kvd, ff, L = s.d_model, s.qd, s.kvd, s.d_ff, s.n_layers
     T = N + n_suf
+    B = 2
     g = np.arange(T, dtype=np.float64)  # positions 0..T-1: causal span of token t is t + 1
-    gemm = {}
-    gemm["l0"] = 2.0 * T * (d * qd + qd * d + 3 * d * ff) + 2.0 * n_suf * d * 2 * kvd
+    tot_gemm = 2.0 * T * (d * qd + qd * d + 3 * d * ff) + 2.0 * n_suf * d * 2 * kvd
     attn = 4.0 * qd * float(np.sum(g + 1))
-    cand, sel_rows = N, None
-    tot_gemm = gemm["l0"]
+    dev_bytes = topk_bytes = scatter_bytes = 0.0
+    cand = N
+    exact = sel is not None
     for i in range(1, L):
         k = ks[i]
         tot_gemm += 2.0 * (cand + n_suf) * d * (qd + 2 * kvd) + 2.0 * (k + n_suf) * (qd * d + 3 * d * ff)
-        # attention over each kept query's causal span: the bench's later-layer rows are the top-k of
-        # the candidates; counted with the mean span (N+1)/2 per query (exact spans are data dependent)
-        attn += 4.0 * qd * (k + n_suf) * (T + 1) / 2.0
+        if exact:
+            span = float(np.sum(np.asarray(sel[i], dtype=np.float64) + 1)) + float(np.sum(g[N:] + 1))
+        else:
+            span = (k + n_suf) * (T + 1) / 2.0
+        attn += 4.0 * qd * span
+        dev_bytes += cand * 2 * kvd * B                      # cached K^, V rows of the candidates (fused)
+        topk_bytes += cand * (2 * ((kvd + 63) // 64)) * 4    # per-block Delta_kv partials, fp32
+        scatter_bytes += (k + n_suf) * 2 * kvd * B * 2       # fresh rows read + written into the cache
         cand = k
-    B = 2
     wbytes = L * B * (d * qd + 2 * d * kvd + qd * d + 3 * d * ff)
-    realign_bytes = 2.0 * L * N * kvd * B * 2  # K read+write, V carried over (read+write)
-    return dict(gemm_flops=tot_gemm, attn_flops=attn, weight_bytes=wbytes, realign_bytes=realign_bytes)
+    realign_k = 2.0 * L * N * kvd * B            # K read + write (the algorithmic work, SURVEY §8(a) a1)
+    realign_bytes = 2.0 * realign_k              # out of place: V carried over too (read + write)
+    attn_bytes = L * T * 2 * kvd * B             # every layer's blended K/V read once
+    return dict(gemm_flops=tot_gemm, attn_flops=attn, attn_exact=float(exact), weight_bytes=wbytes,
+                realign_bytes=realign_bytes, realign_k_bytes=realign_k, attn_bytes=attn_bytes,
+                dev_bytes=dev_bytes, topk_bytes=topk_bytes, scatter_bytes=scatter_bytes)
+
+
+def path_roofline(work, prof, ms_step, hbm, tf):
+    """Whole-path fraction: sum over kernel classes of max(FLOP / tensor peak, bytes / HBM
+    peak), divided by the measured step time. prof: measured ms per class (per-launch CUDA events)."""
+    ideal = {
+        "gemm": max(work["gemm_flops"] / (tf * 1e9), work["weight_bytes"] / (hbm * 1e6)),
+        "attention": max(work["attn_flops"] / (tf * 1e9), work["attn_bytes"] / (hbm * 1e6)),
+        "realign": work["realign_k_bytes"] / (hbm * 1e6),
+        "topk": work["topk_bytes"] / (hbm * 1e6),
+        "scatter": work["scatter_bytes"] / (hbm * 1e6),
+    }
+    tot = sum(ideal.values())
+    per = {k: {"ideal_ms": round(v, 4), "ms": round(prof.get(k, 0.0), 4),
+               "frac": round(v / prof[k], 3) if prof.get(k) else None} for k, v in ideal.items()}
+    return {"frac": tot / ms_step, "ideal_ms": tot, "ms_per_step": ms_step, "per_class": per,
+            "note": "sum of per-class max(FLOP/tensor peak, bytes/HBM peak) over the measured step time; "
+                    "GEMM and attention FLOPs on the tensor peak, realign (K read+write only), top-k partials "
+                    "and scatter on HBM; the deviation is fused into the QKV epilogue (inside gemm)"}
 
 
 # ---------------------------------------------------------------------------------------------------
@@ -206,6 +241,63 @@ class OracleSample:
             return os.cpu_count()
 
 
+class _StreamedLayers:
+    """The oracle Model's layer list with layer-streamed weights: layer i is generated (synth recipe, the
+    oracle's own input path) when first indexed and replaced by the next layer, so one layer's fp64
+    weights are resident at a time. gen_s accumulates the (untimed) generation time."""
+
+    def __init__(self, s, seed):
+        self.s, self.seed, self.i, self.w, self.gen_s = s, seed, -1, None, 0.0
+
+    def __len__(self):
+        return self.s.n_layers
+
+    def __getitem__(self, i):
+        if i != self.i:
+            t = time.perf_counter()
+            self.w = None
+            self.w = {k: np.asarray(v, dtype=np.float64) for k, v in W.layer_weights(self.s, i, self.seed,
+                                                                                   "bf16").items()}
+            self.i = i
+            self.gen_s += time.perf_counter() - t
+        return self.w
+
+
+def oracle_full_blend(s, lens, ratio, seed):
+    """The whole fp64 oracle blend of one request (realign + layer 0 + layers 1..L-1), layer-streamed
+    weights, random chunk caches. Returns (compute seconds excluding weight generation, generation s)."""
+    from oracle import cacheblend_oracle as O
+    req = W.Request(list(lens), 0, seed, ratio)
+    N, L = req.n_ctx, s.n_layers
+    ks = O.schedule(ratio, N, L)
+    layers = _StreamedLayers(s, seed)
+    m = O.Model(L, s.d_model, s.n_q_heads, s.n_kv_heads, s.head_dim, s.rope_theta, s.rms_eps,
+                np.asarray(W.embed_weights(s, seed, "bf16"), dtype=np.float64), layers)
+    tok, pos, loc = req.tokens(s.vocab), req.global_positions(), req.local_positions()
+    Kc = np.stack([W.random_cache(s, i, N, seed, "bf16", "k") for i in range(L)]).astype(np.float64)
+    Vc = np.stack([W.random_cache(s, i, N, seed, "bf16", "v") for i in range(L)]).astype(np.float64)
+    layers[0]
+    g0 = layers.gen_s
+    t0 = time.perf_counter()
+    res = O.blend_forward(m, tok, pos, req.chunk_starts(), 0, Kc, Vc, ks)
+    wall = time.perf_counter() - t0
+    return wall - (layers.gen_s - g0), layers.gen_s, res
+
+
+def run_cpu_full(args):
+    """One full oracle blend of the bench workload (validates the sampled cpu_baseline's extrapolation)."""
+    shape_name, lens, ratio = CONFIGS.get(args.config, CONFIGS["mistral"])
+    s = W.MODELS[shape_name]
+    smp = OracleSample(s, lens, ratio, args.seed)
+    est, sample_s = smp.run()
+    full_s, gen_s, _ = oracle_full_blend(s, lens, ratio if args.ratio is None else args.ratio, args.seed)
+    N = sum(lens)
+    print(json.dumps({"kind": "oracle full blend", "workload": f"{shape_name} {len(lens)}x{lens[0]} r={ratio}",
+                      "full_blend_s": full_s, "full_ctx_tok_s": N / full_s, "weight_generation_s_untimed": gen_s,
+                      "sampled_estimate_s": est, "sample_s": sample_s,
+                      "estimate_over_full": est / full_s, "cores": OracleSample.cores()}), flush=True)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -221,19 +313,22 @@ def run_reference(args):
         e, t = smp.run()
         est.append(e)
         samples.append(t)
-    ms = float(np.mean(est)) * 1e3
+    ms_blend = float(np.mean(est)) * 1e3      # one whole blend, extrapolated from the sample
+    ms_step = float(np.mean(samples)) * 1e3   # what each step actually ran (the driver's clock sees this)
     N = sum(lens)
-    v = N / (ms / 1e3)
+    v = N / (ms_blend / 1e3)
     cores = OracleSample.cores()
+    sample = (f"per step: realign all {s.n_layers} layers + layers 0-2 in full (fp64 numpy, "
+              f"{ms_step / 1e3:.1f} s measured); layers 3..{s.n_layers - 1} extrapolated from layer 2 by row counts "
+              f"to {ms_blend / 1e3:.1f} s per blend (value = n_ctx / that); a full oracle blend timed once: "
+              "profiles/r02_cpu_full_blend.json")
     line = {"metric": METRIC, "value": v, "unit": "ctx_tok/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_blend_extrapolated": ms_blend,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter RNG)", "impl": "reference",
             "config": {"workload": f"{shape_name} {len(lens)}x{lens[0]} tokens, r={ratio}, 1 request per GPU",
                        "recompute_ratio": ratio, "n_ctx": N, "parallelism": "request-parallel x1 (rank 0 only)"},
-            "cpu_baseline": {"value": v, "unit": "ctx_tok/s", "cores": cores, "kind": "oracle",
-                             "sample": "per step: realign all layers + layers 0-2 in full (fp64 numpy); layers 3.."
-                                       f"{s.n_layers - 1} extrapolated from layer 2 by row counts; "
-                                       f"{float(np.mean(samples)):.1f} s of CPU work per step"},
+            "cpu_baseline": {"value": v, "unit": "ctx_tok/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "ctx_tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -365,23 +460,41 @@ def run_ours(args):
 
     # per-kernel profile pass (same steps, per-launch CUDA events on the launching stream)
     prof = P.api.profile_steps(ctx, step_eager, max(3, min(args.steps, 10)))
-    work = algorithmic_work(sh, N, 0, ks)  # this rank's share (its heads / features) under head parallelism
+    # the step's selections, for the exact attention FLOP count (one extra eager step, not timed)
+    sel_t = torch.full((L, N), -1, dtype=torch.int32, device=dev)
+    P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, k_out, v_out, ks, h_out=h_out, sel_out=sel_t)
+    sel_np = sel_t.cpu().numpy()
+    sel_sets = [row[row >= 0] for row in sel_np]
+    work = algorithmic_work(sh, N, 0, ks, sel_sets)  # this rank's share (its heads / features) under heads
     hbm, tf_burst, tf_sus, peak_src = measured_peaks()
     gemm_ms = prof.get("gemm", 0.0)
     roof = None
     if gemm_ms > 0:
         achieved = work["gemm_flops"] / (gemm_ms / 1e3) / 1e12
         traffic, tnote = None, None
-        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_traffic.json")
-        if os.path.exists(tpath):  # committed ncu measurement of the largest GEMM launch (bytes per launch)
-            tj = json.load(open(tpath))
-            traffic = tj["dram_bytes"]
-            tnote = (f"{tj['kernel']}: DRAM {tj['dram_bytes']} B vs algorithmic {tj['algorithmic_bytes']} B "
-                     f"per launch ({tj['source']})")
-        roof = {"bound": "tensor", "kernel": "gemm (all projections)", "achieved": achieved, "peak": tf_sus,
-                "unit": "TFLOP/s", "frac": achieved / tf_sus, "traffic": traffic, "traffic_note": tnote,
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
-                "share_of_step": gemm_ms / ms}
+        for tname in ("r02_traffic.json", "r01c_traffic.json"):  # newest committed ncu capture first
+            tpath = os.path.join(ROOT, "profiles", tname)
+            if os.path.exists(tpath):  # committed ncu measurement of the largest GEMM launch (bytes per launch)
+                tj = json.load(open(tpath))
+                traffic = tj["dram_bytes"]
+                tnote = (f"{tj['kernel']}: DRAM {tj['dram_bytes']} B vs algorithmic {tj['algorithmic_bytes']} B "
+                         f"per launch ({tj['source']})")
+                break
+        attn_ms = prof.get("attention", 0.0)
+        realign_ms = prof.get("realign", 0.0)
+        roof = {"bound": "tensor", "kernel": "gemm (all projections)", "achieved": achieved, "peak": tf_burst,
+                "unit": "TFLOP/s", "frac": achieved / tf_burst, "traffic": traffic, "traffic_note": tnote,
+                "peak_source": f"{peak_src} bf16_tflops (burst; the step is ~10 ms of back-to-back kernels)",
+                "frac_vs_sustained": achieved / tf_sus, "sustained_peak": tf_sus,
+                "share_of_step": gemm_ms / ms,
+                "attention": {"achieved": work["attn_flops"] / (attn_ms / 1e3) / 1e12 if attn_ms else None,
+                              "frac": work["attn_flops"] / (attn_ms / 1e3) / 1e12 / tf_burst if attn_ms else None,
+                              "flops": work["attn_flops"], "exact_spans": True},
+                "realign": {"GBps_k_only": work["realign_k_bytes"] / (realign_ms / 1e3) / 1e9 if realign_ms else None,
+                            "frac_k_only": work["realign_k_bytes"] / (realign_ms / 1e3) / 1e9 / hbm if realign_ms else None,
+                            "frac_with_v_copy": work["realign_bytes"] / (realign_ms / 1e3) / 1e9 / hbm if realign_ms else None,
+                            "hbm_peak": hbm},
+                "path": path_roofline(work, prof, ms, hbm, tf_burst)}
     # end to end through the public API: chunk caches + tokens from pinned host memory, h_out back
     e2e = None
     if not args.no_e2e:
@@ -613,7 +726,9 @@ def run_batched(args):
 
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    if a.cpu_full:
+        run_cpu_full(a)
+    elif a.impl == "reference":
         run_reference(a)
     elif a.config == "batched":
         run_batched(a)

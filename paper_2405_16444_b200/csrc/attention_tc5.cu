@@ -248,6 +248,10 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
       }
       __syncwarp();
     }
+    // drain: the release commits of the last K / V stages have no consumer; wait for their arrivals so no
+    // tcgen05.commit arrive is in flight when the CTA exits (compute-sanitizer synccheck: "missing wait")
+    for (int t = max(0, nt - KST); t < nt; ++t) tc::mbar_wait(&k_empty[t % KST], (t / KST) & 1);
+    for (int t = max(0, nt - 2); t < nt; ++t) tc::mbar_wait(&v_empty[t & 1], (t >> 1) & 1);
   } else {
     // ===== softmax / correction / epilogue: two warpgroups, each owns one 64-key half of every row
     // (thread = (row, half)); the halves agree on the row max through shared memory every tile =====
@@ -322,11 +326,11 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
       }
       const float hmx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      xmax[(b * NWG + wg) * 128 + r] = hmx;
+      tc::sts_f32(xmax + (b * NWG + wg) * 128 + r, hmx);
       named_bar_sync(1, NSM);
       float mxall = hmx;
 #pragma unroll
-      for (int j = 0; j < NWG; ++j) mxall = fmaxf(mxall, xmax[(b * NWG + j) * 128 + r]);  // exact, any order
+      for (int j = 0; j < NWG; ++j) mxall = fmaxf(mxall, tc::lds_f32(xmax + (b * NWG + j) * 128 + r));  // exact, any order
       const float mx = mxall * scale_log2;
       if (et == 0) DBG(800 + 4 * t + 1);
       // lazy rescale (identical decision in both halves): move the reference max only when it grew
@@ -374,9 +378,11 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
         }
       }
       l += ((rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y)) + ((rs2[2].x + rs2[2].y) + (rs2[3].x + rs2[3].y));
-      // rescale O only when the reference max moved; PV_{t-1} must be complete (O stable)
+      // PV_{t-1} is complete long before here (issued a whole softmax ago); waiting on every phase keeps
+      // the barrier protocol explicit (compute-sanitizer synccheck) and O stable for the rescale below
+      if (t >= 1) tc::mbar_wait(pv_done, (t - 1) & 1);
+      // rescale O only when the reference max moved
       if (t >= 1 && __any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write
-        tc::mbar_wait(pv_done, (t - 1) & 1);
         if (et == 0) DBG(800 + 4 * t + 2);
         tc::fence_after();
 #pragma unroll
@@ -401,12 +407,12 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
       if (et == 0) DBG(800 + 4 * t + 3);
     }
     // total row sum = all groups (same reference max), in group order
-    xl[wg * 128 + r] = l;
+    tc::sts_f32(xl + wg * 128 + r, l);
     named_bar_sync(1, NSM);
     if constexpr (NWG == 2) {
-      l = xl[r] + xl[128 + r];
+      l = tc::lds_f32(xl + r) + tc::lds_f32(xl + 128 + r);
     } else {
-      l = (xl[r] + xl[128 + r]) + (xl[256 + r] + xl[384 + r]);
+      l = (tc::lds_f32(xl + r) + tc::lds_f32(xl + 128 + r)) + (tc::lds_f32(xl + 256 + r) + tc::lds_f32(xl + 384 + r));
     }
     tc::mbar_wait(pv_done, (nt - 1) & 1);
     tc::fence_after();
@@ -433,10 +439,10 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
         const int old = atomicAdd(tile_cnt + (size_t)tile * n_kv + g, 1);
         const int last = old == n_active - 1;
         if (last) tile_cnt[(size_t)tile * n_kv + g] = 0;  // reset for the next launch
-        *flag = last;
+        tc::sts_s32(flag, last);
       }
       named_bar_sync(1, NSM);
-      write_out = *flag != 0;
+      write_out = tc::lds_s32(flag) != 0;
       if (write_out) {  // last arrival: merge every range's partial in split order
         __threadfence();
         float mstar = -INFINITY;

@@ -9,6 +9,24 @@ namespace tc {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Scalar shared-memory accesses through the 32-bit shared address (a plain pointer into dynamic shared
+// memory compiles to generic LD.E / ST.E, which are ordered against global memory traffic)
+__device__ __forceinline__ void sts_f32(const void* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(const void* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_s32(const void* p, int v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int lds_s32(const void* p) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ long long globaltimer() {
   long long t;

@@ -643,3 +643,42 @@ def test_bad_positions_are_reported(P, bad):
         P.api.blend_request(ctx, mw, torch.from_numpy(tok.astype(np.int32)), torch.from_numpy(pos.astype(np.int32)),
                             list(cs), 0, torch.from_numpy(Kc.astype(np.float32)), torch.from_numpy(Vc.astype(np.float32)),
                             kb, vb, ks, hh)
+
+
+@pytest.mark.parametrize("threads", [0, 256, 512])
+def test_topk_sort_path_bitwise(P, threads):
+    """The bitonic top-k path (n_cand <= block threads, every layer after the first at blend sizes) selects
+    exactly what the radix / drop-smallest paths select (ties -> lower index, R6): a whole small blend, and
+    direct calls on tie-heavy deviations over a sweep of (n_cand, k)."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 17, [300, 211, 157], 4, "bf16", 0.15)
+    outs = []
+    for sort in (0, 1):
+        ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
+        ctx.set_option("topk_threads", threads)
+        ctx.set_option("topk_sort", sort)
+        outs.append(run_blend(P, s, "bf16", 17, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx))
+    for a, b in zip(outs[0]["sel"], outs[1]["sel"]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(outs[0]["h"], outs[1]["h"])
+    ctx = P.Context(s, "bf16", max_tokens=1100)
+    ctx.set_option("topk_threads", threads)
+    lim = threads or 1024
+    g = torch.Generator(device=DEV).manual_seed(threads + 1)
+    for n, k in [(1, 0), (2, 1), (37, 5), (255, 254), (256, 1), (300, 299), (553, 547), (lim, 1), (lim, lim - 1),
+                 (lim, lim // 2)]:
+        n = min(n, lim)
+        k = min(k, n)
+        kn = torch.randint(0, 3, (n, s.n_kv_heads, s.head_dim), device=DEV, generator=g).to(torch.bfloat16)
+        kn[::3] = 0  # many exact ties at zero
+        vn = torch.zeros_like(kn)
+        ref = torch.zeros(n + 20, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=DEV)  # rows = tokens
+        cand = torch.sort(torch.randperm(n + 20, device=DEV, generator=g)[:n])[0].to(torch.int32)
+        res = []
+        for sort in (0, 1):
+            ctx.set_option("topk_sort", sort)
+            res.append(P.api.kv_deviation_topk(ctx, kn, vn, ref, ref, cand, k))
+        d = res[1][2].cpu().numpy()
+        want = np.sort(np.lexsort((np.arange(n), -d))[:k])  # k largest, ties -> lower slot
+        np.testing.assert_array_equal(res[0][1].cpu().numpy(), want, err_msg=f"radix/drop path n={n} k={k}")
+        np.testing.assert_array_equal(res[1][1].cpu().numpy(), want, err_msg=f"sort path n={n} k={k}")
+        assert torch.equal(res[0][0], res[1][0]), (n, k)
