@@ -186,7 +186,11 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
       for (int it = 0; it < 8; ++it) {
         const int m = m_base + it * 4 + r0;
         pre[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+#if defined(CB_EPI_EXP) && (CB_EPI_EXP & 8)
+        if (m < M && col_ok && e.ldo < 0) {  // experiment: no residual loads
+#else
         if (m < M && col_ok) {
+#endif
           const float4* p = reinterpret_cast<const float4*>(base + (size_t)ra[it] * e.ldo + col);
           pre[it] = cont ? __ldcg(p) : *p;
         }
@@ -265,6 +269,8 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
       const int r = it * 4 + r0, m = m_base + r;
 #if defined(CB_EPI_EXP) && (CB_EPI_EXP & 4)
       const bool ok = false;
+#elif defined(CB_EPI_EXP) && (CB_EPI_EXP & 16)
+      const bool ok = m < M && col_ok && e.ldo < 0;  // experiment: no stores (loads stay live)
 #else
       const bool ok = m < M && col_ok;
 #endif
@@ -338,6 +344,97 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
   }
 }
 
+// ---- lean residual epilogue ---------------------------------------------------------------------------
+// EPI_RESID without the split-K continuation, peer push or partial adds (the blend's o_proj / down_proj):
+// the same staged row-contiguous traffic and the same arithmetic (bitwise equal to tile_epilogue), but
+// the per-row operands (validity, source / destination row offsets) are computed once per tile and the
+// cold paths are gone, so the unrolled chunk loop is compact. tools/gemm_trace.py (r02g): the generic
+// loop spent ~0.64 us per 32-column chunk even with every global access compiled out (instruction
+// fetch of the long unrolled body with per-row branches), ~1.3 us with its traffic.
+// Needs e.N % 32 == 0 and 32-bit row offsets ((M + 256) * ldo < 2^31).
+template <int BN, bool NORM>
+__device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base, int n0, uint32_t trow, float4* buf,
+                                           int lane, long long* dbg = nullptr) {
+  const int j = lane & 7, r0 = lane >> 3;
+  const int my_m = m_base + lane;
+  const int my_src = my_m < M ? (e.res_row ? __ldg(e.res_row + my_m) : my_m) : 0;
+  unsigned okmask = 0;
+  int in_off[8], out_off[8];  // element offsets of the rows this lane touches (it * 4 + r0)
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int m = m_base + it * 4 + r0;
+    const int src = __shfl_sync(0xffffffffu, my_src, it * 4 + r0);
+    okmask |= (m < M ? 1u : 0u) << it;
+    in_off[it] = src * e.ldo + 4 * j;
+    out_off[it] = m * e.ldo + 4 * j;
+  }
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
+  float dacc[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) dacc[it] = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    const int n = n0 + c;
+    if (n >= e.N) break;  // warp-uniform
+    float4 pre[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+      pre[it] = ((okmask >> it) & 1) ? *reinterpret_cast<const float4*>(e.h_in + in_off[it] + n)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+    {
+      float v[32];
+      tc::tmem_ld32(trow + c, v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + (uint32_t)(lane * 8 + (q ^ (lane & 7))) * 16u),
+                     "f"(v[4 * q]), "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                     : "memory");
+    }
+    __syncwarp();
+    [[maybe_unused]] float4 gain = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (NORM) gain = __ldg(reinterpret_cast<const float4*>(e.norm_gain + n + 4 * j));
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int r = it * 4 + r0;
+      float4 a;
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+                   : "r"(sbase + (uint32_t)(r * 8 + (j ^ (r & 7))) * 16u)
+                   : "memory");
+      const float4 o = make_float4(pre[it].x + a.x, pre[it].y + a.y, pre[it].z + a.z, pre[it].w + a.w);
+      if ((okmask >> it) & 1) {
+        *reinterpret_cast<float4*>(e.h_out + out_off[it] + n) = o;
+        if constexpr (NORM) {
+          *reinterpret_cast<uint2*>(reinterpret_cast<bf16*>(e.y_out) + out_off[it] + n) =
+              pack4_bf16(make_float4(o.x * gain.x, o.y * gain.y, o.z * gain.z, o.w * gain.w));
+          dacc[it] += (o.x * o.x + o.y * o.y) + (o.z * o.z + o.w * o.w);
+        }
+      }
+    }
+    if constexpr (NORM) {
+      if ((n + 32) % 64 == 0 || c + 32 >= BN) {  // a 64-column block ends: publish (same tree as tile_epilogue)
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          float sq = dacc[it];
+          sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+          sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+          sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+          if (j == 0 && ((okmask >> it) & 1)) e.ss_out[(size_t)(m_base + it * 4 + r0) * e.ld_ss + n / 64] = sq;
+          dacc[it] = 0.f;
+        }
+      }
+    }
+    __syncwarp();  // buffer reused by the next chunk
+    if (dbg != nullptr && lane == 0 && c / 32 < 8) dbg[c / 32] = tc::globaltimer();
+  }
+}
+
+// Whether a RESID tile may take resid_lean (else the generic tile_epilogue).
+__device__ __forceinline__ bool resid_lean_ok(const EpiParams& e, bool cont, int M) {
+  return !cont && e.n_add == 0 && e.push_base[0] == nullptr && (e.N % 32) == 0 &&
+         (long long)(M + 256) * e.ldo < (1ll << 31);
+}
+
 // ---- row-per-lane QKV epilogue with operands issued early -----------------------------------------
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {  // bulk L2 prefetch (16 B multiple)
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -375,39 +472,39 @@ __device__ __forceinline__ void resid_prefetch(const EpiParams& e, int m, bool r
   if (w > 0) prefetch_l2(e.h_in + (size_t)src * e.ldo + n0, (uint32_t)w * 4u);
 }
 
-// EPI_QKV on 64 accumulator columns [n, n + 64) of row m (hd % 64 == 0: the chunk lies in one q, k or
+// EPI_QKV on 32 accumulator columns [n, n + 32) of row m (hd % 32 == 0: the chunk lies in one q, k or
 // v head). Warp-collective. RoPE (cos, sin) and the cached K/V reference are loaded before the TMEM
-// read, so one (L2) latency is exposed per 64 columns. Returns the chunk's squared distance to the
-// reference (0 for q columns and non-candidates). tok = row_tok[m], p = pos[tok].
-__device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool row_ok, uint32_t taddr, int tok, int p,
+// read, so one (L2) latency is exposed per chunk. Returns the chunk's squared distance to the reference
+// (0 for q columns and non-candidates). tok = row_tok[m], p = pos[tok]. 32 columns rather than 64 keep
+// the kernel free of register spills (ptxas: 744-964 B of spills at 64).
+__device__ __forceinline__ float qkv32(const EpiParams& e, int m, int n, bool row_ok, uint32_t taddr, int tok, int p,
                                        float rs) {
   const int c = e.col0 + n;
   const bool is_q = c < e.qd, is_v = c >= e.qd + e.kvd;
   const bool dev_on = row_ok && !is_q && e.dev_part != nullptr && m < e.n_cand;
   const int kv_c = is_q ? 0 : (is_v ? c - e.qd - e.kvd : c - e.qd);
-  float4 cs[16];
-  uint4 ref[8];
+  float4 cs[8];
+  uint4 ref[4];
   if (row_ok && !is_v) {
     const int dim = (is_q ? c : c - e.qd) % e.hd;
     const float4* t = reinterpret_cast<const float4*>(e.rope_tab + (size_t)p * (e.hd >> 1) + (dim >> 1));
 #pragma unroll
-    for (int i = 0; i < 16; ++i) cs[i] = __ldg(t + i);  // (cos, sin) of pairs 2i, 2i+1
+    for (int i = 0; i < 8; ++i) cs[i] = __ldg(t + i);  // (cos, sin) of pairs 2i, 2i+1
   }
   if (dev_on) {
     const uint4* r = reinterpret_cast<const uint4*>(reinterpret_cast<const bf16*>(is_v ? e.v_ref : e.k_ref) +
                                                     (size_t)tok * e.kvd + kv_c);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ref[i] = __ldg(r + i);
+    for (int i = 0; i < 4; ++i) ref[i] = __ldg(r + i);
   }
-  float x[64];
-  tc::tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(x));
-  tc::tmem_ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+  float x[32];
+  tc::tmem_ld32(taddr, x);
   if (!row_ok) return 0.f;
 #pragma unroll
-  for (int i = 0; i < 64; ++i) x[i] *= rs;
+  for (int i = 0; i < 32; ++i) x[i] *= rs;
   if (!is_v) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 8; ++i) {
       const float a0 = x[4 * i], a1 = x[4 * i + 1], b0 = x[4 * i + 2], b1 = x[4 * i + 3];
       x[4 * i] = cs[i].x * a0 - cs[i].y * a1;
       x[4 * i + 1] = cs[i].y * a0 + cs[i].x * a1;
@@ -418,7 +515,7 @@ __device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool ro
   float dev = 0.f;
   if (dev_on) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const uint32_t wv[4] = {ref[i].x, ref[i].y, ref[i].z, ref[i].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -431,7 +528,7 @@ __device__ __forceinline__ float qkv64(const EpiParams& e, int m, int n, bool ro
   bf16* dst = is_q ? reinterpret_cast<bf16*>(e.q_out) + (size_t)m * e.qd + c
                    : reinterpret_cast<bf16*>(is_v ? e.v_out : e.k_out) + (size_t)m * e.kvd + kv_c;
 #pragma unroll
-  for (int g = 0; g < 4; ++g) st_bf16x16(dst + 16 * g, x + 16 * g);
+  for (int g = 0; g < 2; ++g) st_bf16x16(dst + 16 * g, x + 16 * g);
   return dev;
 }
 
@@ -446,11 +543,12 @@ __device__ __forceinline__ void qkv_row(const EpiParams& e, int m, bool row_ok, 
   }
   float dacc = 0.f;
 #pragma unroll 1
-  for (int c = 0; c < OUT_N; c += 64) {
+  for (int c = 0; c < OUT_N; c += 32) {
     const int n = n0 + c;
     if (n >= e.N) break;  // warp-uniform
-    dacc += qkv64(e, m, n, row_ok, trow + c, tok, p, rs);
+    dacc += qkv32(e, m, n, row_ok, trow + c, tok, p, rs);
     const int cl = e.col0 + n;
+    if ((cl + 32) % 64 != 0) continue;  // the 64-column block continues in the next chunk
     if (e.dev_part != nullptr && cl >= e.qd) {  // one partial per 64-column k or v block
       const int kv_col = cl - e.qd;
       const int slot = kv_col < e.kvd ? 2 * (kv_col / 64) : 2 * ((kv_col - e.kvd) / 64) + 1;

@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (!skip_epilogue) {
       if (KIND == EPI_QKV && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
         gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow, rs);
+      } else if (KIND == EPI_RESID && gepi::resid_lean_ok(e, sp > 0, M) && (sp == ksplit - 1)) {
+        long long* tdbg = (dbg != nullptr && it == 0 && warp == 2 && blockIdx.x < 128) ? dbg + 1024 + blockIdx.x * 8 : nullptr;
+        if (e.norm_gain != nullptr) gepi::resid_lean<BN, true>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane, tdbg);
+        else gepi::resid_lean<BN, false>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane, tdbg);
       } else if (gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {  // staged, row-contiguous
         gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane,
                                       sp > 0, sp == ksplit - 1,
