@@ -48,15 +48,19 @@ def parse():
     ap.add_argument("--tp-comm", default="nccl", choices=["nccl", "p2p"],
                     help="--parallel heads: NCCL calls (default) or the library's NVLink peer-memory collectives "
                          "(o_proj / down_proj epilogues push rows to their owners; experimental, DESIGN.md §7)")
-    ap.add_argument("--parallel", default="request", choices=["request", "heads"],
-                    help="N>1: request-parallel (weak scaling, default) or head-parallel tensor parallelism over "
-                         "the N GPUs (strong scaling, NCCL all-gather / all-reduces inside the blend)")
+    ap.add_argument("--parallel", default="auto", choices=["auto", "request", "heads"],
+                    help="N>1: head-parallel tensor parallelism over the N GPUs (strong scaling, NCCL all-gather / "
+                         "all-reduces inside the blend; the default, BASELINE north_star 'head-partitioned at 2, 4 "
+                         "and 8 GPUs') with a request-parallel sub-record (weak scaling, no collective), or "
+                         "request-parallel only")
     ap.add_argument("--ratio", type=float, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-full", action="store_true", help="time one whole fp64 oracle blend (layer-streamed "
                     "weights) and the sampled estimate, then exit (validates the cpu_baseline extrapolation)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-request-sub", action="store_true", help="N>1 head-parallel: skip the request-parallel "
+                    "sub-record")
     ap.add_argument("--no-baselines", action="store_true", help="skip the full-prefill / full-reuse timings")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of one CUDA graph per step")
     ap.add_argument("--no-pdl", action="store_true", help="disable programmatic dependent launch")
@@ -358,7 +362,7 @@ def run_ours(args):
     shape_name, lens, ratio = CONFIGS[args.config]
     ratio = args.ratio if args.ratio is not None else ratio
     s = W.MODELS[shape_name]
-    heads = args.parallel == "heads"
+    heads = args.parallel == "heads" or (args.parallel == "auto" and world > 1)
     # request-parallel (weak scaling): every rank blends its own request; head-parallel (strong scaling):
     # all ranks blend the same request, each with its heads / d_ff features
     seed = args.seed if heads else args.seed + rank
@@ -583,9 +587,68 @@ def run_ours(args):
                 "cpu_baseline": cpu, "e2e": e2e, "baselines": baselines, "controller": controller,
                 "kernel_ms": {k: round(v, 4) for k, v in prof.items()},
                 "work": {k: float(v) for k, v in work.items()}}
+    if heads and world > 1 and not args.no_request_sub:
+        # the same job request-parallel (SURVEY §8(e) partitioning 2): every rank blends its own request on a
+        # full replica, no collective -- measured after the head-parallel buffers are released
+        del mw, k_in, v_in, k_out, v_out, ctx
+        torch.cuda.empty_cache()
+        sub = request_parallel_record(P, args, s, lens, ratio, world, rank, dev)
+        if rank == 0:
+            line["request_parallel"] = sub
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def request_parallel_record(P, args, s, lens, ratio, world, rank, dev):
+    """Request-parallel measurement at N ranks (weak scaling): rank r blends request seed + r on its own full
+    model replica; job value = all ranks' context tokens over the slowest rank's CUDA-event time."""
+    import torch
+    from paper_2405_16444_b200.dist import job_throughput
+    req = W.Request(list(lens), 0, args.seed + rank, ratio)
+    N, L = req.n_ctx, s.n_layers
+    ctx = P.Context(s, "bf16", max_tokens=max(N, max(lens)), max_pos=max(2 * N, 4096))
+    mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
+    tok = torch.from_numpy(req.tokens(s.vocab)).to(dev)
+    pos = torch.from_numpy(req.global_positions()).to(dev)
+    cs = req.chunk_starts()
+    k_in = torch.empty(L, N, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+    v_in = torch.empty_like(k_in)
+    for c in range(len(lens)):
+        a, b = int(cs[c]), int(cs[c + 1])
+        kc = torch.empty(L, b - a, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=dev)
+        vc = torch.empty_like(kc)
+        P.blend_forward(ctx, mw, tok[a:b].contiguous(), torch.arange(b - a, dtype=torch.int32, device=dev), [0],
+                        b - a, None, None, kc, vc, [0] * L)
+        k_in[:, a:b] = kc
+        v_in[:, a:b] = vc
+    ks = P.schedule(ratio, N, L)
+    k_out, v_out = torch.empty_like(k_in), torch.empty_like(v_in)
+    h_out = torch.empty(ks[-1], s.d_model, dtype=torch.float32, device=dev)
+    fn = lambda: P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, k_out, v_out, ks, h_out=h_out)
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(args.warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    import torch.distributed as dist
+    dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    value, ms_max, tok_all = job_throughput(N, e0.elapsed_time(e1) / args.steps, dev)
+    return {"value": value, "unit": "ctx_tok/s", "ms_per_step": ms_max, "scaling": "weak", "ctx_tokens": tok_all,
+            "parallelism": f"request-parallel x{world} (one request per GPU, full replica, no collective)"}
 
 
 def run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args):

@@ -319,6 +319,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = attention_tc6_init();
   c->topk_drop_max = 48;
   c->topk_sort = 1;
+  c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
   c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
   c->mlp_fused = 0;  // experimental: measured ~0.3 ms/step slower (merge + residual epilogues at the end)
   if (st == CB_OK && c->m.dtype == CB_BF16) st = gemm_mlp_init(c);
@@ -500,6 +501,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     CB_REQUIRE(value == 0 || value == 256 || value == 512 || value == 1024, CB_E_INVALID_ARG,
                "topk_threads must be 0, 256, 512 or 1024");
     c->topk_threads = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "attn_pair") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "attn_pair must be 0, 1 or 2");
+    c->attn_pair = (int)value;
     return CB_OK;
   }
   if (std::strcmp(name, "topk_sort") == 0) {

@@ -82,6 +82,7 @@ struct cb_ctx {
   float* mlp_part;            // [3][T][d] fp32 partial products of down-projection K blocks 0..2
   int mlp_split;              // cb_set_option("mlp_split", S): K blocks of the MLP at blend sizes (1 = off)
   int topk_drop_max;          // cb_set_option("topk_drop", n): drop-smallest top-k path when n_cand - k <= n
+  int attn_pair;              // cb_set_option("attn_pair", 0/1/2): light/heavy row-tile pairing (attention_tc5.cu)
   int topk_sort;              // cb_set_option("topk_sort", 0/1): bitonic path when n_cand <= top-k threads
   int topk_threads;           // cb_set_option("topk_threads", 256 | 512 | 1024): top-k block size (0 = 1024)
   int mlp_fused;              // cb_set_option("mlp_fused", S): one persistent gate_up + down kernel (0 = off)

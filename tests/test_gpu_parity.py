@@ -329,6 +329,36 @@ def test_attention_tc5_split_merge(P, splits, impl):
         assert torch.equal(P.api.op_attention(ctx, *args, impl=impl), out)
 
 
+@pytest.mark.parametrize("order", ["sorted", "shuffled"])
+@pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (777, 50, 1), (130, 3, 8), (4100, 900, 4),
+                                          (2048, 256, 2)])
+def test_attention_tc5_pairing(P, T, n_sel, n_kv, order):
+    """Causal balance (attn_pair): row tile p paired with row tile T-1-p, the heavy one's key range cut
+    between two CTAs and merged by the last arrival; odd tile counts leave the middle tile whole; unsorted
+    query tokens take the heavier tile of each pair. Oracle parity, close to the unpaired kernel, bitwise
+    reproducible across launches."""
+    s = shape("small", n_kv_heads=n_kv)
+    g = lambda st, n, H: rng.values(15, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
+    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
+    rows = np.sort(np.random.default_rng(T + 7).choice(T, n_sel, replace=False)).astype(np.int32)
+    if order == "shuffled":
+        rows = rows[np.random.default_rng(3).permutation(n_sel)]
+    qrow = np.arange(n_sel, dtype=np.int32)
+    ctx = P.Context(s, "bf16", max_tokens=T)
+    args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
+            to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
+    ctx.set_option("attn_pair", 0)
+    base = P.api.op_attention(ctx, *args, impl=2)
+    ctx.set_option("attn_pair", 2)
+    out = P.api.op_attention(ctx, *args, impl=2)
+    pos = np.arange(T)
+    ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
+    assert rel_err(np32(out), ref) < 1e-2
+    assert rel_err(np32(out), np32(base)) < 4e-3
+    for _ in range(2):
+        assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
+
+
 # ---- (c) the whole blend ------------------------------------------------------------------------
 def _oracle_case(name, seed, lens, n_suf, dtype, ratio, **over):
     s = shape(name, **over)

@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--splits", default="0,1,2,3,4,6")
     ap.add_argument("--impls", default="2,4")
+    ap.add_argument("--pairs", default="0,1")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -32,8 +33,10 @@ def main():
         qrow = torch.arange(n_sel, dtype=torch.int32, device="cuda")
         qtok = torch.from_numpy(rows).cuda()
         flops = 4.0 * s.n_q_heads * s.head_dim * float(np.sum(rows + 1))
-        for impl, splits in [(int(i), int(x)) for i in a.impls.split(",") for x in a.splits.split(",")]:
+        for impl, splits, pair in [(int(i), int(x), int(pp)) for i in a.impls.split(",") for x in a.splits.split(",")
+                                   for pp in a.pairs.split(",")]:
             ctx.set_option("attn_splits", splits)
+            ctx.set_option("attn_pair", pair)
             fn = lambda: P.api.op_attention(ctx, q, qrow, qtok, k, v, T, impl=impl)
             for _ in range(3):
                 fn()
@@ -45,7 +48,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.iters * 1e3
-            print(f"rows={n_sel:5d} impl={impl} splits={splits}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s",
+            print(f"rows={n_sel:5d} impl={impl} splits={splits} pair={pair}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s",
                   flush=True)
 
 

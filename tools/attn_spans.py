@@ -13,12 +13,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     n_sel = int(sys.argv[1]) if len(sys.argv) > 1 else 460
     splits = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    pair = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     import paper_2405_16444_b200 as P
     from synth import workload as W
     s = W.MODELS["mistral-7b"]
     T = 3072
     ctx = P.Context(s, "bf16", max_tokens=T)
     ctx.set_option("attn_splits", splits)
+    ctx.set_option("attn_pair", pair)
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
     rows = np.sort(np.random.default_rng(n_sel).choice(T, n_sel, replace=False)).astype(np.int32)
@@ -37,7 +39,8 @@ def main():
     spans = [(i, (a[i, 0] - t0) / 1e3, (a[i, 1] - t0) / 1e3) for i in range(370) if used[i]]
     ends = sorted(e for _, _, e in spans)
     print(f"{len(spans)} CTAs, last end {ends[-1]:.1f} us, median end {ends[len(ends) // 2]:.1f}")
-    for i, b, e in spans[::8]:
+    step = int(os.environ.get("SPAN_STEP", "8"))
+    for i, b, e in spans[::step]:
         print(f"{i:4d} {b:7.2f} -> {e:7.2f}  ({e - b:6.2f})")
 
 
