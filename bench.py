@@ -532,12 +532,22 @@ def run_ours(args):
         ks0 = [N] + [0] * (L - 1)
         ms_reuse = timed(lambda: P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, k_out, v_out, ks0,
                                                  h_out=h_full), nb)
+        # prefix caching: only the first chunk's KV is reused (it IS a prefix, so exact); every
+        # later token is prefilled -- the first chunk as cached context, the rest as the uncached suffix
+        n0 = int(cs[1])
+        k0, v0 = k_in[:, :n0].contiguous(), v_in[:, :n0].contiguous()  # the prefix chunk's cache, outside timing
+        ms_prefix = timed(lambda: P.blend_forward(ctx, mw, tok, pos, [0, n0], N - n0, k0, v0, k_out, v_out,
+                                                  [n0] + [0] * (L - 1), h_out=h_full), nb)
+        del k0, v0
         del h_full
-        baselines = {"full_prefill_ms": ms_full, "full_kv_reuse_ms": ms_reuse, "blend_ms": ms_max,
-                     "blend_speedup_vs_full_prefill": ms_full / ms_max,
+        baselines = {"full_prefill_ms": ms_full, "prefix_caching_ms": ms_prefix, "full_kv_reuse_ms": ms_reuse,
+                     "blend_ms": ms_max, "blend_speedup_vs_full_prefill": ms_full / ms_max,
+                     "blend_speedup_vs_prefix_caching": ms_prefix / ms_max,
                      "note": "same library kernels and inputs, one CUDA graph each; full prefill = every token "
-                             "recomputed (no cache), full KV reuse = r=0 (realign + full layer 0 only). The paper "
-                             "quotes 2.2-3.3x TTFT vs full prefill on its GPUs (P:731), context only"}
+                             "recomputed (no cache); prefix caching = the first chunk's KV reused, the other "
+                             f"{len(lens) - 1} chunks prefilled (P:374-391); full KV reuse = r=0 (realign + full "
+                             "layer 0 only). The paper quotes 2.2-3.3x TTFT vs full prefill on its GPUs (P:731), "
+                             "context only"}
     # the loading controller for this request with the chunk KV in pinned
     # host memory: T_load from the measured host->HBM copy rate of one layer, Prefill from the full-prefill
     # baseline above (per layer), r = max(r_eq, 15 %)

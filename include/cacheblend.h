@@ -107,6 +107,13 @@ CB_API cb_status cb_controller_ratio(double prefill_ms, double kv_bytes_per_toke
                                      double bytes_per_ms, double r_min, double* r_out, double* load_ms_out);
 CB_API cb_status cb_controller_pick_device(double prefill_ms, const double* load_ms, const double* cost,
                                            int32_t n_dev, double r_fixed, int32_t* pick_out);
+/* The controller driving the blend ("the fusor then recomputes r% of the tokens"):
+ * r = cb_controller_ratio(prefill_ms, kv_bytes_per_token, n_ctx, bytes_per_ms, r_min) and the per-layer
+ * counts k_sched_out[n_layers] = cb_schedule(r, n_ctx, n_layers), ready for cb_blend_request /
+ * cb_blend_forward. r_out / load_ms_out optional. Errors as the two calls. */
+CB_API cb_status cb_controller_schedule(double prefill_ms, double kv_bytes_per_token, double bytes_per_ms,
+                                        double r_min, int32_t n_ctx, int32_t n_layers, int32_t* k_sched_out,
+                                        double* r_out, double* load_ms_out);
 
 /* ---- (a) positional recovery --------------------------------------------------------------- */
 /* Footnote P:208-211, Appendix: K_out[s][t] = R(dst_pos[t] - src_pos[t]) K_src[s][t]
@@ -180,7 +187,7 @@ CB_API cb_status cb_blend_forward(cb_ctx* ctx, const cb_layer_w* w, const void* 
 /* The same blend with the request's inputs in HOST memory (pinned for asynchronous copies), as the
  * paper's loading path does (fetch_kv -> synchronize -> prefill_layer): layer i's chunk
  * KV is copied into k_blend/v_blend layer i on the context's copy stream while layer i-1 computes,
- * and layer i waits only for its own copy (two-stream layer pipelining, P:2509, P:2655-2671).
+ * and layer i waits only for its own copy (two-stream layer pipelining, P:2509, P:2660-2671).
  * tok_host, pos_host : host int32[N + n_suffix];  k_in_host, v_in_host: host [n_layers][N][n_kv][hd]
  * k_blend, v_blend   : DEVICE out KV^new [n_layers][N + n_suffix][n_kv][hd] (stays on the GPU for decode)
  * sel_out_host       : host int32[k_sched[L-1]] (S_{L-1}) or NULL;  h_out_host: host fp32 rows as in

@@ -60,19 +60,21 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "topk_drop"   n = top-k drops the n_cand - k smallest one by one when that count is <= n (default 48)
  *   "gemm_tail"   0 = auto (cost model), 1 = never (default; measured faster), 2 = always cut the remainder
  *                 tiles of a pair GEMM's last round into K pieces (merged in piece order by the last piece)
- *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM per tile, 3 = mma.sync, 4 = persistent tcgen05
- *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor (impl 4: key chunks per row tile)
+ *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM per tile
+ *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor
+ *   "attn_pair"   0 = off (default; measured neutral), 1 = when the (row tile, kv head) grid is one wave, 2 =
+ *                 always: row tile p paired with row tile T-1-p in a 2-CTA cluster, the heavier one's key range
+ *                 cut between the two CTAs and merged through distributed shared memory
+ *   "q_split"     1 = layer 1 projects Q for the kept rows only, after the top-k (default), 0 = Q for all
+ *                 candidates in the fused QKV GEMM
+ *   "topk_sort"   1 = bitonic block sort when the candidates fit the top-k block (default), 0 = radix / drop
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
  *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
  *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue
  *                 kind k (0 store, 1 store_f32, 2 qkv, 3 residual, 4 swiglu)
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
  *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
- *   "mlp_fused"   0 = two separate GEMMs (default); 2..4 = the blend MLP (rows <= 768) as one persistent
- *                 kernel: gate_up tiles + the down projection cut into that many K blocks that start as soon
- *                 as their activations exist (experiment; parity-green, measured ~0.3 ms/step slower)
- *   "mlp_split"   1 = off (default); 2..4 = gate_up in K blocks on the caller's stream with the matching
- *                 down-projection blocks on an internal stream (experiment; measured slower) */
+ *   "topk_threads" 0 = 1024 (default), 256 or 512 threads in the top-k block */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Read-only facts about the context: "num_sms", "gemm_max_pairs" (co-resident 2-CTA clusters of the

@@ -481,7 +481,7 @@ def full_prefill_macs(model: Model, tok, pos) -> int:
 # ---------------------------------------------------------------------------------------
 def t_recompute(ratio: float, prefill_ms: float) -> float:
     """Recompute delay estimator: T_recompute(r%, LLM, L) = r% x Prefill(LLM, L) (footnote),
-    Prefill profiled offline. Per layer (P:2655-2659 compare one layer's recompute with one layer's load)."""
+    Prefill profiled offline. Per layer (P:2666-2670 compare one layer's recompute with one layer's load)."""
     return float(ratio) * float(prefill_ms)
 
 

@@ -68,6 +68,8 @@ _SIGS = {
                                        c_i32, c_i32, c_i32p, c_i32, c_vp, c_vp, c_i32p, c_vp, c_vp, c_vp]),
     "cb_kv_to_paged": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i64, c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_vp]),
     "cb_controller_ratio": (c_i32, [c_f64, c_f64, c_i64, c_f64, c_f64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64)]),
+    "cb_controller_schedule": (c_i32, [c_f64, c_f64, c_f64, c_f64, c_i32, c_i32, ctypes.POINTER(c_i32),
+                                       ctypes.POINTER(c_f64), ctypes.POINTER(c_f64)]),
     "cb_controller_pick_device": (c_i32, [c_f64, ctypes.POINTER(c_f64), ctypes.POINTER(c_f64), c_i32, c_f64,
                                           ctypes.POINTER(c_i32)]),
     "cb_set_comm": (c_i32, [c_vp, c_vp, c_i32, c_i32]),

@@ -335,6 +335,16 @@ def controller_ratio(prefill_ms: float, kv_bytes_per_token: float, n_tokens: int
     return r.value, ld.value
 
 
+def controller_schedule(prefill_ms: float, kv_bytes_per_token: float, bytes_per_ms: float, n_ctx: int,
+                        n_layers: int, r_min: float = 0.15):
+    """cb_controller_schedule: (k_sched, r, T_load ms) -- the controller's ratio turned into per-layer counts."""
+    k = (ctypes.c_int32 * n_layers)()
+    r, ld = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    check(lib().cb_controller_schedule(float(prefill_ms), float(kv_bytes_per_token), float(bytes_per_ms),
+                                       float(r_min), int(n_ctx), int(n_layers), k, ctypes.byref(r), ctypes.byref(ld)))
+    return list(k), r.value, ld.value
+
+
 def controller_pick_device(prefill_ms: float, load_ms: Sequence[float], cost: Sequence[float],
                            r_fixed: float = 0.15) -> int:
     """cb_controller_pick_device: index of the cheapest storage device whose load is hidden, or -1."""

@@ -18,17 +18,10 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
 bool gemm_tc_ok(const cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e);
 cb_status launch_attention_simt(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
                                 const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
-cb_status launch_attention_tc(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
-                              const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
-bool attention_tc_ok(const cb_ctx* c);
 cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
                                const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
 bool attention_tc5_ok(const cb_ctx* c);
 cb_status attention_tc5_init();
-cb_status launch_attention_tc6(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows,
-                               const void* k, const void* v, int n_keys, void* out, cudaStream_t s);
-bool attention_tc6_ok(const cb_ctx* c, int n_rows);
-cb_status attention_tc6_init();
 cb_status topk_init_attrs();
 cb_status gemm_tc_init(cb_ctx* c);
 void gemm_tc_destroy(cb_ctx* c);
@@ -41,11 +34,6 @@ void gemm_tc_pairs_cap(cb_ctx* c, int kind, int v);
 void gemm_tc_balance(cb_ctx* c, int v);
 void gemm_tc_force_pair(cb_ctx* c, int v);
 int gemm_tc_max_pairs(const cb_ctx* c);
-cb_status attention_tc_init();
-cb_status gemm_mlp_init(cb_ctx* c);
-bool mlp_fused_ok(const cb_ctx* c, int M);
-cb_status launch_mlp_fused(cb_ctx* c, const void* x, const void* w_gate_up, void* act, const void* w_down, int M,
-                           const EpiParams& egu, const EpiParams& edn, cudaStream_t s);
 
 // ---- error reporting ------------------------------------------------------------------------------
 static thread_local char g_err[1024] = "";
@@ -122,7 +110,7 @@ cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb,
     if (gemm_tc_ok(c, A, lda, B, ldb, M, K, e)) return launch_gemm_tc(c, A, lda, B, ldb, M, K, e, s);
     CB_REQUIRE(impl != 2, CB_E_UNSUPPORTED, "tcgen05 GEMM does not take this shape (M=%d N=%d K=%d)", M, e.N, K);
   }
-  CB_REQUIRE(e.norm_gain == nullptr && e.ss_in == nullptr && e.n_add == 0, CB_E_UNSUPPORTED,
+  CB_REQUIRE(e.norm_gain == nullptr && e.ss_in == nullptr, CB_E_UNSUPPORTED,
              "fused RMSNorm requested on a GEMM outside the tcgen05 path");
   return launch_gemm_simt(c, A, lda, B, ldb, M, K, e, s);
 }
@@ -131,18 +119,9 @@ cb_status launch_attention(cb_ctx* c, const void* q, const int* q_row, const int
                            const void* v, int n_keys, void* out, int impl, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
   if (impl == 0) impl = c->attn_impl;
-  if (impl == 4) {  // experimental (not the default): slower than impl 2 at blend sizes, see DESIGN.md
-    CB_REQUIRE(attention_tc6_ok(c, n_rows), CB_E_UNSUPPORTED,
-               "persistent tcgen05 attention needs bf16, head_dim 128 and <= 512 row tiles");
-    return launch_attention_tc6(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
-  }
   if (impl == 2 || (impl == 0 && attention_tc5_ok(c))) {
     CB_REQUIRE(attention_tc5_ok(c), CB_E_UNSUPPORTED, "tcgen05 attention needs bf16 and head_dim 128");
     return launch_attention_tc5(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
-  }
-  if (impl == 3) {
-    CB_REQUIRE(attention_tc_ok(c), CB_E_UNSUPPORTED, "mma.sync attention needs bf16 and head_dim 128");
-    return launch_attention_tc(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
   }
   return launch_attention_simt(c, q, q_row, q_tok, n_rows, k, v, n_keys, out, s);
 }
@@ -199,7 +178,6 @@ size_t carve(cb_ctx* c, const cb_model* m, int T, char* base) {
   o->dev = cv.take<float>((size_t)T * 4);
   o->dev_part = cv.take<float>((size_t)2 * ((kvd + 63) / 64) * T * 4);
   o->ss = cv.take<float>((size_t)T * ((d + 63) / 64) * 4);
-  o->mlp_part = cv.take<float>((size_t)3 * T * d * 4);
   o->row_tok[0] = cv.take<int>((size_t)T * 4);
   o->row_tok[1] = cv.take<int>((size_t)T * 4);
   o->qrow = cv.take<int>((size_t)T * 4);
@@ -306,23 +284,17 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   for (auto& ev : c->ev_realign)
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   if ((e = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e);
-  for (auto& ev : c->ev_mlp)
-    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
-  c->mlp_split = 1;  // the stream split measured slower (extra launches expose prologues/epilogues)
   c->layer_ev.resize(model->n_layers + 1);
   for (auto& ev : c->layer_ev)
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return fail(e);
   cb_status st = topk_init_attrs();
   if (st == CB_OK) st = gemm_tc_init(c);
-  if (st == CB_OK) st = attention_tc_init();
   if (st == CB_OK) st = attention_tc5_init();
-  if (st == CB_OK) st = attention_tc6_init();
   c->topk_drop_max = 48;
   c->topk_sort = 1;
   c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
+  c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
   c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
-  c->mlp_fused = 0;  // experimental: measured ~0.3 ms/step slower (merge + residual epilogues at the end)
-  if (st == CB_OK && c->m.dtype == CB_BF16) st = gemm_mlp_init(c);
   if (st != CB_OK) {
     cudaFree(c->rope_tab);
     cudaFree(c->err_word);
@@ -344,9 +316,6 @@ extern "C" cb_status cb_destroy(cb_ctx* c) {
   for (auto ev : c->ev_realign) if (ev) cudaEventDestroy(ev);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
-  if (c->mlp_scr) cudaFree(c->mlp_scr);
-  if (c->mlp_cnt) cudaFree(c->mlp_cnt);
-  for (auto ev : c->ev_mlp) if (ev) cudaEventDestroy(ev);
   if (c->dbg_buf) cudaFree(c->dbg_buf);
   comm_destroy(c);
   gemm_tc_destroy(c);
@@ -415,16 +384,6 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     }
     return CB_OK;
   }
-  if (std::strcmp(name, "mlp_fused") == 0) {
-    CB_REQUIRE(value == 0 || (value >= 2 && value <= 4), CB_E_INVALID_ARG, "mlp_fused must be 0 or 2..4");
-    c->mlp_fused = (int)value;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "mlp_split") == 0) {
-    CB_REQUIRE(value >= 1 && value <= 4, CB_E_INVALID_ARG, "mlp_split must be 1..4");
-    c->mlp_split = (int)value;
-    return CB_OK;
-  }
   if (std::strcmp(name, "fuse_norm") == 0) {
     c->no_fuse_norm = value == 0;
     return CB_OK;
@@ -465,7 +424,7 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     return CB_OK;
   }
   if (std::strcmp(name, "attn_impl") == 0) {
-    CB_REQUIRE(value >= 0 && value <= 4, CB_E_INVALID_ARG, "attn_impl must be 0..4");
+    CB_REQUIRE(value == 0 || value == 1 || value == 2, CB_E_INVALID_ARG, "attn_impl must be 0 (auto), 1 (SIMT) or 2 (tcgen05)");
     c->attn_impl = (int)value;
     return CB_OK;
   }
@@ -501,6 +460,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     CB_REQUIRE(value == 0 || value == 256 || value == 512 || value == 1024, CB_E_INVALID_ARG,
                "topk_threads must be 0, 256, 512 or 1024");
     c->topk_threads = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "q_split") == 0) {
+    c->q_split = value != 0;
     return CB_OK;
   }
   if (std::strcmp(name, "attn_pair") == 0) {
@@ -560,6 +523,18 @@ extern "C" cb_status cb_controller_pick_device(double prefill_ms, const double* 
   for (int d = 0; d < n_dev; ++d)  // cheapest device with T_recompute >= T_load; ties -> earlier
     if (t_rec >= load_ms[d] && (best < 0 || cost[d] < cost[best])) best = d;
   *pick_out = best;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_controller_schedule(double prefill_ms, double kv_bytes_per_token, double bytes_per_ms,
+                                            double r_min, int32_t n_ctx, int32_t n_layers, int32_t* k_sched_out,
+                                            double* r_out, double* load_ms_out) {
+  CB_REQUIRE(k_sched_out != nullptr, CB_E_INVALID_ARG, "k_sched_out is NULL");
+  double r = 0.0, ld = 0.0;
+  CB_TRY(cb_controller_ratio(prefill_ms, kv_bytes_per_token, n_ctx, bytes_per_ms, r_min, &r, &ld));
+  CB_TRY(cb_schedule(r, n_ctx, n_layers, k_sched_out));
+  if (r_out) *r_out = r;
+  if (load_ms_out) *load_ms_out = ld;
   return CB_OK;
 }
 
@@ -733,54 +708,8 @@ cb_status mlp_block(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int Q, c
     CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
     return push ? comm_allreduce_pushed(c, b.h_out, Q, s) : comm_allreduce_f32(c, b.h_out, (size_t)Q * d, s);
   }
-  // MLP split (blend sizes): gate_up in S feature blocks on the caller's stream; the down projection of
-  // block k (a K block of W_down) on the aux stream as soon as block k's activations exist, writing an
-  // fp32 partial; the last block adds h_in + the partials in block order + its own product. The down
-  // blocks fill the SMs gate_up leaves idle (its last wave, per-block grids), instead of running after it.
-  if (mlp_fused_ok(c, Q) && gemm_tc_ok(c, c->x, d, w.w_gate_up, d, Q, d, eg) &&
-      gemm_tc_ok(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed)) {
-    CB_TRY(launch_mlp_fused(c, c->x, w.w_gate_up, c->act, w.w_down, Q, eg, ed, s));
-    if (fuse_next && b.next_ready) *b.next_ready = true;
-    return CB_OK;
-  }
-  const int S = c->mlp_split;
-  const int fb = m.d_ff / S;
-  const bool split = S > 1 && Q <= 768 && m.dtype == CB_BF16 && m.d_ff % (S * 16) == 0 &&
-                     gemm_tc_ok(c, c->x, d, w.w_gate_up, d, Q, d, eg) && fuse_next == (ed.norm_gain != nullptr);
-  if (!split) {
-    CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
-    CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
-    if (fuse_next && b.next_ready) *b.next_ready = true;
-    return CB_OK;
-  }
-  const size_t B = dtype_bytes(m.dtype);
-  cudaStream_t a = c->aux_stream;
-  CB_CUDA(cudaEventRecord(c->ev_mlp[0], s));
-  CB_CUDA(cudaStreamWaitEvent(a, c->ev_mlp[0], 0));  // fork: the aux stream sees o-proj's h / y / ss
-  for (int k = 0; k < S; ++k) {
-    EpiParams gk = eg;  // features [k fb, (k+1) fb): gate rows k fb.., up rows ff + k fb.., act columns k fb..
-    gk.N = fb;
-    gk.act = (char*)c->act + (size_t)k * fb * B;
-    CB_TRY(launch_gemm(c, c->x, d, (const char*)w.w_gate_up + (size_t)k * fb * d * B, d, Q, d, gk, 0, s));
-    CB_CUDA(cudaEventRecord(c->ev_mlp[1 + k], s));
-  }
-  for (int k = 0; k < S; ++k) {
-    CB_CUDA(cudaStreamWaitEvent(a, c->ev_mlp[1 + k], 0));
-    const void* A = (const char*)c->act + (size_t)k * fb * B;
-    const void* Bw = (const char*)w.w_down + (size_t)k * fb * B;
-    if (k + 1 < S) {  // partial product of K block k
-      EpiParams pk{};
-      pk.kind = EPI_STORE_F32; pk.M = Q; pk.N = d; pk.ldo = d; pk.outf = c->mlp_part + (size_t)k * c->max_tokens * d;
-      CB_TRY(launch_gemm(c, A, m.d_ff, Bw, m.d_ff, Q, fb, pk, 0, a));
-    } else {
-      EpiParams lk = ed;
-      lk.n_add = S - 1;
-      for (int j = 0; j + 1 < S; ++j) lk.add_part[j] = c->mlp_part + (size_t)j * c->max_tokens * d;
-      CB_TRY(launch_gemm(c, A, m.d_ff, Bw, m.d_ff, Q, fb, lk, 0, a));
-    }
-  }
-  CB_CUDA(cudaEventRecord(c->ev_mlp[5], a));
-  CB_CUDA(cudaStreamWaitEvent(s, c->ev_mlp[5], 0));  // join
+  CB_TRY(launch_gemm(c, c->x, d, w.w_gate_up, d, Q, d, eg, 0, s));
+  CB_TRY(launch_gemm(c, c->act, m.d_ff, w.w_down, m.d_ff, Q, m.d_ff, ed, 0, s));
   if (fuse_next && b.next_ready) *b.next_ready = true;
   return CB_OK;
 }
@@ -842,7 +771,18 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
     e.k_ref = kb; e.v_ref = vb; e.n_cand = n_cand; e.ld_part = c->max_tokens;
     e.dev_part = dev_part + (c->tp_world > 1 ? 2 * nb_local * c->tp_rank * c->max_tokens : 0);
   }
-  CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, R, d, e, 0, s));
+  // Q is only needed for the kept rows (the HKVD queries). Where the selection drops many
+  // candidates (layer 1: C_1 = all tokens, |S_1| ~ r N) project K, V for every candidate (Delta_kv needs
+  // them) and Q after the top-k, for the kept rows only.
+  const size_t B = dtype_bytes(m.dtype);
+  const bool split_q = fuse_dev && c->q_split && Q > 0 && 4 * (n_cand - k) > n_cand;
+  EpiParams eq = e;
+  if (split_q) {
+    e.col0 = qd; e.N = 2 * kvd;
+    CB_TRY(launch_gemm(c, c->x, d, (const char*)w.w_qkv + (size_t)qd * d * B, d, R, d, e, 0, s));
+  } else {
+    CB_TRY(launch_gemm(c, c->x, d, w.w_qkv, d, R, d, e, 0, s));
+  }
   if (fuse_dev) CB_TRY(comm_allgather_f32(c, dev_part, 2 * nb_local * c->max_tokens, s));  // (i)
   // 3. HKVD = top-k of Delta_kv (Insight 1)
   float* dev = dev_out ? dev_out : c->dev;
@@ -855,8 +795,19 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
   if (Q == 0) return CB_OK;
   // 4. only the KV of the HKVD tokens (and the suffix) is updated (R3)
   CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));
+  const int* q_rows = c->qrow;  // row of each kept query in c->q
+  if (split_q) {
+    // the kept rows of the projection input (and their RMSNorm blocks) gathered, then Q over them:
+    // c->act and c->attn are free until the attention / MLP of this layer
+    float* ssq = eq.ss_in ? reinterpret_cast<float*>(c->attn) : nullptr;
+    CB_TRY(launch_gather_rows(c, c->x, eq.ss_in, c->qrow, Q, eq.ld_ss, c->act, ssq, s));
+    eq.M = Q; eq.N = qd; eq.col0 = 0; eq.row_tok = b.qtok; eq.ss_in = ssq;
+    eq.dev_part = nullptr; eq.k_ref = nullptr; eq.v_ref = nullptr; eq.n_cand = 0;
+    CB_TRY(launch_gemm(c, c->act, d, w.w_qkv, d, Q, d, eq, 0, s));
+    q_rows = c->iota;
+  }
   // 5. attention of the selected queries over all tokens, then W_o + residual, MLP + residual
-  CB_TRY(launch_attention(c, c->q, c->qrow, b.qtok, Q, kb, vb, N + n_suf, c->attn, 0, s));
+  CB_TRY(launch_attention(c, c->q, q_rows, b.qtok, Q, kb, vb, N + n_suf, c->attn, 0, s));
   return mlp_block(c, w, b, Q, c->qrow, s);
 }
 

@@ -105,9 +105,6 @@ struct EpiParams {
   // (blocks summed in order) -- RMSNorm's per-row factor taken out of the projection.
   const float* norm_gain; void* y_out; float* ss_out;
   const float* ss_in; int ld_ss, norm_d; float norm_eps;
-  // EPI_RESID (tcgen05 staged path): fp32 partial products of earlier K blocks (row-major, ld = ldo) added
-  // in this order after h_in and before the accumulator: h_out = (((h_in + p0) + p1) + ...) + acc
-  const float* add_part[3]; int n_add;
   // Head-parallel fused reduce-scatter (comm.cu): when push_base[0] is set, the fp32 output row m of
   // EPI_STORE_F32 / EPI_RESID goes to push_base[m / push_rows] + push_off (this rank's receive plane in the
   // block of the rank that owns row m, over NVLink) instead of outf / h_out.

@@ -60,7 +60,7 @@ struct cb_ctx {
   int* attn_work;       // [2] persistent attention: item claim counter, finished-CTA counter (zero between launches)
   long long attn_part_rows;
   int gemm_sched;   // cb_set_option("gemm_sched")
-  int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05, 3 mma.sync
+  int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
   int attn_nopk;    // cb_set_option("attn_packed", 0): scalar FFMA/FADD in the softmax (A/B of FFMA2/FADD2)
   int attn_wg4;     // cb_set_option("attn_wg4"): four softmax warpgroups (32 keys per thread) instead of two
@@ -78,16 +78,11 @@ struct cb_ctx {
   // request mode: copy stream + per-layer "layer KV landed" events (P:2509 fetch/synchronize)
   cudaStream_t copy_stream;
   cudaStream_t aux_stream;    // MLP split: the down-projection blocks run here, overlapping gate_up blocks
-  cudaEvent_t ev_mlp[6];      // fork, gate_up block 0..3 done, join
-  float* mlp_part;            // [3][T][d] fp32 partial products of down-projection K blocks 0..2
-  int mlp_split;              // cb_set_option("mlp_split", S): K blocks of the MLP at blend sizes (1 = off)
   int topk_drop_max;          // cb_set_option("topk_drop", n): drop-smallest top-k path when n_cand - k <= n
+  int q_split;                // cb_set_option("q_split", 0/1): layer-1 Q projected after the selection (kept rows)
   int attn_pair;              // cb_set_option("attn_pair", 0/1/2): light/heavy row-tile pairing (attention_tc5.cu)
   int topk_sort;              // cb_set_option("topk_sort", 0/1): bitonic path when n_cand <= top-k threads
   int topk_threads;           // cb_set_option("topk_threads", 256 | 512 | 1024): top-k block size (0 = 1024)
-  int mlp_fused;              // cb_set_option("mlp_fused", S): one persistent gate_up + down kernel (0 = off)
-  float* mlp_scr;             // fused MLP: fp32 partials of the down projection's K blocks
-  int* mlp_cnt;               // fused MLP: block / merge counters (zero between launches)
   cudaEvent_t ev_ready;
   cudaEvent_t ev_realign[2];  // realign of layers 1..L-1 on the aux stream: fork, done
   int realign_overlap;        // cb_set_option("realign_overlap"): that realign runs under layer 0
@@ -200,6 +195,8 @@ cb_status launch_embed_norm(cb_ctx* c, const void* embed, const int* tok, const 
 cb_status launch_rmsnorm(cb_ctx* c, const float* h, const float* gain, int n_rows, void* x, cudaStream_t s);
 cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int* qrow, const int* qtok, int n,
                             void* kb, void* vb, cudaStream_t s);
+cb_status launch_gather_rows(cb_ctx* c, const void* x, const float* ss, const int* qrow, int n, int ld_ss, void* xq,
+                             float* ssq, cudaStream_t s);
 cb_status launch_local_pos(cb_ctx* c, const int* chunk_start_host, int n_chunks, int* src_pos, cudaStream_t s);
 // device positions: 0 <= pos[t] < max_pos (else CB_DEVERR_POS_RANGE) and strictly increasing (else CB_DEVERR_POS_ORDER)
 cb_status launch_pos_check(cb_ctx* c, const int* pos, int T, cudaStream_t s);

@@ -283,6 +283,32 @@ cb_status launch_scatter_kv(cb_ctx* c, const void* kf, const void* vf, const int
 }
 
 // ---------------------------------------------------------------------------------------------
+// Kept-query rows of the projection input (layer 1's Q-after-selection): xq[j] = x[qrow[j]] (bf16 rows
+// of d) and, with the fused RMSNorm, ssq[j] = ss[qrow[j]] (ld_ss sum-of-squares blocks). Block per row.
+// ---------------------------------------------------------------------------------------------
+__global__ void gather_rows_kernel(const bf16* __restrict__ x, const float* __restrict__ ss, const int* __restrict__ qrow,
+                                   int d, int ld_ss, bf16* __restrict__ xq, float* __restrict__ ssq) {
+  pdl_enter();
+  const int j = blockIdx.x;
+  const size_t src = (size_t)__ldg(qrow + j);
+  for (int e = threadIdx.x * 8; e < d; e += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(xq + (size_t)j * d + e) = __ldg(reinterpret_cast<const uint4*>(x + src * d + e));
+  if (ss != nullptr)
+    for (int b = threadIdx.x; b < ld_ss; b += blockDim.x) ssq[(size_t)j * ld_ss + b] = __ldg(ss + src * ld_ss + b);
+}
+
+cb_status launch_gather_rows(cb_ctx* c, const void* x, const float* ss, const int* qrow, int n, int ld_ss, void* xq,
+                             float* ssq, cudaStream_t s) {
+  if (n == 0) return CB_OK;
+  const int d = c->m.d_model;
+  CB_REQUIRE(c->m.dtype == CB_BF16 && d % 8 == 0, CB_E_UNSUPPORTED, "gather_rows: bf16 rows of a multiple of 8");
+  ProfScope ps_(c, PROF_MISC, s);
+  CB_LAUNCH(c, gather_rows_kernel, n, 128, 0, s, (const bf16*)x, ss, qrow, d, ld_ss, (bf16*)xq, ssq);
+  CB_LAUNCHED(c);
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 // chunk-local positions from chunk starts passed by value (no host->device copy, graph-safe)
 // ---------------------------------------------------------------------------------------------
 struct ChunkTable {

@@ -195,22 +195,6 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
           pre[it] = cont ? __ldcg(p) : *p;
         }
       }
-      if (!cont && e.n_add > 0) {  // earlier K blocks' partials (MLP split), added in block order
-#pragma unroll
-        for (int pi = 0; pi < 3; ++pi) {
-          if (pi >= e.n_add) break;
-          float4 q[8];
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int m = m_base + it * 4 + r0;
-            q[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (m < M && col_ok) q[it] = __ldcg(reinterpret_cast<const float4*>(e.add_part[pi] + (size_t)m * e.ldo + col));
-          }
-#pragma unroll
-          for (int it = 0; it < 8; ++it)
-            pre[it] = make_float4(pre[it].x + q[it].x, pre[it].y + q[it].y, pre[it].z + q[it].z, pre[it].w + q[it].w);
-        }
-      }
     }
     if constexpr (KIND == EPI_QKV) {
       qc = e.col0 + n;  // column of the fused [q | k | v] output
@@ -345,7 +329,7 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
 }
 
 // ---- lean residual epilogue ---------------------------------------------------------------------------
-// EPI_RESID without the split-K continuation, peer push or partial adds (the blend's o_proj / down_proj):
+// EPI_RESID without the split-K continuation or peer push (the blend's o_proj / down_proj):
 // the same staged row-contiguous traffic and the same arithmetic (bitwise equal to tile_epilogue), but
 // the per-row operands (validity, source / destination row offsets) are computed once per tile and the
 // cold paths are gone, so the unrolled chunk loop is compact. tools/gemm_trace.py (r02g): the generic
@@ -431,7 +415,7 @@ __device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base
 
 // Whether a RESID tile may take resid_lean (else the generic tile_epilogue).
 __device__ __forceinline__ bool resid_lean_ok(const EpiParams& e, bool cont, int M) {
-  return !cont && e.n_add == 0 && e.push_base[0] == nullptr && (e.N % 32) == 0 &&
+  return !cont && e.push_base[0] == nullptr && (e.N % 32) == 0 &&
          (long long)(M + 256) * e.ldo < (1ll << 31);
 }
 

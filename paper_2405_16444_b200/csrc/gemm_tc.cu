@@ -351,6 +351,7 @@ struct TmKeyHash {
 // tail_p K pieces that fill that round; the last piece of a tile to finish merges (gemm_tc2.cu).
 struct Plan {
   int bn, sk_ctas, grid, pair, ksplit, tail_r = 0, tail_p = 1;
+  double cost = 0.0;  // model cycles per SM
 };
 constexpr int MAX_TAIL_P = 4;  // gemm_tc2.cu merges at most 4 pieces
 constexpr double TAIL_MERGE_CYC = 6000.0;  // partial store + merge reads + TMEM rewrite
@@ -433,8 +434,10 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
     }
     }
   }
+  best.cost = best_cost;
   return best;
 }
+
 }  // namespace
 
 struct TmapCache {
@@ -531,7 +534,7 @@ static cb_status launch_bn(cb_ctx* c, const void* A, int lda, const void* B, int
 cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
                          const EpiParams& e, cudaStream_t s) {
   // the stream-K fixup path has no fused-RMSNorm producer: plain data-parallel then
-  const int sched = ((e.norm_gain != nullptr || e.n_add > 0) && c->gemm_sched == 2) ? 1 : c->gemm_sched;
+  const int sched = (e.norm_gain != nullptr && c->gemm_sched == 2) ? 1 : c->gemm_sched;
   const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit,
                             c->tmaps->force_tail, c->tmaps->no192, c->tmaps->pairs_cap[e.kind],

@@ -1,5 +1,5 @@
 """Loading controller (§6): the oracle pinned to the paper's worked examples
-(tests/golden/controller.json, P:2655-2659), and the library's host implementation (cb_controller_*,
+(tests/golden/controller.json, P:2666-2670), and the library's host implementation (cb_controller_*,
 no GPU needed) checked against the oracle."""
 import json
 import os
@@ -69,3 +69,19 @@ def test_library_controller_matches_oracle():
         api.controller_ratio(0.0, 1.0, 1, 1.0)
     with pytest.raises(api.CacheBlendError):
         api.controller_ratio(1.0, 1.0, 1, 1.0, r_min=1.5)
+
+
+def test_library_controller_schedule():
+    """cb_controller_schedule = cb_schedule(cb_controller_ratio(...)): the controller's ratio drives the
+    blend's per-layer counts."""
+    from paper_2405_16444_b200 import api
+    from paper_2405_16444_b200.build import build
+    build()
+    rng = np.random.default_rng(1)
+    for _ in range(100):
+        pre, kv, bpm = rng.uniform(0.05, 50), rng.uniform(1e3, 1e6), rng.uniform(1e3, 1e8)
+        n, L = int(rng.integers(1, 20000)), int(rng.integers(2, 81))
+        ks, r, ld = api.controller_schedule(pre, kv, bpm, n, L, 0.15)
+        r2, ld2 = api.controller_ratio(pre, kv, n, bpm, 0.15)
+        assert r == r2 and ld == ld2
+        assert ks == O.schedule(r, n, L)

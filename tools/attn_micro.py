@@ -15,7 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--splits", default="0,1,2,3,4,6")
-    ap.add_argument("--impls", default="2,4")
+    ap.add_argument("--impls", default="2")
     ap.add_argument("--pairs", default="0,1")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
