@@ -67,7 +67,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *                 cut between the two CTAs and merged through distributed shared memory
  *   "q_split"     1 = layer 1 projects Q for the kept rows only, after the top-k (default), 0 = Q for all
  *                 candidates in the fused QKV GEMM
- *   "topk_sort"   1 = bitonic block sort when the candidates fit the top-k block (default), 0 = radix / drop
+ *   "topk_sort"   1 = bitonic block sort when the candidates fit the top-k block, 0 = radix / drop-smallest
+ *                 (default: the sort measured slower inside the blend)
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
  *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
  *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue

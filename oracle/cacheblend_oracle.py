@@ -405,6 +405,50 @@ def blend_forward(model: Model, tok: np.ndarray, pos: np.ndarray, chunk_starts: 
     return BlendResult(K, V, sel, devs, cands, h, h_layers, mc.macs if mc else 0)
 
 
+def attention_probs(q: np.ndarray, q_pos: np.ndarray, k: np.ndarray, k_pos: np.ndarray) -> np.ndarray:
+    """The forward attention matrix A: softmax(q k^T / sqrt(hd)) of each query row and q head over all
+    given keys, masked by original position (key visible iff k_pos <= q_pos), GQA as causal_attention.
+    q [R][n_q][hd] (rotated), k [T][n_kv][hd] (rotated). Returns [n_q][R][T]."""
+    R, n_q, hd = q.shape
+    grp = n_q // k.shape[1]
+    visible = np.asarray(k_pos)[None, :] <= np.asarray(q_pos)[:, None]
+    A = np.zeros((n_q, R, k.shape[0]), dtype=F64)
+    for h in range(n_q):
+        s = (q[:, h, :] @ k[:, h // grp, :].T) / math.sqrt(hd)
+        s[~visible] = -np.inf
+        s -= s.max(axis=1, keepdims=True)
+        p = np.exp(s)
+        A[h] = p / p.sum(axis=1, keepdims=True)
+    return A
+
+
+def attention_deviation(model: Model, tok: np.ndarray, pos: np.ndarray, chunk_starts: Sequence[int], n_suf: int,
+                        Kc: np.ndarray, Vc: np.ndarray, k_sched: Sequence[int],
+                        force_sel: Optional[Sequence[np.ndarray]] = None) -> np.ndarray:
+    """Attention deviation per layer, Delta_attn(A_i, A_i^full): the L-2 norm of the difference
+    between the forward attention matrix of layer i after the blend and after full prefill (reading R16: the
+    matrix of the query rows -- the n_suf uncached suffix tokens, the user query of P:2793 -- over every key;
+    each side's queries come from its own layer input, i.e. the hidden states its KV produced).
+    Returns [L] (layer 0 is exactly 0: its KV and its queries do not depend on cross-chunk attention)."""
+    if n_suf < 1:
+        raise ValueError("attention deviation needs query (suffix) rows")
+    tok, pos = np.asarray(tok), np.asarray(pos).astype(np.int64)
+    qpos = pos[-n_suf:]
+    res = blend_forward(model, tok, pos, chunk_starts, n_suf, Kc, Vc, k_sched, force_sel=force_sel,
+                        keep_layers=True)
+    h_full = model.embed[tok]
+    out = np.zeros(model.n_layers, dtype=F64)
+    for i in range(model.n_layers):
+        hb = model.embed[tok[-n_suf:]] if i == 0 else res.h_layers[i - 1][-n_suf:]
+        qb = qkv(model, i, hb, qpos)[0]
+        qf, kf, vf = qkv(model, i, h_full, pos)
+        a_blend = attention_probs(qb, qpos, res.K[i], pos)
+        a_full = attention_probs(qf[-n_suf:], qpos, kf, pos)
+        out[i] = float(np.sqrt(np.sum((a_blend - a_full) ** 2)))
+        h_full = attn_out_mlp(model, i, h_full, causal_attention(qf, pos, kf, vf, pos))
+    return out
+
+
 def blend_replay_rows(tok: np.ndarray, pos: np.ndarray, chunk_starts: Sequence[int], Kc: np.ndarray,
                       Vc: np.ndarray, force_sel: Sequence[np.ndarray], layer_model, embed_rows: np.ndarray,
                       dev_rows_1: Sequence[int] = (), h_rows_last: Optional[Sequence[int]] = None,

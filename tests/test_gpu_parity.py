@@ -518,12 +518,14 @@ def test_blend_request_equals_forward(P, name, dtype, n_suf):
     np.testing.assert_array_equal(sel.numpy()[:ks[-1]], a["sel"][-1])
 
 
-@pytest.mark.parametrize("load_ms,seed", [(0.01, 1), (0.3, 2), (0.8, 3)])
+@pytest.mark.parametrize("load_ms,seed", [(0.01, 1), (0.3, 2), (0.5, 3)])
 def test_controller_driven_request_matches_oracle(P, load_ms, seed):
     """the loading controller picks r = max(r_eq, 15 %) from the per-layer prefill time and
     the KV load time, cb_controller_schedule turns it into k_i, and cb_blend_request (host chunk
     KV fetched layer by layer on the copy stream) blends at that schedule: compared directly with the fp64
-    oracle at the same schedule (tiny model, fp32 mode; selections identical up to near-ties)."""
+    oracle at the same schedule (tiny model, fp32 mode; selections identical up to near-ties). Ratios stay
+    below the share of tokens outside the first chunk: the first chunk's deviations are 0 up to the storage
+    rounding of its cache, so beyond that count the choice among them is arbitrary on both sides (R7)."""
     s, m, req, tok, pos, cs, Kc, Vc, _ = _oracle_case("tiny", seed, [32, 32, 32], 4, "f32", 0.15)
     N, L = req.n_ctx, s.n_layers
     kv_tok = 2 * s.kvd * 4  # K and V of one token and layer, fp32
