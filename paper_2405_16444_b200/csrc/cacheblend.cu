@@ -293,7 +293,8 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   c->topk_drop_max = 48;
   c->topk_sort = 0;  // bitonic path measured slower in the blend (13.5 vs 10.5 us per launch, profiles/r02)
   c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
-  c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
+  c->q_split = 1;
+  c->gemm_pf = 1;    // layer 1: Q projected for the kept rows only, after the selection
   c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
   if (st != CB_OK) {
     cudaFree(c->rope_tab);
@@ -460,6 +461,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     CB_REQUIRE(value == 0 || value == 256 || value == 512 || value == 1024, CB_E_INVALID_ARG,
                "topk_threads must be 0, 256, 512 or 1024");
     c->topk_threads = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_pf") == 0) {
+    c->gemm_pf = value != 0;
     return CB_OK;
   }
   if (std::strcmp(name, "q_split") == 0) {

@@ -329,7 +329,7 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
 }
 
 // ---- lean residual epilogue ---------------------------------------------------------------------------
-// EPI_RESID without the split-K continuation or peer push (the blend's o_proj / down_proj):
+// EPI_RESID without a peer push (the blend's o_proj / down_proj, every piece of a k-split chain):
 // the same staged row-contiguous traffic and the same arithmetic (bitwise equal to tile_epilogue), but
 // the per-row operands (validity, source / destination row offsets) are computed once per tile and the
 // cold paths are gone, so the unrolled chunk loop is compact. tools/gemm_trace.py (r02g): the generic
@@ -338,10 +338,12 @@ __device__ __forceinline__ void tile_epilogue(const EpiParams& e, int M, int m_b
 // Needs e.N % 32 == 0 and 32-bit row offsets ((M + 256) * ldo < 2^31).
 template <int BN, bool NORM>
 __device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base, int n0, uint32_t trow, float4* buf,
-                                           int lane, long long* dbg = nullptr) {
+                                           int lane, long long* dbg = nullptr, bool cont = false) {
+  // cont: a later piece of a k-split chain adds onto the running sum in h_out (rows in place, read past L1)
   const int j = lane & 7, r0 = lane >> 3;
   const int my_m = m_base + lane;
-  const int my_src = my_m < M ? (e.res_row ? __ldg(e.res_row + my_m) : my_m) : 0;
+  const int my_src = my_m < M ? (cont ? my_m : (e.res_row ? __ldg(e.res_row + my_m) : my_m)) : 0;
+  const float* base = cont ? e.h_out : e.h_in;
   unsigned okmask = 0;
   int in_off[8], out_off[8];  // element offsets of the rows this lane touches (it * 4 + r0)
 #pragma unroll
@@ -363,7 +365,8 @@ __device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base
     float4 pre[8];
 #pragma unroll
     for (int it = 0; it < 8; ++it)
-      pre[it] = ((okmask >> it) & 1) ? *reinterpret_cast<const float4*>(e.h_in + in_off[it] + n)
+      pre[it] = ((okmask >> it) & 1) ? (cont ? __ldcg(reinterpret_cast<const float4*>(base + in_off[it] + n))
+                                            : *reinterpret_cast<const float4*>(base + in_off[it] + n))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
     {
       float v[32];
@@ -414,8 +417,8 @@ __device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base
 }
 
 // Whether a RESID tile may take resid_lean (else the generic tile_epilogue).
-__device__ __forceinline__ bool resid_lean_ok(const EpiParams& e, bool cont, int M) {
-  return !cont && e.push_base[0] == nullptr && (e.N % 32) == 0 &&
+__device__ __forceinline__ bool resid_lean_ok(const EpiParams& e, int M) {
+  return e.push_base[0] == nullptr && (e.N % 32) == 0 &&
          (long long)(M + 256) * e.ldo < (1ll << 31);
 }
 

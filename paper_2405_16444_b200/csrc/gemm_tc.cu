@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (KIND == EPI_QKV && n_con == 0 && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
           gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow, rs);
-        } else if (KIND == EPI_RESID && n_con == 0 && gepi::resid_lean_ok(e, false, M)) {
+        } else if (KIND == EPI_RESID && n_con == 0 && gepi::resid_lean_ok(e, M)) {
           if (e.norm_gain != nullptr)
             gepi::resid_lean<BN, true>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane);
           else

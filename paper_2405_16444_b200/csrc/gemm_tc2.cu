@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
                     int m_tiles, int n_tiles, EpiParams e, int ksplit, int* __restrict__ kflags,
                     int tail_r, int tail_p, float* __restrict__ tscr, int* __restrict__ tcnt,
-                    long long* __restrict__ dbg) {
+                    long long* __restrict__ dbg, const char* __restrict__ pf_b, long long pf_row_bytes) {
   // debug_trace: globaltimer (ns) events of each CTA's first work item at dbg[blockIdx.x * 8 + event]
 #define DBG2(ev) do { if (dbg != nullptr && blockIdx.x < 256) dbg[blockIdx.x * 8 + (ev)] = tc::globaltimer(); } while (0)
   using C = Cfg2<BN>;
@@ -106,6 +106,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc::cluster_sync();  // barriers of both CTAs initialised before any remote arrive / transaction
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Weights do not depend on the previous kernel: before waiting for it, pull this CTA's B rows of its first
+  // tile into L2 (one bulk prefetch). A CTA that starts on an SM the previous kernel already left (its tail:
+  // the attention's light row tiles, a partial last GEMM round) streams its weights from HBM during that tail,
+  // and its mainloop then waits on L2 instead of HBM latency.
+  if (pf_b != nullptr && warp == 0 && lane == 0 && pair < items) {
+    const WorkItem w0 = work_item(pair, tiles, num_kb, ksplit, tail_r, tail_p);
+    const int nb0 = w0.t / m_tiles;
+    const int row0 = SW ? (rank == 0 ? nb0 * OUT_N : e.ff + nb0 * OUT_N) : nb0 * BN + (int)rank * C::B_HALF;
+    const long long rows_total = SW ? 2LL * e.ff : (long long)e.N;
+    const long long nrows = rows_total - row0 < C::B_HALF ? rows_total - row0 : C::B_HALF;
+    if (nrows > 0) {
+      const char* p = pf_b + (long long)row0 * pf_row_bytes;
+      long long bytes = nrows * pf_row_bytes;
+      while (bytes > 0) {  // the bulk prefetch size is a 32-bit count of 16-byte multiples
+        const uint32_t chunk = (uint32_t)(bytes < (1ll << 30) ? bytes : (1ll << 30)) & ~15u;
+        if (chunk == 0) break;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(chunk) : "memory");
+        p += chunk;
+        bytes -= chunk;
+      }
+    }
+  }
   pdl_enter();  // prologue above overlapped the previous kernel; its outputs are visible from here
   if (threadIdx.x == 0) DBG2(0);
 
@@ -242,10 +264,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (!skip_epilogue) {
       if (KIND == EPI_QKV && e.hd % 64 == 0 && !gepi::staged_kind<KIND>()) {
         gepi::qkv_row<OUT_N>(e, m, m < M, nb * OUT_N, trow, rs);
-      } else if (KIND == EPI_RESID && gepi::resid_lean_ok(e, sp > 0, M) && (sp == ksplit - 1)) {
+      } else if (KIND == EPI_RESID && gepi::resid_lean_ok(e, M)) {
         long long* tdbg = (dbg != nullptr && it == 0 && warp == 2 && blockIdx.x < 128) ? dbg + 1024 + blockIdx.x * 8 : nullptr;
-        if (e.norm_gain != nullptr) gepi::resid_lean<BN, true>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane, tdbg);
-        else gepi::resid_lean<BN, false>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane, tdbg);
+        float4* wb = ebuf + (warp - 2) * gepi::EPI_WARP_F4;
+        // the fused RMSNorm producer runs on the last piece of a k-split chain only (the finished sum)
+        if (e.norm_gain != nullptr && sp == ksplit - 1)
+          gepi::resid_lean<BN, true>(e, M, m0 + q * 32, nb * OUT_N, trow, wb, lane, tdbg, sp > 0);
+        else
+          gepi::resid_lean<BN, false>(e, M, m0 + q * 32, nb * OUT_N, trow, wb, lane, tdbg, sp > 0);
       } else if (gepi::staged_kind<KIND>() && (KIND != EPI_QKV || e.hd % 32 == 0)) {  // staged, row-contiguous
         gepi::tile_epilogue<KIND, BN>(e, M, m0 + q * 32, nb * OUT_N, trow, ebuf + (warp - 2) * gepi::EPI_WARP_F4, lane,
                                       sp > 0, sp == ksplit - 1,
@@ -322,7 +348,8 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
   CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
                     m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
-                    (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr));
+                    (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr,
+                    c->gemm_pf ? (const char*)B : nullptr, (long long)ldb * 2));
   CB_LAUNCHED(c);
   return CB_OK;
 }

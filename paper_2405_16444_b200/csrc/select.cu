@@ -4,6 +4,12 @@
 
 #include "ctx.h"
 
+__device__ __forceinline__ long long tc_globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Delta_kv[j] = sum_h ( ||k_new[j,h] - k_ref[tok_j,h]||^2 + ||v_new[j,h] - v_ref[tok_j,h]||^2 ).
 // One warp per candidate; per-head partials are warp-reduced in a fixed tree and summed over heads
@@ -122,8 +128,13 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
                                                             int* __restrict__ qrow, int* __restrict__ qtok,
                                                             int* __restrict__ sel_tok, int* err,
                                                             const float* __restrict__ dev_part, int n_kv, int ld_part,
-                                                            int dev_mode, int drop_max, int sort_path) {
+                                                            int dev_mode, int drop_max, int sort_path,
+                                                            long long* __restrict__ dbg) {
+  // debug_trace 200: globaltimer of the phases (entry, inputs visible, Delta_kv summed, selected, done)
+#define TK_DBG(i) do { if (dbg != nullptr && threadIdx.x == 0) dbg[i] = tc_globaltimer(); } while (0)
+  TK_DBG(0);
   pdl_enter();
+  TK_DBG(1);
   extern __shared__ unsigned keys[];
   __shared__ int hist[256];
   __shared__ int sm_warp[32];
@@ -156,6 +167,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
     }
     __syncthreads();
   }
+  TK_DBG(2);
 
   // suffix rows are always kept
   for (int s = tid; s < n_suf; s += blockDim.x) {
@@ -235,7 +247,37 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   // complement of "k largest, ties to the lower index") instead of four radix passes.
   constexpr unsigned DROPPED = 0xFFFFFFFFu;  // above every key (keys are bits of non-negative floats)
   const bool drop_path = k < n_cand && n_cand - k <= drop_max;
-  if (drop_path) {
+  if (drop_path && n_cand <= 1024) {
+    // one warp, 32 keys per lane in registers: d rounds of (lane minimum, warp minimum) with no block barrier
+    // (the block-wide loop below costs two barriers per dropped key). Same order, same selection.
+    __syncthreads();
+    if (tid < 32) {
+      unsigned long long v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int j = tid + 32 * q;
+        v[q] = j < n_cand ? (((unsigned long long)keys[j] << 32) | (unsigned)(0x7FFFFFFF - j)) : ~0ull;
+      }
+      for (int r = 0; r < n_cand - k; ++r) {
+        unsigned long long b = v[0];
+#pragma unroll
+        for (int q = 1; q < 32; ++q) b = v[q] < b ? v[q] : b;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
+          b = y < b ? y : b;
+        }
+        const int jd = 0x7FFFFFFF - (int)(unsigned)(b & 0xFFFFFFFFu);
+        if ((jd & 31) == tid) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (q == (jd >> 5)) v[q] = ~0ull;
+          keys[jd] = DROPPED;
+        }
+      }
+    }
+    __syncthreads();
+  } else if (drop_path) {
     __syncthreads();
     __shared__ unsigned long long sm_best[32];
     for (int r = 0; r < n_cand - k; ++r) {
@@ -313,6 +355,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   } else {
     prefix = 0; rem = n_cand;  // take everything: every key >= 0 qualifies via the eq path below
   }
+  TK_DBG(3);
   const unsigned vstar = prefix;
   const bool all = (k >= n_cand);
   // drop path: sel = not dropped, expressed through the same compaction (key > vstar, no ties)
@@ -323,7 +366,8 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   int n_eq = 0;
   if (!all && !drop_path)
     for (int j = j0; j < j1; ++j) n_eq += (keys[j] == vstar);
-  const int eq_before = block_excl_scan(n_eq, sm_warp, &sm_total);
+  // (block-uniform) only the radix path has ties at the k-th value to resolve
+  const int eq_before = (all || drop_path) ? 0 : block_excl_scan(n_eq, sm_warp, &sm_total);
   int n_sel = 0, eq = eq_before;
   for (int j = j0; j < j1; ++j) {
     const unsigned key = keys[j];
@@ -345,6 +389,8 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
       ++out;
     }
   }
+  TK_DBG(4);
+#undef TK_DBG
 }
 
 cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix, int N,
@@ -360,7 +406,8 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   const size_t smem = std::max((size_t)std::max(1, n_cand) * sizeof(unsigned), (size_t)nt * 2 * 8);
   CB_LAUNCH(c, (topk_kernel), 1, nt, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
                                             c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64 * std::max(1, c->tp_world), ld_part,
-                                            dev_mode, c->topk_drop_max, c->topk_sort ? 1 : 0);
+                                            dev_mode, c->topk_drop_max, c->topk_sort ? 1 : 0,
+                                            c->dbg_sel == 200 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
   return CB_OK;
 }

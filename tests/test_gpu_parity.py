@@ -438,6 +438,19 @@ def test_blend_small_bf16_replay(P, n_suf):
         assert ok, f"layer {i}: {flips} flips outside the band {band}"
 
 
+@pytest.mark.parametrize("ksplit", [2, 3])
+def test_blend_small_bf16_ksplit_chain(P, ksplit):
+    """The small-model bf16 blend with the residual GEMMs (o_proj, down_proj) as k-split chains: every piece
+    runs the lean residual epilogue, later pieces add onto h_out, the last one also produces the fused RMSNorm
+    operands of the next projection. Replay parity against the oracle."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 8, [300, 211, 157], 6, "bf16", 0.15)
+    ora = O.blend_forward(m, tok, pos, cs, 6, Kc, Vc, ks)
+    ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
+    ctx.set_option("gemm_ksplit", ksplit)
+    res = run_blend(P, s, "bf16", 8, req, tok, pos, cs, Kc, Vc, ks, force_sel=ora.sel, ctx=ctx)
+    _compare(res, ora, s, TOL["bf16"])
+
+
 @pytest.mark.parametrize("q_split", [0, 1])
 def test_blend_small_bf16_q_after_selection(P, q_split):
     """Layer 1 projects K, V for every candidate and Q only for the kept rows after the top-k (gathered
