@@ -293,8 +293,8 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   c->topk_drop_max = 48;
   c->topk_sort = 0;  // bitonic path measured slower in the blend (13.5 vs 10.5 us per launch, profiles/r02)
   c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
-  c->q_split = 1;
-  c->gemm_pf = 1;    // layer 1: Q projected for the kept rows only, after the selection
+  c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
+  c->gemm_pf = 0;    // measured neutral-to-slower (9.60 vs 9.54 ms/step, paired runs), DESIGN.md §6.1
   c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
   if (st != CB_OK) {
     cudaFree(c->rope_tab);

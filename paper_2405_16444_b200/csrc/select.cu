@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
         }
       }
       dev[j] = tot;
+      const unsigned u = __float_as_uint(tot);
+      keys[j] = (u & 0x80000000u) ? 0u : u;  // the select keys, without re-reading dev (-0.0 -> 0)
     }
     __syncthreads();
   }
@@ -238,10 +240,11 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
     return;
   }
 
-  for (int j = tid; j < n_cand; j += blockDim.x) {
-    unsigned u = __float_as_uint(dev[j]);
-    keys[j] = (u & 0x80000000u) ? 0u : u;  // -0.0 -> 0
-  }
+  if (dev_part == nullptr)  // (with the partials the keys were written while summing)
+    for (int j = tid; j < n_cand; j += blockDim.x) {
+      unsigned u = __float_as_uint(dev[j]);
+      keys[j] = (u & 0x80000000u) ? 0u : u;  // -0.0 -> 0
+    }
   // Gradual filtering keeps almost every candidate (k_i / k_(i-1) ~ 0.99 after layer 1): when only a few
   // are dropped, drop them one at a time (block argmin by (key, larger index first), which is exactly the
   // complement of "k largest, ties to the lower index") instead of four radix passes.
@@ -259,9 +262,14 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
         v[q] = j < n_cand ? (((unsigned long long)keys[j] << 32) | (unsigned)(0x7FFFFFFF - j)) : ~0ull;
       }
       for (int r = 0; r < n_cand - k; ++r) {
-        unsigned long long b = v[0];
+        unsigned long long t16[16];  // lane minimum as a 5-level tree (not a 31-long dependency chain)
 #pragma unroll
-        for (int q = 1; q < 32; ++q) b = v[q] < b ? v[q] : b;
+        for (int q = 0; q < 16; ++q) t16[q] = v[2 * q] < v[2 * q + 1] ? v[2 * q] : v[2 * q + 1];
+#pragma unroll
+        for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+          for (int q = 0; q < w; ++q) t16[q] = t16[q] < t16[q + w] ? t16[q] : t16[q + w];
+        unsigned long long b = t16[0];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
@@ -360,6 +368,29 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   const bool all = (k >= n_cand);
   // drop path: sel = not dropped, expressed through the same compaction (key > vstar, no ties)
 
+  if (drop_path && n_cand <= (int)blockDim.x) {
+    // one candidate per thread: warp ballots and one exchange of warp counts (one barrier) place each kept
+    // slot at its rank, in slot order
+    const bool sel = tid < n_cand && keys[tid] != DROPPED;
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    const int lane = tid & 31, w = tid >> 5;
+    if (lane == 0) sm_warp[w] = __popc(bal);
+    __syncthreads();
+    const int nw = (int)(blockDim.x >> 5);
+    int before = lane < w ? sm_warp[lane] : 0;  // warps before this one (w <= 31)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    (void)nw;
+    if (sel) {
+      const int out = before + __popc(bal & ((1u << lane) - 1u));
+      const int t = cand_tok[tid];
+      qrow[out] = tid;
+      qtok[out] = t;
+      if (sel_tok) sel_tok[out] = t;
+    }
+    TK_DBG(4);
+    return;
+  }
   // contiguous segment per thread so that slot order is preserved by the scans
   const int seg = (n_cand + blockDim.x - 1) / blockDim.x;
   const int j0 = min(n_cand, tid * seg), j1 = min(n_cand, j0 + seg);
