@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -56,6 +57,8 @@ def parse():
     ap.add_argument("--ratio", type=float, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--attn-deviation", action="store_true", help="GPU measurement of the attention deviation "
+                    "curve (SURVEY §8(f) N2, Fig. ca_reduction) for --config, then exit")
     ap.add_argument("--cpu-full", action="store_true", help="time one whole fp64 oracle blend (layer-streamed "
                     "weights) and the sampled estimate, then exit (validates the cpu_baseline extrapolation)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -705,6 +708,105 @@ def run_e2e(P, ctx, mw, req, s, ks, k_in, v_in, tok_h, dev, args):
                     "h_out D2H; KV^new stays on the GPU" + (" (CUDA graph)" if graphed else "")}
 
 
+def run_attn_deviation(args):
+    """SURVEY §8(f) N2 on the GPU path: attention deviation Delta_attn(A_i, A_i^full) (reading R16) of
+    a request with a 32-token query suffix, per recompute ratio, for the HKVD selection (the blend's own top-k)
+    and for a random nested selection of the same sizes (Fig. ca_reduction). Every layer runs through
+    cb_blend_layer (library kernels); the suffix rows' queries and the attention matrices of this analysis are
+    formed from the layer outputs with torch (fp32) -- measurement code, not the blend path."""
+    import torch
+    import paper_2405_16444_b200 as P
+    from paper_2405_16444_b200.build import build
+    build()
+    shape_name, lens, _ = CONFIGS[args.config if args.config in CONFIGS else "mistral"]
+    s = W.MODELS[shape_name]
+    n_suf = 32
+    req = W.Request(list(lens), n_suf, args.seed, 0.15)
+    N, T, L = req.n_ctx, req.n_total, s.n_layers
+    qd, hd = s.qd, s.head_dim
+    dev = torch.device("cuda", 0)
+    ctx = P.Context(s, "bf16", max_tokens=T, max_pos=max(2 * T, 4096))
+    mw = P.ModelWeights.synth(s, args.seed, "bf16", dev)
+    tok = torch.from_numpy(req.tokens(s.vocab)).to(dev)
+    pos = torch.from_numpy(req.global_positions()).to(dev)
+    cs = req.chunk_starts()
+    k_in = torch.empty(L, N, s.n_kv_heads, hd, dtype=torch.bfloat16, device=dev)
+    v_in = torch.empty_like(k_in)
+    for c in range(len(lens)):  # chunk caches: standalone prefill of each chunk at local positions (P:1600)
+        a, b = int(cs[c]), int(cs[c + 1])
+        kc = torch.empty(L, b - a, s.n_kv_heads, hd, dtype=torch.bfloat16, device=dev)
+        vc = torch.empty_like(kc)
+        P.blend_forward(ctx, mw, tok[a:b].contiguous(), torch.arange(b - a, dtype=torch.int32, device=dev), [0],
+                        b - a, None, None, kc, vc, [0] * L)
+        k_in[:, a:b] = kc
+        v_in[:, a:b] = vc
+    inv = 1.0 / (s.rope_theta ** (torch.arange(0, hd, 2, device=dev, dtype=torch.float64) / hd))
+    qpos = pos[N:].double()
+    ang = qpos[:, None] * inv[None, :]
+    cos, sin = torch.cos(ang).float(), torch.sin(ang).float()
+    G = s.n_q_heads // s.n_kv_heads
+
+    def attn_matrix(i, h_suf, kb):
+        """A_i of the suffix rows: softmax(q K^T / sqrt(hd)) over all T keys, masked by position, [n_q][32][T]."""
+        w = mw.layers[i]
+        x = h_suf * torch.rsqrt(h_suf.pow(2).mean(-1, keepdim=True) + s.rms_eps) * w["attn_norm"]
+        q = (x @ w["w_qkv"][:qd].float().T).view(n_suf, s.n_q_heads, hd)
+        q0, q1 = q[..., 0::2], q[..., 1::2]  # interleaved pairs (2i, 2i+1), R9
+        qr = torch.empty_like(q)
+        qr[..., 0::2] = q0 * cos[:, None] - q1 * sin[:, None]
+        qr[..., 1::2] = q0 * sin[:, None] + q1 * cos[:, None]
+        k = kb.float().repeat_interleave(G, dim=1)  # [T][n_q][hd]
+        sc = torch.einsum("rhd,thd->hrt", qr, k) / math.sqrt(hd)
+        mask = pos[None, :] > pos[N:][:, None]  # key after the query: hidden
+        sc = sc.masked_fill(mask[None], float("-inf"))
+        return torch.softmax(sc, dim=-1)
+
+    def stepped(ks, force=None, full=False):
+        """Per layer: the suffix rows' input h and this layer's blended K after the layer ran."""
+        kb = torch.empty(L, T, s.n_kv_heads, hd, dtype=torch.bfloat16, device=dev)
+        vb = torch.empty_like(kb)
+        if not full:
+            kb[:, :N] = k_in
+            vb[:, :N] = v_in
+            loc = torch.from_numpy(np.concatenate([req.local_positions(), np.zeros(n_suf)]).astype(np.int32)).to(dev)
+            P.rope_realign(ctx, kb, kb, loc, pos, L, T, T * s.kvd)
+        h = P.api.op_embed(ctx, mw.embed, tok)
+        Nn = 0 if full else N
+        cand = torch.arange(Nn, dtype=torch.int32, device=dev)
+        outs = []
+        for i in range(L):
+            nc = cand.numel()
+            h_suf = h[nc:nc + (T - Nn if full else n_suf)][-n_suf:].clone()
+            if i == 0:
+                P.blend_layer(ctx, 0, mw, h, cand, Nn, T - Nn if full else n_suf, kb[0], vb[0], pos, Nn)
+            else:
+                fs = None if force is None else torch.from_numpy(force[i].astype(np.int32)).to(dev)
+                sel, _ = P.blend_layer(ctx, i, mw, h, cand, 0 if full else ks[i], T - Nn if full else n_suf, kb[i],
+                                       vb[i], pos, Nn, force_sel=fs)
+                cand = sel.clone()
+            outs.append((h_suf, kb[i]))
+        return outs
+
+    full = stepped(None, full=True)
+    a_full = [attn_matrix(i, hs, kb) for i, (hs, kb) in enumerate(full)]
+    ratios = [0.0, 0.05, 0.1, 0.15, 0.2, 0.3, 0.5, 1.0]
+    curve = {"hkvd": [], "random": []}
+    for r in ratios:
+        ks = P.schedule(r, N, L)
+        for mode in ("hkvd", "random"):
+            force = W.nested_selection(args.seed + 100, N, ks) if mode == "random" else None
+            out = stepped(ks, force=force)
+            d = [float(torch.linalg.vector_norm(attn_matrix(i, hs, kb) - a_full[i])) for i, (hs, kb) in enumerate(out)]
+            curve[mode].append(float(np.mean(d[1:])))
+    torch.cuda.synchronize()
+    print(json.dumps({"kind": "attention deviation (P:119-121, R16), mean over layers 1..L-1",
+                      "workload": f"{shape_name} {len(lens)}x{lens[0]} + {n_suf}-token query suffix, random-init weights",
+                      "ratios": ratios, "hkvd": curve["hkvd"], "random": curve["random"],
+                      "note": "blend layers through cb_blend_layer (HKVD = the library's own top-k; random = a seeded "
+                              "nested selection of the same k_i as force_sel); full prefill = the same request as "
+                              "an uncached all-suffix blend; A_i of the suffix rows formed with torch fp32"}), flush=True)
+
+
 def run_batched(args):
     """independent Mistral-shape requests, longest-first over the ranks, each rank
     blending its own requests back to back (one CUDA graph per request). Weak scaling, no collective on
@@ -801,6 +903,8 @@ if __name__ == "__main__":
     a = parse()
     if a.cpu_full:
         run_cpu_full(a)
+    elif a.attn_deviation:
+        run_attn_deviation(a)
     elif a.impl == "reference":
         run_reference(a)
     elif a.config == "batched":
