@@ -76,8 +76,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
  *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
  *   "topk_threads" 0 = 1024 (default), 256 or 512 threads in the top-k block
- *   "gemm_pf"     1 = pair GEMMs bulk-prefetch their first tile's weight rows into L2 before the PDL wait
- *                 (experiment, measured neutral), 0 = off (default) */
+ *   "gemm_pf"     1 = pair GEMMs load the weight (B) halves of their first pipeline stages before the PDL
+ *                 wait, the A halves after it (experiment, measured neutral), 0 = off (default) */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Read-only facts about the context: "num_sms", "gemm_max_pairs" (co-resident 2-CTA clusters of the

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
                     int m_tiles, int n_tiles, EpiParams e, int ksplit, int* __restrict__ kflags,
                     int tail_r, int tail_p, float* __restrict__ tscr, int* __restrict__ tcnt,
-                    long long* __restrict__ dbg, const char* __restrict__ pf_b, long long pf_row_bytes) {
+                    long long* __restrict__ dbg, const char* __restrict__ pf_b) {
   // debug_trace: globaltimer (ns) events of each CTA's first work item at dbg[blockIdx.x * 8 + event]
 #define DBG2(ev) do { if (dbg != nullptr && blockIdx.x < 256) dbg[blockIdx.x * 8 + (ev)] = tc::globaltimer(); } while (0)
   using C = Cfg2<BN>;
@@ -106,26 +106,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc::cluster_sync();  // barriers of both CTAs initialised before any remote arrive / transaction
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // Weights do not depend on the previous kernel: before waiting for it, pull this CTA's B rows of its first
-  // tile into L2 (one bulk prefetch). A CTA that starts on an SM the previous kernel already left (its tail:
-  // the attention's light row tiles, a partial last GEMM round) streams its weights from HBM during that tail,
-  // and its mainloop then waits on L2 instead of HBM latency.
-  if (pf_b != nullptr && warp == 0 && lane == 0 && pair < items) {
+  // Weights do not depend on the previous kernel: before waiting for it (PDL), the producer puts the B (weight)
+  // loads of its first work item's first stages in flight, so after the wait those k-blocks only wait for A
+  // (activations the previous kernel just wrote, L2-resident).
+  int pre = 0;  // stages of the first work item whose B load is already in flight (uniform in warp 0)
+  if (pf_b != nullptr && warp == 0 && pair < items) {
     const WorkItem w0 = work_item(pair, tiles, num_kb, ksplit, tail_r, tail_p);
     const int nb0 = w0.t / m_tiles;
-    const int row0 = SW ? (rank == 0 ? nb0 * OUT_N : e.ff + nb0 * OUT_N) : nb0 * BN + (int)rank * C::B_HALF;
-    const long long rows_total = SW ? 2LL * e.ff : (long long)e.N;
-    const long long nrows = rows_total - row0 < C::B_HALF ? rows_total - row0 : C::B_HALF;
-    if (nrows > 0) {
-      const char* p = pf_b + (long long)row0 * pf_row_bytes;
-      long long bytes = nrows * pf_row_bytes;
-      while (bytes > 0) {  // the bulk prefetch size is a 32-bit count of 16-byte multiples
-        const uint32_t chunk = (uint32_t)(bytes < (1ll << 30) ? bytes : (1ll << 30)) & ~15u;
-        if (chunk == 0) break;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(chunk) : "memory");
-        p += chunk;
-        bytes -= chunk;
-      }
+    const int b_row0 = SW ? (rank == 0 ? nb0 * OUT_N : e.ff + nb0 * OUT_N) : nb0 * BN + (int)rank * C::B_HALF;
+    pre = w0.kb1 - w0.kb0 < C::STAGES ? w0.kb1 - w0.kb0 : C::STAGES;
+    for (int st = 0; st < pre && lane == 0; ++st) {  // lane 0 is also the producer below
+      uint8_t* sa = smem + st * C::STAGE_BYTES;
+      if (leader) tc::mbar_arrive_expect_tx(&full[st], 2 * C::STAGE_BYTES);
+      tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[st], (w0.kb0 + st) * BK, b_row0);
     }
   }
   pdl_enter();  // prologue above overlapped the previous kernel; its outputs are visible from here
@@ -133,7 +126,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs) =====
-    if (tc::elect_one()) {
+    if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int i = pair; i < items; i += n_pairs) {
@@ -142,11 +135,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
         const int b_row = SW ? (rank == 0 ? nb * OUT_N : e.ff + nb * OUT_N) : nb * BN + (int)rank * C::B_HALF;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
-          if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
-          tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
+          if (i == pair && kb - w.kb0 < pre) {  // fresh stage, B already in flight: only A
+            tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
+          } else {
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
+            tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
         if (i == pair) DBG2(1);
@@ -349,7 +346,7 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
                     m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
                     (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr,
-                    c->gemm_pf ? (const char*)B : nullptr, (long long)ldb * 2));
+                    c->gemm_pf ? (const char*)B : nullptr));
   CB_LAUNCHED(c);
   return CB_OK;
 }
