@@ -603,7 +603,11 @@ def run_ours(args):
     if heads and world > 1 and not args.no_request_sub:
         # the same job request-parallel (SURVEY §8(e) partitioning 2): every rank blends its own request on a
         # full replica, no collective -- measured after the head-parallel buffers are released
-        del mw, k_in, v_in, k_out, v_out, ctx
+        step = step_eager = graph = None  # the closures hold the head-parallel buffers too
+        del mw, k_in, v_in, k_out, v_out, ctx, step, step_eager, graph
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
         torch.cuda.empty_cache()
         sub = request_parallel_record(P, args, s, lens, ratio, world, rank, dev)
         if rank == 0:
