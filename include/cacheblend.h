@@ -214,8 +214,8 @@ CB_API cb_status cb_kv_to_paged(cb_ctx* ctx, const void* k_blend, const void* v_
                                 void* k_pages, void* v_pages, int32_t n_pages, int64_t dst_layer_stride, void* stream);
 
 /* ---- chunk KV store (§6 "KV cache store") ---------------------------- */
-/* Maps a chunk's hash to its precomputed KV cache, on one storage level (host RAM), evicting the
- * least recently used entry when full. Entries: K and V of one chunk, each [L][n_tok][n_kv][hd]
+/* Maps a chunk's hash to its precomputed KV cache in host RAM, evicting the least recently used
+ * entry when full -- to an optional disk level (cb_store_set_disk). Entries: K and V of one chunk, each [L][n_tok][n_kv][hd]
  * in the model dtype with K rotated at chunk-local positions (as cb_blend_forward's k_in). pinned = 1:
  * page-locked entries, needed by cb_blend_request_store (asynchronous per-layer DMA); 0: malloc (host
  * bookkeeping only). Thread-safe. Host-side bookkeeping: no method arithmetic. */
@@ -242,6 +242,16 @@ CB_API cb_status cb_store_lookup(cb_store* store, const cb_chunk_key* key, int32
                                  const void** k_out, const void** v_out);
 /* out6 = {used bytes, capacity, entries, hits, misses, evictions}. */
 CB_API cb_status cb_store_stats(cb_store* store, int64_t* out6);
+/* Second storage level (the store spans storage devices; KV written to disk and read back,
+ * P:2514-2516): entries evicted from RAM are written as one file per chunk into `dir` (which must exist and
+ * be writable) while the disk level holds at most capacity_bytes, itself evicting its least recently used
+ * files. A lookup with touch != 0 (and cb_blend_request_store) reads a disk entry back into RAM as the most
+ * recently used entry; cb_store_lookup with touch = 0 reports its n_tok with NULL pointers. capacity_bytes
+ * = 0 disables the level and deletes its files; the store deletes its files on destroy. Errors: unwritable
+ * dir -> INVALID_ARG; an unreadable file -> CB_E_CUDA (the entry is dropped). */
+CB_API cb_status cb_store_set_disk(cb_store* store, const char* dir, size_t capacity_bytes);
+/* out6 = {disk bytes used, disk capacity, disk entries, disk hits (promotions), spills, disk evictions}. */
+CB_API cb_status cb_store_disk_stats(cb_store* store, int64_t* out6);
 /* The first n keys in recency order (most recent first); n_out = number of entries. */
 CB_API cb_status cb_store_keys(cb_store* store, cb_chunk_key* keys, int32_t n, int32_t* n_out);
 /* cb_blend_request with chunk c's KV fetched from the store under chunk_keys[c] (host cb_chunk_key[n_chunks]):

@@ -63,6 +63,8 @@ _SIGS = {
     "cb_store_put": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32]),
     "cb_store_lookup": (c_i32, [c_vp, c_vp, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_vp), ctypes.POINTER(c_vp)]),
     "cb_store_stats": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
+    "cb_store_set_disk": (c_i32, [c_vp, ctypes.c_char_p, ctypes.c_size_t]),
+    "cb_store_disk_stats": (c_i32, [c_vp, ctypes.POINTER(c_i64)]),
     "cb_store_keys": (c_i32, [c_vp, c_vp, c_i32, ctypes.POINTER(c_i32)]),
     "cb_blend_request_store": (c_i32, [c_vp, c_vp, c_vp, ctypes.POINTER(CbLayerW), c_vp, c_vp, c_vp,
                                        c_i32, c_i32, c_i32p, c_i32, c_vp, c_vp, c_i32p, c_vp, c_vp, c_vp]),

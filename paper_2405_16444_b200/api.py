@@ -304,6 +304,32 @@ class Store:
         check(lib().cb_store_stats(self.handle, o))
         return dict(zip(("used", "capacity", "entries", "hits", "misses", "evictions"), list(o)))
 
+    def set_disk(self, directory: str, capacity_bytes: int):
+        """A disk level under `directory` (cb_store_set_disk): RAM evictions spill there; lookups read back."""
+        check(lib().cb_store_set_disk(self.handle, str(directory).encode(), int(capacity_bytes)))
+
+    def disk_stats(self) -> Dict[str, int]:
+        o = (ctypes.c_int64 * 6)()
+        check(lib().cb_store_disk_stats(self.handle, o))
+        return dict(zip(("used", "capacity", "entries", "hits", "spills", "evictions"), list(o)))
+
+    def get(self, key: bytes, shape, dtype) -> Optional[tuple]:
+        """(k, v) host copies of the entry (promoted from disk if there), or None on a miss. shape: [L][n_tok][n_kv][hd]
+        with n_tok (or any dimension) given as -1 = the entry's token count."""
+        n = ctypes.c_int32(0)
+        kp, vp = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib().cb_store_lookup(self.handle, _key(key), 1, ctypes.byref(n), ctypes.byref(kp), ctypes.byref(vp)))
+        if n.value < 0:
+            return None
+        shape = tuple(n.value if d == -1 else d for d in shape)  # -1: the entry's token count
+        count = int(np.prod(shape))
+        nbytes = count * torch.empty(0, dtype=dtype).element_size()
+        out = []
+        for ptr in (kp.value, vp.value):
+            buf = (ctypes.c_char * nbytes).from_address(ptr)
+            out.append(torch.frombuffer(bytearray(buf), dtype=dtype).reshape(shape))
+        return tuple(out)
+
     def keys(self) -> List[bytes]:
         n = ctypes.c_int32(0)
         check(lib().cb_store_keys(self.handle, None, 0, ctypes.byref(n)))

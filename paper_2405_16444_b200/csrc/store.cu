@@ -7,8 +7,10 @@
 // P:2723). Entries live in pinned host memory so the per-layer fetch is an asynchronous DMA on the
 // context's copy stream. An entry is [L][n_tok][n_kv][head_dim] K then V in the model dtype (chunk-local
 // RoPE, as cb_blend_forward's k_in). Host-only bookkeeping: no method arithmetic lives here.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <list>
 #include <mutex>
 #include <string>
@@ -30,6 +32,17 @@ struct Entry {
 };
 }  // namespace
 
+namespace {
+// Second storage level (the store spans storage devices, LRU-evicting when they are full; the
+// paper writes KV to disk and reads it back with torch.load): one file per chunk in a directory.
+struct DiskEntry {
+  std::string key;
+  int32_t n_tok;
+  int64_t bytes;  // of K (and of V)
+  std::string path;
+};
+}  // namespace
+
 struct cb_store {
   size_t capacity;
   size_t used = 0;
@@ -38,6 +51,12 @@ struct cb_store {
   std::list<Entry> lru;  // front = most recently used
   std::unordered_map<std::string, std::list<Entry>::iterator> index;  // full digest -> entry
   long long hits = 0, misses = 0, evictions = 0;
+  // disk level (cb_store_set_disk): entries evicted from RAM are written here; a lookup promotes them back
+  std::string disk_dir;
+  size_t disk_capacity = 0, disk_used = 0;
+  std::list<DiskEntry> dlru;
+  std::unordered_map<std::string, std::list<DiskEntry>::iterator> dindex;
+  long long disk_hits = 0, spills = 0, disk_evictions = 0;
 };
 
 namespace {
@@ -58,6 +77,110 @@ void* host_alloc(cb_store* st, size_t n) {
   if (!st->pinned) return malloc(n);
   void* p = nullptr;
   return cudaHostAlloc(&p, n, cudaHostAllocDefault) == cudaSuccess ? p : nullptr;
+}
+
+// ---- disk level ---------------------------------------------------------------------------------------
+// File: "CBKV" | u32 version 1 | i32 n_tok | i64 bytes | 32-byte key | K bytes | V bytes.
+constexpr char kMagic[4] = {'C', 'B', 'K', 'V'};
+
+std::string hex_of(const std::string& key) {
+  static const char* d = "0123456789abcdef";
+  std::string h;
+  for (unsigned char ch : key) { h += d[ch >> 4]; h += d[ch & 15]; }
+  return h;
+}
+
+void disk_drop(cb_store* st, std::list<DiskEntry>::iterator it) {
+  std::remove(it->path.c_str());
+  st->disk_used -= 2 * (size_t)it->bytes;
+  st->dindex.erase(it->key);
+  st->dlru.erase(it);
+}
+
+// Write a RAM entry (about to leave RAM) to the disk level, evicting the disk's least recently used files
+// until it fits. Entries larger than the disk level are dropped (the store then misses them, as a RAM-only
+// store would). Called with the store locked, after the entry's in-flight fetches completed.
+void spill(cb_store* st, const Entry& e) {
+  if (st->disk_capacity == 0 || 2 * (size_t)e.bytes > st->disk_capacity) return;
+  auto old = st->dindex.find(e.key);
+  if (old != st->dindex.end()) disk_drop(st, old->second);
+  while (st->disk_used + 2 * (size_t)e.bytes > st->disk_capacity && !st->dlru.empty()) {
+    disk_drop(st, std::prev(st->dlru.end()));
+    ++st->disk_evictions;
+  }
+  const std::string path = st->disk_dir + "/" + hex_of(e.key) + ".cbkv";
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return;
+  const uint32_t ver = 1;
+  bool ok = std::fwrite(kMagic, 1, 4, f) == 4 && std::fwrite(&ver, 4, 1, f) == 1 &&
+            std::fwrite(&e.n_tok, 4, 1, f) == 1 && std::fwrite(&e.bytes, 8, 1, f) == 1 &&
+            std::fwrite(e.key.data(), 1, 32, f) == 32 && std::fwrite(e.k, 1, (size_t)e.bytes, f) == (size_t)e.bytes &&
+            std::fwrite(e.v, 1, (size_t)e.bytes, f) == (size_t)e.bytes;
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) {
+    std::remove(path.c_str());
+    return;
+  }
+  st->dlru.push_front(DiskEntry{e.key, e.n_tok, e.bytes, path});
+  st->dindex[e.key] = st->dlru.begin();
+  st->disk_used += 2 * (size_t)e.bytes;
+  ++st->spills;
+}
+
+// Evict RAM entries (LRU first, each spilled to disk) until `need` more bytes fit. `keep` entries (already
+// at the front of the order) are never evicted; false if they alone do not leave room.
+bool make_room(cb_store* st, size_t need, size_t keep = 0) {
+  while (st->used + need > st->capacity && st->lru.size() > keep) {
+    Entry& victim = st->lru.back();
+    if (victim.used) cudaEventSynchronize(victim.last_use);  // no fetch may still read it
+    spill(st, victim);
+    st->index.erase(victim.key);
+    free_entry(st, victim);
+    st->lru.pop_back();
+    ++st->evictions;
+  }
+  return st->used + need <= st->capacity;
+}
+
+// Read a disk entry back into RAM as the most recently used entry (the disk copy is removed).
+cb_status promote(cb_store* st, std::list<DiskEntry>::iterator dit, size_t keep, std::list<Entry>::iterator* out) {
+  // untrack the disk copy first (its file stays until read): the spills that make room in RAM must not evict it
+  const DiskEntry de = *dit;
+  st->disk_used -= 2 * (size_t)de.bytes;
+  st->dindex.erase(de.key);
+  st->dlru.erase(dit);
+  if (!make_room(st, 2 * (size_t)de.bytes, keep)) {
+    std::remove(de.path.c_str());
+    cb_set_error("KV store: RAM capacity %zu cannot hold the request's chunks", st->capacity);
+    return CB_E_SHAPE;
+  }
+  Entry e{de.key, host_alloc(st, (size_t)de.bytes), host_alloc(st, (size_t)de.bytes), de.bytes, de.n_tok, nullptr, false};
+  FILE* f = std::fopen(de.path.c_str(), "rb");
+  char magic[4];
+  uint32_t ver = 0;
+  int32_t n_tok = 0;
+  int64_t bytes = 0;
+  char key[32];
+  bool ok = f && e.k && e.v && std::fread(magic, 1, 4, f) == 4 && std::memcmp(magic, kMagic, 4) == 0 &&
+            std::fread(&ver, 4, 1, f) == 1 && ver == 1 && std::fread(&n_tok, 4, 1, f) == 1 && n_tok == de.n_tok &&
+            std::fread(&bytes, 8, 1, f) == 1 && bytes == de.bytes && std::fread(key, 1, 32, f) == 32 &&
+            std::memcmp(key, de.key.data(), 32) == 0 && std::fread(e.k, 1, (size_t)bytes, f) == (size_t)bytes &&
+            std::fread(e.v, 1, (size_t)bytes, f) == (size_t)bytes;
+  if (f) std::fclose(f);
+  if (ok && st->pinned) ok = cudaEventCreateWithFlags(&e.last_use, cudaEventDisableTiming) == cudaSuccess;
+  std::remove(de.path.c_str());
+  if (!ok) {
+    st->used += 2 * (size_t)e.bytes;
+    free_entry(st, e);
+    cb_set_error("KV store: disk entry %s unreadable", de.path.c_str());
+    return CB_E_CUDA;
+  }
+  st->used += 2 * (size_t)e.bytes;
+  st->lru.push_front(e);
+  st->index[e.key] = st->lru.begin();
+  ++st->disk_hits;
+  *out = st->lru.begin();
+  return CB_OK;
 }
 }  // namespace
 
@@ -150,7 +273,37 @@ extern "C" cb_status cb_store_create(size_t capacity_bytes, int32_t pinned, cb_s
 extern "C" cb_status cb_store_destroy(cb_store* s) {
   if (!s) return CB_OK;
   for (auto& e : s->lru) free_entry(s, e);
+  for (auto& d : s->dlru) std::remove(d.path.c_str());  // the store owns its files
   delete s;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_store_set_disk(cb_store* s, const char* dir, size_t capacity_bytes) {
+  CB_REQUIRE(s != nullptr, CB_E_INVALID_ARG, "store is NULL");
+  std::lock_guard<std::mutex> lk(s->mu);
+  while (!s->dlru.empty()) disk_drop(s, std::prev(s->dlru.end()));
+  s->disk_capacity = 0;
+  if (capacity_bytes == 0) return CB_OK;
+  CB_REQUIRE(dir != nullptr && dir[0] != 0, CB_E_INVALID_ARG, "cb_store_set_disk: dir is empty");
+  const std::string probe = std::string(dir) + "/.cbkv_probe";
+  FILE* f = std::fopen(probe.c_str(), "wb");
+  CB_REQUIRE(f != nullptr, CB_E_INVALID_ARG, "cb_store_set_disk: cannot write to %s", dir);
+  std::fclose(f);
+  std::remove(probe.c_str());
+  s->disk_dir = dir;
+  s->disk_capacity = capacity_bytes;
+  return CB_OK;
+}
+
+extern "C" cb_status cb_store_disk_stats(cb_store* s, int64_t* out6) {
+  CB_REQUIRE(s && out6, CB_E_INVALID_ARG, "cb_store_disk_stats: bad arguments");
+  std::lock_guard<std::mutex> lk(s->mu);
+  out6[0] = (int64_t)s->disk_used;
+  out6[1] = (int64_t)s->disk_capacity;
+  out6[2] = (int64_t)s->dlru.size();
+  out6[3] = s->disk_hits;
+  out6[4] = s->spills;
+  out6[5] = s->disk_evictions;
   return CB_OK;
 }
 
@@ -167,13 +320,9 @@ extern "C" cb_status cb_store_put(cb_store* s, const cb_chunk_key* key_d, const 
     s->lru.erase(it->second);
     s->index.erase(it);
   }
-  while (s->used + 2 * (size_t)bytes > s->capacity && !s->lru.empty()) {  // evict least recently used
-    Entry& victim = s->lru.back();
-    s->index.erase(victim.key);
-    free_entry(s, victim);
-    s->lru.pop_back();
-    ++s->evictions;
-  }
+  auto dit = s->dindex.find(key);
+  if (dit != s->dindex.end()) disk_drop(s, dit->second);
+  make_room(s, 2 * (size_t)bytes);  // evict least recently used, spilled to the disk level if any
   Entry e{key, host_alloc(s, (size_t)bytes), host_alloc(s, (size_t)bytes), bytes, n_tok, nullptr, false};
   if (!e.k || !e.v) {
     if (s->pinned) { if (e.k) cudaFreeHost(e.k); if (e.v) cudaFreeHost(e.v); }
@@ -209,6 +358,22 @@ extern "C" cb_status cb_store_lookup(cb_store* s, const cb_chunk_key* key, int32
   std::lock_guard<std::mutex> lk(s->mu);
   auto it = s->index.find(key_str(key));
   if (it == s->index.end()) {
+    auto dit = s->dindex.find(key_str(key));
+    if (dit != s->dindex.end()) {  // on the disk level: promoted to RAM by a touching lookup
+      if (!touch) {
+        *n_tok_out = dit->second->n_tok;
+        if (k_out) *k_out = nullptr;
+        if (v_out) *v_out = nullptr;
+        return CB_OK;
+      }
+      std::list<Entry>::iterator e;
+      CB_TRY(promote(s, dit->second, 0, &e));
+      ++s->hits;
+      *n_tok_out = e->n_tok;
+      if (k_out) *k_out = e->k;
+      if (v_out) *v_out = e->v;
+      return CB_OK;
+    }
     if (touch) ++s->misses;
     *n_tok_out = -1;
     if (k_out) *k_out = nullptr;
@@ -270,20 +435,39 @@ extern "C" cb_status cb_blend_request_store(cb_ctx* c, cb_store* store, const cb
   std::lock_guard<std::mutex> lk(store->mu);
   std::vector<const Entry*> ent(n_chunks > 0 && N > 0 ? n_chunks : 0);
   {
+    // every chunk present (RAM or disk) before anything moves: a miss is an error (the caller prefills it)
     for (size_t ci = 0; ci < ent.size(); ++ci) {
-      const int n_c = chunk_start[ci + 1] - chunk_start[ci];
-      auto it = store->index.find(key_str(&chunk_keys[ci]));
-      if (it == store->index.end()) {
+      const std::string k = key_str(&chunk_keys[ci]);
+      if (store->index.find(k) == store->index.end() && store->dindex.find(k) == store->dindex.end()) {
         ++store->misses;
         const uint8_t* kb = chunk_keys[ci].bytes;
         cb_set_error("chunk %zu (key %02x%02x%02x%02x...) is not in the KV store", ci, kb[0], kb[1], kb[2], kb[3]);
         return CB_E_MISS;
       }
+    }
+    // the RAM-resident chunks first move to the front, then the disk-resident ones are read back behind them;
+    // evictions for the promotions take the least recently used entries, never this request's (keep)
+    size_t keep = 0;
+    for (size_t ci = 0; ci < ent.size(); ++ci) {
+      auto it = store->index.find(key_str(&chunk_keys[ci]));
+      if (it == store->index.end()) continue;
+      store->lru.splice(store->lru.begin(), store->lru, it->second);
+      ++keep;
+    }
+    for (size_t ci = 0; ci < ent.size(); ++ci) {
+      const std::string k = key_str(&chunk_keys[ci]);
+      auto it = store->index.find(k);
+      if (it == store->index.end()) {
+        std::list<Entry>::iterator e;
+        CB_TRY(promote(store, store->dindex.find(k)->second, keep, &e));
+        ++keep;
+        it = store->index.find(k);
+      }
+      const int n_c = chunk_start[ci + 1] - chunk_start[ci];
       CB_REQUIRE(it->second->n_tok == n_c && it->second->bytes == (int64_t)((size_t)L * n_c * row), CB_E_SHAPE,
                  "chunk %zu: stored entry has %d tokens / %lld bytes, request needs %d / %zu", ci, it->second->n_tok,
                  (long long)it->second->bytes, n_c, (size_t)L * n_c * row);
       ++store->hits;
-      store->lru.splice(store->lru.begin(), store->lru, it->second);
       ent[ci] = &*it->second;
     }
   }

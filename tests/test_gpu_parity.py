@@ -641,6 +641,44 @@ def test_blend_request_store_equals_forward(P, name, dtype, n_suf):
     assert st["misses"] == 1 and st["hits"] >= len(keys)
 
 
+def test_blend_request_store_from_disk_equals_forward(P, tmp_path):
+    """The store's RAM level holds only one chunk (plus filler entries); the other chunks of the request were
+    spilled to the disk level and are read back (promoted) by cb_blend_request_store before the layer-pipelined
+    fetch: exactly cb_blend_forward's result; the request's chunks end up in RAM, the fillers on disk."""
+    name, dtype, n_suf = "small", "bf16", 5
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case(name, 9, [40, 57, 31], n_suf, dtype, 0.2)
+    a = run_blend(P, s, dtype, 9, req, tok, pos, cs, Kc, Vc, ks)
+    td = P.api.TORCH_DTYPES[dtype]
+    per_tok = 2 * s.n_layers * s.kvd * 2  # K + V bytes of one token
+    store = P.api.Store(per_tok * (128 + 60), pinned=True)  # RAM: all three chunks only after evicting fillers
+    store.set_disk(str(tmp_path), 1 << 30)
+    mid = P.api.model_identity(s, dtype, "synth seed 9")
+    keys = []
+    for c in range(len(cs) - 1):
+        sl = slice(int(cs[c]), int(cs[c + 1]))
+        keys.append(P.api.chunk_digest(mid, tok[sl]))
+        store.put(keys[-1], torch.from_numpy(np.ascontiguousarray(Kc[:, sl])).to(td).contiguous(),
+                  torch.from_numpy(np.ascontiguousarray(Vc[:, sl])).to(td).contiguous())
+    filler = torch.zeros(s.n_layers, 50, s.n_kv_heads, s.head_dim, dtype=td)
+    for j in range(3):  # push the chunks out of RAM
+        store.put(P.api.chunk_digest(b"filler", [j]), filler, filler)
+    on_disk = sum(store.lookup(k, touch=False) > 0 and k not in store.keys() for k in keys)
+    assert on_disk >= 2, store.keys()
+    T = req.n_total
+    kb = torch.empty(s.n_layers, T, s.n_kv_heads, s.head_dim, dtype=td, device=DEV)
+    vb = torch.empty_like(kb)
+    hh = torch.empty(ks[-1] + n_suf, s.d_model, dtype=torch.float32).pin_memory()
+    P.api.blend_request_store(a["ctx"], store, keys, a["mw"], torch.from_numpy(tok.astype(np.int32)).pin_memory(),
+                              torch.from_numpy(pos.astype(np.int32)).pin_memory(), list(cs), n_suf, kb, vb, ks, hh)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(np32(kb), a["K"])
+    np.testing.assert_array_equal(np32(vb), a["V"])
+    np.testing.assert_array_equal(hh.numpy(), a["h"])
+    assert set(keys) <= set(store.keys())
+    d = store.disk_stats()
+    assert d["hits"] >= on_disk and d["spills"] >= on_disk
+
+
 # ---- half-split RoPE checkpoints through the loader conversion (SURVEY §8(c) R9, §8(f) N3) -------------------
 def test_blend_half_split_rope_checkpoint(P, monkeypatch):
     """A model and chunk caches in the half-split RoPE convention (the oracle rotates (i, i + hd/2) pairs

@@ -100,3 +100,84 @@ def test_put_errors(api):
     with pytest.raises(api.CacheBlendError):
         st.put(_k(1), torch.zeros(1, 20, 1, 1), torch.zeros(1, 20, 1, 1))  # 160 B > 100 B
     assert st.lookup(_k(1), touch=False) == -1
+
+
+def test_two_level_lru_matches_model(api, tmp_path):
+    """RAM + disk levels (the store spans storage devices, LRU-evicting when full): RAM
+    evictions spill to disk files (the disk level evicting its own least recently used files), a touching
+    lookup reads a disk entry back into RAM; checked step by step against a two-OrderedDict model, with every
+    entry's bytes verified after it comes back from disk."""
+    rng = np.random.default_rng(2)
+    cap_r, cap_d = 12_000, 30_000
+    st = api.Store(cap_r, pinned=False)
+    st.set_disk(str(tmp_path), cap_d)
+    ram, disk = collections.OrderedDict(), collections.OrderedDict()  # key -> entry bytes (K + V); LRU first
+    content = {}
+    c = dict(hits=0, misses=0, evictions=0, dhits=0, spills=0, devict=0)
+
+    def spill(key, nb):
+        if nb > cap_d:
+            return
+        while disk and sum(disk.values()) + nb > cap_d:
+            disk.popitem(last=False)
+            c["devict"] += 1
+        disk[key] = nb
+        c["spills"] += 1
+
+    def make_room(nb):
+        while ram and sum(ram.values()) + nb > cap_r:
+            key, vb = ram.popitem(last=False)
+            spill(key, vb)
+            c["evictions"] += 1
+
+    for step in range(2500):
+        key = int(rng.integers(0, 30))
+        if rng.random() < 0.45:
+            n = int(rng.integers(1, 1000))
+            k = torch.arange(n, dtype=torch.float32) + step
+            st.put(_k(key), k.view(1, n, 1, 1), (-k).view(1, n, 1, 1))
+            ram.pop(key, None)
+            disk.pop(key, None)
+            make_room(8 * n)
+            ram[key] = 8 * n
+            content[key] = k
+        else:
+            got = st.get(_k(key), (1, -1, 1, 1), torch.float32) if key in content else None
+            if key in ram:
+                c["hits"] += 1
+                ram.move_to_end(key)
+            elif key in disk:
+                nb = disk.pop(key)
+                make_room(nb)
+                ram[key] = nb
+                c["hits"] += 1
+                c["dhits"] += 1
+            else:
+                if key in content:
+                    assert got is None
+                else:
+                    assert st.lookup(_k(key)) == -1
+                c["misses"] += 1
+                continue
+            kk, vv = got
+            assert torch.equal(kk.flatten(), content[key]) and torch.equal(vv.flatten(), -content[key])
+        assert st.keys() == [_k(x) for x in reversed(ram.keys())]
+    s, d = st.stats(), st.disk_stats()
+    assert s["used"] == sum(ram.values()) and d["used"] == sum(disk.values()) <= cap_d
+    assert (s["hits"], s["misses"], s["evictions"]) == (c["hits"], c["misses"], c["evictions"])
+    assert (d["entries"], d["hits"], d["spills"], d["evictions"]) == (len(disk), c["dhits"], c["spills"], c["devict"])
+    assert len(list(tmp_path.glob("*.cbkv"))) == len(disk)
+    st.close()
+    assert not list(tmp_path.glob("*.cbkv"))  # the store deletes its files
+
+
+def test_disk_level_errors(api, tmp_path):
+    st = api.Store(1000, pinned=False)
+    with pytest.raises(api.CacheBlendError):
+        st.set_disk(str(tmp_path / "missing"), 10_000)
+    st.set_disk(str(tmp_path), 10_000)
+    st.put(_k(1), torch.ones(1, 100, 1, 1), torch.ones(1, 100, 1, 1))  # 800 B
+    st.put(_k(2), torch.ones(1, 100, 1, 1), torch.ones(1, 100, 1, 1))  # evicts 1 to disk
+    assert st.lookup(_k(1), touch=False) == 100 and st.disk_stats()["entries"] == 1
+    st.set_disk(str(tmp_path), 0)  # disabling drops the level and its files
+    assert st.lookup(_k(1), touch=False) == -1 and not list(tmp_path.glob("*.cbkv"))
