@@ -72,16 +72,20 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
  *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
  *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue
- *                 kind k (0 store, 1 store_f32, 2 qkv, 3 residual, 4 swiglu)
+ *                 kind k (0 store, 1 store_f32, 2 qkv, 3 residual, 4 swiglu); 300 = per-k-block producer /
+ *                 MMA clock64 timeline of CTA pair 0 of the pair GEMM (tools/gemm_stages.py)
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
  *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
  *   "topk_threads" 0 = 1024 (default), 256 or 512 threads in the top-k block
  *   "gemm_pf"     1 = pair GEMMs load the weight (B) halves of their first pipeline stages before the PDL
- *                 wait, the A halves after it (experiment, measured neutral), 0 = off (default) */
+ *                 wait, the A halves after it (experiment, measured neutral), 0 = off (default)
+ *   "gemm_mc"     A-multicast 4-CTA clusters (two CTA pairs sharing their A rows) in the pair GEMM:
+ *                 2 = where the planner expects a shorter k-loop (default), 1 = always (whole tiles), 0 = off */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Read-only facts about the context: "num_sms", "gemm_max_pairs" (co-resident 2-CTA clusters of the
- * CTA-pair GEMM, from cudaOccupancyMaxActiveClusters). Unknown names -> INVALID_ARG. */
+ * CTA-pair GEMM, from cudaOccupancyMaxActiveClusters), "gemm_max_clusters4" (co-resident 4-CTA clusters of
+ * it, for gemm_mc). Unknown names -> INVALID_ARG. */
 CB_API cb_status cb_get_info(cb_ctx* ctx, const char* name, int64_t* value);
 
 /* Number of kernel launches the context issued since creation (for bench's gpu_launches). */

@@ -294,6 +294,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   c->topk_sort = 0;  // bitonic path measured slower in the blend (13.5 vs 10.5 us per launch, profiles/r02)
   c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
   c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
+  c->gemm_mc = 2;    // auto: A-multicast clusters where the planner expects a shorter k-loop
   c->gemm_pf = 0;    // measured neutral-to-slower (9.60 vs 9.54 ms/step, paired runs), DESIGN.md §6.1
   c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
   if (st != CB_OK) {
@@ -359,6 +360,7 @@ extern "C" cb_status cb_get_info(cb_ctx* c, const char* name, int64_t* value) {
   CB_REQUIRE(c && name && value, CB_E_INVALID_ARG, "cb_get_info: NULL argument");
   if (std::strcmp(name, "num_sms") == 0) { *value = c->num_sms; return CB_OK; }
   if (std::strcmp(name, "gemm_max_pairs") == 0) { *value = gemm_tc_max_pairs(c); return CB_OK; }
+  if (std::strcmp(name, "gemm_max_clusters4") == 0) { *value = c->max_clusters4; return CB_OK; }
   cb_set_error("unknown info '%s'", name);
   return CB_E_INVALID_ARG;
 }
@@ -461,6 +463,11 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     CB_REQUIRE(value == 0 || value == 256 || value == 512 || value == 1024, CB_E_INVALID_ARG,
                "topk_threads must be 0, 256, 512 or 1024");
     c->topk_threads = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "gemm_mc") == 0) {
+    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_mc must be 0, 1 or 2");
+    c->gemm_mc = (int)value;
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_pf") == 0) {

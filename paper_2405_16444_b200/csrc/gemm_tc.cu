@@ -350,7 +350,7 @@ struct TmKeyHash {
 // Pair plans may also cut each remainder tile (tiles % pairs, when it is a small last round) into
 // tail_p K pieces that fill that round; the last piece of a tile to finish merges (gemm_tc2.cu).
 struct Plan {
-  int bn, sk_ctas, grid, pair, ksplit, tail_r = 0, tail_p = 1;
+  int bn, sk_ctas, grid, pair, ksplit, tail_r = 0, tail_p = 1, mc = 0;
   double cost = 0.0;  // model cycles per SM
 };
 constexpr int MAX_TAIL_P = 4;  // gemm_tc2.cu merges at most 4 pieces
@@ -360,7 +360,8 @@ constexpr int MAX_KSPLIT = 4;
 constexpr double KSPLIT_EPI_CYC = 3000.0;  // one more serialised fp32 read-modify-write epilogue
 
 Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid, int K, int force_sched, int force_bn, int force_pair,
-               int force_ksplit, int force_tail, bool no192, int pairs_cap, bool balance, bool no224) {
+               int force_ksplit, int force_tail, bool no192, int pairs_cap, bool balance, bool no224, int mc_mode = 0,
+               int max_cl4 = 0) {
   if (pairs_cap > 0 && pairs_cap < max_pairs) max_pairs = pairs_cap;
   const int num_kb = (K + BK - 1) / BK;
   Plan best{256, 0, 1, 0, 1};
@@ -403,6 +404,24 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
           const double cost =
               (double)((tiles * ks + grid - 1) / grid) * ((num_kb + ks - 1) / ks) * cyc + (ks - 1) * KSPLIT_EPI_CYC;
           if (cost < best_cost) { best_cost = cost; best = Plan{bn, 0, pair ? 2 * grid : grid, pair, ks}; }
+          // A-multicast clusters of two pairs (gemm_mc): the pairs of a row tile share A, halving its L2 reads.
+          // The single-wave small-M GEMMs are bound by chip-wide L2 reads (A is re-read by every column tile;
+          // tools/gemm_stages.py: ~500 cycles per k-block whatever the tile width), so their k-loop shortens;
+          // tiles of 224/256 columns are MMA-bound and gain nothing (tools/gemm_micro.py --mcs 0,1). Only
+          // max_cl4 (33 on B200) 4-CTA clusters are co-resident, fewer than 74 / 2, so it pays when the
+          // clusters' rounds are no more than the pairs' rounds. Not for the SwiGLU GEMM: its many-round
+          // 224/192-wide tiles run at the power-capped tensor peak and were slower in clusters (125 -> 134 us).
+          if (pair && ks == 1 && mc_mode && max_cl4 > 0 && ((bn <= 192 && !sw) || mc_mode == 1)) {
+            const int n_t = (int)(tiles / m_tiles);
+            const long long units = (long long)m_tiles * ((n_t + 1) / 2);
+            const long long rounds = (units + max_cl4 - 1) / max_cl4;
+            const double c_mc = (double)rounds * num_kb * cyc * (bn <= 192 ? 0.8 : 1.0);
+            if (c_mc < best_cost || mc_mode == 1) {
+              best_cost = c_mc;
+              best = Plan{bn, 0, 2 * (int)(2 * ((units + rounds - 1) / rounds)), 1, 1};
+              best.mc = 1;
+            }
+          }
           if (pair && ks == 1 && force_tail != 1) {  // remainder tiles cut into K pieces
             const long long rounds = tiles / units, rem = tiles % units;
             if (rounds >= 1 && rem > 0) {
@@ -460,8 +479,8 @@ struct TmapCache {
 
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
                           int bn, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p, float* tscr,
-                          int* tcnt, cudaStream_t s);
-cb_status gemm_tc2_init(int num_sms, int* max_pairs);
+                          int* tcnt, int mc, cudaStream_t s);
+cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4);
 constexpr int KFLAGS = 4096;  // >= 8 per tile for every tile of a split-K launch (tiles * ksplit <= 74 pairs)
 
 cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
@@ -538,10 +557,11 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
   const Plan pl = plan_gemm(c->num_sms, c->tmaps->max_pairs, M, e.N, e.kind == EPI_SWIGLU, e.kind == EPI_RESID, K, sched,
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit,
                             c->tmaps->force_tail, c->tmaps->no192, c->tmaps->pairs_cap[e.kind],
-                            c->tmaps->balance, c->tmaps->no224);
+                            c->tmaps->balance, c->tmaps->no224, e.push_base[0] != nullptr ? 0 : c->gemm_mc,
+                            c->max_clusters4);
   if (pl.pair)
     return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, pl.tail_r,
-                           pl.tail_p, c->tmaps->tscr, c->tmaps->tcnt, s);
+                           pl.tail_p, c->tmaps->tscr, c->tmaps->tcnt, pl.mc, s);
   ProfScope ps_(c, PROF_GEMM, s);
   if (pl.bn == 256) return launch_bn<256>(c, A, lda, B, ldb, M, K, e, pl, s);
   return launch_bn<128>(c, A, lda, B, ldb, M, K, e, pl, s);
@@ -579,7 +599,7 @@ cb_status gemm_tc_init(cb_ctx* c) {
   CB_TRY(set_attrs<256>());
   CB_TRY(set_attrs<128>());
   c->tmaps = new TmapCache();
-  CB_TRY(gemm_tc2_init(c->num_sms, &c->tmaps->max_pairs));
+  CB_TRY(gemm_tc2_init(c->num_sms, &c->tmaps->max_pairs, &c->max_clusters4));
   CB_CUDA(cudaMalloc(&c->tmaps->part, (size_t)c->num_sms * BM * SLOT_COLS * sizeof(float)));
   CB_CUDA(cudaMalloc(&c->tmaps->flags, (size_t)c->num_sms * sizeof(int)));
   CB_CUDA(cudaMemset(c->tmaps->flags, 0, (size_t)c->num_sms * sizeof(int)));

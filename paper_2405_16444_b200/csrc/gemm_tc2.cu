@@ -70,9 +70,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
                     int m_tiles, int n_tiles, EpiParams e, int ksplit, int* __restrict__ kflags,
                     int tail_r, int tail_p, float* __restrict__ tscr, int* __restrict__ tcnt,
-                    long long* __restrict__ dbg, const char* __restrict__ pf_b) {
+                    long long* __restrict__ dbg, const char* __restrict__ pf_b, long long* __restrict__ strace, int mc) {
   // debug_trace: globaltimer (ns) events of each CTA's first work item at dbg[blockIdx.x * 8 + event]
 #define DBG2(ev) do { if (dbg != nullptr && blockIdx.x < 256) dbg[blockIdx.x * 8 + (ev)] = tc::globaltimer(); } while (0)
+  // stage trace (debug_trace 300, pair 0 only, first 256 k-blocks): strace[rank * 256 + kb] = producer's empty
+  // wait done, strace[512 + kb] = MMA warp's full wait done (leader)
+  const bool st_on = strace != nullptr && (blockIdx.x >> 1) == 0;
   using C = Cfg2<BN>;
   constexpr bool SW = (KIND == EPI_SWIGLU);
   constexpr int OUT_N = SW ? BN / 2 : BN;
@@ -87,17 +90,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);  // tail merge: "this CTA merges" broadcast
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = tc::cluster_ctarank();
+  // mc: 4-CTA clusters of two CTA pairs on the same row tile and neighbouring column tiles (2q, 2q + 1);
+  // the pairs share their A rows, each A half-box multicast from one CTA of each pair to both (halving the
+  // L2 reads of A, which every column tile re-reads). Whole tiles only (no k-split or tail pieces).
+  const uint32_t crank = tc::cluster_ctarank();
+  const uint32_t rank = crank & 1;  // rank within the CTA pair
   const bool leader = rank == 0;
   const int num_kb = (K + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int unit = mc ? (int)(blockIdx.x >> 2) : pair;  // scheduling unit: the cluster (mc) or the pair
+  const int n_units = mc ? (int)(gridDim.x >> 2) : n_pairs;
+  const int pic = (blockIdx.x >> 1) & 1;  // pair within the cluster (mc)
   const int tiles = m_tiles * n_tiles;
-  const int items = tail_p > 1 ? tiles - tail_r + tail_r * tail_p : tiles * ksplit;  // see work_item()
+  const int items = mc ? m_tiles * ((n_tiles + 1) / 2)
+                       : tail_p > 1 ? tiles - tail_r + tail_r * tail_p : tiles * ksplit;  // see work_item()
+  const auto item = [&](int i) -> WorkItem {
+    if (!mc) return work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+    WorkItem w;
+    w.t = i % m_tiles + m_tiles * (2 * (i / m_tiles) + pic);  // may name column tile n_tiles (odd n_tiles)
+    w.sp = 0; w.kb0 = 0; w.kb1 = num_kb; w.piece = -1;
+    return w;
+  };
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < C::STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], mc ? 2 : 1); }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
     tc::fence_barrier_init();
   }
@@ -110,7 +128,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // loads of its first work item's first stages in flight, so after the wait those k-blocks only wait for A
   // (activations the previous kernel just wrote, L2-resident).
   int pre = 0;  // stages of the first work item whose B load is already in flight (uniform in warp 0)
-  if (pf_b != nullptr && warp == 0 && pair < items) {
+  if (pf_b != nullptr && !mc && warp == 0 && pair < items) {
     const WorkItem w0 = work_item(pair, tiles, num_kb, ksplit, tail_r, tail_p);
     const int nb0 = w0.t / m_tiles;
     const int b_row0 = SW ? (rank == 0 ? nb0 * OUT_N : e.ff + nb0 * OUT_N) : nb0 * BN + (int)rank * C::B_HALF;
@@ -129,24 +147,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int i = pair; i < items; i += n_pairs) {
-        const WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+      const int half = (int)(crank >> 1);  // mc: the 64-row half of the shared A box this CTA loads
+      const uint16_t amask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
+      for (int i = unit; i < items; i += n_units) {
+        const WorkItem w = item(i);
         const int t = w.t;
         const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
         const int b_row = SW ? (rank == 0 ? nb * OUT_N : e.ff + nb * OUT_N) : nb * BN + (int)rank * C::B_HALF;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
-          if (i == pair && kb - w.kb0 < pre) {  // fresh stage, B already in flight: only A
+          if (mc) {  // both pairs freed the stage (empty counts two commits), then half of A for both pairs
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            if (st_on && i == unit && kb < 256) strace[rank * 256 + kb] = clock64();
+            if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tc::tma_load_2d_2sm_mc(sa + half * (A_BYTES / 2), &tmA, &full[stage], kb * BK, m0 + half * 64, amask);
+            tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
+          } else if (i == pair && kb - w.kb0 < pre) {  // fresh stage, B already in flight: only A
             tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
           } else {
             tc::mbar_wait(&empty[stage], phase ^ 1);
+            if (st_on && i == pair && kb < 256) strace[rank * 256 + kb] = clock64();
             if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
             tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (i == pair) DBG2(1);
+        if (i == unit) DBG2(1);
       }
     }
   } else if (warp == 1) {
@@ -156,8 +183,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int i = pair; i < items; i += n_pairs, ++it) {
-        const WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+      for (int i = unit; i < items; i += n_units, ++it) {
+        const WorkItem w = item(i);
         const int acc = it & 1;
         tc::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc::fence_after();
@@ -166,14 +193,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           tc::mbar_wait(&full[stage], phase);
           tc::fence_after();
+          if (st_on && it == 0 && kb < 256 && lane == 0) strace[512 + kb] = clock64();
           if (tc::elect_one()) {
             const uint8_t* sa = smem + stage * C::STAGE_BYTES;
             const uint64_t adesc = tc::sdesc_sw128(sa), bdesc = tc::sdesc_sw128(sa + A_BYTES);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               tc::mma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
-            tc::mma_commit_2sm(&empty[stage]);
-            if (kb == kb1 - 1) tc::mma_commit_2sm(&tfull[acc]);
+            if (mc) {  // the stage is free for both pairs' producers once both pairs' MMAs read it
+              tc::mma_commit_2sm_mask(&empty[stage], 0xF);
+              if (kb == kb1 - 1) tc::mma_commit_2sm_mask(&tfull[acc], (uint16_t)(3u << (crank & 2u)));
+            } else {
+              tc::mma_commit_2sm(&empty[stage]);
+              if (kb == kb1 - 1) tc::mma_commit_2sm(&tfull[acc]);
+            }
           }
           __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -186,19 +219,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     int it = 0;
-    for (int i = pair; i < items; i += n_pairs, ++it) {
-      const WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+    for (int i = unit; i < items; i += n_units, ++it) {
+      const WorkItem w = item(i);
       const int t = w.t, sp = w.sp;
       const int acc = it & 1;
       const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
+      const bool col_ok = nb < n_tiles;  // mc with odd n_tiles: the last cluster's second pair has no tile
       // split-K chain (RESID only): split sp adds onto h_out after split sp - 1 of the same 32 rows
       // published it — a fixed order, so the sum is deterministic. flag = number of splits done.
       int* flag = kflags + ((size_t)t * 2 + rank) * 4 + q;
-      if constexpr (KIND == EPI_QKV) gepi::qkv_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
+      if constexpr (KIND == EPI_QKV) gepi::qkv_prefetch(e, m0 + row, col_ok && m0 + row < M, nb * OUT_N, OUT_N);
       // fused RMSNorm consumer: the row factor is ready before the accumulator (1 if off)
       [[maybe_unused]] const float rs = gepi::row_rs(e, m0 + row, m0 + row < M);
       if constexpr (KIND == EPI_RESID) {
-        if (sp == 0) gepi::resid_prefetch(e, m0 + row, m0 + row < M, nb * OUT_N, OUT_N);
+        if (sp == 0) gepi::resid_prefetch(e, m0 + row, col_ok && m0 + row < M, nb * OUT_N, OUT_N);
       }
       tc::mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc::fence_after();
@@ -220,7 +254,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m = m0 + row;
       const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::ACC_STRIDE;
       float dacc = 0.f;
-      bool skip_epilogue = false;
+      bool skip_epilogue = !col_ok;
       if (w.piece >= 0) {
         // tail piece: publish this K piece's fp32 partial (this CTA's 128 rows x BN); the last piece of
         // the tile to arrive sums all pieces in piece order into its TMEM accumulator, then runs the
@@ -334,19 +368,19 @@ cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long 
 template <int KIND, int BN>
 static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K,
                               const EpiParams& e, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p,
-                              float* tscr, int* tcnt, cudaStream_t s) {
+                              float* tscr, int* tcnt, int mc, cudaStream_t s) {
   using C = Cfg2<BN>;
   constexpr bool sw = KIND == EPI_SWIGLU;
   constexpr int out_n = sw ? BN / 2 : BN;
   const long long b_rows = sw ? 2LL * e.ff : (long long)e.N;
   CUtensorMap ta, tb;
-  CB_TRY(gemm_tmap(c, A, M, K, lda, 128, &ta));
+  CB_TRY(gemm_tmap(c, A, M, K, lda, mc ? 64 : 128, &ta));  // mc: each CTA loads (and multicasts) half of A
   CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, C::B_HALF, &tb));
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
-  CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, 2, ta, tb, M, K,
-                    m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
+  CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, mc ? 4 : 2, ta, tb,
+                    M, K, m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
                     (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr,
-                    c->gemm_pf ? (const char*)B : nullptr));
+                    c->gemm_pf && !mc ? (const char*)B : nullptr, c->dbg_sel == 300 ? c->dbg_buf : nullptr, mc));
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -354,26 +388,28 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
 // Pair tiles of 256 x BN; n_pairs CTA pairs (grid = 2 * n_pairs).
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
                           int bn, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p, float* tscr,
-                          int* tcnt, cudaStream_t s) {
+                          int* tcnt, int mc, cudaStream_t s) {
   ProfScope ps_(c, PROF_GEMM, s);
   // k-split chains continue from the running sum in local h_out; a peer-memory push (fused reduce-scatter)
   // sends each piece's rows to their owner instead, so pushed GEMMs always run whole tiles
   if (e.kind != EPI_RESID || e.push_base[0] != nullptr) ksplit = 1;
   if (ksplit > 1) tail_p = 1;
+  // mc (plan_gemm): A-multicast clusters of two pairs, whole tiles only; n_pairs = 2 x the cluster count
+  if (ksplit > 1 || tail_p > 1 || e.push_base[0] != nullptr) mc = 0;
   if (bn == 224) {  // SwiGLU only: 112 gate + 112 up columns (14336 = 128 x 112 features, Mistral d_ff)
     CB_REQUIRE(e.kind == EPI_SWIGLU, CB_E_INVALID_ARG, "224-wide pair tiles are for the SwiGLU GEMM only");
     return launch2_kind<EPI_SWIGLU, 224>(c, A, lda, B, ldb, M, K, e, n_pairs, 1, kflags, tail_r, tail_p, tscr, tcnt,
-                                         s);
+                                         mc, s);
   }
 #define L2_(KIND_)                                                                                      \
   return bn == 256                                                                                      \
              ? launch2_kind<KIND_, 256>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
-                                        tcnt, s)                                                             \
+                                        tcnt, mc, s)                                                             \
          : bn == 192                                                                                         \
              ? launch2_kind<KIND_, 192>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
-                                        tcnt, s)                                                             \
+                                        tcnt, mc, s)                                                             \
              : launch2_kind<KIND_, 128>(c, A, lda, B, ldb, M, K, e, n_pairs, ksplit, kflags, tail_r, tail_p, tscr, \
-                                        tcnt, s)
+                                        tcnt, mc, s)
   switch (e.kind) {
     case EPI_STORE: L2_(EPI_STORE);
     case EPI_STORE_F32: L2_(EPI_STORE_F32);
@@ -398,7 +434,7 @@ template <int BN> static cb_status set_attrs2() {
 }
 
 // How many 2-CTA clusters of the kernel can be co-resident (GPC boundaries can leave fewer than SMs / 2).
-template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms, int* out) {
+template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms, int* out, int csize = 2) {
   using C = Cfg2<BN>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms);
@@ -406,7 +442,7 @@ template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms,
   cfg.dynamicSmemBytes = C::SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[0].val.clusterDim.x = csize; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
@@ -415,7 +451,7 @@ template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms,
   return CB_OK;
 }
 
-cb_status gemm_tc2_init(int num_sms, int* max_pairs) {
+cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4) {
   CB_TRY(set_attrs2<256>());
   CB_TRY(set_attrs2<192>());
   CB_TRY(set_attrs2<128>());
@@ -430,5 +466,12 @@ cb_status gemm_tc2_init(int num_sms, int* max_pairs) {
   if (c3 < *max_pairs) *max_pairs = c3;
   if (c4 < *max_pairs) *max_pairs = c4;
   CB_REQUIRE(*max_pairs >= 1, CB_E_CUDA, "no CTA pair of the tcgen05 GEMM fits on this device");
+  int d4[4] = {0, 0, 0, 0};
+  CB_TRY(max_pairs2<256>(num_sms, &d4[0], 4));
+  CB_TRY(max_pairs2<128>(num_sms, &d4[1], 4));
+  CB_TRY(max_pairs2<192>(num_sms, &d4[2], 4));
+  CB_TRY((max_pairs2<224, EPI_SWIGLU>(num_sms, &d4[3], 4)));
+  *max_clusters4 = d4[0];
+  for (int i = 1; i < 4; ++i) if (d4[i] < *max_clusters4) *max_clusters4 = d4[i];
   return CB_OK;
 }

@@ -193,6 +193,21 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t d_tmem, uint64_t a_desc, u
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 // Arrive on the barrier at this offset in both CTAs once all prior pair MMAs completed.
+// multicast A-half load of a 4-CTA cluster (two CTA pairs): the box lands at the same offset in every CTA of
+// `mask`; each destination's complete_tx goes to its pair leader's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(smem_u32(bar)), "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
