@@ -80,7 +80,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "gemm_pf"     1 = pair GEMMs load the weight (B) halves of their first pipeline stages before the PDL
  *                 wait, the A halves after it (experiment, measured neutral), 0 = off (default)
  *   "gemm_mc"     A-multicast 4-CTA clusters (two CTA pairs sharing their A rows) in the pair GEMM:
- *                 2 = where the planner expects a shorter k-loop (default), 1 = always (whole tiles), 0 = off */
+ *                 2 = where the planner expects a shorter k-loop (default), 1 = always (whole tiles), 0 = off,
+ *                 3 = 8-CTA clusters (2 row x 2 column tiles, B multicast as well; measured neutral, opt-in) */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 
 /* Read-only facts about the context: "num_sms", "gemm_max_pairs" (co-resident 2-CTA clusters of the

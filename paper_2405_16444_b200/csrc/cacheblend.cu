@@ -361,6 +361,7 @@ extern "C" cb_status cb_get_info(cb_ctx* c, const char* name, int64_t* value) {
   if (std::strcmp(name, "num_sms") == 0) { *value = c->num_sms; return CB_OK; }
   if (std::strcmp(name, "gemm_max_pairs") == 0) { *value = gemm_tc_max_pairs(c); return CB_OK; }
   if (std::strcmp(name, "gemm_max_clusters4") == 0) { *value = c->max_clusters4; return CB_OK; }
+  if (std::strcmp(name, "gemm_max_clusters8") == 0) { *value = c->max_clusters8; return CB_OK; }
   cb_set_error("unknown info '%s'", name);
   return CB_E_INVALID_ARG;
 }
@@ -466,7 +467,7 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     return CB_OK;
   }
   if (std::strcmp(name, "gemm_mc") == 0) {
-    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "gemm_mc must be 0, 1 or 2");
+    CB_REQUIRE(value >= 0 && value <= 3, CB_E_INVALID_ARG, "gemm_mc must be 0, 1, 2 or 3");
     c->gemm_mc = (int)value;
     return CB_OK;
   }

@@ -79,8 +79,9 @@ struct cb_ctx {
   cudaStream_t copy_stream;
   cudaStream_t aux_stream;    // MLP split: the down-projection blocks run here, overlapping gate_up blocks
   int topk_drop_max;          // cb_set_option("topk_drop", n): drop-smallest top-k path when n_cand - k <= n
-  int gemm_mc;                // cb_set_option("gemm_mc", 0 off / 1 on / 2 auto): A-multicast 4-CTA clusters (pair GEMM)
+  int gemm_mc;                // cb_set_option("gemm_mc"): 0 off, 1 4-CTA clusters, 2 auto, 3 8-CTA clusters (pair GEMM)
   int max_clusters4;          // co-resident 4-CTA clusters of the pair GEMM (0: none)
+  int max_clusters8;          // co-resident 8-CTA clusters of the pair GEMM (0: none)
   int gemm_pf;                // cb_set_option("gemm_pf", 0/1): first stages' weight loads before the PDL wait
   int q_split;                // cb_set_option("q_split", 0/1): layer-1 Q projected after the selection (kept rows)
   int attn_pair;              // cb_set_option("attn_pair", 0/1/2): light/heavy row-tile pairing (attention_tc5.cu)

@@ -357,11 +357,13 @@ constexpr int MAX_TAIL_P = 4;  // gemm_tc2.cu merges at most 4 pieces
 constexpr double TAIL_MERGE_CYC = 6000.0;  // partial store + merge reads + TMEM rewrite
 
 constexpr int MAX_KSPLIT = 4;
+constexpr double MC4_FACTOR = 0.8;  // k-loop of A-multicast 4-CTA clusters vs pairs (tools/gemm_micro.py --mcs)
+constexpr double MC8_FACTOR = 0.7;  // A+B multicast 8-CTA clusters
 constexpr double KSPLIT_EPI_CYC = 3000.0;  // one more serialised fp32 read-modify-write epilogue
 
 Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid, int K, int force_sched, int force_bn, int force_pair,
                int force_ksplit, int force_tail, bool no192, int pairs_cap, bool balance, bool no224, int mc_mode = 0,
-               int max_cl4 = 0) {
+               int max_cl4 = 0, int max_cl8 = 0) {
   if (pairs_cap > 0 && pairs_cap < max_pairs) max_pairs = pairs_cap;
   const int num_kb = (K + BK - 1) / BK;
   Plan best{256, 0, 1, 0, 1};
@@ -411,15 +413,32 @@ Plan plan_gemm(int num_sms, int max_pairs, int M, int N_out, bool sw, bool resid
           // max_cl4 (33 on B200) 4-CTA clusters are co-resident, fewer than 74 / 2, so it pays when the
           // clusters' rounds are no more than the pairs' rounds. Not for the SwiGLU GEMM: its many-round
           // 224/192-wide tiles run at the power-capped tensor peak and were slower in clusters (125 -> 134 us).
-          if (pair && ks == 1 && mc_mode && max_cl4 > 0 && ((bn <= 192 && !sw) || mc_mode == 1)) {
+          if (pair && ks == 1 && (mc_mode == 1 || mc_mode == 2) && max_cl4 > 0 &&
+              ((bn <= 192 && !sw) || mc_mode == 1)) {
             const int n_t = (int)(tiles / m_tiles);
             const long long units = (long long)m_tiles * ((n_t + 1) / 2);
             const long long rounds = (units + max_cl4 - 1) / max_cl4;
-            const double c_mc = (double)rounds * num_kb * cyc * (bn <= 192 ? 0.8 : 1.0);
+            const double c_mc = (double)rounds * num_kb * cyc * (bn <= 192 ? MC4_FACTOR : 1.0);
             if (c_mc < best_cost || mc_mode == 1) {
               best_cost = c_mc;
               best = Plan{bn, 0, 2 * (int)(2 * ((units + rounds - 1) / rounds)), 1, 1};
               best.mc = 1;
+            }
+          }
+          // 8-CTA clusters (2 row tiles x 2 column tiles): B quarter-boxes multicast across the row tiles too.
+          // Opt-in (gemm_mc = 3): only 15 such clusters are co-resident (60 pairs), and on the blend shapes
+          // they were neutral to slower than the 4-CTA clusters (o_proj 401 rows 21.6 vs 22.0 us, QKV 579 rows
+          // 27.3 vs 28.4, QKV 401 rows 37.1 vs 23.2, down 579 rows 86.4 vs 65.4; profiles/r02_gemm_mc.txt).
+          if (pair && ks == 1 && mc_mode == 3 && max_cl8 > 0 && !sw && m_tiles >= 2) {
+            const int n_t = (int)(tiles / m_tiles);
+            const long long units = (long long)((m_tiles + 1) / 2) * ((n_t + 1) / 2);
+            const long long rounds = (units + max_cl8 - 1) / max_cl8;
+            // a spare row tile (odd m_tiles) costs like a real one
+            const double c_mc = (double)rounds * num_kb * cyc * MC8_FACTOR;
+            if (c_mc < best_cost || mc_mode == 3) {
+              best_cost = c_mc;
+              best = Plan{bn, 0, 4 * (int)(2 * ((units + rounds - 1) / rounds)), 1, 1};
+              best.mc = 2;
             }
           }
           if (pair && ks == 1 && force_tail != 1) {  // remainder tiles cut into K pieces
@@ -480,7 +499,7 @@ struct TmapCache {
 cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,
                           int bn, int n_pairs, int ksplit, int* kflags, int tail_r, int tail_p, float* tscr,
                           int* tcnt, int mc, cudaStream_t s);
-cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4);
+cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4, int* max_clusters8);
 constexpr int KFLAGS = 4096;  // >= 8 per tile for every tile of a split-K launch (tiles * ksplit <= 74 pairs)
 
 cb_status gemm_tmap(cb_ctx* c, const void* p, long long rows, long long k, long long ld, int box_rows,
@@ -558,7 +577,7 @@ cb_status launch_gemm_tc(cb_ctx* c, const void* A, int lda, const void* B, int l
                             c->tmaps->force_bn, c->tmaps->force_pair, c->tmaps->force_ksplit,
                             c->tmaps->force_tail, c->tmaps->no192, c->tmaps->pairs_cap[e.kind],
                             c->tmaps->balance, c->tmaps->no224, e.push_base[0] != nullptr ? 0 : c->gemm_mc,
-                            c->max_clusters4);
+                            c->max_clusters4, c->max_clusters8);
   if (pl.pair)
     return launch_gemm_tc2(c, A, lda, B, ldb, M, K, e, pl.bn, pl.grid / 2, pl.ksplit, c->tmaps->kflags, pl.tail_r,
                            pl.tail_p, c->tmaps->tscr, c->tmaps->tcnt, pl.mc, s);
@@ -599,7 +618,7 @@ cb_status gemm_tc_init(cb_ctx* c) {
   CB_TRY(set_attrs<256>());
   CB_TRY(set_attrs<128>());
   c->tmaps = new TmapCache();
-  CB_TRY(gemm_tc2_init(c->num_sms, &c->tmaps->max_pairs, &c->max_clusters4));
+  CB_TRY(gemm_tc2_init(c->num_sms, &c->tmaps->max_pairs, &c->max_clusters4, &c->max_clusters8));
   CB_CUDA(cudaMalloc(&c->tmaps->part, (size_t)c->num_sms * BM * SLOT_COLS * sizeof(float)));
   CB_CUDA(cudaMalloc(&c->tmaps->flags, (size_t)c->num_sms * sizeof(int)));
   CB_CUDA(cudaMemset(c->tmaps->flags, 0, (size_t)c->num_sms * sizeof(int)));

@@ -38,6 +38,7 @@ template <int BN> struct Cfg2 {
 //                last piece to finish (fixed piece order) before the tile's epilogue.
 struct WorkItem {
   int t, sp, kb0, kb1, piece;
+  int mt, nt;  // row tile and column tile (mc: may lie past the last tile -> no epilogue)
 };
 __device__ __forceinline__ WorkItem work_item(int i, int tiles, int num_kb, int ksplit, int tail_r, int tail_p) {
   WorkItem w;
@@ -58,6 +59,7 @@ __device__ __forceinline__ WorkItem work_item(int i, int tiles, int num_kb, int 
     w.t = i % tiles; w.sp = i / tiles;
     w.kb0 = w.sp * num_kb / ksplit; w.kb1 = (w.sp + 1) * num_kb / ksplit;
   }
+  w.mt = -1; w.nt = -1;  // set by the caller from t
   return w;
 }
 
@@ -98,24 +100,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const bool leader = rank == 0;
   const int num_kb = (K + BK - 1) / BK;
   const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-  const int unit = mc ? (int)(blockIdx.x >> 2) : pair;  // scheduling unit: the cluster (mc) or the pair
-  const int n_units = mc ? (int)(gridDim.x >> 2) : n_pairs;
-  const int pic = (blockIdx.x >> 1) & 1;  // pair within the cluster (mc)
+  // mc == 2: 8-CTA clusters of four pairs (2 row tiles x 2 column tiles); in addition each B quarter-box is
+  // loaded by one CTA and multicast to the CTA of the other row tile that holds the same B half.
+  const int csh = mc == 2 ? 3 : 2;
+  const int unit = mc ? (int)(blockIdx.x >> csh) : pair;  // scheduling unit: the cluster (mc) or the pair
+  const int n_units = mc ? (int)(gridDim.x >> csh) : n_pairs;
+  const int pic = (blockIdx.x >> 1) & 1;  // pair within the 4-CTA cluster (mc 1)
+  const int pq = (blockIdx.x >> 1) & 3;   // pair within the 8-CTA cluster (mc 2)
   const int tiles = m_tiles * n_tiles;
-  const int items = mc ? m_tiles * ((n_tiles + 1) / 2)
-                       : tail_p > 1 ? tiles - tail_r + tail_r * tail_p : tiles * ksplit;  // see work_item()
+  const int items = mc == 2 ? ((m_tiles + 1) / 2) * ((n_tiles + 1) / 2)
+                    : mc ? m_tiles * ((n_tiles + 1) / 2)
+                         : tail_p > 1 ? tiles - tail_r + tail_r * tail_p : tiles * ksplit;  // see work_item()
   const auto item = [&](int i) -> WorkItem {
-    if (!mc) return work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+    if (!mc) {
+      WorkItem w = work_item(i, tiles, num_kb, ksplit, tail_r, tail_p);
+      w.mt = w.t % m_tiles; w.nt = w.t / m_tiles;
+      return w;
+    }
     WorkItem w;
-    w.t = i % m_tiles + m_tiles * (2 * (i / m_tiles) + pic);  // may name column tile n_tiles (odd n_tiles)
     w.sp = 0; w.kb0 = 0; w.kb1 = num_kb; w.piece = -1;
+    if (mc == 2) {  // 8-CTA cluster: pairs (row tile 2a + bit 1 of pq, column tile 2b + bit 0 of pq)
+      const int mt2 = (m_tiles + 1) / 2;
+      w.mt = 2 * (i % mt2) + (pq >> 1);
+      w.nt = 2 * (i / mt2) + (pq & 1);
+    } else {  // 4-CTA cluster: same row tile, column tiles 2b, 2b + 1
+      w.mt = i % m_tiles;
+      w.nt = 2 * (i / m_tiles) + pic;
+    }
+    w.t = w.mt + m_tiles * w.nt;  // unused in mc mode (no k-split flags, no tail pieces)
     return w;
   };
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], mc ? 2 : 1); }
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], mc == 2 ? 4 : mc ? 2 : 1);
+    }
     for (int s = 0; s < 2; ++s) { tc::mbar_init(&tfull[s], 1); tc::mbar_init(&tempty[s], 8); }
     tc::fence_barrier_init();
   }
@@ -147,12 +169,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const int half = (int)(crank >> 1);  // mc: the 64-row half of the shared A box this CTA loads
+      const int half = (int)((crank >> 1) & 1);  // mc: the 64-row half of the shared A box this CTA loads
       const uint16_t amask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
+      const int bq = (int)((crank >> 2) & 1);     // mc 2: the quarter of this pair's B half this CTA loads
+      const uint16_t bmask = (uint16_t)((1u << crank) | (1u << (crank ^ 4u)));
       for (int i = unit; i < items; i += n_units) {
         const WorkItem w = item(i);
-        const int t = w.t;
-        const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
+        const int m0 = w.mt * 256 + (int)rank * 128, nb = w.nt;
         const int b_row = SW ? (rank == 0 ? nb * OUT_N : e.ff + nb * OUT_N) : nb * BN + (int)rank * C::B_HALF;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -161,7 +184,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (st_on && i == unit && kb < 256) strace[rank * 256 + kb] = clock64();
             if (leader) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             tc::tma_load_2d_2sm_mc(sa + half * (A_BYTES / 2), &tmA, &full[stage], kb * BK, m0 + half * 64, amask);
-            tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
+            if (mc == 2)
+              tc::tma_load_2d_2sm_mc(sa + A_BYTES + bq * (C::B_BYTES / 2), &tmB, &full[stage], kb * BK,
+                                     b_row + bq * (C::B_HALF / 2), bmask);
+            else
+              tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
           } else if (i == pair && kb - w.kb0 < pre) {  // fresh stage, B already in flight: only A
             tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
           } else {
@@ -200,9 +227,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               tc::mma_bf16_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
-            if (mc) {  // the stage is free for both pairs' producers once both pairs' MMAs read it
-              tc::mma_commit_2sm_mask(&empty[stage], 0xF);
-              if (kb == kb1 - 1) tc::mma_commit_2sm_mask(&tfull[acc], (uint16_t)(3u << (crank & 2u)));
+            if (mc) {  // the stage is free for the producers once every pair of the cluster read it
+              tc::mma_commit_2sm_mask(&empty[stage], mc == 2 ? 0xFF : 0xF);
+              if (kb == kb1 - 1) tc::mma_commit_2sm_mask(&tfull[acc], (uint16_t)(3u << (crank & 6u)));
             } else {
               tc::mma_commit_2sm(&empty[stage]);
               if (kb == kb1 - 1) tc::mma_commit_2sm(&tfull[acc]);
@@ -223,8 +250,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const WorkItem w = item(i);
       const int t = w.t, sp = w.sp;
       const int acc = it & 1;
-      const int m0 = (t % m_tiles) * 256 + (int)rank * 128, nb = t / m_tiles;
-      const bool col_ok = nb < n_tiles;  // mc with odd n_tiles: the last cluster's second pair has no tile
+      const int m0 = w.mt * 256 + (int)rank * 128, nb = w.nt;
+      const bool col_ok = nb < n_tiles && w.mt < m_tiles;  // mc: a cluster's spare pair past the last tile
       // split-K chain (RESID only): split sp adds onto h_out after split sp - 1 of the same 32 rows
       // published it — a fixed order, so the sum is deterministic. flag = number of splits done.
       int* flag = kflags + ((size_t)t * 2 + rank) * 4 + q;
@@ -375,9 +402,10 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   const long long b_rows = sw ? 2LL * e.ff : (long long)e.N;
   CUtensorMap ta, tb;
   CB_TRY(gemm_tmap(c, A, M, K, lda, mc ? 64 : 128, &ta));  // mc: each CTA loads (and multicasts) half of A
-  CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, C::B_HALF, &tb));
+  CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, mc == 2 ? C::B_HALF / 2 : C::B_HALF, &tb));  // mc 2: B quarter-boxes
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
-  CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s, mc ? 4 : 2, ta, tb,
+  CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s,
+                    mc == 2 ? 8 : mc ? 4 : 2, ta, tb,
                     M, K, m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
                     (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr,
                     c->gemm_pf && !mc ? (const char*)B : nullptr, c->dbg_sel == 300 ? c->dbg_buf : nullptr, mc));
@@ -396,6 +424,7 @@ cb_status launch_gemm_tc2(cb_ctx* c, const void* A, int lda, const void* B, int 
   if (ksplit > 1) tail_p = 1;
   // mc (plan_gemm): A-multicast clusters of two pairs, whole tiles only; n_pairs = 2 x the cluster count
   if (ksplit > 1 || tail_p > 1 || e.push_base[0] != nullptr) mc = 0;
+  if (mc == 2) CB_REQUIRE(e.kind != EPI_SWIGLU, CB_E_INVALID_ARG, "8-CTA multicast clusters exclude the SwiGLU GEMM");
   if (bn == 224) {  // SwiGLU only: 112 gate + 112 up columns (14336 = 128 x 112 features, Mistral d_ff)
     CB_REQUIRE(e.kind == EPI_SWIGLU, CB_E_INVALID_ARG, "224-wide pair tiles are for the SwiGLU GEMM only");
     return launch2_kind<EPI_SWIGLU, 224>(c, A, lda, B, ldb, M, K, e, n_pairs, 1, kflags, tail_r, tail_p, tscr, tcnt,
@@ -437,7 +466,7 @@ template <int BN> static cb_status set_attrs2() {
 template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms, int* out, int csize = 2) {
   using C = Cfg2<BN>;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(num_sms);
+  cfg.gridDim = dim3(num_sms / csize * csize);  // a whole number of clusters
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cudaLaunchAttribute at[1];
@@ -451,7 +480,7 @@ template <int BN, int KIND = EPI_RESID> static cb_status max_pairs2(int num_sms,
   return CB_OK;
 }
 
-cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4) {
+cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4, int* max_clusters8) {
   CB_TRY(set_attrs2<256>());
   CB_TRY(set_attrs2<192>());
   CB_TRY(set_attrs2<128>());
@@ -473,5 +502,11 @@ cb_status gemm_tc2_init(int num_sms, int* max_pairs, int* max_clusters4) {
   CB_TRY((max_pairs2<224, EPI_SWIGLU>(num_sms, &d4[3], 4)));
   *max_clusters4 = d4[0];
   for (int i = 1; i < 4; ++i) if (d4[i] < *max_clusters4) *max_clusters4 = d4[i];
+  int d8[3] = {0, 0, 0};  // no SwiGLU in 8-CTA clusters
+  CB_TRY(max_pairs2<256>(num_sms, &d8[0], 8));
+  CB_TRY(max_pairs2<128>(num_sms, &d8[1], 8));
+  CB_TRY(max_pairs2<192>(num_sms, &d8[2], 8));
+  *max_clusters8 = d8[0];
+  for (int i = 1; i < 3; ++i) if (d8[i] < *max_clusters8) *max_clusters8 = d8[i];
   return CB_OK;
 }
