@@ -191,6 +191,48 @@ def test_gemm_tail_pieces(P, M, N, K, bn, resid):
         assert torch.equal(run(), C)
 
 
+@pytest.mark.parametrize("M,N,K,bn", [(401, 4096, 4096, 128), (579, 4096, 4096, 192), (300, 4224, 1024, 128),
+                                      (1000, 2048, 512, 256), (37, 384, 256, 128), (513, 1000 + 24, 640, 192)])
+def test_gemm_multicast_clusters(P, M, N, K, bn):
+    """Pair GEMM in 4-CTA clusters sharing A by TMA multicast (gemm_mc = 1) and in 8-CTA clusters sharing A and
+    B (gemm_mc = 3), odd column / row tile counts included (a spare pair computes no epilogue): the same
+    accumulation order as plain pairs, so bitwise equal fp32, bf16 and residual outputs; fp64 reference."""
+    ctx = P.Context(shape("small"), "bf16", max_tokens=8)
+    ctx.set_option("gemm_pair", 1)
+    ctx.set_option("gemm_bn", bn)
+    g = torch.Generator(device=DEV).manual_seed(M + N + K + bn)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)
+    C0 = torch.randn(M, N, device=DEV, generator=g)
+    outs = []
+    for mc in (0, 1, 3):
+        ctx.set_option("gemm_mc", mc)
+        outs.append((P.api.op_gemm(ctx, A, B, out_f32=True, impl=2), P.api.op_gemm(ctx, A, B, out_f32=False, impl=2),
+                     P.api.op_gemm_resid(ctx, A, B, C0.clone(), impl=2)))
+    ref = (A.double() @ B.double().T).cpu().numpy()
+    assert rel_err(np32(outs[0][0]), ref) < 5e-5
+    assert rel_err(np32(outs[0][2]), ref + C0.double().cpu().numpy()) < 5e-5
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("mc", [1, 3])
+def test_blend_multicast_clusters_bitwise(P, mc):
+    """The small bf16 blend with every eligible pair GEMM (QKV with fused RoPE / Delta_kv, o_proj and down_proj
+    with the residual + RMSNorm epilogues) forced into multicast clusters: bitwise the plain-pair result."""
+    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 14, [300, 211, 157], 7, "bf16", 0.15)
+    outs = []
+    for v in (0, mc):
+        ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
+        ctx.set_option("gemm_mc", v)
+        outs.append(run_blend(P, s, "bf16", 14, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx))
+    for key in ("K", "V", "h"):
+        np.testing.assert_array_equal(outs[0][key], outs[1][key])
+    for a, b in zip(outs[0]["sel"], outs[1]["sel"]):
+        np.testing.assert_array_equal(a, b)
+
+
 @pytest.mark.parametrize("lens", [[200, 317, 150], [40, 30]])
 def test_blend_swiglu_224_tiles(P, lens):
     """gate_up on 256 x 224 CTA-pair tiles (112 gate + 112 up features; d_ff = 2816 leaves a ragged last

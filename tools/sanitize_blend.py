@@ -3,7 +3,8 @@
   compute-sanitizer --tool memcheck python tools/sanitize_blend.py [case ...]
 
 Cases exercise every kernel family on the blend path, including the cross-CTA protocols: the pair
-GEMM with a forced split-K chain (`gemm_ksplit`) and with the tail pieces (`gemm_tail`), attention
+GEMM with a forced split-K chain (`gemm_ksplit`), with the tail pieces (`gemm_tail`) and in TMA-multicast
+clusters of 4 and 8 CTAs (`gemm_mc`), attention
 with forced split-KV and the last-arriver merge (`attn_splits`), the top-k kernel, the request path.
 Inputs are seeded synthetic (random chunk caches), no oracle: this checks memory/sync hazards only.
 """
@@ -30,6 +31,8 @@ CASES = {
     "small_bf16_tail": ("small", "bf16", [200, 317, 150], 0, 0.15, {"gemm_tail": 2}),
     "small_bf16_attn_split": ("small", "bf16", [200, 317, 150], 0, 0.3, {"attn_splits": 3}),
     "small_bf16_single_cta": ("small", "bf16", [200, 317, 150], 0, 0.15, {"gemm_pair": 2}),
+    "small_bf16_mc4": ("small", "bf16", [200, 317, 150], 6, 0.15, {"gemm_mc": 1}),
+    "small_bf16_mc8": ("small", "bf16", [200, 317, 150], 6, 0.15, {"gemm_mc": 3}),
 }
 
 
