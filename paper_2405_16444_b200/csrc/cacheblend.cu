@@ -901,8 +901,9 @@ cb_status check_forward(cb_ctx* c, const cb_layer_w* w, const void* embed, const
 }
 
 // Layers 0..L-1 of the blend. realign_per_layer: request mode, where layer i's chunk KV lands in
-// k_blend/v_blend on the copy stream (event layer_ev[i]) and is realigned in place right before
-// layer i (fetch_kv / synchronize / prefill_layer); otherwise the realign already ran.
+// k_blend/v_blend on the copy stream and is realigned in place there, right after its copy (event
+// layer_ev[i]); layer i waits for that event (fetch_kv / synchronize / prefill_layer). Otherwise
+// the realign already ran.
 cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const int* tok, const int* pos, int N,
                        int n_suffix, void* k_blend, void* v_blend, const int* k_sched, const int* force_sel,
                        int* sel_out, float* dev_out, float* h_out, cudaStream_t s, bool realign_per_layer,
@@ -913,10 +914,8 @@ cb_status blend_layers(cb_ctx* c, const cb_layer_w* w, const void* embed, const 
   const size_t layer_stride = (size_t)T * kvd;
   auto realign_layer = [&](int i) -> cb_status {
     if (!realign_per_layer || N == 0) return CB_OK;
-    CB_CUDA(cudaStreamWaitEvent(s, c->layer_ev[i], 0));  // synchronize(): layer i's KV is on the GPU
-    char* kb = (char*)k_blend + (size_t)i * layer_stride * B;
-    return launch_realign(c, kb, kb, nullptr, nullptr, c->src_pos, pos, 1, N, (long long)layer_stride,
-                          (long long)layer_stride, s);
+    CB_CUDA(cudaStreamWaitEvent(s, c->layer_ev[i], 0));  // synchronize(): layer i's KV is on the GPU, realigned
+    return CB_OK;
   };
   CB_TRY(launch_pos_check(c, pos, T, s));  // positions in range and strictly increasing (device error word)
   // (a2) layer 0 in full
@@ -1015,15 +1014,20 @@ cb_status blend_request_impl(cb_ctx* c, const cb_layer_w* w, const void* embed, 
   CB_CUDA(cudaStreamWaitEvent(cs, c->ev_ready, 0));
   CB_CUDA(cudaMemcpyAsync(c->tok_d, tok_host, (size_t)T * 4, cudaMemcpyHostToDevice, cs));
   CB_CUDA(cudaMemcpyAsync(c->pos_d, pos_host, (size_t)T * 4, cudaMemcpyHostToDevice, cs));
+  if (N > 0) CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, cs));
   CB_CUDA(cudaEventRecord(c->layer_ev[L], cs));
-  // fetch_kv(layer i) for every layer, in layer order on the copy stream
+  // fetch_kv(layer i) for every layer, in layer order on the copy stream, each layer's K
+  // realigned right behind its copy on the same stream: the copies run ahead of the compute, so the realign
+  // kernels (HBM-bound, a few us each) stay off the compute stream's critical path
   for (int i = 0; i < L && N > 0; ++i) {
     const size_t row = (size_t)kvd * B;
-    CB_TRY(fetch(i, (char*)k_blend + (size_t)i * T * row, (char*)v_blend + (size_t)i * T * row, cs));
+    char* kb = (char*)k_blend + (size_t)i * T * row;
+    CB_TRY(fetch(i, kb, (char*)v_blend + (size_t)i * T * row, cs));
+    CB_TRY(launch_realign(c, kb, kb, nullptr, nullptr, c->src_pos, c->pos_d, 1, N, (long long)T * kvd,
+                          (long long)T * kvd, cs));
     CB_CUDA(cudaEventRecord(c->layer_ev[i], cs));
   }
   CB_CUDA(cudaStreamWaitEvent(s, c->layer_ev[L], 0));
-  if (N > 0) CB_TRY(launch_local_pos(c, chunk_start, n_chunks, c->src_pos, s));
   const int final_rows = (L == 1 ? N : k_sched[L - 1]) + n_suffix;
   CB_TRY(blend_layers(c, w, embed, c->tok_d, c->pos_d, N, n_suffix, k_blend, v_blend, k_sched, nullptr, nullptr,
                       nullptr, h_out_host, s, true));
