@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
   const long long t_start = tc::globaltimer();
 #endif
 #ifdef CB_ATTN_TRACE  // tools/attn_trace.py: clock64 pipeline events of CTA 0 (build with -DCB_ATTN_TRACE)
-  const bool dbg_on = dbg != nullptr && blockIdx.x == 0;
+#ifndef CB_ATTN_TRACE_CTA
+#define CB_ATTN_TRACE_CTA 0  // which CTA's pipeline to trace (-DCB_ATTN_TRACE_CTA=n)
+#endif
+  const bool dbg_on = dbg != nullptr && blockIdx.x == CB_ATTN_TRACE_CTA;
 #define DBG(i) do { if (dbg_on && (i) < 2048) dbg[i] = clock64(); } while (0)
 #else
 #define DBG(i) do { } while (0)

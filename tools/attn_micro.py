@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--splits", default="0,1,2,3,4,6")
     ap.add_argument("--impls", default="2")
     ap.add_argument("--pairs", default="0,1")
+    ap.add_argument("--pdl", type=int, default=1)
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -25,6 +26,7 @@ def main():
     s = W.MODELS["mistral-7b"]
     T = 3072
     ctx = P.Context(s, "bf16", max_tokens=T)
+    ctx.set_option("pdl", a.pdl)
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
     for n_sel in (3072, 553, 460, 369):

@@ -21,6 +21,7 @@ def main():
     ctx = P.Context(s, "bf16", max_tokens=T)
     ctx.set_option("attn_splits", splits)
     ctx.set_option("attn_pair", pair)
+    ctx.set_option("pdl", int(os.environ.get("CB_PDL", "1")))
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
     rows = np.sort(np.random.default_rng(n_sel).choice(T, n_sel, replace=False)).astype(np.int32)
@@ -40,8 +41,15 @@ def main():
     ends = sorted(e for _, _, e in spans)
     print(f"{len(spans)} CTAs, last end {ends[-1]:.1f} us, median end {ends[len(ends) // 2]:.1f}")
     step = int(os.environ.get("SPAN_STEP", "8"))
+    G, n_kv = s.n_q_heads // s.n_kv_heads, s.n_kv_heads
+    tiles = (n_sel * G + 127) // 128
+    def n_kt(cta):  # key tiles of the CTA's row tile (splits = 1, no pairing): tokens [32 p, 32 p + 32)
+        p = tiles - 1 - cta // n_kv
+        last = rows[min(n_sel, (p + 1) * 128 // G) - 1]
+        return (int(last) + 1 + 127) // 128
     for i, b, e in spans[::step]:
-        print(f"{i:4d} {b:7.2f} -> {e:7.2f}  ({e - b:6.2f})")
+        extra = f"  kt={n_kt(i):3d}  {(e - b) / n_kt(i):5.2f} us/tile" if splits <= 1 and not pair else ""
+        print(f"{i:4d} {b:7.2f} -> {e:7.2f}  ({e - b:6.2f}){extra}")
 
 
 if __name__ == "__main__":
