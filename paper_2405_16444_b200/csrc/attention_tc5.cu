@@ -25,7 +25,9 @@
 // (deterministic) and writes the output -- no separate merge launch.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 
 #include "ctx.h"
@@ -341,7 +343,9 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
     const int tile = seg[si].tile, jb = seg[si].jb, nt = seg[si].je - seg[si].jb, kmin = seg[si].kmin;
     const int n_active = seg[si].n_active;
     const bool partial = n_active > 1;
-    const size_t part_row0 = ((size_t)seg[si].sidx * n_kv + g) * R;
+    // partial slots: rows padded to whole tiles; inside a tile's block the float4s are thread-major
+    // ([OW / 4][NSM]), so the partial stores and the merge's loads are coalesced across a warp
+    const size_t part_row0 = ((size_t)seg[si].sidx * n_kv + g) * (size_t)(((R + BM - 1) / BM) * BM);
     const int rho = tile * BM + r;
     const bool valid = rho < R;
     const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
@@ -571,9 +575,10 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
     }
     if (partial) {
       if (valid) {
-        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + rho) * HD + wg * OW);
+        float4* dst = reinterpret_cast<float4*>(opart + (part_row0 + (size_t)tile * BM) * HD) + et;
 #pragma unroll
-        for (int i = 0; i < OW / 4; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+        for (int i = 0; i < OW / 4; ++i)
+          __stcg(dst + i * NSM, make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
         if (wg == 0) ml[part_row0 + rho] = make_float2(m_used, l);
       }
       __threadfence();  // partials visible device-wide before the arrival is counted
@@ -591,20 +596,21 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
         __threadfence();
         float mstar = -INFINITY;
         for (int sp = 0; sp < n_active; ++sp)
-          if (valid) mstar = fmaxf(mstar, __ldcg(&ml[((size_t)sp * n_kv + g) * R + rho].x));
+          if (valid) mstar = fmaxf(mstar, __ldcg(&ml[((size_t)sp * n_kv + g) * (size_t)(((R + BM - 1) / BM) * BM) + rho].x));
         float lt = 0.f;
 #pragma unroll
         for (int i = 0; i < OW; ++i) o[i] = 0.f;
+        const size_t rpad = (size_t)(((R + BM - 1) / BM) * BM);
         for (int sp = 0; sp < n_active && valid; ++sp) {
-          const size_t prow = ((size_t)sp * n_kv + g) * R + rho;
-          const float2 ms = __ldcg(&ml[prow]);
+          const size_t prow = ((size_t)sp * n_kv + g) * rpad;
+          const float2 ms = __ldcg(&ml[prow + rho]);
           if (ms.x == -INFINITY) continue;
           const float f = ex2(ms.x - mstar);
           lt += ms.y * f;
-          const float4* src = reinterpret_cast<const float4*>(opart + prow * HD + wg * OW);
+          const float4* src = reinterpret_cast<const float4*>(opart + (prow + (size_t)tile * BM) * HD) + et;
 #pragma unroll
           for (int i = 0; i < OW / 4; ++i) {
-            const float4 x = __ldcg(src + i);
+            const float4 x = __ldcg(src + i * NSM);
             o[4 * i] += x.x * f; o[4 * i + 1] += x.y * f; o[4 * i + 2] += x.z * f; o[4 * i + 3] += x.w * f;
           }
         }
@@ -684,6 +690,39 @@ cb_status kv_tmap5(const cb_ctx* c, const void* p, int n_keys, CUtensorMap* out)
 
 bool attention_tc5_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.head_dim == HD && g_encode5 != nullptr; }
 
+// Split count for a grid of at least half a wave: list-schedule the CTAs in launch order (heaviest row tiles
+// first, then their later key ranges) on num_sms SMs with a per-CTA cost of F + key tiles (+ M for a CTA that
+// writes and merges partials), and take the split count with the shortest makespan. Row tile p is assumed to
+// reach key tile ceil(max_kt (p + 1) / tiles) (selected tokens spread over the context; the suffix last).
+// Costs in key-tile units, measured on B200 (tools/attn_spans.py): CTA time ~ 8 + 1.0 x key tiles us; a split
+// range adds ~1.5 (partial write, merge by the last arrival; thread-major partials).
+static int attn_pick_splits(int tiles, int max_kt, int n_kv, int num_sms) {
+  constexpr double F = 8.0, M = 1.5;
+  int best = 1;
+  double best_t = 1e30;
+  for (int ns = 1; ns <= 3; ++ns) {
+    const int kps = (max_kt + ns - 1) / ns;
+    std::vector<double> sm(num_sms, 0.0);
+    double span = 0.0;
+    for (int p = tiles - 1; p >= 0; --p) {
+      const int kt = (int)(((long long)max_kt * (p + 1) + tiles - 1) / tiles);
+      const int active = (kt + kps - 1) / kps;
+      for (int sp = 0; sp < ns; ++sp) {
+        const int len = std::min(kt, (sp + 1) * kps) - sp * kps;
+        if (len <= 0) continue;
+        const double d = F + len + (active > 1 ? M : 0.0);
+        for (int h = 0; h < n_kv; ++h) {
+          auto it = std::min_element(sm.begin(), sm.end());
+          *it += d;
+          span = std::max(span, *it);
+        }
+      }
+    }
+    if (span < best_t - 0.5) { best_t = span; best = ns; }
+  }
+  return best;
+}
+
 cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,
                                const void* v, int n_keys, void* out, cudaStream_t s) {
   if (n_rows == 0) return CB_OK;
@@ -709,8 +748,10 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
     // measured (tools/attn_micro.py): extra CTAs only pay off when the (row tile, head) grid leaves
     // more than half of the SMs idle -- split CTAs run as extra waves with their own prologues
     n_splits = (int)std::min<long long>((c->num_sms + base - 1) / base, (max_kt + 3) / 4);
+  } else {
+    n_splits = attn_pick_splits(tiles, max_kt, n_kv, c->num_sms);
   }
-  n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)R * n_kv)));
+  n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)tiles * BM * n_kv)));  // padded slots
   n_splits = std::max(1, std::min(n_splits, 16));
   const int kt_per_split = (max_kt + n_splits - 1) / n_splits;
   CB_REQUIRE(base <= c->attn_cnt_n, CB_E_SHAPE, "attention: %lld row tiles exceed the counter array", base);

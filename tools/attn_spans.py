@@ -43,12 +43,21 @@ def main():
     step = int(os.environ.get("SPAN_STEP", "8"))
     G, n_kv = s.n_q_heads // s.n_kv_heads, s.n_kv_heads
     tiles = (n_sel * G + 127) // 128
-    def n_kt(cta):  # key tiles of the CTA's row tile (splits = 1, no pairing): tokens [32 p, 32 p + 32)
-        p = tiles - 1 - cta // n_kv
+    ns = max(splits, 1)
+
+    def n_kt(cta):  # key tiles of the CTA's range (no pairing): row tile p holds tokens [32 p, 32 p + 32)
+        rest = cta // n_kv
+        p = tiles - 1 - rest // ns
         last = rows[min(n_sel, (p + 1) * 128 // G) - 1]
-        return (int(last) + 1 + 127) // 128
+        kt = (int(last) + 1 + 127) // 128
+        if ns == 1:
+            return kt
+        per = (24 + ns - 1) // ns  # kt_per_split for T = 3072 keys
+        sp = rest % ns
+        return max(0, min(kt, (sp + 1) * per) - sp * per)
     for i, b, e in spans[::step]:
-        extra = f"  kt={n_kt(i):3d}  {(e - b) / n_kt(i):5.2f} us/tile" if splits <= 1 and not pair else ""
+        k_ = n_kt(i) if not pair else 0
+        extra = f"  kt={k_:3d}  {(e - b) / max(k_, 1):5.2f} us/tile" if not pair else ""
         print(f"{i:4d} {b:7.2f} -> {e:7.2f}  ({e - b:6.2f}){extra}")
 
 
