@@ -24,6 +24,9 @@ def main():
     tok = torch.from_numpy(req.tokens(s.vocab)).cuda()
     pos = torch.from_numpy(req.global_positions()).cuda()
     ks = P.schedule(0.15, N, L)
+    for kv in filter(None, os.environ.get("CB_OPTS", "").split(",")):  # e.g. CB_OPTS=topk_drop2=0
+        name, val = kv.split("=")
+        ctx.set_option(name, int(val))
     for trace in (0, 0, 200):
         ctx.set_option("debug_trace", trace)
         P.blend_forward(ctx, mw, tok, pos, list(req.chunk_starts()), 0, k_in, v_in, k_out, v_out, ks)
