@@ -661,311 +661,6 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-// Two key streams per CTA (an in-CTA split of the key range): the CTA's key tiles alternate between stream 0
-// (tiles jb, jb + 2, ..) and stream 1 (jb + 1, jb + 3, ..). Softmax warpgroup X owns stream X: thread = one
-// query row with all 128 scores of the tile (no cross-warpgroup row-max exchange), its own S/P buffer (TMEM
-// columns 128 X ..), O accumulator (256 + 128 X ..) and running (m, l). The two chains are independent, so on
-// every SMSP one stream's TMEM round trips, row max and barrier waits overlap the other stream's exponentials,
-// and the tensor pipe alternates QK^T / PV of the two streams. At the end the two (O, m, l) merge on-chip
-// (each warpgroup then owns 64 output columns) and the split-KV partial / write path is the same as above.
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); Q is staged in shared memory (SWIZZLE_128B).
-// POLY: share of the exponentials on the FMA pipe (ex2_poly): 0 none, 1 one in four, 2 one in two.
-constexpr int DUAL_NT = 64 + 256;
-template <int POLY>
-__global__ void __launch_bounds__(DUAL_NT, 1)
-    attn_dual_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
-                     int n_rows, int n_keys, bf16* __restrict__ out, int n_q, int n_kv, float scale_log2,
-                     int kt_per_split, int n_splits, float* __restrict__ opart, float2* __restrict__ ml,
-                     int* __restrict__ tile_cnt, long long* __restrict__ dbg) {
-  pdl_enter();
-#ifdef CB_ATTN_TRACE
-  const long long t_start = tc::globaltimer();
-#endif
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + TILE;              // [KST] stages
-  uint8_t* sV = smem + (1 + KST) * TILE;  // [2] stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
-  uint64_t* k_full = bars;        // [3] K tile landed
-  uint64_t* k_empty = bars + 3;   // [3] QK^T MMAs done reading the K stage
-  uint64_t* v_full = bars + 6;    // [2] V tile landed
-  uint64_t* v_empty = bars + 8;   // [2] PV MMAs done reading the V stage
-  uint64_t* s_full = bars + 10;   // [2] per stream: S in its TMEM buffer
-  uint64_t* p_full = bars + 12;   // [2] per stream: P written over S (4 warps)
-  uint64_t* pv_done = bars + 14;  // [2] per stream: PV accumulated into its O
-  uint64_t* q_full = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
-  float* xm = reinterpret_cast<float*>(bars + 18);  // [2 streams][128 rows] m, then l, then the merge flag
-  float* xl = xm + 2 * 128;
-  int* flag = reinterpret_cast<int*>(xl + 2 * 128);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = n_q / n_kv, R = n_rows * G;
-  const int qd = n_q * HD;
-  // 1-D grid, kv head fastest, heaviest row tiles first (as attn_tc5_kernel without pairing)
-  const int g = (int)blockIdx.x % n_kv;
-  const int tiles = gridDim.x / (n_splits * n_kv);
-  const int rest = (int)blockIdx.x / n_kv;
-  const int tile = tiles - 1 - rest / n_splits;
-  const int split = rest % n_splits;
-  int n_kt, kmin;
-  tile_span(q_tok, tile, R, G, n_keys, n_kt, kmin);
-  const int jb = split * kt_per_split, je = min(n_kt, jb + kt_per_split);
-  if (jb >= je) return;  // nothing in this range (the tile's other CTAs do not count it)
-  const int n_active = (n_kt + kt_per_split - 1) / kt_per_split;
-  const int nt = je - jb, n0 = (nt + 1) / 2, n1 = nt / 2;  // stream 0 / 1 tile counts
-
-  if (warp == 0 && lane == 0) {
-    tc::tma_prefetch(&tmK);
-    tc::tma_prefetch(&tmV);
-    for (int b = 0; b < KST; ++b) {
-      tc::mbar_init(&k_full[b], 1);
-      tc::mbar_init(&k_empty[b], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&v_full[b], 1);
-      tc::mbar_init(&v_empty[b], 1);
-      tc::mbar_init(&s_full[b], 1);
-      tc::mbar_init(&p_full[b], 4);
-      tc::mbar_init(&pv_done[b], 1);
-    }
-    tc::mbar_init(q_full, 256);
-    tc::fence_barrier_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ===== TMA producer: key tiles jb .. je-1 in order (= the MMA consumption order of the two streams) for K
-    // and for V; K runs up to KST tiles ahead =====
-    if (tc::elect_one()) {
-      auto load = [&](uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int key0) {
-        tc::mbar_arrive_expect_tx(bar, TILE);
-        tc::tma_load_3d(dst, m, bar, 0, g, key0);
-        tc::tma_load_3d(dst + ATOM, m, bar, 64, g, key0);
-      };
-      int tk = 0, tv = 0;
-      while (tk < nt || tv < nt) {
-        if (tk < nt && (tk < KST || tc::mbar_test(&k_empty[tk % KST], (tk / KST - 1) & 1))) {
-          load(sK + (tk % KST) * TILE, &tmK, &k_full[tk % KST], (jb + tk) * BC);
-          ++tk;
-        }
-        if (tv < tk && (tv < 2 || tc::mbar_test(&v_empty[tv & 1], ((tv >> 1) - 1) & 1))) {
-          load(sV + (tv & 1) * TILE, &tmV, &v_full[tv & 1], (jb + tv) * BC);
-          ++tv;
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===== MMA issuer. Order: S0(0) S1(0) | PV0(0) S0(1) PV1(0) S1(1) | PV0(1) S0(2) .. -- K and V stages are
-    // consumed in key-tile order. S_X(i+1) overwrites P_X(i): it is issued after PV_X(i) on the in-order
-    // tensor pipe. =====
-    constexpr uint32_t IDESC_S = tc::idesc_bf16(BM, BC);
-    constexpr uint32_t IDESC_PV = tc::idesc_bf16_bmn(BM, HD);
-    int kpos = 0, vpos = 0;
-    auto issue_s = [&](int X) {
-      const int kb = kpos % KST;
-      tc::mbar_wait(&k_full[kb], (kpos / KST) & 1);
-      tc::fence_after();
-      if (tc::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint64_t a = tc::sdesc_sw128(sQ + (kk >> 2) * ATOM) + 2 * (kk & 3);
-          const uint64_t bd = tc::sdesc_sw128(sK + kb * TILE + (kk >> 2) * ATOM) + 2 * (kk & 3);
-          tc::mma_bf16(tmem + X * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        tc::mma_commit(&s_full[X]);
-        tc::mma_commit(&k_empty[kb]);
-      }
-      __syncwarp();
-      ++kpos;
-    };
-    auto issue_pv = [&](int X, int i) {
-      const int vb = vpos & 1;
-      tc::mbar_wait(&p_full[X], i & 1);
-      tc::mbar_wait(&v_full[vb], (vpos >> 1) & 1);
-      tc::fence_after();
-      if (tc::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < BC / 16; ++kk) {  // P (bf16 pairs) of keys 16 kk .. at columns 8 kk .. of S_X
-          const uint64_t bd = tc::sdesc_sw128_mn(sV + vb * TILE + kk * 2048, ATOM);
-          tc::mma_bf16_ts(tmem + 256 + X * 128, tmem + X * 128 + 8 * kk, bd, IDESC_PV, (i > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(&pv_done[X]);
-        tc::mma_commit(&v_empty[vb]);
-      }
-      __syncwarp();
-      ++vpos;
-    };
-    tc::mbar_wait(q_full, 0);
-    issue_s(0);
-    if (n1 > 0) issue_s(1);
-    for (int i = 0; i < n0; ++i) {
-      issue_pv(0, i);
-      if (i + 1 < n0) issue_s(0);
-      if (i < n1) {
-        issue_pv(1, i);
-        if (i + 1 < n1) issue_s(1);
-      }
-    }
-    // drain the release commits of the last K / V stages (no consumer; compute-sanitizer synccheck)
-    for (int t = max(0, nt - KST); t < nt; ++t) tc::mbar_wait(&k_empty[t % KST], (t / KST) & 1);
-    for (int t = max(0, nt - 2); t < nt; ++t) tc::mbar_wait(&v_empty[t & 1], (t >> 1) & 1);
-  } else {
-    // ===== softmax of stream X, then the on-chip merge of the two streams and the output =====
-    const int X = (warp - 2) >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..255
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int rho = tile * BM + r;
-    const bool valid = rho < R;
-    const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
-    const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
-    {  // stage this row's column half X of Q (one SWIZZLE_128B column block)
-      const bf16* src = q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD;
-      const uint32_t dq = tc::smem_u32(sQ);
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8) {
-        const int ch = X * 8 + c8;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dq + sw_off(r, ch)), "l"(src + ch * 8),
-                     "r"(valid ? 16 : 0)
-                     : "memory");
-      }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      tc::fence_proxy_async();
-      tc::mbar_arrive(q_full);
-    }
-    const uint32_t tS = tmem + lane_base + X * 128, tO = tmem + lane_base + 256 + X * 128;
-    const int nX = X == 0 ? n0 : n1;
-    float m_used = -INFINITY, l = 0.f;
-    for (int i = 0; i < nX; ++i) {
-      tc::mbar_wait(&s_full[X], i & 1);
-      tc::fence_after();
-      float s[BC];
-      {
-        uint32_t w[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tmem_ld32_nw(tS + c * 32, w[c]);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) s[c * 32 + j] = __uint_as_float(w[c][j]);
-      }
-      const int key0 = (jb + 2 * i + X) * BC;
-      float mx8[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) mx8[j] = -INFINITY;
-      if (key0 + BC - 1 > kmin) {  // the tile reaches past some row's token: mask by position
-#pragma unroll
-        for (int j = 0; j < BC; ++j) {
-          if (key0 + j > tok) s[j] = -INFINITY;
-          mx8[j & 7] = fmaxf(mx8[j & 7], s[j]);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < BC; ++j) mx8[j & 7] = fmaxf(mx8[j & 7], s[j]);
-      }
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
-      // lazy rescale: move the reference max only when it grew by more than 2^8
-      float corr = 1.f;
-      if (mx > m_used + RESCALE_THRESHOLD || (m_used == -INFINITY && mx != -INFINITY)) {
-        if (m_used != -INFINITY) corr = ex2(m_used - mx);
-        m_used = mx;
-      }
-      const float nref = m_used == -INFINITY ? 0.f : -m_used;
-      l *= corr;
-      const float2 sc2 = make_float2(scale_log2, scale_log2), nr2 = make_float2(nref, nref);
-      float2 rs2[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) rs2[j] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < BC / 2; ++j) {
-        float2 xa = __ffma2_rn(make_float2(s[2 * j], s[2 * j + 1]), sc2, nr2);
-        xa.x = ex2(xa.x);
-        xa.y = (POLY == 2 || (POLY == 1 && (j & 1))) ? ex2_poly(xa.y) : ex2(xa.y);
-        s[2 * j] = xa.x;
-        s[2 * j + 1] = xa.y;
-        rs2[j & 3] = __fadd2_rn(rs2[j & 3], xa);
-      }
-      l += ((rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y)) + ((rs2[2].x + rs2[2].y) + (rs2[3].x + rs2[3].y));
-      {  // P (bf16 pairs, keys 2c and 2c + 1 in column c) over columns 0..63 of S_X (S_X is fully read)
-        uint32_t pk[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) pk[j] = pack2(s[2 * j], s[2 * j + 1]);
-        tc::tmem_st32u(tS, pk);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) pk[j] = pack2(s[64 + 2 * j], s[64 + 2 * j + 1]);
-        tc::tmem_st32u(tS + 32, pk);
-      }
-      // PV_X(i-1) completed before S_X(i) (in-order pipe); the explicit wait keeps the protocol checkable
-      if (i >= 1) tc::mbar_wait(&pv_done[X], (i - 1) & 1);
-      if (i >= 1 && __any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write of O_X
-        tc::fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float o[32];
-          tc::tmem_ld32(tO + c * 32, o);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] *= corr;
-          tc::tmem_st32(tO + c * 32, o);
-        }
-      }
-      tc::tmem_st_wait();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&p_full[X]);
-    }
-    // merge the streams: both warpgroups see both rows' (m, l); warpgroup X then owns output columns 64 X ..
-    tc::sts_f32(xm + X * 128 + r, m_used);
-    tc::sts_f32(xl + X * 128 + r, l);
-    named_bar_sync(1, 256);
-    const float m0 = tc::lds_f32(xm + r), l0 = tc::lds_f32(xl + r);
-    const float m1 = tc::lds_f32(xm + 128 + r), l1 = tc::lds_f32(xl + 128 + r);
-    tc::mbar_wait(&pv_done[0], (n0 - 1) & 1);
-    if (n1 > 0) tc::mbar_wait(&pv_done[1], (n1 - 1) & 1);
-    tc::fence_after();
-    const float ms = fmaxf(m0, m1);
-    const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - ms);
-    const float f1 = (n1 == 0 || m1 == -INFINITY) ? 0.f : ex2(m1 - ms);
-    l = l0 * f0 + l1 * f1;
-    float o[64];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {  // 16 columns at a time (register budget: 10 warps -> <= 168 per thread)
-      float a[16];
-      tc::tmem_ld16(tmem + lane_base + 256 + X * 64 + c * 16, a);
-      if (n1 > 0) {
-        float b[16];
-        tc::tmem_ld16(tmem + lane_base + 384 + X * 64 + c * 16, b);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) o[c * 16 + j] = a[j] * f0 + b[j] * f1;
-      } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) o[c * 16 + j] = a[j] * f0;
-      }
-    }
-    finish_rows<256, 64>(o, ms, l, n_active > 1, n_active == 1, n_active, split, tile, g, n_kv, R, rho, valid, rt, hh,
-                         qd, et, X, flag, opart, ml, tile_cnt, out);
-  }
-  tc::fence_before();
-  __syncthreads();
-#ifdef CB_ATTN_TRACE
-  if (dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 370) {
-    dbg[1300 + 2 * blockIdx.x] = t_start;
-    dbg[1300 + 2 * blockIdx.x + 1] = tc::globaltimer();
-  }
-#else
-  (void)dbg;
-#endif
-  if (warp == 1) tc::tmem_dealloc(tmem, 512);
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 g_encode5 = nullptr;
 
 // Tensor maps of K/V buffers, cached across calls and contexts: the key holds every field the map encodes
@@ -1014,7 +709,8 @@ bool attention_tc5_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.he
 // reach key tile ceil(max_kt (p + 1) / tiles) (selected tokens spread over the context; the suffix last).
 // Costs in key-tile units, measured on B200 (tools/attn_spans.py): CTA time ~ 8 + 1.0 x key tiles us; a split
 // range adds ~1.5 (partial write, merge by the last arrival; thread-major partials).
-static int attn_pick_splits(int tiles, int max_kt, int n_kv, int num_sms, double F, double M) {
+static int attn_pick_splits(int tiles, int max_kt, int n_kv, int num_sms) {
+  constexpr double F = 8.0, M = 1.5;
   int best = 1;
   double best_t = 1e30;
   for (int ns = 1; ns <= 3; ++ns) {
@@ -1066,9 +762,7 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
     // more than half of the SMs idle -- split CTAs run as extra waves with their own prologues
     n_splits = (int)std::min<long long>((c->num_sms + base - 1) / base, (max_kt + 3) / 4);
   } else {
-    // dual-stream kernel: ~0.55 us per key tile (two tiles in flight), so the fixed cost weighs more in tile units
-    n_splits = c->attn_dual ? attn_pick_splits(tiles, max_kt, n_kv, c->num_sms, c->attn_dual_f, c->attn_dual_m)
-                            : attn_pick_splits(tiles, max_kt, n_kv, c->num_sms, 8.0, 1.5);
+    n_splits = attn_pick_splits(tiles, max_kt, n_kv, c->num_sms);
   }
   n_splits = std::min(n_splits, (int)(c->attn_part_rows / ((long long)tiles * BM * n_kv)));  // padded slots
   n_splits = std::max(1, std::min(n_splits, 16));
@@ -1080,14 +774,6 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   // pair mode: 2-CTA clusters (light + heavy part, heavy rest), ceil(T / 2) per kv head
   dim3 grid(pair_mode ? 2 * ((tiles + 1) / 2) * n_kv : tiles * n_splits * n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
-  if (c->attn_dual && !pair_mode) {
-    auto dk = c->attn_poly == 2 ? attn_dual_kernel<2> : c->attn_poly == 1 ? attn_dual_kernel<1> : attn_dual_kernel<0>;
-    CB_CUDA(launch_k(c, dk, grid, dim3(DUAL_NT), SMEM, s, 1, tk, tv, (const bf16*)q, q_row, q_tok, n_rows,
-                     n_keys, (bf16*)out, c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
-                     c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr));
-    CB_LAUNCHED(c);
-    return CB_OK;
-  }
   auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, true, true, 2>
             : c->attn_poly == 1 ? attn_tc5_kernel<1, true, true, 2>
             : !c->attn_qtm ? attn_tc5_kernel<0, false, true, 2>
@@ -1111,9 +797,6 @@ cb_status attention_tc5_init() {
   }
   if (g_kvmaps == nullptr) g_kvmaps = new std::unordered_map<KvKey, CUtensorMap, KvKeyHash>();
   CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_dual_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_dual_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_dual_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));

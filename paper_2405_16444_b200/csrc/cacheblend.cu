@@ -292,11 +292,6 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = attention_tc5_init();
   c->topk_drop_max = 48;
   c->topk_sort = 0;  // bitonic path measured slower in the blend (13.5 vs 10.5 us per launch, profiles/r02)
-  c->topk_scatter = 0;
-  c->topk_scatter_ctas = 64;
-  c->attn_dual = 0;  // measured neutral in the blend (paired A/B), DESIGN.md §6.1
-  c->attn_dual_f = 14.0;
-  c->attn_dual_m = 2.5;
   c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
   c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
   c->gemm_mc = 2;    // auto: A-multicast clusters where the planner expects a shorter k-loop
@@ -482,27 +477,6 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   }
   if (std::strcmp(name, "q_split") == 0) {
     c->q_split = value != 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "topk_scatter") == 0) {
-    c->topk_scatter = value != 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "topk_scatter_ctas") == 0) {
-    CB_REQUIRE(value >= 1 && value <= 1024, CB_E_INVALID_ARG, "topk_scatter_ctas must be 1..1024");
-    c->topk_scatter_ctas = (int)value;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_dual") == 0) {
-    c->attn_dual = value != 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_dual_f") == 0) {  // split cost model, tenths of a key tile
-    c->attn_dual_f = value / 10.0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_dual_m") == 0) {
-    c->attn_dual_m = value / 10.0;
     return CB_OK;
   }
   if (std::strcmp(name, "attn_pair") == 0) {
@@ -829,13 +803,11 @@ cb_status layer_blend(cb_ctx* c, const cb_layer_w& w, const LayerBufs& b, int n_
     CB_TRY(launch_deviation(c, c->kf, c->vf, kb, vb, b.row_tok, n_cand, dev_mode, dev, s));
     CB_TRY(comm_allreduce_f32(c, dev, (size_t)n_cand, s));  // (i) unfused: sum the ranks' head sums
   }
-  // 4. only the KV of the HKVD tokens (and the suffix) is updated (R3): fused into the top-k launch
-  //    (every CTA repeats the selection and scatters its share of the rows), else a separate kernel
-  bool scattered = false;
   CB_TRY(launch_topk(c, dev, b.row_tok, n_cand, k, n_suf, N, force_sel, c->qrow, b.qtok, sel_tok, s,
-                     fuse_dev ? dev_part : nullptr, c->max_tokens, dev_mode, c->kf, c->vf, kb, vb, &scattered));
+                     fuse_dev ? dev_part : nullptr, c->max_tokens, dev_mode));
   if (Q == 0) return CB_OK;
-  if (!scattered) CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));
+  // 4. only the KV of the HKVD tokens (and the suffix) is updated (R3)
+  CB_TRY(launch_scatter_kv(c, c->kf, c->vf, c->qrow, b.qtok, Q, kb, vb, s));
   const int* q_rows = c->qrow;  // row of each kept query in c->q
   if (split_q) {
     // the kept rows of the projection input (and their RMSNorm blocks) gathered, then Q over them:

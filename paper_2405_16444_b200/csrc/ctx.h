@@ -84,10 +84,6 @@ struct cb_ctx {
   int max_clusters8;          // co-resident 8-CTA clusters of the pair GEMM (0: none)
   int gemm_pf;                // cb_set_option("gemm_pf", 0/1): first stages' weight loads before the PDL wait
   int q_split;                // cb_set_option("q_split", 0/1): layer-1 Q projected after the selection (kept rows)
-  int topk_scatter;           // cb_set_option("topk_scatter"): KV scatter fused into the top-k launch
-  int topk_scatter_ctas;      // its grid cap (cb_set_option("topk_scatter_ctas"))
-  int attn_dual;              // cb_set_option("attn_dual"): two key streams per CTA (attn_dual_kernel)
-  double attn_dual_f, attn_dual_m;  // its split cost model: fixed CTA cost, split merge cost (key-tile units)
   int attn_pair;              // cb_set_option("attn_pair", 0/1/2): light/heavy row-tile pairing (attention_tc5.cu)
   int topk_sort;              // cb_set_option("topk_sort", 0/1): bitonic path when n_cand <= top-k threads
   int topk_threads;           // cb_set_option("topk_threads", 256 | 512 | 1024): top-k block size (0 = 1024)
@@ -215,8 +211,7 @@ cb_status launch_deviation(cb_ctx* c, const void* k_new, const void* v_new, cons
 // [2 n_kv][ld_part] into dev (fixed head order, dev_mode selects K / V / both).
 cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix,
                       int N, const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s,
-                      const float* dev_part = nullptr, int ld_part = 0, int dev_mode = CB_DEV_KV, const void* kf = nullptr,
-                      const void* vf = nullptr, void* kb = nullptr, void* vb = nullptr, bool* scattered = nullptr);
+                      const float* dev_part = nullptr, int ld_part = 0, int dev_mode = CB_DEV_KV);
 // GEMM: acc = A[M][K] . B[N_b][K]^T; for SWIGLU B holds 2*ff rows and e.N = ff.
 // impl: 0 auto, 1 simt, 2 tcgen05.
 cb_status launch_gemm(cb_ctx* c, const void* A, int lda, const void* B, int ldb, int M, int K, const EpiParams& e,

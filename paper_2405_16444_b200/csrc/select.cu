@@ -122,15 +122,14 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sm_warp, int* total) 
   return r;
 }
 
-// The selection (every CTA of a fused launch computes it identically): CTA 0 writes dev and the index outputs,
-// and every CTA records the kept candidate slots in shared memory (sel_list[r] = slot of kept row r, r < k)
-// for the scatter that follows in the same launch.
-__device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* __restrict__ cand_tok, int n_cand, int k,
-                                            int n_suf, int N, const int* __restrict__ force_sel,
-                                            int* __restrict__ qrow, int* __restrict__ qtok, int* __restrict__ sel_tok,
-                                            int* err, const float* __restrict__ dev_part, int n_kv, int ld_part,
-                                            int dev_mode, int drop_max, int sort_path, long long* __restrict__ dbg,
-                                            int* sel_list) {
+__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ dev,
+                                                            const int* __restrict__ cand_tok, int n_cand, int k,
+                                                            int n_suf, int N, const int* __restrict__ force_sel,
+                                                            int* __restrict__ qrow, int* __restrict__ qtok,
+                                                            int* __restrict__ sel_tok, int* err,
+                                                            const float* __restrict__ dev_part, int n_kv, int ld_part,
+                                                            int dev_mode, int drop_max, int sort_path,
+                                                            long long* __restrict__ dbg) {
   // debug_trace 200: globaltimer of the phases (entry, inputs visible, Delta_kv summed, selected, done)
 #define TK_DBG(i) do { if (dbg != nullptr && threadIdx.x == 0) dbg[i] = tc_globaltimer(); } while (0)
   TK_DBG(0);
@@ -142,16 +141,6 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
   __shared__ int sm_total;
   __shared__ int sm_digit, sm_rem;
   const int tid = threadIdx.x;
-  const bool w0 = blockIdx.x == 0;  // the CTA that writes the global outputs
-  auto emit = [&](int out, int j) {  // kept row `out` is candidate slot j
-    if (sel_list) sel_list[out] = j;
-    if (w0) {
-      const int t = cand_tok[j];
-      qrow[out] = j;
-      qtok[out] = t;
-      if (sel_tok) sel_tok[out] = t;
-    }
-  };
 
   if (dev_part != nullptr) {  // Delta_kv from the QKV epilogue's per-(64-col block, k|v) partials, in order
     for (int j = tid; j < n_cand; j += blockDim.x) {
@@ -174,7 +163,7 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
           tot += a + b;
         }
       }
-      if (w0) dev[j] = tot;
+      dev[j] = tot;
       const unsigned u = __float_as_uint(tot);
       keys[j] = (u & 0x80000000u) ? 0u : u;  // the select keys, without re-reading dev (-0.0 -> 0)
     }
@@ -183,11 +172,10 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
   TK_DBG(2);
 
   // suffix rows are always kept
-  if (w0)
-    for (int s = tid; s < n_suf; s += blockDim.x) {
-      qrow[k + s] = n_cand + s;
-      qtok[k + s] = N + s;
-    }
+  for (int s = tid; s < n_suf; s += blockDim.x) {
+    qrow[k + s] = n_cand + s;
+    qtok[k + s] = N + s;
+  }
   if (force_sel != nullptr) {  // replay mode (R14)
     for (int r = tid; r < k; r += blockDim.x) {
       const int t = force_sel[r];
@@ -197,15 +185,12 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
         if (cand_tok[mid] < t) lo = mid + 1; else hi = mid;
       }
       if (lo >= n_cand || cand_tok[lo] != t) {
-        if (w0) atomicOr(err, CB_DEVERR_FORCE_SEL);
+        atomicOr(err, CB_DEVERR_FORCE_SEL);
         lo = min(lo, n_cand - 1);
       }
-      if (sel_list) sel_list[r] = lo;
-      if (w0) {
-        qrow[r] = lo;
-        qtok[r] = t;
-        if (sel_tok) sel_tok[r] = t;
-      }
+      qrow[r] = lo;
+      qtok[r] = t;
+      if (sel_tok) sel_tok[r] = t;
     }
     return;
   }
@@ -246,7 +231,12 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
     __syncthreads();
     const bool sel = tid < n_cand && mine >= sm_thr;
     const int out = block_excl_scan(sel ? 1 : 0, sm_warp, &sm_total);
-    if (sel) emit(out, tid);
+    if (sel) {
+      const int t = cand_tok[tid];
+      qrow[out] = tid;
+      qtok[out] = t;
+      if (sel_tok) sel_tok[out] = t;
+    }
     return;
   }
 
@@ -391,7 +381,13 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
     (void)nw;
-    if (sel) emit(before + __popc(bal & ((1u << lane) - 1u)), tid);
+    if (sel) {
+      const int out = before + __popc(bal & ((1u << lane) - 1u));
+      const int t = cand_tok[tid];
+      qrow[out] = tid;
+      qtok[out] = t;
+      if (sel_tok) sel_tok[out] = t;
+    }
     TK_DBG(4);
     return;
   }
@@ -416,56 +412,21 @@ __device__ __forceinline__ void topk_select(float* __restrict__ dev, const int* 
     const unsigned key = keys[j];
     bool sel = drop_path ? key != DROPPED : (all || key > vstar);
     if (!drop_path && !all && key == vstar) { sel = eq < rem; ++eq; }
-    if (sel) emit(out++, j);
+    if (sel) {
+      const int t = cand_tok[j];
+      qrow[out] = j;
+      qtok[out] = t;
+      if (sel_tok) sel_tok[out] = t;
+      ++out;
+    }
   }
   TK_DBG(4);
 #undef TK_DBG
 }
 
-// Optional fused KV scatter (step a5): the kept rows' new K, V (rows sel_list[r] of kf / vf) and the suffix rows
-// (n_cand + s) go to their token rows of the layer cache kb / vb. Row r of the k + n_suf is copied by CTA
-// r % gridDim.x, in 16-byte vectors.
-struct ScatterArgs {
-  const uint4* kf;
-  const uint4* vf;
-  uint4* kb;
-  uint4* vb;
-  int row_vecs;  // 16-byte vectors per K (or V) row
-};
-
-__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ dev,
-                                                            const int* __restrict__ cand_tok, int n_cand, int k,
-                                                            int n_suf, int N, const int* __restrict__ force_sel,
-                                                            int* __restrict__ qrow, int* __restrict__ qtok,
-                                                            int* __restrict__ sel_tok, int* err,
-                                                            const float* __restrict__ dev_part, int n_kv, int ld_part,
-                                                            int dev_mode, int drop_max, int sort_path,
-                                                            long long* __restrict__ dbg, ScatterArgs sa, int list_off) {
-  extern __shared__ unsigned char topk_smem[];
-  int* sel_list = sa.kb != nullptr ? reinterpret_cast<int*>(topk_smem + list_off) : nullptr;
-  topk_select(dev, cand_tok, n_cand, k, n_suf, N, force_sel, qrow, qtok, sel_tok, err, dev_part, n_kv, ld_part,
-              dev_mode, drop_max, sort_path, blockIdx.x == 0 ? dbg : nullptr, sel_list);
-  if (sa.kb == nullptr) return;
-  __syncthreads();  // sel_list complete
-  const int Q = k + n_suf, G = gridDim.x, nv = sa.row_vecs;
-  const int my_rows = (Q - (int)blockIdx.x + G - 1) / G;
-  const int work = my_rows * 2 * nv;
-#pragma unroll 4
-  for (int e = threadIdx.x; e < work; e += blockDim.x) {
-    const int i = e / (2 * nv), rem = e - i * 2 * nv;
-    const int r = (int)blockIdx.x + i * G;
-    const int src = r < k ? sel_list[r] : n_cand + (r - k);
-    const int dst = r < k ? __ldg(cand_tok + src) : N + (r - k);
-    if (rem < nv) sa.kb[(size_t)dst * nv + rem] = __ldg(sa.kf + (size_t)src * nv + rem);
-    else sa.vb[(size_t)dst * nv + rem - nv] = __ldg(sa.vf + (size_t)src * nv + rem - nv);
-  }
-}
-
 cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, int k_keep, int n_suffix, int N,
                       const int* force_sel, int* qrow, int* qtok, int* sel_tok, cudaStream_t s,
-                      const float* dev_part, int ld_part, int dev_mode, const void* kf, const void* vf, void* kb,
-                      void* vb, bool* scattered) {
-  if (scattered) *scattered = false;
+                      const float* dev_part, int ld_part, int dev_mode) {
   CB_REQUIRE(n_cand <= TOPK_MAX_CAND, CB_E_SHAPE, "top-k: n_cand %d exceeds %d", n_cand, TOPK_MAX_CAND);
   if (k_keep + n_suffix == 0 && (dev_part == nullptr || n_cand == 0)) return CB_OK;
   ProfScope ps_(c, PROF_TOPK, s);
@@ -473,27 +434,11 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   int nt = TOPK_THREADS;
   if (c->topk_threads > 0) nt = c->topk_threads;
   // keys (radix / drop paths) or the sort path's two buffers of nt packed 64-bit keys
-  const size_t base = (std::max((size_t)std::max(1, n_cand) * sizeof(unsigned), (size_t)nt * 2 * 8) + 15) / 16 * 16;
-  // fused scatter: every CTA repeats the selection and copies its share of the kept rows (one launch instead
-  // of top-k + scatter); the kept-slot list needs k_keep more ints of shared memory
-  const int Q = k_keep + n_suffix;
-  const size_t row_bytes = (size_t)c->m.n_kv_heads * c->m.head_dim * dtype_bytes(c->m.dtype);
-  const bool fuse = kb != nullptr && c->topk_scatter && Q > 0 && row_bytes % 16 == 0 &&
-                    base + (size_t)k_keep * 4 <= (size_t)TOPK_MAX_CAND * sizeof(unsigned);
-  ScatterArgs sa{};
-  int grid = 1;
-  size_t smem = base;
-  if (fuse) {
-    sa = ScatterArgs{(const uint4*)kf, (const uint4*)vf, (uint4*)kb, (uint4*)vb, (int)(row_bytes / 16)};
-    grid = std::max(1, std::min(c->topk_scatter_ctas, (Q + 7) / 8));
-    smem = base + (size_t)std::max(1, k_keep) * 4;
-    if (scattered) *scattered = true;
-  }
-  CB_LAUNCH(c, (topk_kernel), grid, nt, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok,
-                                            sel_tok, c->err_word, dev_part,
-                                            c->m.n_kv_heads * c->m.head_dim / 64 * std::max(1, c->tp_world), ld_part,
+  const size_t smem = std::max((size_t)std::max(1, n_cand) * sizeof(unsigned), (size_t)nt * 2 * 8);
+  CB_LAUNCH(c, (topk_kernel), 1, nt, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
+                                            c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64 * std::max(1, c->tp_world), ld_part,
                                             dev_mode, c->topk_drop_max, c->topk_sort ? 1 : 0,
-                                            c->dbg_sel == 200 ? c->dbg_buf : nullptr, sa, (int)base);
+                                            c->dbg_sel == 200 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
   return CB_OK;
 }

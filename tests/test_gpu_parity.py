@@ -269,11 +269,10 @@ def test_attention_parity(P, dtype, name):
     assert rel_err(np32(out), ref) < (1e-5 if dtype == "f32" else 1e-2)
 
 
-@pytest.mark.parametrize("dual", [1, 0])
 @pytest.mark.parametrize("impl", [2])
 @pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (1000, 1000, 2), (777, 50, 1), (130, 3, 8),
-                                          (4100, 900, 4), (129, 1, 2), (257, 2, 1)])
-def test_attention_tensor_core(P, T, n_sel, n_kv, impl, dual):
+                                          (4100, 900, 4)])
+def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     """Tensor-core flash attention (tcgen05/TMEM; bf16, hd 128, GQA packing, position-aware key skip,
     split-KV) against the oracle."""
     s = shape("small", n_kv_heads=n_kv)
@@ -284,7 +283,6 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl, dual):
     qbuf = np.zeros_like(q[:n_sel])
     qbuf[qrow] = q[rows]
     ctx = P.Context(s, "bf16", max_tokens=T)
-    ctx.set_option("attn_dual", dual)
     out = P.api.op_attention(ctx, to_dev(qbuf, torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
                              to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T, impl=impl)
     pos = np.arange(T)
@@ -305,7 +303,6 @@ def test_attention_tc5_variants(P, T, n_sel, n_kv, opt):
     rows = np.sort(np.random.default_rng(T + 1).choice(T, n_sel, replace=False)).astype(np.int32)
     qrow = np.arange(n_sel, dtype=np.int32)
     ctx = P.Context(s, "bf16", max_tokens=T)
-    ctx.set_option("attn_dual", 0)  # the single-stream kernel's options
     args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
             to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
     base = P.api.op_attention(ctx, *args, impl=2)
@@ -328,7 +325,6 @@ def test_attention_tc5_softmax_groups_split(P, splits, wg4):
     q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
     rows = np.sort(np.random.default_rng(5).choice(T, n_sel, replace=False)).astype(np.int32)
     ctx = P.Context(s, "bf16", max_tokens=T)
-    ctx.set_option("attn_dual", 0)  # the single-stream kernel's options
     ctx.set_option("attn_wg4", wg4)
     ctx.set_option("attn_splits", splits)
     args = (to_dev(q[rows], torch.bfloat16), to_dev(np.arange(n_sel, dtype=np.int32), torch.int32),
@@ -340,10 +336,9 @@ def test_attention_tc5_softmax_groups_split(P, splits, wg4):
         assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
 
 
-@pytest.mark.parametrize("dual", [1, 0])
 @pytest.mark.parametrize("impl", [2])
 @pytest.mark.parametrize("splits", [1, 2, 5, 16])
-def test_attention_tc5_split_merge(P, splits, impl, dual):
+def test_attention_tc5_split_merge(P, splits, impl):
     """tcgen05 attention with the key range of every row tile cut into `splits` pieces and merged
     in-kernel by the last-arriving CTA (split order, deterministic): oracle parity and bitwise
     reproducibility across launches (the arrival counters reset themselves)."""
@@ -355,7 +350,6 @@ def test_attention_tc5_split_merge(P, splits, impl, dual):
     qrow = np.arange(n_sel, dtype=np.int32)
     ctx = P.Context(s, "bf16", max_tokens=T)
     ctx.set_option("attn_splits", splits)
-    ctx.set_option("attn_dual", dual)
     args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
             to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
     out = P.api.op_attention(ctx, *args, impl=impl)
@@ -363,34 +357,6 @@ def test_attention_tc5_split_merge(P, splits, impl, dual):
     assert rel_err(np32(out), ref) < 1e-2
     for _ in range(2):
         assert torch.equal(P.api.op_attention(ctx, *args, impl=impl), out)
-
-
-@pytest.mark.parametrize("poly", [0, 1, 2])
-@pytest.mark.parametrize("T,n_sel,n_kv,splits", [(300, 7, 2, 0), (3072, 460, 2, 0), (3072, 553, 8, 2), (4100, 900, 4, 3),
-                                                 (777, 50, 1, 0), (2048, 2048, 2, 0)])
-def test_attention_dual_stream(P, T, n_sel, n_kv, splits, poly):
-    """Two key streams per CTA (attn_dual_kernel: alternate key tiles per softmax warpgroup, own S/P, O and
-    (m, l), merged on-chip), with and without split-KV and the FMA-pipe exponentials: oracle tolerance, close
-    to the single-stream kernel, bitwise reproducible across launches."""
-    s = shape("small", n_kv_heads=n_kv)
-    g = lambda st, n, H: rng.values(16, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
-    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
-    rows = np.sort(np.random.default_rng(T + 11).choice(T, n_sel, replace=False)).astype(np.int32)
-    ctx = P.Context(s, "bf16", max_tokens=T)
-    args = (to_dev(q[rows], torch.bfloat16), to_dev(np.arange(n_sel, dtype=np.int32), torch.int32),
-            to_dev(rows, torch.int32), to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
-    ctx.set_option("attn_splits", splits)
-    ctx.set_option("attn_dual", 0)
-    base = P.api.op_attention(ctx, *args, impl=2)
-    ctx.set_option("attn_dual", 1)
-    ctx.set_option("attn_poly", poly)
-    out = P.api.op_attention(ctx, *args, impl=2)
-    pos = np.arange(T)
-    ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
-    assert rel_err(np32(out), ref) < 1e-2
-    assert rel_err(np32(out), np32(base)) < 4e-3
-    for _ in range(2):
-        assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
 
 
 @pytest.mark.parametrize("order", ["sorted", "shuffled"])
@@ -409,7 +375,6 @@ def test_attention_tc5_pairing(P, T, n_sel, n_kv, order):
         rows = rows[np.random.default_rng(3).permutation(n_sel)]
     qrow = np.arange(n_sel, dtype=np.int32)
     ctx = P.Context(s, "bf16", max_tokens=T)
-    ctx.set_option("attn_dual", 0)  # the single-stream kernel's options
     args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
             to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
     ctx.set_option("attn_pair", 0)
@@ -885,25 +850,3 @@ def test_topk_sort_path_bitwise(P, threads):
         np.testing.assert_array_equal(res[0][1].cpu().numpy(), want, err_msg=f"radix/drop path n={n} k={k}")
         np.testing.assert_array_equal(res[1][1].cpu().numpy(), want, err_msg=f"sort path n={n} k={k}")
         assert torch.equal(res[0][0], res[1][0]), (n, k)
-
-
-@pytest.mark.parametrize("threads", [0, 256])
-def test_topk_fused_scatter_bitwise(P, threads):
-    """The KV scatter fused into the top-k launch (every CTA repeats the selection and copies its share of the
-    kept rows; several grid sizes, rows per CTA uneven) gives exactly the selections, K, V and h of the top-k +
-    separate scatter kernel on a whole small blend, including the replay mode (force_sel)."""
-    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 19, [300, 211, 157], 4, "bf16", 0.15)
-    for force in (False, True):
-        outs = []
-        for scat, ctas in [(0, 64), (1, 64), (1, 1), (1, 3), (1, 7)]:
-            ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
-            ctx.set_option("topk_threads", threads)
-            ctx.set_option("topk_scatter", scat)
-            ctx.set_option("topk_scatter_ctas", ctas)
-            fs = outs[0]["sel"] if force and outs else None
-            outs.append(run_blend(P, s, "bf16", 19, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx, force_sel=fs))
-        for o in outs[1:]:
-            for a, b in zip(outs[0]["sel"], o["sel"]):
-                np.testing.assert_array_equal(a, b)
-            for key in ("K", "V", "h"):
-                np.testing.assert_array_equal(outs[0][key], o[key])

@@ -18,9 +18,6 @@ def main():
     ap.add_argument("--impls", default="2")
     ap.add_argument("--pairs", default="0,1")
     ap.add_argument("--pdl", type=int, default=1)
-    ap.add_argument("--duals", default="0,1")
-    ap.add_argument("--polys", default="0")
-    ap.add_argument("--rows", default="3072,553,460,369")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -32,17 +29,14 @@ def main():
     ctx.set_option("pdl", a.pdl)
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
-    for n_sel in [int(x) for x in a.rows.split(",")]:
+    for n_sel in (3072, 553, 460, 369):
         rows = np.sort(np.random.default_rng(n_sel).choice(T, n_sel, replace=False)).astype(np.int32)
         q = torch.randn(n_sel, s.n_q_heads * s.head_dim, device="cuda").to(torch.bfloat16)
         qrow = torch.arange(n_sel, dtype=torch.int32, device="cuda")
         qtok = torch.from_numpy(rows).cuda()
         flops = 4.0 * s.n_q_heads * s.head_dim * float(np.sum(rows + 1))
-        for impl, splits, pair, dual, poly in [(int(i), int(x), int(pp), int(dd), int(py)) for i in a.impls.split(",")
-                                               for x in a.splits.split(",") for pp in a.pairs.split(",")
-                                               for dd in a.duals.split(",") for py in a.polys.split(",")]:
-            ctx.set_option("attn_dual", dual)
-            ctx.set_option("attn_poly", poly)
+        for impl, splits, pair in [(int(i), int(x), int(pp)) for i in a.impls.split(",") for x in a.splits.split(",")
+                                   for pp in a.pairs.split(",")]:
             ctx.set_option("attn_splits", splits)
             ctx.set_option("attn_pair", pair)
             fn = lambda: P.api.op_attention(ctx, q, qrow, qtok, k, v, T, impl=impl)
@@ -56,7 +50,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.iters * 1e3
-            print(f"rows={n_sel:5d} impl={impl} splits={splits} pair={pair} dual={dual} poly={poly}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s",
+            print(f"rows={n_sel:5d} impl={impl} splits={splits} pair={pair}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s",
                   flush=True)
 
 
