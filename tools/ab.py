@@ -1,6 +1,8 @@
 """Interleaved A/B timing of the Mistral 6x512 blend under two option sets (one CUDA graph each, replayed
 alternately so clock / power drift hits both equally).
-python tools/ab.py "gemm_no192=1" "gemm_no192=0" [rounds]"""
+python tools/ab.py "gemm_no192=1" "gemm_no192=0" [rounds] [--e2e]
+--e2e: the request path (cb_blend_request: pinned host chunk KV, layer-pipelined H2D, h_out D2H) instead of
+the device-resident forward."""
 import os
 import statistics
 import sys
@@ -16,8 +18,10 @@ def opts(spec):
 
 
 def main():
-    A, B = sys.argv[1], sys.argv[2]
-    rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+    e2e = "--e2e" in sys.argv
+    argv = [a for a in sys.argv if a != "--e2e"]
+    A, B = argv[1], argv[2]
+    rounds = int(argv[3]) if len(argv) > 3 else 40
     from paper_2405_16444_b200.build import build
     build()
     import paper_2405_16444_b200 as P
@@ -42,6 +46,12 @@ def main():
         h_out = torch.empty(ks[-1], s.d_model, dtype=torch.float32, device=dev)
         f = lambda kb=kb, vb=vb, h_out=h_out: P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, kb, vb, ks,
                                                                h_out=h_out)
+        if e2e:
+            kh, vh = k_in.cpu().pin_memory(), v_in.cpu().pin_memory()
+            toks, poss = tok.cpu().pin_memory(), pos.cpu().pin_memory()
+            hh = torch.empty(ks[-1], s.d_model, dtype=torch.float32).pin_memory()
+            f = lambda kb=kb, vb=vb, kh=kh, vh=vh, toks=toks, poss=poss, hh=hh: P.api.blend_request(
+                ctx, mw, toks, poss, list(cs), 0, kh, vh, kb, vb, ks, hh)
         f()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
