@@ -709,7 +709,7 @@ bool attention_tc5_ok(const cb_ctx* c) { return c->m.dtype == CB_BF16 && c->m.he
 // reach key tile ceil(max_kt (p + 1) / tiles) (selected tokens spread over the context; the suffix last).
 // Costs in key-tile units, measured on B200 (tools/attn_spans.py): CTA time ~ 8 + 1.0 x key tiles us; a split
 // range adds ~1.5 (partial write, merge by the last arrival; thread-major partials).
-static int attn_pick_splits(int tiles, int max_kt, int n_kv, int num_sms) {
+static int attn_pick_splits_uncached(int tiles, int max_kt, int n_kv, int num_sms) {
   constexpr double F = 8.0, M = 1.5;
   int best = 1;
   double best_t = 1e30;
@@ -734,6 +734,20 @@ static int attn_pick_splits(int tiles, int max_kt, int n_kv, int num_sms) {
     if (span < best_t - 0.5) { best_t = span; best = ns; }
   }
   return best;
+}
+
+// The list scheduling costs ~10^5 host operations (tens of us per eager launch): memoised per shape.
+static int attn_pick_splits(int tiles, int max_kt, int n_kv, int num_sms) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int> memo;
+  const uint64_t key = ((uint64_t)tiles << 40) ^ ((uint64_t)max_kt << 20) ^ ((uint64_t)n_kv << 10) ^ (uint64_t)num_sms;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  const int ns = attn_pick_splits_uncached(tiles, max_kt, n_kv, num_sms);
+  if (memo.size() > 65536) memo.clear();
+  memo.emplace(key, ns);
+  return ns;
 }
 
 cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const int* q_tok, int n_rows, const void* k,

@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--impls", default="2")
     ap.add_argument("--pairs", default="0,1")
     ap.add_argument("--pdl", type=int, default=1)
+    ap.add_argument("--rows", default="3072,553,460,369")
+    ap.add_argument("--opts", default="", help="extra option sets to compare, ';'-separated, e.g. 'attn_ipk=1;attn_poly=1'")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -29,16 +31,21 @@ def main():
     ctx.set_option("pdl", a.pdl)
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
-    for n_sel in (3072, 553, 460, 369):
+    base = {"attn_splits": 0, "attn_pair": 0}
+    variants = [""] + [v for v in a.opts.split(";") if v]
+    for n_sel in [int(x) for x in a.rows.split(",")]:
         rows = np.sort(np.random.default_rng(n_sel).choice(T, n_sel, replace=False)).astype(np.int32)
         q = torch.randn(n_sel, s.n_q_heads * s.head_dim, device="cuda").to(torch.bfloat16)
         qrow = torch.arange(n_sel, dtype=torch.int32, device="cuda")
         qtok = torch.from_numpy(rows).cuda()
         flops = 4.0 * s.n_q_heads * s.head_dim * float(np.sum(rows + 1))
-        for impl, splits, pair in [(int(i), int(x), int(pp)) for i in a.impls.split(",") for x in a.splits.split(",")
-                                   for pp in a.pairs.split(",")]:
-            ctx.set_option("attn_splits", splits)
-            ctx.set_option("attn_pair", pair)
+        for impl, splits, pair, var in [(int(i), int(x), int(pp), v) for i in a.impls.split(",")
+                                        for x in a.splits.split(",") for pp in a.pairs.split(",") for v in variants]:
+            opts = dict(base)
+            opts.update({"attn_splits": splits, "attn_pair": pair})
+            opts.update({kv.split("=")[0]: int(kv.split("=")[1]) for kv in var.split(",") if kv})
+            for name, val in opts.items():
+                ctx.set_option(name, val)
             fn = lambda: P.api.op_attention(ctx, q, qrow, qtok, k, v, T, impl=impl)
             for _ in range(3):
                 fn()
@@ -50,8 +57,11 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.iters * 1e3
-            print(f"rows={n_sel:5d} impl={impl} splits={splits} pair={pair}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s",
-                  flush=True)
+            print(f"rows={n_sel:5d} impl={impl} splits={splits} pair={pair} [{var}]: {us:8.1f} us  "
+                  f"{flops / us / 1e6:7.1f} TFLOP/s", flush=True)
+            for kv in var.split(","):  # back to the defaults for the next variant
+                if kv:
+                    ctx.set_option(kv.split("=")[0], 0)
 
 
 if __name__ == "__main__":
