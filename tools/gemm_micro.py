@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--only", default="", help="comma list of shape names")
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--mcs", default="0", help="gemm_mc values (A-multicast 4-CTA clusters)")
+    ap.add_argument("--rotate", type=int, default=1,
+                    help="cycle over this many copies of B (weights), so they stream from HBM as in the blend")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -44,7 +46,7 @@ def main():
         if only and name not in only:
             continue
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-        B = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        Bs = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(max(1, a.rotate))]
         C = torch.zeros(M, N, device="cuda", dtype=torch.float32 if a.resid else torch.bfloat16)
         for mode, bn, pr, ks, mc in [(int(m), int(b), int(p), int(k), int(x)) for m in a.modes.split(",")
                                      for b in a.bns.split(",") for p in a.pairs.split(",") for k in a.ksplits.split(",")
@@ -54,9 +56,13 @@ def main():
             ctx.set_option("gemm_bn", bn)
             ctx.set_option("gemm_pair", pr)
             ctx.set_option("gemm_ksplit", ks)
-            fn = lambda: P.api.check(P.api.lib().cb_op_gemm(ctx.handle, A.data_ptr(), B.data_ptr(), C.data_ptr(),
-                                                            M, N, K, 2 if a.resid else 0, 2,
-                                                            torch.cuda.current_stream().cuda_stream))
+            it = [0]
+
+            def fn():
+                B = Bs[it[0] % len(Bs)]
+                it[0] += 1
+                P.api.check(P.api.lib().cb_op_gemm(ctx.handle, A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K,
+                                                   2 if a.resid else 0, 2, torch.cuda.current_stream().cuda_stream))
             for _ in range(3):
                 fn()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
