@@ -39,9 +39,8 @@ CB_API cb_status cb_op_gemm(cb_ctx* ctx, const void* A, const void* B, void* C, 
  * index q_tok[r]) and q head h: out[r][h] = softmax_j(q.k_j / sqrt(hd)) v_j over keys j <= q_tok[r]
  * of k, v [n_keys][n_kv][hd], kv head h / (n_q / n_kv).  Token positions are strictly increasing, so
  * "key position <= query position" is "j <= q_tok[r]".  out: [n_rows][n_q * hd] (model dtype).
- * impl: 0 = auto (2 for bf16 / head_dim 128), 1 = SIMT, 2 = tcgen05/TMEM one CTA per row tile, 3 = mma.sync,
- * 4 = experimental persistent tcgen05 (LPT queue of (row tile, kv head, key chunk) items, two key streams
- * per item with P in TMEM, in-kernel chunk merge); 2-4 need bf16, head_dim 128. */
+ * impl: 0 = auto (2 for bf16 / head_dim 128), 1 = SIMT, 2 = tcgen05/TMEM one CTA per (row tile, kv head,
+ * key range) with split-KV merged in-kernel (needs bf16, head_dim 128). */
 CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_row, const int32_t* q_tok,
                           int32_t n_rows, const void* k, const void* v, int32_t n_keys, void* out, int32_t impl,
                           void* stream);
@@ -62,13 +61,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *                 tiles of a pair GEMM's last round into K pieces (merged in piece order by the last piece)
  *   "attn_impl"   0 = auto, 1 = SIMT, 2 = tcgen05/TMEM per tile
  *   "attn_splits" 0 = auto, 1..16 = force the split-KV factor
- *   "attn_pair"   0 = off (default; measured neutral), 1 = when the (row tile, kv head) grid is one wave, 2 =
- *                 always: row tile p paired with row tile T-1-p in a 2-CTA cluster, the heavier one's key range
- *                 cut between the two CTAs and merged through distributed shared memory
  *   "q_split"     1 = layer 1 projects Q for the kept rows only, after the top-k (default), 0 = Q for all
  *                 candidates in the fused QKV GEMM
- *   "topk_sort"   1 = bitonic block sort when the candidates fit the top-k block, 0 = radix / drop-smallest
- *                 (default: the sort measured slower inside the blend)
  *   "fuse_deviation" 1 = Delta_kv in the tcgen05 QKV epilogue (default), 0 = separate kernel
  *   "debug_trace" 1 = record pipeline events of one CTA of the tcgen05 attention and per-CTA events of
  *                 the CTA-pair GEMM (tuning; each launch overwrites); 100 + k = only pair GEMMs of epilogue
@@ -77,8 +71,6 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
  *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
  *   "topk_threads" 0 = 1024 (default), 256 or 512 threads in the top-k block
- *   "gemm_pf"     1 = pair GEMMs load the weight (B) halves of their first pipeline stages before the PDL
- *                 wait, the A halves after it (experiment, measured neutral), 0 = off (default)
  *   "gemm_mc"     A-multicast 4-CTA clusters (two CTA pairs sharing their A rows) in the pair GEMM:
  *                 2 = where the planner expects a shorter k-loop (default), 1 = always (whole tiles), 0 = off,
  *                 3 = 8-CTA clusters (2 row x 2 column tiles, B multicast as well; measured neutral, opt-in) */

@@ -5,17 +5,17 @@
 // One CTA = one kv head g x 128 (query token, q head of g) rows (GQA packing: every K/V tile serves
 // all G q heads of the group) x one split of the key range (split-KV for the later layers' few
 // hundred queries). Warp roles:
-//   warp 0     TMA: K and V tiles (128 keys x 128, two 64-column SWIZZLE_128B boxes each) into a
-//              2-stage ring (3-D tensor map over [keys][kv heads][hd])
-//   warp 1     MMA issuer: S_t = Q K_t^T (M=128, N=128 keys, K=16) into one of two TMEM S buffers,
-//              then O += P_t V_t (A = P from shared memory, B = V MN-major) into the TMEM O buffer.
+//   warp 0     TMA: K and V tiles (128 keys x 128, two 64-column SWIZZLE_128B boxes each) into a 3-stage K
+//              ring and a 2-stage V ring (3-D tensor map over [keys][kv heads][hd]), K running ahead of V
+//   warp 1     MMA issuer: S_t = Q K_t^T (M=128, N=128 keys, K=16; A = Q from TMEM) into one of two TMEM S
+//              buffers, then O += P_t V_t (A = P from TMEM, B = V MN-major) into the TMEM O buffer.
 //              S_{t+1} is issued before waiting for P_t, so QK^T overlaps the softmax of tile t.
 //   warps 2-9  softmax: two warpgroups, thread = (query row, 64-key half). Each tcgen05.lds its half of
 //              the S row, masks by original position, and the two halves agree on the row max through
 //              shared memory; online softmax in the log2 domain with lazy rescaling (O is rescaled in
-//              TMEM only when the row max grows by more than 2^8); P (bf16) goes to shared memory in
-//              the K-major SWIZZLE_128B layout the MMA reads (one column block per half); finally
-//              O / l (or the split partial), each half writing its 64 output columns.
+//              TMEM only when the row max grows by more than 2^8); P (bf16 pairs) is written over the
+//              half's own S columns, where the PV MMA reads it; finally O / l (or the split partial),
+//              each half writing its 64 output columns.
 // Key tiles past the CTA's last query token are never loaded; only tiles reaching past its first
 // query token are masked.
 // Load balance: the rows are in token order, so the last row tiles see the most keys. Every row tile
@@ -23,6 +23,9 @@
 // heaviest first. When a row tile has more than one non-empty range, each CTA writes an fp32 partial
 // (O, m, l) and bumps the tile's counter; the last one to arrive merges all partials in split order
 // (deterministic) and writes the output -- no separate merge launch.
+// Variants measured and removed (source in git history): a share of the exponentials on
+// the FMA pipe, four softmax warpgroups, Q staged in shared memory, light/heavy row-tile pairing in
+// 2-CTA clusters with a DSMEM merge, two key streams per CTA, P packed on the integer pipe.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -35,15 +38,15 @@
 
 namespace {
 constexpr int HD = 128, BM = 128, BC = 128;
-// NWG softmax warpgroups: thread = (query row, KW = 128 / NWG keys of the tile, the same KW O columns)
-template <int NWG> constexpr int nt_of() { return 64 + 128 * NWG; }
-template <int NWG> constexpr int smem_of() { return 6 * (2 * 128 * 128) + 1024 + 256 + (3 * NWG + 1) * 128 * 4 + 64; }
+constexpr int KW = 64, OW = 64, NSM = 256;  // per softmax thread: 64 keys of a tile, 64 output columns; 256 threads
+constexpr int NTHREADS = 64 + NSM;
 constexpr int ATOM = 128 * 128;    // 128 rows x 128 B (64 bf16): one SWIZZLE_128B column block
 constexpr int TILE = 2 * ATOM;     // 128 rows x 128 bf16
-constexpr int KST = 3;            // K ring stages (V: 2); P lives in TMEM, so SMEM = Q + 3 K + 2 V
-constexpr int SMEM = smem_of<4>();  // + alignment + barriers + exchange (xmax [2][NWG][128], l [NWG][128], flag)
+constexpr int KST = 3;             // K ring stages (V: 2); Q and P live in TMEM, so SMEM = 3 K + 2 V
+// + alignment + barriers + exchange (xmax [2 parity][2][128], l [2][128], flag)
+constexpr int SMEM = 5 * TILE + 1024 + 256 + 7 * 128 * 4 + 64;
 constexpr float RESCALE_THRESHOLD = 8.0f;    // log2 units
-constexpr uint32_t QCOL = 384;               // TMEM columns of Q (QTM): 64 x 32-bit = 128 bf16 per row
+constexpr uint32_t QCOL = 384;               // TMEM columns of Q: 64 x 32-bit = 128 bf16 per row
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -53,44 +56,11 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ~2 ulp; ex2(-inf) 
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA / integer pipes instead of MUFU (the softmax is MUFU-bound: 16 ex2/clk/SM): round
-// x to an integer j with the 1.5 * 2^23 trick, 2^(x - j) on [-0.5, 0.5] by a degree-3 minimax polynomial
-// (relative error 7.5e-5, below the bf16 rounding of P), 2^j added into the exponent bits. x is clamped
-// at -126, so masked scores give ~1e-38 instead of 0 (negligible against any visible key's weight).
-__device__ __forceinline__ float ex2_poly(float x) {
-  const float t = fmaxf(x, -126.f);
-  const float r = t + 12582912.f;
-  const float f = t - (r - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05517132f, f, 0.24261054f), f, 0.69326099f), f, 0.99992811f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
-}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-// N consecutive 32-bit TMEM columns of this thread's lane (N = 16 or 32; no wait)
-template <int N>
-__device__ __forceinline__ void tmem_st_words(uint32_t taddr, const uint32_t (&w)[N]) {
-  if constexpr (N == 32) {
-    tc::tmem_st32u(taddr, w);
-  } else {
-    static_assert(N == 16, "16 or 32 columns");
-    float f[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(w[i]);
-    tc::tmem_st16(taddr, f);
-  }
-}
-// byte offset of 16-B chunk `ch` (0..15) of row `r` in a [2 atoms][128 rows][128 B] swizzled tile
-__device__ __forceinline__ uint32_t sw_off(int r, int ch) {
-  return (uint32_t)((ch >> 3) * ATOM + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
-}
 
-// One work segment of a CTA: GQA-packed row tile, key-tile range [jb, je), number of segments covering the
-// tile (n_active > 1: write an fp32 partial into slot sidx and merge), the tile's first query token (kmin).
-struct Seg {
-  int tile, jb, je, n_active, sidx, kmin, xch;  // xch: merge with the cluster peer's part through DSMEM
-};
 // Key tiles a row tile needs (through its last query token) and its first query token.
 __device__ __forceinline__ void tile_span(const int* __restrict__ q_tok, int tile, int R, int G, int n_keys, int& n_kt,
                                           int& kmin) {
@@ -109,7 +79,6 @@ __device__ __forceinline__ void tile_span(const int* __restrict__ q_tok, int til
 // the row's reference max (log2 domain), l its exp sum. A row tile covered by one CTA writes O / l. Covered by
 // several (split-KV), each CTA writes an fp32 partial (thread-major slots: coalesced stores and loads), counts
 // its arrival, and the last arrival merges every split's partial in split order (deterministic) and writes.
-template <int NSM, int OW>
 __device__ __forceinline__ void finish_rows(float (&o)[OW], float m_used, float l, bool partial, bool write_out,
                                             int n_active, int sidx, int tile, int g, int n_kv, int R, int rho,
                                             bool valid, int rt, int hh, int qd, int et, int wg, int* flag,
@@ -176,26 +145,17 @@ __device__ __forceinline__ void finish_rows(float (&o)[OW], float m_used, float 
   }
 }
 
-// POLY: share of the softmax exponentials computed by ex2_poly (0: none, 1: 1 in 4, 2: 1 in 2).
-// QTM: Q lives in TMEM (columns 384..447, written by the softmax threads with tcgen05.st) and S = Q K^T
-// reads it as the A operand from tensor memory, so the QK^T MMAs read only K from shared memory.
-// PK: packed fp32x2 FFMA2 / FADD2 for the exponent argument and the row sum (bitwise the same results).
-// NWG: softmax warpgroups (2: 64 keys per thread; 4: 32 keys per thread, twice the warps per SMSP to
-// hide the softmax's dependency latencies).
-template <int POLY, bool QTM, bool PK, int NWG>
-__global__ void __launch_bounds__(nt_of<NWG>(), 1)
+__global__ void __launch_bounds__(NTHREADS, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                     const bf16* __restrict__ q, const int* __restrict__ q_row, const int* __restrict__ q_tok,
                     int n_rows, int n_keys, bf16* __restrict__ out, int n_q, int n_kv, float scale_log2,
                     int kt_per_split, int n_splits, float* __restrict__ opart, float2* __restrict__ ml,
-                    int* __restrict__ tile_cnt, long long* __restrict__ dbg, int pair_mode) {
+                    int* __restrict__ tile_cnt, long long* __restrict__ dbg) {
   pdl_enter();
 #ifdef CB_ATTN_TRACE
   const long long t_start = tc::globaltimer();
-#endif
-#ifdef CB_ATTN_TRACE  // tools/attn_trace.py: clock64 pipeline events of CTA 0 (build with -DCB_ATTN_TRACE)
 #ifndef CB_ATTN_TRACE_CTA
-#define CB_ATTN_TRACE_CTA 0  // which CTA's pipeline to trace (-DCB_ATTN_TRACE_CTA=n)
+#define CB_ATTN_TRACE_CTA 0  // which CTA's pipeline to trace (-DCB_ATTN_TRACE_CTA=n; tools/attn_trace.py)
 #endif
   const bool dbg_on = dbg != nullptr && blockIdx.x == CB_ATTN_TRACE_CTA;
 #define DBG(i) do { if (dbg_on && (i) < 2048) dbg[i] = clock64(); } while (0)
@@ -204,10 +164,9 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
 #endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + TILE;          // [KST] stages
-  uint8_t* sV = smem + (1 + KST) * TILE;  // [2] stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * TILE);
+  uint8_t* sK = smem;                 // [KST] stages
+  uint8_t* sV = smem + KST * TILE;    // [2] stages
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (KST + 2) * TILE);
   uint64_t* k_full = bars;            // [3]  K tile landed
   uint64_t* k_empty = bars + 3;       // [3]  S MMAs done reading the K stage
   uint64_t* v_full = bars + 6;        // [2]  V tile landed
@@ -217,66 +176,25 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
   uint64_t* p_full = bars + 13;       // P_t written over S_t (8 softmax warps)
   uint64_t* pv_done = bars + 14;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
-  // after xmax [2][NWG][128], l [NWG][128] and the merge flag (bars + 16 ..): the DSMEM exchange barriers
-  uint64_t* xch_full = bars + 16 + (3 * NWG * 128 + 8) / 2;
-  uint64_t* xch_done = xch_full + 1;
+  float* xmax = reinterpret_cast<float*>(bars + 16);  // [2 parity][2 halves][128 rows], then l [2][128], flag
+  float* xl = xmax + 2 * 2 * 128;
+  int* flag = reinterpret_cast<int*>(xl + 2 * 128);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = n_q / n_kv, R = n_rows * G;
   const int qd = n_q * HD;
-  // A CTA runs one or two segments (row tile, key-tile range [jb, je)); a row tile covered by several
-  // segments (n_active) writes fp32 partials and the last one to finish merges them.
-  Seg seg[2];
-  int nseg = 0, g, role = 0;
-  if (!pair_mode) {
-    // 1-D grid, kv head fastest: the heaviest row tiles (latest tokens) of EVERY head launch first, then
-    // their later key ranges, then lighter tiles (a global longest-first order across heads)
-    g = (int)blockIdx.x % n_kv;
-    const int tiles = gridDim.x / (n_splits * n_kv);
-    const int rest = (int)blockIdx.x / n_kv;
-    const int tile = tiles - 1 - rest / n_splits;
-    const int split = rest % n_splits;
-    int n_kt, kmin;
-    tile_span(q_tok, tile, R, G, n_keys, n_kt, kmin);
-    const int jb = split * kt_per_split, je = min(n_kt, jb + kt_per_split);
-    if (jb < je) seg[nseg++] = Seg{tile, jb, je, (n_kt + kt_per_split - 1) / kt_per_split, split, kmin, 0};
-  } else {
-    // causal balance (one wave, 2-CTA clusters): row tile p (light) is paired with row tile T-1-p (heavy);
-    // cluster rank 0 runs the light tile and the first `cut` key tiles of the heavy one, rank 1 the rest,
-    // so both do (span_lo + span_hi) / 2 key tiles; the two parts of the heavy tile are merged through
-    // distributed shared memory. An odd tile count leaves the middle tile to a cluster of its own.
-    role = (int)blockIdx.x & 1;
-    const int hg = (int)blockIdx.x >> 1;
-    g = hg % n_kv;
-    const int pp = hg / n_kv, T = (R + BM - 1) / BM, np = T / 2;
-    if (pp >= np) {
-      if (role == 0) {
-        int n_kt, kmin;
-        tile_span(q_tok, np, R, G, n_keys, n_kt, kmin);
-        seg[nseg++] = Seg{np, 0, n_kt, 1, 0, kmin, 0};
-      }
-    } else {
-      int lo = pp, hi = T - 1 - pp, s_lo, k_lo, s_hi, k_hi;
-      tile_span(q_tok, lo, R, G, n_keys, s_lo, k_lo);
-      tile_span(q_tok, hi, R, G, n_keys, s_hi, k_hi);
-      if (s_lo > s_hi) {  // unsorted queries: the heavier tile is the one that gets split
-        int x = lo; lo = hi; hi = x;
-        x = s_lo; s_lo = s_hi; s_hi = x;
-        x = k_lo; k_lo = k_hi; k_hi = x;
-      }
-      const int cut = (s_hi - s_lo) / 2;
-      if (role == 0) {
-        seg[nseg++] = Seg{lo, 0, s_lo, 1, 0, k_lo, 0};
-        if (cut > 0) seg[nseg++] = Seg{hi, 0, cut, 1, 0, k_hi, 1};
-      } else {
-        seg[nseg++] = Seg{hi, cut, s_hi, 1, 0, k_hi, cut > 0 ? 1 : 0};
-      }
-    }
-  }
-  if (nseg == 0) {  // nothing for this range (the tile's other CTAs do not count it)
-    if (pair_mode) tc::cluster_sync();  // the partner's prologue sync
-    return;
-  }
+  // 1-D grid, kv head fastest: the heaviest row tiles (latest tokens) of EVERY head launch first, then their
+  // later key ranges, then lighter tiles (a global longest-first order across heads)
+  const int g = (int)blockIdx.x % n_kv;
+  const int tiles = gridDim.x / (n_splits * n_kv);
+  const int rest = (int)blockIdx.x / n_kv;
+  const int tile = tiles - 1 - rest / n_splits;
+  const int split = rest % n_splits;
+  int n_kt, kmin;
+  tile_span(q_tok, tile, R, G, n_keys, n_kt, kmin);
+  const int jb = split * kt_per_split, je = min(n_kt, jb + kt_per_split);
+  if (jb >= je) return;  // nothing in this range (the tile's other CTAs do not count it)
+  const int nt = je - jb, n_active = (n_kt + kt_per_split - 1) / kt_per_split;
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmK);
@@ -290,48 +208,38 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
       tc::mbar_init(&v_empty[b], 1);
       tc::mbar_init(&s_full[b], 1);
     }
-    tc::mbar_init(q_full, 128 * NWG);
-    tc::mbar_init(p_full, 4 * NWG);
+    tc::mbar_init(q_full, NSM);
+    tc::mbar_init(p_full, NSM / 32);
     tc::mbar_init(pv_done, 1);
-    tc::mbar_init(xch_full, 128 * NWG);  // the cluster peer's softmax threads: "my partial is in my smem"
-    tc::mbar_init(xch_done, 128 * NWG);  // the cluster peer's softmax threads: "done reading yours"
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   tc::fence_before();
   __syncthreads();
-  if (pair_mode) tc::cluster_sync();  // both CTAs' barriers initialised before any remote arrive
   tc::fence_after();
   DBG(1200);
-  const uint32_t tmem = *tmem_slot;  // S0: cols [0,128), S1: [128,256), O: [256,384)
+  const uint32_t tmem = *tmem_slot;  // S0: cols [0,128), S1: [128,256), O: [256,384), Q: [384,448)
 
   if (warp == 0) {
-    // ===== TMA producer: K_t as soon as S_{t-2} released its stage, V_t once PV_{t-2} did, so K runs
-    // about one tile ahead of V (S_t needs K_t long before PV_t needs V_t) =====
+    // ===== TMA producer: K_t as soon as S_{t-3} released its stage, V_t once PV_{t-2} did, so K runs
+    // ahead of V (S_t needs K_t a whole softmax before PV_t needs V_t) =====
     if (tc::elect_one()) {
       auto load = [&](uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int key0) {
         tc::mbar_arrive_expect_tx(bar, TILE);
         tc::tma_load_3d(dst, m, bar, 0, g, key0);
         tc::tma_load_3d(dst + ATOM, m, bar, 64, g, key0);
       };
-      // K and V streams advance independently (K runs up to KST tiles ahead: S_t needs K_t a full
-      // softmax earlier than PV_t needs V_t), polling their empty barriers; TK / TV count tiles across
-      // the CTA's segments (ring stages and phases continue)
-      int TK = 0, TV = 0;
-      for (int si = 0; si < nseg; ++si) {
-        const int jb = seg[si].jb, nt = seg[si].je - seg[si].jb;
-        int tk = 0, tv = 0;
-        while (tk < nt || tv < nt) {
-          if (tk < nt && (TK < KST || tc::mbar_test(&k_empty[TK % KST], (TK / KST - 1) & 1))) {
-            DBG(4 * TK);
-            load(sK + (TK % KST) * TILE, &tmK, &k_full[TK % KST], (jb + tk) * BC);
-            ++tk; ++TK;
-          }
-          if (tv < tk && (TV < 2 || tc::mbar_test(&v_empty[TV & 1], ((TV >> 1) - 1) & 1))) {
-            DBG(4 * TV + 1);
-            load(sV + (TV & 1) * TILE, &tmV, &v_full[TV & 1], (jb + tv) * BC);
-            ++tv; ++TV;
-          }
+      int tk = 0, tv = 0;  // the K and V streams advance independently, polling their empty barriers
+      while (tk < nt || tv < nt) {
+        if (tk < nt && (tk < KST || tc::mbar_test(&k_empty[tk % KST], (tk / KST - 1) & 1))) {
+          DBG(4 * tk);
+          load(sK + (tk % KST) * TILE, &tmK, &k_full[tk % KST], (jb + tk) * BC);
+          ++tk;
+        }
+        if (tv < tk && (tv < 2 || tc::mbar_test(&v_empty[tv & 1], ((tv >> 1) - 1) & 1))) {
+          DBG(4 * tv + 1);
+          load(sV + (tv & 1) * TILE, &tmV, &v_full[tv & 1], (jb + tv) * BC);
+          ++tv;
         }
       }
     }
@@ -342,7 +250,7 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
     const uint32_t tO = tmem + 256;
     // S_{t+2} reuses TMEM buffer t % 2, which holds P_t: it is issued after PV_t on the in-order
     // tensor pipe, so no extra barrier is needed
-    auto issue_s = [&](int t, uint32_t qcol) {
+    auto issue_s = [&](int t) {
       const int b = t & 1, kb = t % KST;
       tc::mbar_wait(&k_full[kb], (t / KST) & 1);
       if (lane == 0) DBG(400 + 4 * t);
@@ -351,115 +259,68 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint64_t bd = tc::sdesc_sw128(sK + kb * TILE + (kk >> 2) * ATOM) + 2 * (kk & 3);
-          if constexpr (QTM) {
-            tc::mma_bf16_ts(tmem + b * 128, tmem + qcol + 8 * kk, bd, IDESC_S, kk > 0 ? 1u : 0u);
-          } else {
-            const uint64_t a = tc::sdesc_sw128(sQ + (kk >> 2) * ATOM) + 2 * (kk & 3);
-            tc::mma_bf16(tmem + b * 128, a, bd, IDESC_S, kk > 0 ? 1u : 0u);
-          }
+          tc::mma_bf16_ts(tmem + b * 128, tmem + QCOL + 8 * kk, bd, IDESC_S, kk > 0 ? 1u : 0u);
         }
         tc::mma_commit(&s_full[b]);
         tc::mma_commit(&k_empty[kb]);
       }
       __syncwarp();
     };
-    int T0 = 0;  // tiles of the earlier segments (barrier phases continue across segments)
-    for (int si = 0; si < nseg; ++si) {
-      const int nt = seg[si].je - seg[si].jb;
-      // Q of this segment is in place: in TMEM both segments' Q are written up front (QCOL, QCOL + 64), so
-      // only the first segment waits; staged in shared memory, each segment refills sQ after the last one
-      if (!QTM || si == 0) tc::mbar_wait(q_full, QTM ? 0 : (si & 1));
-      const uint32_t qcol = QCOL + (QTM ? 64u * si : 0u);
-      issue_s(T0, qcol);
-      for (int t = 0; t < nt; ++t) {
-        const int Tg = T0 + t;
-        if (t + 1 < nt) issue_s(Tg + 1, qcol);
-        tc::mbar_wait(p_full, Tg & 1);
-        tc::mbar_wait(&v_full[Tg & 1], (Tg >> 1) & 1);
-        if (lane == 0) DBG(400 + 4 * Tg + 1);
-        tc::fence_after();
-        if (tc::elect_one()) {
-          const int b = Tg & 1;
+    tc::mbar_wait(q_full, 0);
+    issue_s(0);
+    for (int t = 0; t < nt; ++t) {
+      if (t + 1 < nt) issue_s(t + 1);
+      tc::mbar_wait(p_full, t & 1);
+      tc::mbar_wait(&v_full[t & 1], (t >> 1) & 1);
+      if (lane == 0) DBG(400 + 4 * t + 1);
+      tc::fence_after();
+      if (tc::elect_one()) {
+        const int b = t & 1;
 #pragma unroll
-          for (int kk = 0; kk < BC / 16; ++kk) {  // 16 keys per step; P in TMEM (keys 0-63 at columns
-            // 0-31 of the S buffer, keys 64-127 at columns 64-95: each softmax half over its own S)
-            constexpr int KWc = BC / NWG;  // keys per softmax group: P of group q at columns q * KWc ..
-            const uint32_t a = tmem + b * 128 + (kk * 16 / KWc) * KWc + ((kk * 16) % KWc) / 2;
-            const uint64_t bd = tc::sdesc_sw128_mn(sV + b * TILE + kk * 2048, ATOM);
-            tc::mma_bf16_ts(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
-          }
-          tc::mma_commit(pv_done);
-          tc::mma_commit(&v_empty[b]);
+        for (int kk = 0; kk < BC / 16; ++kk) {  // 16 keys per step; P in TMEM (keys 0-63 at columns 0-31 of
+          // the S buffer, keys 64-127 at columns 64-95: each softmax half over its own S)
+          const uint32_t a = tmem + b * 128 + (kk * 16 / KW) * KW + ((kk * 16) % KW) / 2;
+          const uint64_t bd = tc::sdesc_sw128_mn(sV + b * TILE + kk * 2048, ATOM);
+          tc::mma_bf16_ts(tO, a, bd, IDESC_PV, (t > 0 || kk > 0) ? 1u : 0u);
         }
-        __syncwarp();
+        tc::mma_commit(pv_done);
+        tc::mma_commit(&v_empty[b]);
       }
-      T0 += nt;
+      __syncwarp();
     }
     // drain: the release commits of the last K / V stages have no consumer; wait for their arrivals so no
     // tcgen05.commit arrive is in flight when the CTA exits (compute-sanitizer synccheck: "missing wait")
-    for (int t = max(0, T0 - KST); t < T0; ++t) tc::mbar_wait(&k_empty[t % KST], (t / KST) & 1);
-    for (int t = max(0, T0 - 2); t < T0; ++t) tc::mbar_wait(&v_empty[t & 1], (t >> 1) & 1);
+    for (int t = max(0, nt - KST); t < nt; ++t) tc::mbar_wait(&k_empty[t % KST], (t / KST) & 1);
+    for (int t = max(0, nt - 2); t < nt; ++t) tc::mbar_wait(&v_empty[t & 1], (t >> 1) & 1);
   } else {
     // ===== softmax / correction / epilogue: two warpgroups, each owns one 64-key half of every row
     // (thread = (row, half)); the halves agree on the row max through shared memory every tile =====
-    const int wg = (warp - 2) >> 2;              // 0: keys / O columns 0..63, 1: 64..127
+    const int wg = (warp - 2) >> 2;  // 0: keys / O columns 0..63, 1: 64..127
     const int r = (warp & 3) * 32 + lane;
-    constexpr int KW = BC / NWG, OW = HD / NWG, NSM = 128 * NWG;
-    const int et = threadIdx.x - 64;             // 0..NSM-1 among softmax threads
+    const int et = threadIdx.x - 64;  // 0..NSM-1 among softmax threads
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    float* xmax = reinterpret_cast<float*>(bars + 16);  // [2 parity][NWG][128 rows], then l [NWG][128]
-    float* xl = xmax + 2 * NWG * 128;
-    int T0 = 0;  // tiles of the earlier segments (barrier phases continue across segments)
-    for (int si = 0; si < nseg; ++si) {
-    const int tile = seg[si].tile, jb = seg[si].jb, nt = seg[si].je - seg[si].jb, kmin = seg[si].kmin;
-    const int n_active = seg[si].n_active;
-    const bool partial = n_active > 1;
     const int rho = tile * BM + r;
     const bool valid = rho < R;
     const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
     const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
-    if constexpr (QTM) {  // this row's KW elements of Q -> TMEM columns QCOL + 64 s + wg * KW / 2 .. (s = segment)
-      if (si == 0) {
-        for (int s2 = 0; s2 < nseg; ++s2) {
-          const int rho2 = seg[s2].tile * BM + r;
-          const bool valid2 = rho2 < R;
-          const int rt2 = valid2 ? rho2 / G : 0, hh2 = g * G + (valid2 ? rho2 % G : 0);
-          const uint4* src =
-              reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt2) * qd + (size_t)hh2 * HD + wg * KW);
-          uint32_t pk[KW / 2];
-#pragma unroll
-          for (int c8 = 0; c8 < KW / 8; ++c8) {
-            const uint4 u = valid2 ? __ldg(src + c8) : make_uint4(0u, 0u, 0u, 0u);
-            pk[4 * c8] = u.x; pk[4 * c8 + 1] = u.y; pk[4 * c8 + 2] = u.z; pk[4 * c8 + 3] = u.w;
-          }
-          tmem_st_words<KW / 2>(tmem + lane_base + QCOL + 64 * s2 + wg * (KW / 2), pk);
-        }
-        tc::tmem_st_wait();
-        tc::fence_before();
-        tc::mbar_arrive(q_full);
-      }
-    } else {  // stage this row's half of Q (one SWIZZLE_128B column block)
-      const bf16* src = q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD;
-      const uint32_t dq = tc::smem_u32(sQ);
+    {  // this row's 64 elements of Q (half wg) -> TMEM columns QCOL + 32 wg .. (bf16 pairs), the QK^T A operand
+      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD + wg * KW);
+      uint32_t pk[KW / 2];
 #pragma unroll
       for (int c8 = 0; c8 < KW / 8; ++c8) {
-        const int ch = wg * (KW / 8) + c8;
-        const int sz = valid ? 16 : 0;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dq + sw_off(r, ch)), "l"(src + ch * 8),
-                     "r"(sz)
-                     : "memory");
+        const uint4 u = valid ? __ldg(src + c8) : make_uint4(0u, 0u, 0u, 0u);
+        pk[4 * c8] = u.x; pk[4 * c8 + 1] = u.y; pk[4 * c8 + 2] = u.z; pk[4 * c8 + 3] = u.w;
       }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      tc::fence_proxy_async();
+      tc::tmem_st32u(tmem + lane_base + QCOL + wg * (KW / 2), pk);
+      tc::tmem_st_wait();
+      tc::fence_before();
       tc::mbar_arrive(q_full);
-      if (et == 0) DBG(1201);
     }
     float m_used = -INFINITY, l = 0.f;
     for (int t = 0; t < nt; ++t) {
-      const int Tg = T0 + t;
-      const int b = Tg & 1;
-      tc::mbar_wait(&s_full[b], (Tg >> 1) & 1);
-      if (et == 0) DBG(800 + 4 * Tg);
+      const int b = t & 1;
+      tc::mbar_wait(&s_full[b], (t >> 1) & 1);
+      if (et == 0) DBG(800 + 4 * t);
       tc::fence_after();
       float s[KW];
 #pragma unroll
@@ -487,13 +348,11 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
       }
       const float hmx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      tc::sts_f32(xmax + (b * NWG + wg) * 128 + r, hmx);
+      tc::sts_f32(xmax + (b * 2 + wg) * 128 + r, hmx);
       named_bar_sync(1, NSM);
-      float mxall = hmx;
-#pragma unroll
-      for (int j = 0; j < NWG; ++j) mxall = fmaxf(mxall, tc::lds_f32(xmax + (b * NWG + j) * 128 + r));  // exact, any order
-      const float mx = mxall * scale_log2;
-      if (et == 0) DBG(800 + 4 * Tg + 1);
+      const float mx = fmaxf(tc::lds_f32(xmax + (b * 2) * 128 + r), tc::lds_f32(xmax + (b * 2 + 1) * 128 + r)) *
+                       scale_log2;  // exact, any order
+      if (et == 0) DBG(800 + 4 * t + 1);
       // lazy rescale (identical decision in both halves): move the reference max only when it grew
       // by more than 2^8
       float corr = 1.f;
@@ -512,39 +371,20 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
       for (int i = 0; i < 4; ++i) rs2[i] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int i = 0; i < KW / 2; ++i) {
-        float2 xa;
-        if constexpr (PK) {
-          xa = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nr2);
-        } else {
-          xa.x = fmaf(s[2 * i], scale_log2, nref);
-          xa.y = fmaf(s[2 * i + 1], scale_log2, nref);
-        }
-        if constexpr (POLY == 1) {
-          xa.x = ex2(xa.x);
-          xa.y = (i & 1) ? ex2_poly(xa.y) : ex2(xa.y);  // -inf -> 0 (MUFU)
-        } else if constexpr (POLY == 2) {
-          xa.x = ex2(xa.x);
-          xa.y = ex2_poly(xa.y);
-        } else {
-          xa.x = ex2(xa.x);
-          xa.y = ex2(xa.y);
-        }
+        float2 xa = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nr2);
+        xa.x = ex2(xa.x);
+        xa.y = ex2(xa.y);
         s[2 * i] = xa.x;
         s[2 * i + 1] = xa.y;
-        if constexpr (PK) {
-          rs2[i & 3] = __fadd2_rn(rs2[i & 3], xa);
-        } else {
-          rs2[i & 3].x += xa.x;
-          rs2[i & 3].y += xa.y;
-        }
+        rs2[i & 3] = __fadd2_rn(rs2[i & 3], xa);
       }
       l += ((rs2[0].x + rs2[0].y) + (rs2[1].x + rs2[1].y)) + ((rs2[2].x + rs2[2].y) + (rs2[3].x + rs2[3].y));
       // PV_{t-1} is complete long before here (issued a whole softmax ago); waiting on every phase keeps
       // the barrier protocol explicit (compute-sanitizer synccheck) and O stable for the rescale below
-      if (t >= 1) tc::mbar_wait(pv_done, (Tg - 1) & 1);
+      if (t >= 1) tc::mbar_wait(pv_done, (t - 1) & 1);
       // rescale O only when the reference max moved
       if (t >= 1 && __any_sync(0xffffffffu, corr != 1.f)) {  // warp-collective TMEM read-modify-write
-        if (et == 0) DBG(800 + 4 * Tg + 2);
+        if (et == 0) DBG(800 + 4 * t + 2);
         tc::fence_after();
 #pragma unroll
         for (int c = 0; c < OW / 32; ++c) {
@@ -555,27 +395,23 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
           tc::tmem_st32(tmem + lane_base + 256 + wg * OW + c * 32, o);
         }
       }
-      {  // P (bf16 pairs) over this group's own S columns: keys wg*KW .. -> columns b*128 + wg*KW ..
+      {  // P (bf16 pairs) over this half's own S columns: keys wg*KW .. -> columns b*128 + wg*KW ..
         uint32_t pk[KW / 2];
 #pragma unroll
         for (int i = 0; i < KW / 2; ++i) pk[i] = pack2(s[2 * i], s[2 * i + 1]);
-        tmem_st_words<KW / 2>(tmem + lane_base + b * 128 + wg * KW, pk);
+        tc::tmem_st32u(tmem + lane_base + b * 128 + wg * KW, pk);
       }
       tc::tmem_st_wait();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full);
-      if (et == 0) DBG(800 + 4 * Tg + 3);
+      if (et == 0) DBG(800 + 4 * t + 3);
     }
-    // total row sum = all groups (same reference max), in group order
+    // total row sum = both halves (same reference max), in half order
     tc::sts_f32(xl + wg * 128 + r, l);
     named_bar_sync(1, NSM);
-    if constexpr (NWG == 2) {
-      l = tc::lds_f32(xl + r) + tc::lds_f32(xl + 128 + r);
-    } else {
-      l = (tc::lds_f32(xl + r) + tc::lds_f32(xl + 128 + r)) + (tc::lds_f32(xl + 256 + r) + tc::lds_f32(xl + 384 + r));
-    }
-    tc::mbar_wait(pv_done, (T0 + nt - 1) & 1);
+    l = tc::lds_f32(xl + r) + tc::lds_f32(xl + 128 + r);
+    tc::mbar_wait(pv_done, (nt - 1) & 1);
     tc::fence_after();
     float o[OW];
 #pragma unroll
@@ -585,73 +421,14 @@ __global__ void __launch_bounds__(nt_of<NWG>(), 1)
 #pragma unroll
       for (int i = 0; i < 32; ++i) o[c * 32 + i] = x[i];
     }
-    bool write_out = !partial && !seg[si].xch;
-    if (seg[si].xch) {
-      // This CTA holds one key range of the heavy tile, the cluster peer the other. Each thread puts its
-      // unnormalised O half-row and (m, l) into its own shared memory (the K ring: every load and MMA of
-      // this CTA is done), signals the peer, and merges with the peer's part read through DSMEM: rank 0
-      // writes output columns 0..63, rank 1 columns 64..127. The merge is evaluated in the same order (rank
-      // 0's part, then rank 1's) on both sides, like the global split merge.
-      const uint32_t xo = tc::smem_u32(sK);                       // [NWG][128 rows][OW] fp32, swizzled
-      const uint32_t xmv = xo + (uint32_t)(NWG * 128 * OW * 4);   // [128] (m, l) pairs
-      const uint32_t my_o = xo + (uint32_t)((wg * 128 + r) * OW * 4);
-#pragma unroll
-      for (int i = 0; i < OW / 4; ++i)
-        tc::sts_f4(my_o + (uint32_t)((i ^ (r & (OW / 4 - 1))) * 16),
-                   make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]));
-      if (wg == 0) {  // row statistics (identical in both groups): m in the log2 domain, l the row total
-        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(xmv + (uint32_t)(r * 8)), "f"(m_used), "f"(l) : "memory");
-      }
-      const uint32_t peer = (uint32_t)(role ^ 1);
-      tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(xch_full), peer));
-      tc::mbar_wait_cluster(xch_full, 0);
-      if (wg == role && valid) {
-        const uint32_t po = tc::mapa(my_o, peer);
-        float4 ml_peer;
-        ml_peer.x = tc::ld_cluster_f32(tc::mapa(xmv + (uint32_t)(r * 8), peer));
-        ml_peer.y = tc::ld_cluster_f32(tc::mapa(xmv + (uint32_t)(r * 8 + 4), peer));
-        const float m0 = role == 0 ? m_used : ml_peer.x, l0 = role == 0 ? l : ml_peer.y;
-        const float m1 = role == 0 ? ml_peer.x : m_used, l1 = role == 0 ? ml_peer.y : l;
-        const float ms = fmaxf(m0, m1);
-        const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - ms), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - ms);
-        const float lt = l0 * f0 + l1 * f1;
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)rt * qd + (size_t)hh * HD + wg * OW);
-#pragma unroll
-        for (int c8 = 0; c8 < OW / 8; ++c8) {
-          float mo[8];
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int i = 2 * c8 + h2;
-            const float4 pv = tc::ld_cluster_f4(po + (uint32_t)((i ^ (r & (OW / 4 - 1))) * 16));
-            const float a0 = role == 0 ? o[4 * i] : pv.x, b0 = role == 0 ? pv.x : o[4 * i];
-            const float a1 = role == 0 ? o[4 * i + 1] : pv.y, b1 = role == 0 ? pv.y : o[4 * i + 1];
-            const float a2 = role == 0 ? o[4 * i + 2] : pv.z, b2 = role == 0 ? pv.z : o[4 * i + 2];
-            const float a3 = role == 0 ? o[4 * i + 3] : pv.w, b3 = role == 0 ? pv.w : o[4 * i + 3];
-            mo[4 * h2] = (a0 * f0 + b0 * f1) * inv;
-            mo[4 * h2 + 1] = (a1 * f0 + b1 * f1) * inv;
-            mo[4 * h2 + 2] = (a2 * f0 + b2 * f1) * inv;
-            mo[4 * h2 + 3] = (a3 * f0 + b3 * f1) * inv;
-          }
-          uint4 w;
-          w.x = pack2(mo[0], mo[1]); w.y = pack2(mo[2], mo[3]); w.z = pack2(mo[4], mo[5]); w.w = pack2(mo[6], mo[7]);
-          dst[c8] = w;
-        }
-      }
-      tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(xch_done), peer));  // done reading the peer's part
-      tc::mbar_wait_cluster(xch_done, 0);  // the peer is done reading mine: my shared memory may go
-    }
-    finish_rows<NSM, OW>(o, m_used, l, partial, write_out, n_active, seg[si].sidx, tile, g, n_kv, R, rho, valid, rt, hh,
-                         qd, et, wg, reinterpret_cast<int*>(xl + NWG * 128), opart, ml, tile_cnt, out);
-    T0 += nt;
-    }  // segments
-    (void)et;
+    finish_rows(o, m_used, l, n_active > 1, n_active == 1, n_active, split, tile, g, n_kv, R, rho, valid, rt, hh, qd,
+                et, wg, flag, opart, ml, tile_cnt, out);
   }
   tc::fence_before();
   __syncthreads();
   DBG(1202);
 #ifdef CB_ATTN_TRACE
-  // per-CTA span (globaltimer) of every CTA with linear id < 512 at dbg[1300 + 2 id]
+  // per-CTA span (globaltimer) of every CTA with linear id < 370 at dbg[1300 + 2 id]
   if (dbg != nullptr && threadIdx.x == 0) {
     const int id = blockIdx.x;
     if (id < 370) { dbg[1300 + 2 * id] = t_start; dbg[1300 + 2 * id + 1] = tc::globaltimer(); }
@@ -761,15 +538,7 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   const int max_kt = (n_keys + BC - 1) / BC;
   const long long base = (long long)tiles * n_kv;
   int n_splits = 1;
-  // causal balance by pairing light and heavy row tiles (2-CTA clusters, one wave):
-  // option attn_pair 0 = off (default: measured neutral, the kernel is power-bound at full occupancy),
-  // 1 = when the grid is one wave, 2 = always
-  int pair_mode = 0;
-  if (c->attn_splits == 0 &&
-      (c->attn_pair == 2 || (c->attn_pair == 1 && base <= (long long)c->num_sms && 2 * base >= (long long)c->num_sms)))
-    pair_mode = 1;
-  if (pair_mode) {
-  } else if (c->attn_splits > 0) {
+  if (c->attn_splits > 0) {
     n_splits = c->attn_splits;
   } else if (2 * base < (long long)c->num_sms) {
     // measured (tools/attn_micro.py): extra CTAs only pay off when the (row tile, head) grid leaves
@@ -785,18 +554,11 @@ cb_status launch_attention_tc5(cb_ctx* c, const void* q, const int* q_row, const
   CUtensorMap tk, tv;
   CB_TRY(kv_tmap(c, k, n_keys, &tk));
   CB_TRY(kv_tmap(c, v, n_keys, &tv));
-  // pair mode: 2-CTA clusters (light + heavy part, heavy rest), ceil(T / 2) per kv head
-  dim3 grid(pair_mode ? 2 * ((tiles + 1) / 2) * n_kv : tiles * n_splits * n_kv);
+  dim3 grid(tiles * n_splits * n_kv);
   ProfScope ps_(c, PROF_ATTN, s);
-  auto kern = c->attn_poly == 2 ? attn_tc5_kernel<2, true, true, 2>
-            : c->attn_poly == 1 ? attn_tc5_kernel<1, true, true, 2>
-            : !c->attn_qtm ? attn_tc5_kernel<0, false, true, 2>
-            : c->attn_nopk ? attn_tc5_kernel<0, true, false, 2>
-            : c->attn_wg4 ? attn_tc5_kernel<0, true, true, 4> : attn_tc5_kernel<0, true, true, 2>;
-  const int nthreads = c->attn_wg4 && !c->attn_poly && c->attn_qtm && !c->attn_nopk ? nt_of<4>() : nt_of<2>();
-  CB_CUDA(launch_k(c, kern, grid, dim3(nthreads), SMEM, s, pair_mode ? 2 : 1, tk, tv, (const bf16*)q, q_row, q_tok,
-                   n_rows, n_keys, (bf16*)out, c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
-                   c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr, pair_mode));
+  CB_CUDA(launch_k(c, attn_tc5_kernel, grid, dim3(NTHREADS), SMEM, s, 1, tk, tv, (const bf16*)q, q_row, q_tok, n_rows,
+                   n_keys, (bf16*)out, c->m.n_q_heads, n_kv, scale_log2, kt_per_split, n_splits, c->attn_part,
+                   c->attn_ml, c->attn_cnt, c->dbg_sel == 1 ? c->dbg_buf : nullptr));
   CB_LAUNCHED(c);
   return CB_OK;
 }
@@ -810,11 +572,6 @@ cb_status attention_tc5_init() {
     g_encode5 = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (g_kvmaps == nullptr) g_kvmaps = new std::unordered_map<KvKey, CUtensorMap, KvKeyHash>();
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, false, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<1, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<2, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel<0, true, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+  CB_CUDA(cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
   return CB_OK;
 }

@@ -291,12 +291,8 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = gemm_tc_init(c);
   if (st == CB_OK) st = attention_tc5_init();
   c->topk_drop_max = 48;
-  c->topk_sort = 0;  // bitonic path measured slower in the blend (13.5 vs 10.5 us per launch, profiles/r02)
-  c->attn_pair = 0;  // measured neutral at blend sizes (power-bound at full occupancy), DESIGN.md §6
   c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
   c->gemm_mc = 2;    // auto: A-multicast clusters where the planner expects a shorter k-loop
-  c->gemm_pf = 0;    // measured neutral-to-slower (9.60 vs 9.54 ms/step, paired runs), DESIGN.md §6.1
-  c->attn_qtm = 1;  // Q in TMEM for QK^T: paired A/B -0.065 ms/step (tools/ab.py attn_qtm=0 attn_qtm=1)
   if (st != CB_OK) {
     cudaFree(c->rope_tab);
     cudaFree(c->err_word);
@@ -405,23 +401,6 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     c->tp_nofuse = value == 0;
     return CB_OK;
   }
-  if (std::strcmp(name, "attn_packed") == 0) {
-    c->attn_nopk = value == 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_wg4") == 0) {
-    c->attn_wg4 = value != 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_qtm") == 0) {
-    c->attn_qtm = value != 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_poly") == 0) {
-    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "attn_poly must be 0, 1 or 2");
-    c->attn_poly = (int)value;
-    return CB_OK;
-  }
   if (std::strcmp(name, "attn_splits") == 0) {
     CB_REQUIRE(value >= 0 && value <= 16, CB_E_INVALID_ARG, "attn_splits must be 0..16");
     c->attn_splits = (int)value;
@@ -471,21 +450,8 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
     c->gemm_mc = (int)value;
     return CB_OK;
   }
-  if (std::strcmp(name, "gemm_pf") == 0) {
-    c->gemm_pf = value != 0;
-    return CB_OK;
-  }
   if (std::strcmp(name, "q_split") == 0) {
     c->q_split = value != 0;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "attn_pair") == 0) {
-    CB_REQUIRE(value >= 0 && value <= 2, CB_E_INVALID_ARG, "attn_pair must be 0, 1 or 2");
-    c->attn_pair = (int)value;
-    return CB_OK;
-  }
-  if (std::strcmp(name, "topk_sort") == 0) {
-    c->topk_sort = value != 0;
     return CB_OK;
   }
   if (std::strcmp(name, "topk_drop") == 0) {

@@ -62,10 +62,6 @@ struct cb_ctx {
   int gemm_sched;   // cb_set_option("gemm_sched")
   int attn_impl;    // cb_set_option("attn_impl"): 0 auto, 1 SIMT, 2 tcgen05
   int attn_splits;  // cb_set_option("attn_splits"): 0 auto, else forced split-KV factor
-  int attn_nopk;    // cb_set_option("attn_packed", 0): scalar FFMA/FADD in the softmax (A/B of FFMA2/FADD2)
-  int attn_wg4;     // cb_set_option("attn_wg4"): four softmax warpgroups (32 keys per thread) instead of two
-  int attn_qtm;     // cb_set_option("attn_qtm"): Q in TMEM as the QK^T A operand (tcgen05 attention)
-  int attn_poly;    // cb_set_option("attn_poly"): share of softmax exp2 on the FMA pipe (0, 1 = 1/4, 2 = 1/2)
   int no_fuse_norm;  // cb_set_option("fuse_norm", 0): separate RMSNorm kernels between the projections
   int no_fuse_dev;  // cb_set_option("fuse_deviation", 0) disables the QKV-epilogue deviation
   int dbg_sel;         // debug_trace value: 1 = attention + every CTA-pair GEMM, 100 + k = pair GEMMs of kind k only
@@ -82,10 +78,7 @@ struct cb_ctx {
   int gemm_mc;                // cb_set_option("gemm_mc"): 0 off, 1 4-CTA clusters, 2 auto, 3 8-CTA clusters (pair GEMM)
   int max_clusters4;          // co-resident 4-CTA clusters of the pair GEMM (0: none)
   int max_clusters8;          // co-resident 8-CTA clusters of the pair GEMM (0: none)
-  int gemm_pf;                // cb_set_option("gemm_pf", 0/1): first stages' weight loads before the PDL wait
   int q_split;                // cb_set_option("q_split", 0/1): layer-1 Q projected after the selection (kept rows)
-  int attn_pair;              // cb_set_option("attn_pair", 0/1/2): light/heavy row-tile pairing (attention_tc5.cu)
-  int topk_sort;              // cb_set_option("topk_sort", 0/1): bitonic path when n_cand <= top-k threads
   int topk_threads;           // cb_set_option("topk_threads", 256 | 512 | 1024): top-k block size (0 = 1024)
   cudaEvent_t ev_ready;
   cudaEvent_t ev_realign[2];  // realign of layers 1..L-1 on the aux stream: fork, done

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K,
                     int m_tiles, int n_tiles, EpiParams e, int ksplit, int* __restrict__ kflags,
                     int tail_r, int tail_p, float* __restrict__ tscr, int* __restrict__ tcnt,
-                    long long* __restrict__ dbg, const char* __restrict__ pf_b, long long* __restrict__ strace, int mc) {
+                    long long* __restrict__ dbg, long long* __restrict__ strace, int mc) {
   // debug_trace: globaltimer (ns) events of each CTA's first work item at dbg[blockIdx.x * 8 + event]
 #define DBG2(ev) do { if (dbg != nullptr && blockIdx.x < 256) dbg[blockIdx.x * 8 + (ev)] = tc::globaltimer(); } while (0)
   // stage trace (debug_trace 300, pair 0 only, first 256 k-blocks): strace[rank * 256 + kb] = producer's empty
@@ -146,21 +146,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc::cluster_sync();  // barriers of both CTAs initialised before any remote arrive / transaction
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // Weights do not depend on the previous kernel: before waiting for it (PDL), the producer puts the B (weight)
-  // loads of its first work item's first stages in flight, so after the wait those k-blocks only wait for A
-  // (activations the previous kernel just wrote, L2-resident).
-  int pre = 0;  // stages of the first work item whose B load is already in flight (uniform in warp 0)
-  if (pf_b != nullptr && !mc && warp == 0 && pair < items) {
-    const WorkItem w0 = work_item(pair, tiles, num_kb, ksplit, tail_r, tail_p);
-    const int nb0 = w0.t / m_tiles;
-    const int b_row0 = SW ? (rank == 0 ? nb0 * OUT_N : e.ff + nb0 * OUT_N) : nb0 * BN + (int)rank * C::B_HALF;
-    pre = w0.kb1 - w0.kb0 < C::STAGES ? w0.kb1 - w0.kb0 : C::STAGES;
-    for (int st = 0; st < pre && lane == 0; ++st) {  // lane 0 is also the producer below
-      uint8_t* sa = smem + st * C::STAGE_BYTES;
-      if (leader) tc::mbar_arrive_expect_tx(&full[st], 2 * C::STAGE_BYTES);
-      tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[st], (w0.kb0 + st) * BK, b_row0);
-    }
-  }
   pdl_enter();  // prologue above overlapped the previous kernel; its outputs are visible from here
   if (threadIdx.x == 0) DBG2(0);
 
@@ -189,8 +174,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                      b_row + bq * (C::B_HALF / 2), bmask);
             else
               tc::tma_load_2d_2sm(sa + A_BYTES, &tmB, &full[stage], kb * BK, b_row);
-          } else if (i == pair && kb - w.kb0 < pre) {  // fresh stage, B already in flight: only A
-            tc::tma_load_2d_2sm(sa, &tmA, &full[stage], kb * BK, m0);
           } else {
             tc::mbar_wait(&empty[stage], phase ^ 1);
             if (st_on && i == pair && kb < 256) strace[rank * 256 + kb] = clock64();
@@ -408,7 +391,7 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
                     mc == 2 ? 8 : mc ? 4 : 2, ta, tb,
                     M, K, m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
                     (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr,
-                    c->gemm_pf && !mc ? (const char*)B : nullptr, c->dbg_sel == 300 ? c->dbg_buf : nullptr, mc));
+                    c->dbg_sel == 300 ? c->dbg_buf : nullptr, mc));
   CB_LAUNCHED(c);
   return CB_OK;
 }

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
                                                             int* __restrict__ qrow, int* __restrict__ qtok,
                                                             int* __restrict__ sel_tok, int* err,
                                                             const float* __restrict__ dev_part, int n_kv, int ld_part,
-                                                            int dev_mode, int drop_max, int sort_path,
+                                                            int dev_mode, int drop_max,
                                                             long long* __restrict__ dbg) {
   // debug_trace 200: globaltimer of the phases (entry, inputs visible, Delta_kv summed, selected, done)
 #define TK_DBG(i) do { if (dbg != nullptr && threadIdx.x == 0) dbg[i] = tc_globaltimer(); } while (0)
@@ -195,50 +195,6 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
     return;
   }
   if (k == 0) return;
-
-  // At most one candidate per thread (every layer after the first at blend sizes): sort the packed keys
-  // (Delta_kv bits << 32 | ~slot) in one block-wide bitonic network -- descending value, ties to the lower
-  // slot -- and keep every key >= the k-th. One pass of shuffles (strides < 32) and 15 shared-memory steps
-  // instead of the radix passes / drop loop below (same selection: the order is total).
-  if (k < n_cand && n_cand <= (int)blockDim.x && sort_path) {
-    unsigned long long* sb = reinterpret_cast<unsigned long long*>(keys);  // 2 x blockDim packed keys
-    const int P = blockDim.x;  // a power of two (256, 512 or 1024)
-    unsigned long long mine = 0ull;  // padding (tid >= n_cand) sorts below every real key
-    if (tid < n_cand) {
-      const unsigned u = __float_as_uint(dev[tid]);
-      mine = ((unsigned long long)((u & 0x80000000u) ? 0u : u) << 32) | (unsigned)(0xFFFFFFFFu - (unsigned)tid);
-    }
-    unsigned long long v = mine;
-    int buf = 0;
-    for (int kk = 2; kk <= P; kk <<= 1) {
-      const bool desc = (tid & kk) == 0;  // this kk-block ends descending (the last block: the whole array)
-      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        unsigned long long o;
-        if (jj >= 32) {  // double-buffered: one barrier per step
-          sb[buf * P + tid] = v;
-          __syncthreads();
-          o = sb[buf * P + (tid ^ jj)];
-          buf ^= 1;
-        } else {
-          o = __shfl_xor_sync(0xffffffffu, v, jj);
-        }
-        const bool lower = (tid & jj) == 0;
-        v = (lower == desc) ? (o > v ? o : v) : (o < v ? o : v);
-      }
-    }
-    __shared__ unsigned long long sm_thr;
-    if (tid == k - 1) sm_thr = v;  // the k-th largest packed key
-    __syncthreads();
-    const bool sel = tid < n_cand && mine >= sm_thr;
-    const int out = block_excl_scan(sel ? 1 : 0, sm_warp, &sm_total);
-    if (sel) {
-      const int t = cand_tok[tid];
-      qrow[out] = tid;
-      qtok[out] = t;
-      if (sel_tok) sel_tok[out] = t;
-    }
-    return;
-  }
 
   if (dev_part == nullptr)  // (with the partials the keys were written while summing)
     for (int j = tid; j < n_cand; j += blockDim.x) {
@@ -433,11 +389,10 @@ cb_status launch_topk(cb_ctx* c, float* dev, const int* cand_tok, int n_cand, in
   // threads: 1024, or fewer when the candidates are few (cheaper block barriers), cb_set_option("topk_threads")
   int nt = TOPK_THREADS;
   if (c->topk_threads > 0) nt = c->topk_threads;
-  // keys (radix / drop paths) or the sort path's two buffers of nt packed 64-bit keys
-  const size_t smem = std::max((size_t)std::max(1, n_cand) * sizeof(unsigned), (size_t)nt * 2 * 8);
+  const size_t smem = (size_t)std::max(1, n_cand) * sizeof(unsigned);  // the select keys
   CB_LAUNCH(c, (topk_kernel), 1, nt, smem, s, dev, cand_tok, n_cand, k_keep, n_suffix, N, force_sel, qrow, qtok, sel_tok,
                                             c->err_word, dev_part, c->m.n_kv_heads * c->m.head_dim / 64 * std::max(1, c->tp_world), ld_part,
-                                            dev_mode, c->topk_drop_max, c->topk_sort ? 1 : 0,
+                                            dev_mode, c->topk_drop_max,
                                             c->dbg_sel == 200 ? c->dbg_buf : nullptr);
   CB_LAUNCHED(c);
   return CB_OK;

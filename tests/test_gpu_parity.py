@@ -290,42 +290,16 @@ def test_attention_tensor_core(P, T, n_sel, n_kv, impl):
     assert rel_err(np32(out), ref) < 1e-2
 
 
-@pytest.mark.parametrize("opt", [("attn_poly", 1), ("attn_poly", 2), ("attn_qtm", 0), ("attn_packed", 0), ("attn_wg4", 1),
-                                 ("attn_wg4", 0)])
-@pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (4100, 900, 4)])
-def test_attention_tc5_variants(P, T, n_sel, n_kv, opt):
-    """tcgen05 attention variants against the oracle and close to the default kernel: attn_poly (a share of
-    the softmax exponentials on the FMA pipe, degree-3 polynomial with relative error 7.5e-5) and attn_qtm
-    (Q in TMEM as the A operand of QK^T: bitwise the same products, so the same result)."""
-    s = shape("small", n_kv_heads=n_kv)
-    g = lambda st, n, H: rng.values(13, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
-    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
-    rows = np.sort(np.random.default_rng(T + 1).choice(T, n_sel, replace=False)).astype(np.int32)
-    qrow = np.arange(n_sel, dtype=np.int32)
-    ctx = P.Context(s, "bf16", max_tokens=T)
-    args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
-            to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
-    base = P.api.op_attention(ctx, *args, impl=2)
-    ctx.set_option(*opt)
-    out = P.api.op_attention(ctx, *args, impl=2)
-    pos = np.arange(T)
-    ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
-    assert rel_err(np32(out), ref) < 1e-2
-    assert rel_err(np32(out), np32(base)) < 4e-3
-
-
-@pytest.mark.parametrize("wg4", [0, 1])
 @pytest.mark.parametrize("splits", [2, 5])
-def test_attention_tc5_softmax_groups_split(P, splits, wg4):
-    """Two or four softmax warpgroups, with forced split-KV and the in-kernel merge: oracle tolerance and
-    bitwise reproducible across launches."""
+def test_attention_tc5_forced_split(P, splits):
+    """Forced split-KV with the in-kernel merge at the blend's sizes (3072 keys, 460 queries): oracle tolerance
+    and bitwise reproducible across launches."""
     s = shape("small", n_kv_heads=2)
     T, n_sel = 3072, 460
     g = lambda st, n, H: rng.values(14, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
     q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
     rows = np.sort(np.random.default_rng(5).choice(T, n_sel, replace=False)).astype(np.int32)
     ctx = P.Context(s, "bf16", max_tokens=T)
-    ctx.set_option("attn_wg4", wg4)
     ctx.set_option("attn_splits", splits)
     args = (to_dev(q[rows], torch.bfloat16), to_dev(np.arange(n_sel, dtype=np.int32), torch.int32),
             to_dev(rows, torch.int32), to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
@@ -357,36 +331,6 @@ def test_attention_tc5_split_merge(P, splits, impl):
     assert rel_err(np32(out), ref) < 1e-2
     for _ in range(2):
         assert torch.equal(P.api.op_attention(ctx, *args, impl=impl), out)
-
-
-@pytest.mark.parametrize("order", ["sorted", "shuffled"])
-@pytest.mark.parametrize("T,n_sel,n_kv", [(300, 7, 2), (3072, 460, 2), (777, 50, 1), (130, 3, 8), (4100, 900, 4),
-                                          (2048, 256, 2)])
-def test_attention_tc5_pairing(P, T, n_sel, n_kv, order):
-    """Causal balance (attn_pair): row tile p paired with row tile T-1-p, the heavy one's key range cut
-    between two CTAs and merged by the last arrival; odd tile counts leave the middle tile whole; unsorted
-    query tokens take the heavier tile of each pair. Oracle parity, close to the unpaired kernel, bitwise
-    reproducible across launches."""
-    s = shape("small", n_kv_heads=n_kv)
-    g = lambda st, n, H: rng.values(15, st, n * H * s.head_dim, 1.0, 0.0, "bf16").reshape(n, H, s.head_dim)
-    q, k, v = g(1, T, s.n_q_heads), g(2, T, s.n_kv_heads), g(3, T, s.n_kv_heads)
-    rows = np.sort(np.random.default_rng(T + 7).choice(T, n_sel, replace=False)).astype(np.int32)
-    if order == "shuffled":
-        rows = rows[np.random.default_rng(3).permutation(n_sel)]
-    qrow = np.arange(n_sel, dtype=np.int32)
-    ctx = P.Context(s, "bf16", max_tokens=T)
-    args = (to_dev(q[rows], torch.bfloat16), to_dev(qrow, torch.int32), to_dev(rows, torch.int32),
-            to_dev(k, torch.bfloat16), to_dev(v, torch.bfloat16), T)
-    ctx.set_option("attn_pair", 0)
-    base = P.api.op_attention(ctx, *args, impl=2)
-    ctx.set_option("attn_pair", 2)
-    out = P.api.op_attention(ctx, *args, impl=2)
-    pos = np.arange(T)
-    ref = O.causal_attention(q[rows], pos[rows], k, v, pos)
-    assert rel_err(np32(out), ref) < 1e-2
-    assert rel_err(np32(out), np32(base)) < 4e-3
-    for _ in range(2):
-        assert torch.equal(P.api.op_attention(ctx, *args, impl=2), out)
 
 
 # ---- (c) the whole blend ------------------------------------------------------------------------
@@ -814,39 +758,25 @@ def test_bad_positions_are_reported(P, bad):
 
 
 @pytest.mark.parametrize("threads", [0, 256, 512])
-def test_topk_sort_path_bitwise(P, threads):
-    """The bitonic top-k path (n_cand <= block threads, every layer after the first at blend sizes) selects
-    exactly what the radix / drop-smallest paths select (ties -> lower index, R6): a whole small blend, and
-    direct calls on tie-heavy deviations over a sweep of (n_cand, k)."""
-    s, m, req, tok, pos, cs, Kc, Vc, ks = _oracle_case("small", 17, [300, 211, 157], 4, "bf16", 0.15)
-    outs = []
-    for sort in (0, 1):
-        ctx = P.Context(s, "bf16", max_tokens=req.n_total, max_pos=4096)
-        ctx.set_option("topk_threads", threads)
-        ctx.set_option("topk_sort", sort)
-        outs.append(run_blend(P, s, "bf16", 17, req, tok, pos, cs, Kc, Vc, ks, ctx=ctx))
-    for a, b in zip(outs[0]["sel"], outs[1]["sel"]):
-        np.testing.assert_array_equal(a, b)
-    np.testing.assert_array_equal(outs[0]["h"], outs[1]["h"])
+def test_topk_select_paths_exact(P, threads):
+    """The top-k select (drop-smallest loop when few candidates are dropped, MSB radix select otherwise; ties ->
+    lower slot, R6) picks exactly the k largest deviations on tie-heavy inputs over a sweep of (n_cand, k) that
+    crosses the drop / radix boundary and the block size, at 256 / 512 / 1024 threads."""
+    s = shape("small")
     ctx = P.Context(s, "bf16", max_tokens=1100)
     ctx.set_option("topk_threads", threads)
     lim = threads or 1024
     g = torch.Generator(device=DEV).manual_seed(threads + 1)
-    for n, k in [(1, 0), (2, 1), (37, 5), (255, 254), (256, 1), (300, 299), (553, 547), (lim, 1), (lim, lim - 1),
-                 (lim, lim // 2)]:
-        n = min(n, lim)
+    for n, k in [(1, 0), (2, 1), (37, 5), (255, 254), (256, 1), (300, 299), (553, 547), (553, 505), (553, 504),
+                 (lim, 1), (lim, lim - 1), (lim, lim // 2), (1100, 1000)]:
         k = min(k, n)
         kn = torch.randint(0, 3, (n, s.n_kv_heads, s.head_dim), device=DEV, generator=g).to(torch.bfloat16)
         kn[::3] = 0  # many exact ties at zero
         vn = torch.zeros_like(kn)
         ref = torch.zeros(n + 20, s.n_kv_heads, s.head_dim, dtype=torch.bfloat16, device=DEV)  # rows = tokens
         cand = torch.sort(torch.randperm(n + 20, device=DEV, generator=g)[:n])[0].to(torch.int32)
-        res = []
-        for sort in (0, 1):
-            ctx.set_option("topk_sort", sort)
-            res.append(P.api.kv_deviation_topk(ctx, kn, vn, ref, ref, cand, k))
-        d = res[1][2].cpu().numpy()
+        sel_tok, sel_slot, dev = P.api.kv_deviation_topk(ctx, kn, vn, ref, ref, cand, k)
+        d = dev.cpu().numpy()
         want = np.sort(np.lexsort((np.arange(n), -d))[:k])  # k largest, ties -> lower slot
-        np.testing.assert_array_equal(res[0][1].cpu().numpy(), want, err_msg=f"radix/drop path n={n} k={k}")
-        np.testing.assert_array_equal(res[1][1].cpu().numpy(), want, err_msg=f"sort path n={n} k={k}")
-        assert torch.equal(res[0][0], res[1][0]), (n, k)
+        np.testing.assert_array_equal(sel_slot.cpu().numpy(), want, err_msg=f"n={n} k={k}")
+        np.testing.assert_array_equal(sel_tok.cpu().numpy(), cand.cpu().numpy()[want], err_msg=f"n={n} k={k}")

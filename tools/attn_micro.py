@@ -16,10 +16,9 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--splits", default="0,1,2,3,4,6")
     ap.add_argument("--impls", default="2")
-    ap.add_argument("--pairs", default="0,1")
     ap.add_argument("--pdl", type=int, default=1)
     ap.add_argument("--rows", default="3072,553,460,369")
-    ap.add_argument("--opts", default="", help="extra option sets to compare, ';'-separated, e.g. 'attn_ipk=1;attn_poly=1'")
+    ap.add_argument("--opts", default="", help="extra option sets to compare, ';'-separated, e.g. 'attn_splits=2;pdl=0'")
     a = ap.parse_args()
     from paper_2405_16444_b200.build import build
     build()
@@ -31,7 +30,7 @@ def main():
     ctx.set_option("pdl", a.pdl)
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
-    base = {"attn_splits": 0, "attn_pair": 0}
+    base = {"attn_splits": 0}
     variants = [""] + [v for v in a.opts.split(";") if v]
     for n_sel in [int(x) for x in a.rows.split(",")]:
         rows = np.sort(np.random.default_rng(n_sel).choice(T, n_sel, replace=False)).astype(np.int32)
@@ -39,10 +38,10 @@ def main():
         qrow = torch.arange(n_sel, dtype=torch.int32, device="cuda")
         qtok = torch.from_numpy(rows).cuda()
         flops = 4.0 * s.n_q_heads * s.head_dim * float(np.sum(rows + 1))
-        for impl, splits, pair, var in [(int(i), int(x), int(pp), v) for i in a.impls.split(",")
-                                        for x in a.splits.split(",") for pp in a.pairs.split(",") for v in variants]:
+        for impl, splits, var in [(int(i), int(x), v) for i in a.impls.split(",") for x in a.splits.split(",")
+                                  for v in variants]:
             opts = dict(base)
-            opts.update({"attn_splits": splits, "attn_pair": pair})
+            opts.update({"attn_splits": splits})
             opts.update({kv.split("=")[0]: int(kv.split("=")[1]) for kv in var.split(",") if kv})
             for name, val in opts.items():
                 ctx.set_option(name, val)
@@ -57,7 +56,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) / a.iters * 1e3
-            print(f"rows={n_sel:5d} impl={impl} splits={splits} pair={pair} [{var}]: {us:8.1f} us  "
+            print(f"rows={n_sel:5d} impl={impl} splits={splits} [{var}]: {us:8.1f} us  "
                   f"{flops / us / 1e6:7.1f} TFLOP/s", flush=True)
             for kv in var.split(","):  # back to the defaults for the next variant
                 if kv:

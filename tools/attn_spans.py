@@ -13,14 +13,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     n_sel = int(sys.argv[1]) if len(sys.argv) > 1 else 460
     splits = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-    pair = int(sys.argv[3]) if len(sys.argv) > 3 else 0
     import paper_2405_16444_b200 as P
     from synth import workload as W
     s = W.MODELS["mistral-7b"]
     T = 3072
     ctx = P.Context(s, "bf16", max_tokens=T)
     ctx.set_option("attn_splits", splits)
-    ctx.set_option("attn_pair", pair)
     ctx.set_option("pdl", int(os.environ.get("CB_PDL", "1")))
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
@@ -56,8 +54,8 @@ def main():
         sp = rest % ns
         return max(0, min(kt, (sp + 1) * per) - sp * per)
     for i, b, e in spans[::step]:
-        k_ = n_kt(i) if not pair else 0
-        extra = f"  kt={k_:3d}  {(e - b) / max(k_, 1):5.2f} us/tile" if not pair else ""
+        k_ = n_kt(i)
+        extra = f"  kt={k_:3d}  {(e - b) / max(k_, 1):5.2f} us/tile"
         print(f"{i:4d} {b:7.2f} -> {e:7.2f}  ({e - b:6.2f}){extra}")
 
 

@@ -19,7 +19,6 @@ def main():
     s = W.MODELS["mistral-7b"]
     ctx = P.Context(s, "bf16", max_tokens=T)
     ctx.set_option("attn_splits", int(os.environ.get("ATTN_SPLITS", "1")))
-    ctx.set_option("attn_pair", int(os.environ.get("ATTN_PAIR", "0")))
     k = torch.randn(T, s.n_kv_heads, s.head_dim, device="cuda").to(torch.bfloat16)
     v = torch.randn_like(k)
     rows = np.sort(np.random.default_rng(n_sel).choice(T, n_sel, replace=False)).astype(np.int32)
