@@ -71,6 +71,8 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "pdl"         1 = programmatic dependent launch between library kernels (default), 0 = off
  *   "fuse_norm"   1 = RMSNorm fused into the residual / next projection epilogues (default), 0 = kernels
  *   "topk_threads" 0 = 1024 (default), 256 or 512 threads in the top-k block
+ *   "epi_l1pf"    1 = the residual epilogue of the pair GEMM pulls each row's next 32-column residual segment
+ *                 into L1 while the current chunk is stored (default), 0 = off
  *   "gemm_mc"     A-multicast 4-CTA clusters (two CTA pairs sharing their A rows) in the pair GEMM:
  *                 2 = where the planner expects a shorter k-loop (default), 1 = always (whole tiles), 0 = off,
  *                 3 = 8-CTA clusters (2 row x 2 column tiles, B multicast as well; measured neutral, opt-in) */

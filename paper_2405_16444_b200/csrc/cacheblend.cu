@@ -291,6 +291,7 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   if (st == CB_OK) st = gemm_tc_init(c);
   if (st == CB_OK) st = attention_tc5_init();
   c->topk_drop_max = 48;
+  c->epi_l1pf = 1;
   c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
   c->gemm_mc = 2;    // auto: A-multicast clusters where the planner expects a shorter k-loop
   if (st != CB_OK) {
@@ -448,6 +449,10 @@ extern "C" cb_status cb_set_option(cb_ctx* c, const char* name, int64_t value) {
   if (std::strcmp(name, "gemm_mc") == 0) {
     CB_REQUIRE(value >= 0 && value <= 3, CB_E_INVALID_ARG, "gemm_mc must be 0, 1, 2 or 3");
     c->gemm_mc = (int)value;
+    return CB_OK;
+  }
+  if (std::strcmp(name, "epi_l1pf") == 0) {
+    c->epi_l1pf = value != 0;
     return CB_OK;
   }
   if (std::strcmp(name, "q_split") == 0) {

@@ -96,6 +96,7 @@ struct EpiParams {
   const void* k_ref; const void* v_ref; float* dev_part; int n_cand, ld_part;
   // EPI_RESID
   float* h_out; const float* h_in; const int* res_row;
+  int l1pf;                    // lean residual epilogue: pull the next chunk's residual rows into L1 (cb_set_option "epi_l1pf")
   // EPI_SWIGLU
   int ff; void* act;
   // Fused RMSNorm (tcgen05 path; DESIGN R15). Producer (EPI_RESID with norm_gain set): besides h_out it writes

@@ -79,6 +79,7 @@ struct cb_ctx {
   int max_clusters4;          // co-resident 4-CTA clusters of the pair GEMM (0: none)
   int max_clusters8;          // co-resident 8-CTA clusters of the pair GEMM (0: none)
   int q_split;                // cb_set_option("q_split", 0/1): layer-1 Q projected after the selection (kept rows)
+  int epi_l1pf;               // cb_set_option("epi_l1pf"): residual epilogue prefetches the next chunk into L1
   int topk_threads;           // cb_set_option("topk_threads", 256 | 512 | 1024): top-k block size (0 = 1024)
   cudaEvent_t ev_ready;
   cudaEvent_t ev_realign[2];  // realign of layers 1..L-1 on the aux stream: fork, done

@@ -368,6 +368,7 @@ __device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base
       pre[it] = ((okmask >> it) & 1) ? (cont ? __ldcg(reinterpret_cast<const float4*>(base + in_off[it] + n))
                                             : *reinterpret_cast<const float4*>(base + in_off[it] + n))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool more = c + 32 < BN && n + 32 < e.N;  // warp-uniform
     {
       float v[32];
       tc::tmem_ld32(trow + c, v);
@@ -389,6 +390,9 @@ __device__ __forceinline__ void resid_lean(const EpiParams& e, int M, int m_base
                    : "r"(sbase + (uint32_t)(r * 8 + (j ^ (r & 7))) * 16u)
                    : "memory");
       const float4 o = make_float4(pre[it].x + a.x, pre[it].y + a.y, pre[it].z + a.z, pre[it].w + a.w);
+      // the next chunk's residual segment of this row pulled into L1 while this chunk is stored (no registers)
+      if (e.l1pf && j == 0 && more && !cont && ((okmask >> it) & 1))  // one lane per 128-byte row segment
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(base + in_off[it] + n + 32));
       if ((okmask >> it) & 1) {
         *reinterpret_cast<float4*>(e.h_out + out_off[it] + n) = o;
         if constexpr (NORM) {

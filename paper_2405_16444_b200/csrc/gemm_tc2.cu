@@ -383,13 +383,15 @@ static cb_status launch2_kind(cb_ctx* c, const void* A, int lda, const void* B, 
   constexpr bool sw = KIND == EPI_SWIGLU;
   constexpr int out_n = sw ? BN / 2 : BN;
   const long long b_rows = sw ? 2LL * e.ff : (long long)e.N;
+  EpiParams ee = e;
+  ee.l1pf = c->epi_l1pf;
   CUtensorMap ta, tb;
   CB_TRY(gemm_tmap(c, A, M, K, lda, mc ? 64 : 128, &ta));  // mc: each CTA loads (and multicasts) half of A
   CB_TRY(gemm_tmap(c, B, b_rows, K, ldb, mc == 2 ? C::B_HALF / 2 : C::B_HALF, &tb));  // mc 2: B quarter-boxes
   const int m_tiles = (M + 255) / 256, n_tiles = (e.N + out_n - 1) / out_n;
   CB_CUDA(launch_k(c, gemm_tc2_kernel<KIND, BN>, dim3(2 * n_pairs), dim3(NUM_THREADS), C::SMEM, s,
                     mc == 2 ? 8 : mc ? 4 : 2, ta, tb,
-                    M, K, m_tiles, n_tiles, e, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
+                    M, K, m_tiles, n_tiles, ee, ksplit, kflags, tail_r, tail_p, tscr, tcnt,
                     (c->dbg_sel == 1 || c->dbg_sel == 100 + KIND) ? c->dbg_buf : nullptr,
                     c->dbg_sel == 300 ? c->dbg_buf : nullptr, mc));
   CB_LAUNCHED(c);
