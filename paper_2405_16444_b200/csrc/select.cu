@@ -207,35 +207,45 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(float* __restrict__ 
   constexpr unsigned DROPPED = 0xFFFFFFFFu;  // above every key (keys are bits of non-negative floats)
   const bool drop_path = k < n_cand && n_cand - k <= drop_max;
   if (drop_path && n_cand <= 1024) {
-    // one warp, 32 keys per lane in registers: d rounds of (lane minimum, warp minimum) with no block barrier
-    // (the block-wide loop below costs two barriers per dropped key). Same order, same selection.
+    // two warps, 16 keys per lane in registers (slot j = tid + 64 q; at 1024 threads a thread has 64 registers,
+    // too few for 32 keys): d rounds of (lane minimum, warp minimum, the two warps' minima through shared
+    // memory with a 64-thread named barrier) instead of the block-wide loop's two block barriers per key.
+    // Same order, same selection.
     __syncthreads();
-    if (tid < 32) {
-      unsigned long long v[32];
+    if (tid < 64) {
+      __shared__ unsigned long long wbest[2][2];  // [round parity][warp]
+      unsigned k16[16];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const int j = tid + 32 * q;
-        v[q] = j < n_cand ? (((unsigned long long)keys[j] << 32) | (unsigned)(0x7FFFFFFF - j)) : ~0ull;
+      for (int q = 0; q < 16; ++q) {
+        const int j = tid + 64 * q;
+        k16[q] = j < n_cand ? keys[j] : DROPPED;
       }
       for (int r = 0; r < n_cand - k; ++r) {
-        unsigned long long t16[16];  // lane minimum as a 5-level tree (not a 31-long dependency chain)
+        // the next slot to drop: smallest key, ties -> the larger slot (the complement of "k largest, ties
+        // to the lower index"). Lane minimum in four chains, then the largest q holding it from a mask.
+        unsigned m4[4] = {k16[0], k16[1], k16[2], k16[3]};
 #pragma unroll
-        for (int q = 0; q < 16; ++q) t16[q] = v[2 * q] < v[2 * q + 1] ? v[2 * q] : v[2 * q + 1];
+        for (int q = 4; q < 16; ++q) m4[q & 3] = min(m4[q & 3], k16[q]);
+        const unsigned lmin = min(min(m4[0], m4[1]), min(m4[2], m4[3]));
+        unsigned eq = 0;
 #pragma unroll
-        for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-          for (int q = 0; q < w; ++q) t16[q] = t16[q] < t16[q + w] ? t16[q] : t16[q + w];
-        unsigned long long b = t16[0];
+        for (int q = 0; q < 16; ++q) eq |= (k16[q] == lmin ? 1u : 0u) << q;
+        const int bq = 31 - __clz(eq);
+        unsigned long long b = ((unsigned long long)lmin << 32) | (unsigned)(0x7FFFFFFF - (tid + 64 * bq));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
           b = y < b ? y : b;
         }
+        if ((tid & 31) == 0) wbest[r & 1][tid >> 5] = b;
+        asm volatile("bar.sync 2, 64;" ::: "memory");
+        const unsigned long long b0 = wbest[r & 1][0], b1 = wbest[r & 1][1];
+        b = b0 < b1 ? b0 : b1;
         const int jd = 0x7FFFFFFF - (int)(unsigned)(b & 0xFFFFFFFFu);
-        if ((jd & 31) == tid) {
+        if ((jd & 63) == tid) {
 #pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (q == (jd >> 5)) v[q] = ~0ull;
+          for (int q = 0; q < 16; ++q)
+            if (q == (jd >> 6)) k16[q] = DROPPED;
           keys[jd] = DROPPED;
         }
       }
