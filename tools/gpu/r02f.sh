@@ -1,8 +1,12 @@
+#!/bin/bash
+# validation after the epilogue L1 prefetch and the two-warp top-k drop loop
 mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k regex:gemm_tc2 -s 2 -c 1 -o gpurun_out/r02f_oproj \
-    python tools/gemm_trace.py 553 4096 4096 1 1 > gpurun_out/r02f_ncu.log 2>&1
-tail -3 gpurun_out/r02f_ncu.log
-ncu -i gpurun_out/r02f_oproj.ncu-rep --page raw --csv > gpurun_out/r02f_oproj_raw.csv 2>&1
-ncu -i gpurun_out/r02f_oproj.ncu-rep --page source --csv --print-source sass > gpurun_out/r02f_oproj_sass.csv 2>&1
-ncu -i gpurun_out/r02f_oproj.ncu-rep --page details --csv > gpurun_out/r02f_oproj_details.csv 2>&1
-python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "topk_sort" 2>&1 | tail -3
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02f_pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/r02f_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02f_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/r02f_smoke.log
+timeout 900 python bench.py > gpurun_out/r02f_bench.json 2> gpurun_out/r02f_bench.err; echo "bench rc=$?"
+python -c "import json;d=json.loads(open('gpurun_out/r02f_bench.json').read().strip().splitlines()[-1]);print('mistral', d['ms_per_step'], d['value'], d['roofline']['frac'], d['roofline']['path']['frac'], d['roofline']['attention']['frac'], d['e2e']['ms'], d['e2e'].get('paired_overhead_ms'), d['cpu_baseline']['value'], d['gpu_launches'], d['clocks'])"
+CB_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/r02f_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-baselines > gpurun_out/r02f_ncu_list.log 2>&1
+python tools/launch_summary.py gpurun_out/r02f_launches.csv 2 > gpurun_out/r02f_launch_summary.txt 2>&1; head -12 gpurun_out/r02f_launch_summary.txt
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r02f_reference.json 2>&1; echo "reference rc=$?"; tail -c 300 gpurun_out/r02f_reference.json
