@@ -74,7 +74,7 @@ CB_API cb_status cb_op_attention(cb_ctx* ctx, const void* q, const int32_t* q_ro
  *   "epi_l1pf"    1 = the residual epilogue of the pair GEMM pulls each row's next 32-column residual segment
  *                 into L1 while the current chunk is stored (default), 0 = off
  *   "gemm_mc"     A-multicast 4-CTA clusters (two CTA pairs sharing their A rows) in the pair GEMM:
- *                 2 = where the planner expects a shorter k-loop (default), 1 = always (whole tiles), 0 = off,
+ *                 2 = where the planner expects a shorter k-loop, 1 = always (whole tiles), 0 = off (default),
  *                 3 = 8-CTA clusters (2 row x 2 column tiles, B multicast as well; measured neutral, opt-in) */
 CB_API cb_status cb_set_option(cb_ctx* ctx, const char* name, int64_t value);
 

@@ -293,7 +293,8 @@ extern "C" cb_status cb_create(const cb_model* model, int32_t max_tokens, void* 
   c->topk_drop_max = 48;
   c->epi_l1pf = 1;
   c->q_split = 1;    // layer 1: Q projected for the kept rows only, after the selection
-  c->gemm_mc = 2;    // auto: A-multicast clusters where the planner expects a shorter k-loop
+  c->gemm_mc = 0;    // off: with the weights streaming from HBM the clusters no longer shorten the k-loop (paired
+                     // A/B in four orders: -0.11 ms/step without them); 2 = planner-selected
   if (st != CB_OK) {
     cudaFree(c->rope_tab);
     cudaFree(c->err_word);
