@@ -30,7 +30,6 @@ def main():
     req = W.Request([512] * 6, 0, 1, 0.15)
     N, L = req.n_ctx, s.n_layers
     dev = torch.device("cuda", 0)
-    ctx = P.Context(s, "bf16", max_tokens=N, max_pos=2 * N)
     mw = P.ModelWeights.synth(s, 1, "bf16", dev)
     tok = torch.from_numpy(req.tokens(s.vocab)).to(dev)
     pos = torch.from_numpy(req.global_positions()).to(dev)
@@ -40,24 +39,26 @@ def main():
     ks = P.schedule(0.15, N, L)
     graphs = {}
     for name, spec in (("A", A), ("B", B)):
+        # a context of its own per option set: options set for A must not leak into B's graph
+        ctx = P.Context(s, "bf16", max_tokens=N, max_pos=2 * N)
         for k, v in opts(spec):
             ctx.set_option(k, v)
         kb, vb = torch.empty_like(k_in), torch.empty_like(v_in)
         h_out = torch.empty(ks[-1], s.d_model, dtype=torch.float32, device=dev)
-        f = lambda kb=kb, vb=vb, h_out=h_out: P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, kb, vb, ks,
+        f = lambda kb=kb, vb=vb, h_out=h_out, ctx=ctx: P.blend_forward(ctx, mw, tok, pos, list(cs), 0, k_in, v_in, kb, vb, ks,
                                                                h_out=h_out)
         if e2e:
             kh, vh = k_in.cpu().pin_memory(), v_in.cpu().pin_memory()
             toks, poss = tok.cpu().pin_memory(), pos.cpu().pin_memory()
             hh = torch.empty(ks[-1], s.d_model, dtype=torch.float32).pin_memory()
-            f = lambda kb=kb, vb=vb, kh=kh, vh=vh, toks=toks, poss=poss, hh=hh: P.api.blend_request(
+            f = lambda kb=kb, vb=vb, kh=kh, vh=vh, toks=toks, poss=poss, hh=hh, ctx=ctx: P.api.blend_request(
                 ctx, mw, toks, poss, list(cs), 0, kh, vh, kb, vb, ks, hh)
         f()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             f()
-        graphs[name] = (g, f, kb, vb, h_out)
+        graphs[name] = (g, f, kb, vb, h_out, ctx)
     for _ in range(3):
         for g, *_ in graphs.values():
             g.replay()
