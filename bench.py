@@ -488,7 +488,7 @@ def run_ours(args):
     if gemm_ms > 0:
         achieved = work["gemm_flops"] / (gemm_ms / 1e3) / 1e12
         traffic, tnote = None, None
-        for tname in ("r02d_traffic.json", "r02_traffic.json", "r01c_traffic.json"):  # newest committed ncu capture first
+        for tname in ("r02g_traffic.json", "r02d_traffic.json", "r02_traffic.json", "r01c_traffic.json"):  # newest committed ncu capture first
             tpath = os.path.join(ROOT, "profiles", tname)
             if os.path.exists(tpath):  # committed ncu measurement of the largest GEMM launch (bytes per launch)
                 tj = json.load(open(tpath))
