@@ -195,6 +195,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int jb = split * kt_per_split, je = min(n_kt, jb + kt_per_split);
   if (jb >= je) return;  // nothing in this range (the tile's other CTAs do not count it)
   const int nt = je - jb, n_active = (n_kt + kt_per_split - 1) / kt_per_split;
+  // softmax threads: row (token, q head) of this thread and its half of Q, loaded before the prologue so the
+  // gathered-row loads (q_row, then the row) overlap the barrier init and the TMEM allocation
+  const int wg = (warp - 2) >> 2;  // 0: keys / O columns 0..63, 1: 64..127
+  const int r = (warp & 3) * 32 + lane;
+  const int rho = tile * BM + r;
+  const bool valid = warp >= 2 && rho < R;
+  const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
+  uint4 qv[KW / 8];
+#pragma unroll
+  for (int c8 = 0; c8 < KW / 8; ++c8) qv[c8] = make_uint4(0u, 0u, 0u, 0u);
+  if (valid) {
+    const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD + wg * KW);
+#pragma unroll
+    for (int c8 = 0; c8 < KW / 8; ++c8) qv[c8] = __ldg(src + c8);
+  }
 
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmK);
@@ -295,21 +310,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     // ===== softmax / correction / epilogue: two warpgroups, each owns one 64-key half of every row
     // (thread = (row, half)); the halves agree on the row max through shared memory every tile =====
-    const int wg = (warp - 2) >> 2;  // 0: keys / O columns 0..63, 1: 64..127
-    const int r = (warp & 3) * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..NSM-1 among softmax threads
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int rho = tile * BM + r;
-    const bool valid = rho < R;
-    const int rt = valid ? rho / G : 0, hh = g * G + (valid ? rho % G : 0);
     const int tok = valid ? min(__ldg(q_tok + rt), n_keys - 1) : -1;
     {  // this row's 64 elements of Q (half wg) -> TMEM columns QCOL + 32 wg .. (bf16 pairs), the QK^T A operand
-      const uint4* src = reinterpret_cast<const uint4*>(q + (size_t)__ldg(q_row + rt) * qd + (size_t)hh * HD + wg * KW);
       uint32_t pk[KW / 2];
 #pragma unroll
       for (int c8 = 0; c8 < KW / 8; ++c8) {
-        const uint4 u = valid ? __ldg(src + c8) : make_uint4(0u, 0u, 0u, 0u);
-        pk[4 * c8] = u.x; pk[4 * c8 + 1] = u.y; pk[4 * c8 + 2] = u.z; pk[4 * c8 + 3] = u.w;
+        pk[4 * c8] = qv[c8].x; pk[4 * c8 + 1] = qv[c8].y; pk[4 * c8 + 2] = qv[c8].z; pk[4 * c8 + 3] = qv[c8].w;
       }
       tc::tmem_st32u(tmem + lane_base + QCOL + wg * (KW / 2), pk);
       tc::tmem_st_wait();
