@@ -10,7 +10,8 @@
 //   warp 1     MMA issuer: S_t = Q K_t^T (M=128, N=128 keys, K=16; A = Q from TMEM) into one of two TMEM S
 //              buffers, then O += P_t V_t (A = P from TMEM, B = V MN-major) into the TMEM O buffer.
 //              S_{t+1} is issued before waiting for P_t, so QK^T overlaps the softmax of tile t.
-//   warps 2-9  softmax: two warpgroups, thread = (query row, 64-key half). Each tcgen05.lds its half of
+//   warps 2-9  softmax: two warpgroups, thread = (query row, 64-key half). Its half of the gathered Q row is
+//              loaded before the prologue and stored into TMEM after it. Each tcgen05.lds its half of
 //              the S row, masks by original position, and the two halves agree on the row max through
 //              shared memory; online softmax in the log2 domain with lazy rescaling (O is rescaled in
 //              TMEM only when the row max grows by more than 2^8); P (bf16 pairs) is written over the
@@ -25,7 +26,8 @@
 // (deterministic) and writes the output -- no separate merge launch.
 // Variants measured and removed (source in git history): a share of the exponentials on
 // the FMA pipe, four softmax warpgroups, Q staged in shared memory, light/heavy row-tile pairing in
-// 2-CTA clusters with a DSMEM merge, two key streams per CTA, P packed on the integer pipe.
+// 2-CTA clusters with a DSMEM merge, two key streams per CTA, P packed on the integer pipe, the output
+// staged through shared memory, the first K/V tiles issued before the prologue sync.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
