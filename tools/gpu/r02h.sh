@@ -1,8 +1,11 @@
+#!/bin/bash
+# final validation on the final code: GPU suite, smoke, bench line, launch list
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q 2>&1 | tail -4
-for shp in "553 4096 4096 1 1" "553 6144 4096 1 0" "553 4096 14336 1 1"; do
-  echo "== trace $shp"; python tools/gemm_trace.py $shp 2>&1 | head -10
-done > gpurun_out/r02h_gemm_traces.txt
-head -36 gpurun_out/r02h_gemm_traces.txt
-python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r02h_bench.json 2> gpurun_out/r02h_bench.err
-python -c "import json;d=json.loads(open('gpurun_out/r02h_bench.json').read().strip().splitlines()[-1]);print(d['ms_per_step'],d['value'],d['kernel_ms'],d['roofline']['frac'],d['roofline']['path']['frac'])"
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/r02h_pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/r02h_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02h_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/r02h_smoke.log
+timeout 900 python bench.py > gpurun_out/r02h_bench.json 2> gpurun_out/r02h_bench.err; echo "bench rc=$?"
+python -c "import json;d=json.loads(open('gpurun_out/r02h_bench.json').read().strip().splitlines()[-1]);print('mistral', d['ms_per_step'], d['value'], d['roofline']['frac'], d['roofline']['path']['frac'], d['roofline']['attention']['frac'], d['e2e']['ms'], d['e2e'].get('paired_overhead_ms'), d['clocks'])"
+CB_PROFILE_RANGE=1 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/r02h_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-baselines > gpurun_out/r02h_ncu_list.log 2>&1
+python tools/launch_summary.py gpurun_out/r02h_launches.csv 2 > gpurun_out/r02h_launch_summary.txt 2>&1; head -8 gpurun_out/r02h_launch_summary.txt
